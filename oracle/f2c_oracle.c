@@ -1,0 +1,288 @@
+/*
+ * f2c_oracle.c -- plain, slow, obviously-correct CPU oracle for the F2C DCP head.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load this library.  The product path
+ * (paper_2105_10375_b200/) never links, imports or calls it, and shares no code,
+ * header, table or constant with it.
+ *
+ * Everything is fp64, single-threaded, written in the paper's order and notation.
+ * Inputs are the same dtype-rounded bytes the GPU consumes (bf16 bit patterns or
+ * fp32), upcast exactly to double.  Compile with -O2 -ffp-contract=off.
+ *
+ * Citations: P:n = /root/reference/PAPER.md line n (section / equation named
+ * alongside); S:n = SPEC.md line n; D-n = reading n of DESIGN.md section 3.
+ *
+ *   orc_enqueue      Eq. 7 + Algorithm 1: ring of C slots.
+ *   orc_loss         Eq. 6 split, Eq. 8 logits (K=1),
+ *                    Eq. 9 CE with scale s and cosine margin m (D3),
+ *                    L_cos (mean reduction D10), L_total,
+ *                    gradient w.r.t. the raw P-Net features (D12).
+ *   orc_loss_rows    the same definition, evaluated for a subset of rows only
+ *                    (the global normalisers N_pos, N_neg, C_occ and mu are still
+ *                    computed from the whole batch / pool).
+ *   orc_ema          G-Net moving average phi <- m*phi + (1-m)*theta.
+ *
+ * Parity status: every function here is pinned by tests/test_oracle_pins.py
+ * (pins P1-P8 of DESIGN.md section 4).  The semantics choices D3 (margin form),
+ * D8 (newest duplicate is the target) and D10 (mean reduction of phi) have no
+ * paper-printed numbers; they are pinned only by closed forms derived from those
+ * readings ("parity unpinned" with respect to the paper for those choices).
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define ORC_OK 0
+#define ORC_EINVAL 1
+#define ORC_ESHAPE 2
+#define ORC_ECAPACITY 3
+#define ORC_EPAIRING 4
+#define ORC_EZERO 5
+
+/* ---- dtype upcast: 0 = bf16 (uint16 bit pattern), 1 = fp32 ------------------ */
+static double orc_elem(const void *base, int dtype, int64_t idx) {
+    if (dtype == 0) {
+        uint16_t h = ((const uint16_t *)base)[idx];
+        uint32_t w = ((uint32_t)h) << 16;
+        float f;
+        memcpy(&f, &w, sizeof f);
+        return (double)f;
+    }
+    return (double)((const float *)base)[idx];
+}
+
+static size_t orc_esize(int dtype) { return dtype == 0 ? 2u : 4u; }
+
+/* ---- Eq. 7 / Algorithm 1 ------------------------------------------------------
+ * T[C][d] (raw dtype bytes), lab[C], *E = rows ever enqueued, *M_last = size of
+ * the last block.  While E < C this is Algorithm 1's sequential fill of the
+ * unoccupied positions; afterwards it overwrites the oldest rows, which
+ * is Eq. 7's shift up to relabelling of positions (D6, D7). */
+int orc_enqueue(int64_t C, int32_t d, int32_t dtype, void *T, int64_t *lab, int64_t *E,
+                int64_t *M_last, const void *G, const int64_t *y, int64_t M) {
+    if (C < 1 || d < 1 || (dtype != 0 && dtype != 1)) return ORC_EINVAL;
+    if (M < 1 || M > C) return ORC_ECAPACITY;
+    for (int64_t j = 0; j < M; ++j)
+        if (y[j] < 0) return ORC_EINVAL;
+    size_t rb = (size_t)d * orc_esize(dtype);
+    for (int64_t j = 0; j < M; ++j) {
+        int64_t c = (*E + j) % C;
+        memcpy((char *)T + (size_t)c * rb, (const char *)G + (size_t)j * rb, rb);
+        lab[c] = y[j];
+    }
+    *E += M;
+    *M_last = M;
+    return ORC_OK;
+}
+
+/* global write index of the current content of slot c (c < min(E, C)) */
+static int64_t orc_seq(int64_t c, int64_t C, int64_t E) { return c + C * ((E - 1 - c) / C); }
+
+/* ---- shared pieces of the loss definition ------------------------------------ */
+typedef struct {
+    int64_t C, N, E, M_last, C_occ;
+    int32_t d, dtype;
+    const void *T;
+    const int64_t *lab;
+    const void *X;
+    const int64_t *y;
+    double s, m;
+    /* derived */
+    double *n;     /* [N] row norms ||x_i|| */
+    int64_t *t;    /* [N] target slot or -1 (Eq. 6 split) */
+    int64_t N_pos, N_neg;
+    double *mu;    /* [d] sum over occupied slots of T_c */
+} orc_ctx;
+
+/* step 1-4 of the definition: norms, targets, split, mu */
+static int orc_prepare(orc_ctx *q, const int32_t *pairing) {
+    int64_t N = q->N, C = q->C;
+    int32_t d = q->d;
+    q->C_occ = q->E < C ? q->E : C;
+    for (int64_t i = 0; i < N; ++i) {
+        double ss = 0.0;
+        for (int32_t k = 0; k < d; ++k) {
+            double v = orc_elem(q->X, q->dtype, i * d + k);
+            ss += v * v;
+        }
+        q->n[i] = sqrt(ss);
+        if (!(q->n[i] > 0.0)) return ORC_EZERO;
+    }
+    q->N_pos = 0;
+    for (int64_t i = 0; i < N; ++i) {
+        int64_t best = -1, best_seq = -1;
+        for (int64_t c = 0; c < q->C_occ; ++c) {
+            if (q->lab[c] != q->y[i]) continue;
+            int64_t sq = orc_seq(c, C, q->E);
+            if (sq > best_seq) { best_seq = sq; best = c; }
+        }
+        q->t[i] = best;
+        if (pairing && pairing[i] >= 0) {
+            int64_t want = (q->E - q->M_last + pairing[i]) % C;
+            if (pairing[i] >= q->M_last || best != want) return ORC_EPAIRING;
+        }
+        if (best >= 0) q->N_pos++;
+    }
+    q->N_neg = N - q->N_pos;
+    for (int32_t k = 0; k < d; ++k) q->mu[k] = 0.0;
+    for (int64_t c = 0; c < q->C_occ; ++c)
+        for (int32_t k = 0; k < d; ++k) q->mu[k] += orc_elem(q->T, q->dtype, c * d + k);
+    return ORC_OK;
+}
+
+/* per-row loss contribution and gradient (steps 5-9 of the definition).
+ * Writes ell (CE term, in-pool rows) or phi (cosine term, out-of-pool rows),
+ * lse, the gradient dx_i (raw x) and optionally p_i[c] and accumulates dT. */
+static void orc_row(const orc_ctx *q, int64_t i, double *ell, double *phi, double *lse,
+                    double *dx, double *prow, double *dT, double *cos_buf, double *g) {
+    int32_t d = q->d;
+    int64_t Co = q->C_occ;
+    double inv_n = 1.0 / q->n[i];
+    /* x_hat */
+    for (int32_t k = 0; k < d; ++k) g[k] = 0.0;
+    for (int64_t c = 0; c < Co; ++c) {
+        double dot = 0.0;
+        for (int32_t k = 0; k < d; ++k)
+            dot += orc_elem(q->X, q->dtype, i * d + k) * inv_n * orc_elem(q->T, q->dtype, c * d + k);
+        cos_buf[c] = dot; /* Eq. 8 with K = 1: <F_p, T[c]> on the normalised feature */
+    }
+    *ell = 0.0;
+    *phi = 0.0;
+    *lse = 0.0;
+    if (q->t[i] >= 0) {
+        /* Eq. 9 with z_ic = s*cos_ic and the target logit s*(cos_it - m)  (D3) */
+        int64_t t = q->t[i];
+        double zmax = -INFINITY;
+        for (int64_t c = 0; c < Co; ++c) {
+            double z = q->s * cos_buf[c] - (c == t ? q->s * q->m : 0.0);
+            if (z > zmax) zmax = z;
+        }
+        double sum = 0.0;
+        for (int64_t c = 0; c < Co; ++c) {
+            double z = q->s * cos_buf[c] - (c == t ? q->s * q->m : 0.0);
+            sum += exp(z - zmax);
+        }
+        double L = zmax + log(sum);
+        *lse = L;
+        *ell = L - (q->s * cos_buf[t] - q->s * q->m);
+        double w = q->s / (double)q->N_pos;
+        for (int64_t c = 0; c < Co; ++c) {
+            double z = q->s * cos_buf[c] - (c == t ? q->s * q->m : 0.0);
+            double p = exp(z - L);
+            if (prow) prow[c] = p;
+            double gc = w * (p - (c == t ? 1.0 : 0.0)); /* dL/dz * dz/dcos */
+            for (int32_t k = 0; k < d; ++k) g[k] += gc * orc_elem(q->T, q->dtype, c * d + k);
+            if (dT)
+                for (int32_t k = 0; k < d; ++k)
+                    dT[c * d + k] += gc * orc_elem(q->X, q->dtype, i * d + k) * inv_n;
+        }
+    } else {
+        /* L_cos: phi_i = mean over occupied slots of cos(x_i, T_c)  (D10) */
+        if (Co > 0) {
+            double acc = 0.0;
+            for (int64_t c = 0; c < Co; ++c) acc += cos_buf[c];
+            *phi = acc / (double)Co;
+            double w = 1.0 / ((double)q->N_neg * (double)Co);
+            for (int64_t c = 0; c < Co; ++c) {
+                for (int32_t k = 0; k < d; ++k) g[k] += w * orc_elem(q->T, q->dtype, c * d + k);
+                if (dT)
+                    for (int32_t k = 0; k < d; ++k)
+                        dT[c * d + k] += w * orc_elem(q->X, q->dtype, i * d + k) * inv_n;
+            }
+        }
+    }
+    /* normalisation Jacobian: dL/dx = (I - x_hat x_hat^T) g / ||x||  (D12) */
+    double gx = 0.0;
+    for (int32_t k = 0; k < d; ++k) gx += g[k] * orc_elem(q->X, q->dtype, i * d + k) * inv_n;
+    for (int32_t k = 0; k < d; ++k) {
+        double xh = orc_elem(q->X, q->dtype, i * d + k) * inv_n;
+        dx[k] = (g[k] - gx * xh) * inv_n;
+    }
+}
+
+/* Full definition over all N rows.
+ * out3 = {L, L_ce, L_cos}; dx [N*d]; lse [N] (0 for out-of-pool rows); tslot [N];
+ * phi [N] (0 for in-pool rows); ell [N] (0 for out-of-pool rows);
+ * counts = {N_pos, N_neg, C_occ}; P [N * C_occ] or NULL; dT [C * d] or NULL. */
+int orc_loss(int64_t C, int32_t d, int32_t dtype, const void *T, const int64_t *lab, int64_t E,
+             int64_t M_last, int64_t N, const void *X, const int64_t *y, const int32_t *pairing,
+             double s, double m, double *out3, double *dx, double *lse, int64_t *tslot, double *phi,
+             double *ell, int64_t *counts, double *P, double *dT) {
+    if (C < 1 || d < 1 || N < 0 || (dtype != 0 && dtype != 1)) return ORC_EINVAL;
+    if (!(s > 0.0) || !isfinite(m)) return ORC_EINVAL;
+    orc_ctx q = {0};
+    q.C = C; q.N = N; q.E = E; q.M_last = M_last; q.d = d; q.dtype = dtype;
+    q.T = T; q.lab = lab; q.X = X; q.y = y; q.s = s; q.m = m;
+    q.n = (double *)calloc((size_t)(N > 0 ? N : 1), sizeof(double));
+    q.t = (int64_t *)calloc((size_t)(N > 0 ? N : 1), sizeof(int64_t));
+    q.mu = (double *)calloc((size_t)d, sizeof(double));
+    int64_t Cmax = C;
+    double *cos_buf = (double *)calloc((size_t)Cmax, sizeof(double));
+    double *g = (double *)calloc((size_t)d, sizeof(double));
+    int rc = orc_prepare(&q, pairing);
+    if (rc == ORC_OK) {
+        if (dT) memset(dT, 0, (size_t)C * d * sizeof(double));
+        double sce = 0.0, scos = 0.0;
+        for (int64_t i = 0; i < N; ++i) {
+            double e, f, l;
+            orc_row(&q, i, &e, &f, &l, dx + i * d, P ? P + i * q.C_occ : NULL, dT, cos_buf, g);
+            lse[i] = l; phi[i] = f; ell[i] = e; tslot[i] = q.t[i];
+            sce += e;
+            scos += f;
+        }
+        double Lce = q.N_pos > 0 ? sce / (double)q.N_pos : 0.0;  /* 1/I */
+        double Lcos = q.N_neg > 0 ? scos / (double)q.N_neg : 0.0; /* 1/(M-I) */
+        out3[0] = Lce + Lcos; /* L_total = L_ce + L_cos */
+        out3[1] = Lce;
+        out3[2] = Lcos;
+        counts[0] = q.N_pos; counts[1] = q.N_neg; counts[2] = q.C_occ;
+    }
+    free(q.n); free(q.t); free(q.mu); free(cos_buf); free(g);
+    return rc;
+}
+
+/* Same definition for a subset of rows (for configurations too large for the
+ * full O(N*C*d) evaluation).  Normalisers are global.  Outputs are per selected
+ * row: dx [nsel*d], lse, tslot, phi, ell. counts = {N_pos, N_neg, C_occ}. */
+int orc_loss_rows(int64_t C, int32_t d, int32_t dtype, const void *T, const int64_t *lab,
+                  int64_t E, int64_t M_last, int64_t N, const void *X, const int64_t *y,
+                  const int32_t *pairing, double s, double m, int64_t nsel, const int64_t *rows,
+                  double *dx, double *lse, int64_t *tslot, double *phi, double *ell,
+                  int64_t *counts, double *mu_out) {
+    if (C < 1 || d < 1 || N < 0 || (dtype != 0 && dtype != 1)) return ORC_EINVAL;
+    orc_ctx q = {0};
+    q.C = C; q.N = N; q.E = E; q.M_last = M_last; q.d = d; q.dtype = dtype;
+    q.T = T; q.lab = lab; q.X = X; q.y = y; q.s = s; q.m = m;
+    q.n = (double *)calloc((size_t)(N > 0 ? N : 1), sizeof(double));
+    q.t = (int64_t *)calloc((size_t)(N > 0 ? N : 1), sizeof(int64_t));
+    q.mu = (double *)calloc((size_t)d, sizeof(double));
+    double *cos_buf = (double *)calloc((size_t)C, sizeof(double));
+    double *g = (double *)calloc((size_t)d, sizeof(double));
+    int rc = orc_prepare(&q, pairing);
+    if (rc == ORC_OK) {
+        for (int64_t k = 0; k < nsel; ++k) {
+            int64_t i = rows[k];
+            double e, f, l;
+            orc_row(&q, i, &e, &f, &l, dx + k * d, NULL, NULL, cos_buf, g);
+            lse[k] = l; phi[k] = f; ell[k] = e; tslot[k] = q.t[i];
+        }
+        counts[0] = q.N_pos; counts[1] = q.N_neg; counts[2] = q.C_occ;
+        if (mu_out) memcpy(mu_out, q.mu, (size_t)d * sizeof(double));
+    }
+    free(q.n); free(q.t); free(q.mu); free(cos_buf); free(g);
+    return rc;
+}
+
+/* G-Net moving average: g <- m*g + (1-m)*p, evaluated in fp64
+ * exactly in that order, rounded to nearest-even fp32 (D17). */
+int orc_ema(const float *p, float *g, int64_t n, double momentum) {
+    if (n < 0 || !(momentum >= 0.0 && momentum <= 1.0)) return ORC_EINVAL;
+    for (int64_t k = 0; k < n; ++k) {
+        double a = momentum * (double)g[k];
+        double b = (1.0 - momentum) * (double)p[k];
+        g[k] = (float)(a + b);
+    }
+    return ORC_OK;
+}

@@ -1,0 +1,355 @@
+"""Pins of the CPU oracle against what the paper and the mathematics fix
+(pins P1-P8).  None of these compare the oracle with itself:
+each uses a closed form, an independent formulation (textbook Eq. 1/4/5, torch
+autograd of an independently written loss, a literal Eq. 7 shift), finite
+differences of the oracle's own loss value, or an invariant."""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from oracle import BF16, F32, Pool
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden", "closed_forms.json")
+
+
+def _pool_from(rows, dtype=F32):
+    d = len(rows[0][0])
+    p = Pool(len(rows), d, dtype)
+    for vec, lab in rows:  # one enqueue per slot, oldest first
+        G = np.array([vec], dtype=np.float32) if dtype == F32 else oracle.f64_to_bf16(np.array([vec]))
+        p.enqueue(G, np.array([lab]))
+    return p
+
+
+# ----------------------------------------------------------------------------- P4/P5
+@pytest.mark.parametrize("case", json.load(open(GOLD))["cases"], ids=lambda c: c["id"])
+def test_closed_forms(case):
+    p = _pool_from(case["pool"])
+    X = np.array(case["x"], dtype=np.float32)
+    r = p.loss(X, np.array(case["y"]), None, case["s"], case["m"])
+    # inputs are stored as fp32 (0.6, 0.8 are not exact), and s=64 amplifies that
+    # rounding (|dz| <= 64 * 2^-24 per unit input): tolerances reflect it.
+    assert r.L == pytest.approx(case["L"], rel=5e-6, abs=1e-9)
+    if case["dx"] is not None:
+        np.testing.assert_allclose(r.dx, np.array(case["dx"]), rtol=5e-6, atol=1e-9)
+
+
+@pytest.mark.parametrize("case", json.load(open(GOLD))["dT_cases"], ids=lambda c: c["id"])
+def test_closed_form_pool_gradient(case):
+    p = _pool_from(case["pool"])
+    r = p.loss(np.array(case["x"], np.float32), np.array(case["y"]), None, case["s"], case["m"],
+               want_dT=True)
+    np.testing.assert_allclose(r.dT, np.array(case["dT"]), atol=1e-12)
+
+
+def test_duplicate_target_is_newest_and_slot_order_irrelevant():
+    """D8: with the slot contents permuted but the write order (seq) kept, the
+    loss is unchanged (case F enqueued in a different physical order)."""
+    rows = json.load(open(GOLD))["cases"][4]["pool"]
+    base = _pool_from(rows).loss(np.array([[1.0, 0.0]], np.float32), np.array([7]), None, 64, 0.35)
+    # wrap the ring so the same four rows (same write order) land in rotated slots
+    p = Pool(4, 2, F32)
+    p.enqueue(np.zeros((2, 2), np.float32), np.array([100, 101]))  # will be overwritten
+    for vec, lab in rows:
+        p.enqueue(np.array([vec], np.float32), np.array([lab]))
+    r = p.loss(np.array([[1.0, 0.0]], np.float32), np.array([7]), None, 64, 0.35)
+    assert r.L == pytest.approx(base.L, rel=1e-14)
+    assert r.tslot[0] == 0  # newest label-7 row was written 5th -> slot (2+2) % 4 = 0
+    np.testing.assert_allclose(r.dx, base.dx, rtol=1e-13)
+
+
+# ----------------------------------------------------------------------------- P1
+def _logsumexp(a, axis=-1):
+    mx = np.max(a, axis=axis, keepdims=True)
+    return (mx + np.log(np.sum(np.exp(a - mx), axis=axis, keepdims=True))).squeeze(axis)
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_eq4_reduces_to_eq1_full_softmax(seed):
+    """P1: pool = the full classifier W (all n_ID classes, distinct labels), s=1,
+    m=0 -> L equals the textbook full-softmax CE of Eq. 1 on x_hat."""
+    rng = np.random.default_rng(seed)
+    n_id, d, N = 37, 6, 9
+    W = rng.standard_normal((n_id, d)).astype(np.float32)
+    X = rng.standard_normal((N, d)).astype(np.float32)
+    y = rng.integers(0, n_id, N)
+    p = Pool(n_id, d, F32)
+    p.enqueue(W, np.arange(n_id))
+    r = p.loss(X, y, None, 1.0, 0.0)
+    Xh = X.astype(np.float64) / np.linalg.norm(X.astype(np.float64), axis=1, keepdims=True)
+    logits = Xh @ W.astype(np.float64).T                       # W_j^T x_i
+    L_eq1 = -np.mean(logits[np.arange(N), y] - _logsumexp(logits))
+    assert r.N_pos == N and r.N_neg == 0
+    assert abs(r.L - L_eq1) <= 1e-12
+
+
+# ----------------------------------------------------------------------------- P2
+def test_masked_softmax_eq4_eq5_and_autograd_dx():
+    """P2: pool = {W_j : nu_j = 1} with every batch label selected (Eq. 3).
+    Oracle L == Eq. 4; oracle dL/dT_k == Eq. 5 for the selected
+    classifiers; oracle dx == torch autograd of Eq. 4 through x_hat = x/||x||."""
+    rng = np.random.default_rng(5)
+    n_id, d, N, C = 50, 7, 8, 20
+    W = rng.standard_normal((n_id, d)).astype(np.float32)
+    X = rng.standard_normal((N, d)).astype(np.float32)
+    y = rng.choice(n_id, N, replace=True)
+    sel = set(y.tolist())
+    rest = [j for j in range(n_id) if j not in sel]
+    sel = sorted(sel | set(rng.choice(rest, C - len(sel), replace=False).tolist()))
+    nu = np.zeros(n_id)
+    nu[sel] = 1.0
+    p = Pool(C, d, F32)
+    p.enqueue(W[sel], np.array(sel))
+    r = p.loss(X, y, None, 1.0, 0.0, want_dT=True)
+
+    X64, W64 = X.astype(np.float64), W.astype(np.float64)
+    Xh = X64 / np.linalg.norm(X64, axis=1, keepdims=True)
+    logits = Xh @ W64.T
+    masked = np.where(nu[None, :] > 0, logits, -np.inf)
+    L_eq4 = -np.mean(logits[np.arange(N), y] - _logsumexp(masked))
+    assert abs(r.L - L_eq4) <= 1e-12 * max(1.0, abs(L_eq4))
+
+    # Eq. 5: dL/dW_k = -1/N sum_i (delta_{k y_i} - nu_k p_ik) x_i
+    phat = np.exp(masked - _logsumexp(masked)[:, None])
+    dW = np.zeros_like(W64)
+    for k in range(n_id):
+        for i in range(N):
+            dW[k] += -(1.0 / N) * ((1.0 if y[i] == k else 0.0) - nu[k] * phat[i, k]) * Xh[i]
+    np.testing.assert_allclose(r.dT, dW[sel], rtol=1e-8, atol=1e-13)
+
+    xt = torch.tensor(X64, requires_grad=True)
+    xh = xt / xt.norm(dim=1, keepdim=True)
+    lg = xh @ torch.tensor(W64).T
+    lg = lg.masked_fill(torch.tensor(nu)[None, :] == 0, -float("inf"))
+    loss = torch.nn.functional.cross_entropy(lg, torch.tensor(y))
+    loss.backward()
+    np.testing.assert_allclose(r.dx, xt.grad.numpy(), rtol=1e-8, atol=1e-13)
+
+
+def test_margin_scale_dups_outofpool_vs_autograd():
+    """P2': full definition with s, m, duplicate labels and out-of-pool rows; the
+    oracle's hand-derived gradient equals torch autograd of an independently
+    written loss (targets = newest duplicate, D8)."""
+    rng = np.random.default_rng(11)
+    C, d = 12, 6
+    T = rng.standard_normal((C, d)).astype(np.float32)
+    lab = rng.integers(0, 5, C)
+    p = Pool(C, d, F32)
+    p.enqueue(T, lab)
+    N = 7
+    X = (rng.standard_normal((N, d)) * 2).astype(np.float32)
+    y = np.array([0, 1, 2, 3, 4, 9, 11])
+    s, m = 30.0, 0.2
+    r = p.loss(X, y, None, s, m)
+    # independent formulation
+    tgt = []
+    for i in range(N):
+        hits = [c for c in range(C) if lab[c] == y[i]]
+        tgt.append(max(hits) if hits else -1)  # single fill: seq == slot, newest = largest
+    np.testing.assert_array_equal(r.tslot, tgt)
+    xt = torch.tensor(X.astype(np.float64), requires_grad=True)
+    Tt = torch.tensor(T.astype(np.float64))
+    cos = (xt / xt.norm(dim=1, keepdim=True)) @ Tt.T
+    pos = [i for i in range(N) if tgt[i] >= 0]
+    neg = [i for i in range(N) if tgt[i] < 0]
+    z = s * cos
+    ce = 0
+    for i in pos:
+        zi = z[i].clone()
+        zi[tgt[i]] = zi[tgt[i]] - s * m
+        ce = ce + torch.logsumexp(zi, 0) - zi[tgt[i]]
+    loss = ce / len(pos) + sum(cos[i].mean() for i in neg) / len(neg)
+    loss.backward()
+    assert r.L == pytest.approx(loss.item(), rel=1e-12)
+    np.testing.assert_allclose(r.dx, xt.grad.numpy(), rtol=1e-9, atol=1e-12)
+
+
+# ----------------------------------------------------------------------------- P3
+def test_finite_differences_of_oracle_loss():
+    """P3: Richardson-extrapolated central differences of the oracle's L with
+    respect to the raw x.  Inputs are dyadic so x +- h is exact in fp32."""
+    rng = np.random.default_rng(3)
+    C, d, N = 14, 8, 6
+    T = (rng.integers(-128, 128, (C, d)) / 128.0).astype(np.float32)
+    lab = rng.integers(0, 6, C)
+    p = Pool(C, d, F32)
+    p.enqueue(T, lab)
+    X = (rng.integers(-256, 256, (N, d)) / 128.0).astype(np.float32)
+    X[0] *= 3  # ||x|| != 1
+    y = np.array([0, 1, 2, 3, 7, 8])  # some in-pool (incl. duplicates), some out-of-pool
+    s, m = 16.0, 0.35
+    r = p.loss(X, y, None, s, m)
+    assert r.N_pos >= 2 and r.N_neg >= 1
+
+    def L(Xp):
+        return p.loss(Xp, y, None, s, m).L
+
+    h = 2.0 ** -8
+    num = np.zeros_like(r.dx)
+    for i in range(N):
+        for k in range(d):
+            def D(hh):
+                Xa, Xb = X.copy(), X.copy()
+                Xa[i, k] += hh
+                Xb[i, k] -= hh
+                return (L(Xa) - L(Xb)) / (2 * hh)
+            num[i, k] = (4 * D(h / 2) - D(h)) / 3
+    np.testing.assert_allclose(r.dx, num, rtol=1e-6, atol=1e-8)
+
+
+# ----------------------------------------------------------------------------- P6
+def test_invariants_softmax_rows_cosines_and_permutation():
+    """P6: sum_c p_ic = 1; cos in [-1,1] on fp64-unit data (phi in [-1,1], ell >= 0);
+    row-permutation equivariance."""
+    rng = np.random.default_rng(9)
+    C, d, N = 40, 16, 10
+    T = rng.standard_normal((C, d))
+    T /= np.linalg.norm(T, axis=1, keepdims=True)
+    p = Pool(C, d, F32)
+    p.enqueue(T.astype(np.float32), rng.integers(0, 8, C))
+    X = rng.standard_normal((N, d)).astype(np.float32)
+    y = np.concatenate([rng.integers(0, 8, 6), np.arange(100, 104)])
+    r = p.loss(X, y, None, 64.0, 0.35, want_P=True)
+    pos = r.tslot >= 0
+    np.testing.assert_allclose(r.P[pos].sum(axis=1), 1.0, atol=1e-12)
+    assert np.all(r.ell[pos] >= 0)
+    assert np.all(np.abs(r.phi) <= 1.0 + 1e-6)
+    perm = rng.permutation(N)
+    r2 = p.loss(X[perm], y[perm], None, 64.0, 0.35)
+    assert r2.L == pytest.approx(r.L, rel=1e-13)
+    np.testing.assert_allclose(r2.dx, r.dx[perm], rtol=1e-12, atol=1e-15)
+
+
+def test_loss_rows_matches_full():
+    rng = np.random.default_rng(4)
+    C, d, N = 30, 8, 12
+    p = Pool(C, d, BF16)
+    p.enqueue(oracle.f64_to_bf16(rng.standard_normal((C, d))), rng.integers(0, 6, C))
+    X = oracle.f64_to_bf16(rng.standard_normal((N, d)))
+    y = rng.integers(0, 9, N)
+    full = p.loss(X, y, None, 64.0, 0.35)
+    rows = np.array([11, 0, 5])
+    sub = p.loss_rows(X, y, None, 64.0, 0.35, rows)
+    np.testing.assert_allclose(sub["dx"], full.dx[rows], rtol=1e-14)
+    np.testing.assert_allclose(sub["lse"], full.lse[rows], rtol=1e-14)
+    assert sub["N_pos"] == full.N_pos
+
+
+def test_pairing_check_and_errors():
+    p = Pool(8, 2, F32)
+    p.enqueue(np.eye(2, dtype=np.float32).repeat(2, 0), np.array([1, 2, 3, 4]))
+    X = np.array([[1, 0], [0, 1]], np.float32)
+    p.loss(X, np.array([3, 9]), np.array([2, -1], np.int32), 64, 0.35)  # row 0 paired to block row 2
+    with pytest.raises(oracle.OracleError) as e:
+        p.loss(X, np.array([3, 9]), np.array([1, -1], np.int32), 64, 0.35)
+    assert e.value.code == 4
+    with pytest.raises(oracle.OracleError):
+        p.loss(np.zeros((1, 2), np.float32), np.array([1]), None, 64, 0.35)  # zero row
+    with pytest.raises(oracle.OracleError) as e:
+        p.enqueue(np.zeros((9, 2), np.float32), np.arange(9))
+    assert e.value.code == 3
+
+
+# ----------------------------------------------------------------------------- P7
+def _literal_shift(T, lab, occ, G, y):
+    """Eq. 7 literally plus Algorithm 1's fill branch:
+    an array of C rows; the first `occ` are occupied, oldest first."""
+    C, M = len(lab), len(y)
+    if occ + M <= C:            # fill unoccupied positions sequentially
+        T[occ:occ + M] = G
+        lab[occ:occ + M] = y
+        return occ + M
+    # shift out the oldest rows, append the new block at the end
+    k = occ + M - C
+    T[:occ - k] = T[k:occ].copy()
+    lab[:occ - k] = lab[k:occ].copy()
+    T[C - M:] = G
+    lab[C - M:] = y
+    return C
+
+
+def test_enqueue_spec_example_and_wrap():
+    """A,B / C,D / E,F at C=4 -> slots [E,F,C,D]; wrap at C=5, M=2 -> [F,B,C,D,E]
+    which as a ring read from the oldest equals the literal shift [B,C,D,E,F]."""
+    p = Pool(4, 1, F32)
+    for blk in ([1, 2], [3, 4], [5, 6]):
+        p.enqueue(np.array(blk, np.float32)[:, None], np.array(blk))
+    assert p.lab.tolist() == [5, 6, 3, 4]
+    p = Pool(5, 1, F32)
+    for blk in ([1, 2], [3, 4], [5, 6]):
+        p.enqueue(np.array(blk, np.float32)[:, None], np.array(blk))
+    assert p.lab.tolist() == [6, 2, 3, 4, 5]
+    head = int(p.E[0]) % 5
+    assert np.roll(p.lab, -head).tolist() == [2, 3, 4, 5, 6]
+
+
+def test_enqueue_equals_literal_shift_random():
+    """10^3 random blocks of random M <= C at C <= 64; the ring read
+    from its oldest slot equals a literal Eq. 7 shift implementation."""
+    rng = np.random.default_rng(1)
+    for trial in range(4):
+        C, d = int(rng.integers(1, 65)), 3
+        p = Pool(C, d, F32)
+        T_lit = np.zeros((C, d), np.float32)
+        lab_lit = np.full(C, -1, np.int64)
+        occ = 0
+        for it in range(250):
+            M = int(rng.integers(1, C + 1))
+            G = rng.standard_normal((M, d)).astype(np.float32)
+            y = rng.integers(0, 10**6, M)
+            p.enqueue(G, y)
+            occ = _literal_shift(T_lit, lab_lit, occ, G, y)
+            E = int(p.E[0])
+            if E < C:
+                order = np.arange(E)
+            else:
+                order = (np.arange(C) + E) % C  # oldest first
+            np.testing.assert_array_equal(p.T[order], T_lit[:occ])
+            np.testing.assert_array_equal(p.lab[order], lab_lit[:occ])
+
+
+def test_residency_and_last_blocks():
+    """P:207 / S:279 / S:311: with M | C every row stays exactly C/M enqueues; after
+    k enqueues the pool holds exactly the last ceil(C/M) blocks in order (BJ:5)."""
+    C, M = 12, 3
+    p = Pool(C, 1, F32)
+    first_seen, last_seen = {}, {}
+    for k in range(1, 20):
+        ids = np.arange((k - 1) * M, k * M)
+        p.enqueue(ids.astype(np.float32)[:, None], ids)
+        for v in p.lab[: min(k * M, C)]:
+            first_seen.setdefault(int(v), k)
+            last_seen[int(v)] = k
+        nb = math.ceil(C / M)
+        want = np.arange(max(0, k - nb) * M, k * M)
+        assert sorted(p.lab[: min(k * M, C)].tolist()) == want.tolist()
+    for v in range(0, 10 * M):
+        assert last_seen[v] - first_seen[v] + 1 == C // M
+
+
+# ----------------------------------------------------------------------------- P8
+def test_ema_boundaries_and_closed_form():
+    """S:220-222 boundaries, S:510 closed form after n steps, S:227 contraction."""
+    rng = np.random.default_rng(0)
+    th = rng.standard_normal(1000).astype(np.float32)
+    ph = rng.standard_normal(1000).astype(np.float32)
+    np.testing.assert_array_equal(oracle.ema(th, ph, 0.0), th)
+    np.testing.assert_array_equal(oracle.ema(th, ph, 1.0), ph)
+    assert oracle.ema(np.zeros(1, np.float32), np.ones(1, np.float32), 0.999)[0] == np.float32(0.999)
+    m = 0.9
+    g = ph.copy()
+    thetas = [rng.standard_normal(1000).astype(np.float32) for _ in range(25)]
+    for t in thetas:
+        g = oracle.ema(t, g, m)
+    n = len(thetas)
+    cf = m ** n * ph.astype(np.float64) + (1 - m) * sum(
+        m ** i * thetas[n - 1 - i].astype(np.float64) for i in range(n))
+    np.testing.assert_allclose(g, cf, rtol=0, atol=n * 2e-7 * np.abs(cf).max())
+    g1 = oracle.ema(th, ph, 0.7)
+    np.testing.assert_allclose(np.abs(g1.astype(np.float64) - th),
+                               0.7 * np.abs(ph.astype(np.float64) - th), rtol=1e-6, atol=1e-6)
