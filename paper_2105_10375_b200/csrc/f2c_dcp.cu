@@ -1,0 +1,684 @@
+// f2c_dcp.cu -- host side of libf2c_dcp.so: the C ABI of include/f2c_dcp.h,
+// argument validation, state-buffer layout, tensor maps, launch sequencing and the
+// multi-rank protocol (slot-range sharding; NCCL over NVLink, or an emulated world
+// on one device for testing).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+#include <dlfcn.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/f2c_dcp.h"
+#include "dcp_main.cuh"
+#include "kernels.cuh"
+
+using namespace f2c;
+
+// ============================================================================ errors
+static thread_local std::string g_err;
+static thread_local int g_launches = 0;
+
+static int fail(int code, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+#define CUDA_TRY(expr)                                                                       \
+    do {                                                                                     \
+        cudaError_t e_ = (expr);                                                             \
+        if (e_ != cudaSuccess) return fail(F2C_ECUDA, "%s: %s", #expr, cudaGetErrorString(e_)); \
+    } while (0)
+#define LAUNCH_CHECK()                                                                       \
+    do {                                                                                     \
+        ++g_launches;                                                                        \
+        cudaError_t e_ = cudaGetLastError();                                                 \
+        if (e_ != cudaSuccess) return fail(F2C_ECUDA, "launch: %s", cudaGetErrorString(e_)); \
+    } while (0)
+
+// ============================================================================ NCCL (dlopen)
+typedef struct { char internal[128]; } nccl_uid_t;
+typedef void *nccl_comm_t;
+enum { NCCL_INT8 = 0, NCCL_INT64 = 4, NCCL_FLOAT32 = 7, NCCL_FLOAT64 = 8 };
+enum { NCCL_SUM = 0, NCCL_MAX = 2 };
+struct NcclApi {
+    int (*CommInitRank)(nccl_comm_t *, int, nccl_uid_t, int) = nullptr;
+    int (*CommDestroy)(nccl_comm_t) = nullptr;
+    int (*AllGather)(const void *, void *, size_t, int, nccl_comm_t, cudaStream_t) = nullptr;
+    int (*AllReduce)(const void *, void *, size_t, int, int, nccl_comm_t, cudaStream_t) = nullptr;
+    int (*ReduceScatter)(const void *, void *, size_t, int, int, nccl_comm_t, cudaStream_t) = nullptr;
+    int (*GroupStart)() = nullptr;
+    int (*GroupEnd)() = nullptr;
+    const char *(*GetErrorString)(int) = nullptr;
+    bool ok = false;
+};
+static NcclApi &nccl() {
+    static NcclApi api;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);  // the copy torch loaded
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (h) {
+            api.CommInitRank = (decltype(api.CommInitRank))dlsym(h, "ncclCommInitRank");
+            api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
+            api.AllGather = (decltype(api.AllGather))dlsym(h, "ncclAllGather");
+            api.AllReduce = (decltype(api.AllReduce))dlsym(h, "ncclAllReduce");
+            api.ReduceScatter = (decltype(api.ReduceScatter))dlsym(h, "ncclReduceScatter");
+            api.GroupStart = (decltype(api.GroupStart))dlsym(h, "ncclGroupStart");
+            api.GroupEnd = (decltype(api.GroupEnd))dlsym(h, "ncclGroupEnd");
+            api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
+            api.ok = api.CommInitRank && api.AllGather && api.AllReduce && api.ReduceScatter &&
+                     api.GroupStart && api.GroupEnd;
+        }
+    }
+    return api;
+}
+
+// ============================================================================ layout
+static inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+static inline int64_t shard_lo(int64_t C, int W, int r) { return C * r / W; }
+
+constexpr int G_MAX = 256;  // upper bound of the persistent grid (SM count)
+
+struct Layout {
+    size_t T, lab, sc, x_all, y_all, pair_all, blk_x, blk_y, inv_n, hslot, hkeys, hvals, tseq,
+        comp_idx, pos_row, X_pos, row_ab, row_tgt, ttgt, seg_l, seg_mx, seg_O, rowloss, st_lse,
+        st_cos, st_phi, st_ell, rs_buf, rs_all, dx_part, mu_buf, total;
+    int64_t C_loc, N, Mg, R_max, S_max;
+    int H;
+};
+
+static Layout make_layout(int64_t C, int d, int dtype, int W, int rank, int64_t n_loc, int64_t m_loc) {
+    Layout L{};
+    const size_t es = dtype == F2C_BF16 ? 2 : 4;
+    const int r = rank < 0 ? 0 : rank;
+    L.C_loc = shard_lo(C, W, r + 1) - shard_lo(C, W, r);
+    // emulated world: size for the largest shard
+    if (rank < 0) L.C_loc = (C + W - 1) / W;
+    L.N = n_loc * W;
+    L.Mg = m_loc * W;
+    L.R_max = (L.N + 1 + 63) / 64 * 64;
+    L.S_max = L.R_max / 64 + G_MAX;
+    int H = 64;
+    while (H < 2 * L.N) H <<= 1;
+    L.H = H;
+    size_t o = 0;
+    auto take = [&](size_t bytes, size_t al = 256) {
+        o = align_up(o, al);
+        size_t at = o;
+        o += bytes;
+        return at;
+    };
+    L.T = take(static_cast<size_t>(L.C_loc) * d * es, 1024);
+    L.lab = take(static_cast<size_t>(L.C_loc) * 8);
+    L.sc = take(sizeof(Scalars));
+    const bool multi = W > 1;
+    L.x_all = take(multi ? static_cast<size_t>(L.N) * d * es : 0);
+    L.y_all = take(multi ? static_cast<size_t>(L.N) * 8 : 0);
+    L.pair_all = take(multi ? static_cast<size_t>(L.N) * 4 : 0);
+    L.blk_x = take(multi ? static_cast<size_t>(L.Mg) * d * es : 0);
+    L.blk_y = take(multi ? static_cast<size_t>(L.Mg) * 8 : 0);
+    L.inv_n = take(static_cast<size_t>(L.N) * 4);
+    L.hslot = take(static_cast<size_t>(L.N) * 4);
+    L.hkeys = take(static_cast<size_t>(H) * 8);
+    L.hvals = take(static_cast<size_t>(H) * 8);
+    L.tseq = take(static_cast<size_t>(L.N) * 8);
+    L.comp_idx = take(static_cast<size_t>(L.N) * 4);
+    L.pos_row = take(static_cast<size_t>(L.N) * 4);
+    L.X_pos = take(static_cast<size_t>(L.R_max) * d * 2, 1024);
+    L.row_ab = take(static_cast<size_t>(L.R_max) * 8);
+    L.row_tgt = take(static_cast<size_t>(L.R_max) * 4);
+    L.ttgt = take(static_cast<size_t>(L.R_max) * 4);
+    L.seg_l = take(static_cast<size_t>(L.S_max) * 64 * 4);
+    L.seg_mx = take(static_cast<size_t>(L.S_max) * 64 * 4);
+    L.seg_O = take(static_cast<size_t>(L.S_max) * 64 * d * 4);
+    L.rowloss = take(static_cast<size_t>(L.N) * 8);
+    L.st_lse = take(static_cast<size_t>(L.N) * 4);
+    L.st_cos = take(static_cast<size_t>(L.N) * 4);
+    L.st_phi = take(static_cast<size_t>(L.N) * 4);
+    L.st_ell = take(static_cast<size_t>(L.N) * 4);
+    // multi-rank exchange buffers: per compacted row (l_rest, max, ttgt) + tmax
+    L.rs_buf = take(multi ? static_cast<size_t>(L.R_max) * 4 * 4 : 0);
+    L.rs_all = take(multi ? static_cast<size_t>(W) * L.R_max * 4 * 4 : 0);
+    L.dx_part = take(multi ? static_cast<size_t>(L.N) * d * 4 : 0);
+    L.mu_buf = take(static_cast<size_t>(d) * 4);
+    L.total = align_up(o, 1024);
+    return L;
+}
+
+// ============================================================================ handle
+struct Rank {
+    int rank;
+    int64_t lo, hi;
+    Layout L;
+    uint8_t *base;
+    CUtensorMap tmT, tmX;
+    template <typename P>
+    P *at(size_t off) const { return reinterpret_cast<P *>(base + off); }
+    Scalars *sc() const { return at<Scalars>(L.sc); }
+};
+
+struct f2c_dcp {
+    int64_t C;
+    int d, dtype, W;
+    bool emulated;
+    int64_t n_local_max, m_local_max;
+    int64_t E = 0, M_last = 0;
+    int G = 148;
+    std::vector<Rank> ranks;  // 1 (real rank) or W (emulated world)
+    cudaStream_t last_stream = nullptr;
+    nccl_comm_t comm = nullptr;
+    int64_t last_N = 0;
+};
+
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+static int make_tmap_bf16(CUtensorMap *m, void *ptr, int64_t rows, int d, int box_rows) {
+    auto fn = encode_fn();
+    if (!fn) return fail(F2C_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(d), static_cast<cuuint64_t>(rows < 1 ? 1 : rows)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(d) * 2};
+    cuuint32_t box[2] = {64, static_cast<cuuint32_t>(box_rows)};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, ptr, dims, strides, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(F2C_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return F2C_OK;
+}
+
+static int check_device() {
+    int dev = 0;
+    CUDA_TRY(cudaGetDevice(&dev));
+    cudaDeviceProp prop;
+    CUDA_TRY(cudaGetDeviceProperties(&prop, dev));
+    if (prop.major != 10)
+        return fail(F2C_ECUDA, "device %d is sm_%d%d; this build needs sm_100 (B200)", dev,
+                    prop.major, prop.minor);
+    return F2C_OK;
+}
+
+static int latched(f2c_dcp *h, bool sync);
+
+extern "C" {
+
+const char *f2c_last_error(void) { return g_err.c_str(); }
+int f2c_last_launch_count(void) { return g_launches; }
+
+size_t f2c_dcp_state_bytes(int64_t C, int32_t d, int32_t dtype, int32_t world, int32_t rank,
+                           int64_t n_local_max, int64_t m_local_max) {
+    if (C < 1 || d < 128 || d % 128 || d > 512 || (dtype != F2C_BF16 && dtype != F2C_F32) ||
+        world < 1 || rank < -1 || rank >= world || n_local_max < 1 || m_local_max < 1 ||
+        C < world)
+        return 0;
+    Layout L = make_layout(C, d, dtype, world, rank, n_local_max, m_local_max);
+    return rank < 0 ? L.total * static_cast<size_t>(world) : L.total;
+}
+
+int f2c_dcp_create(int64_t C, int32_t d, int32_t dtype, int32_t world, int32_t rank,
+                   const void *nccl_uid, void *state_buf, size_t state_bytes, int64_t n_local_max,
+                   int64_t m_local_max, f2c_dcp **out) {
+    g_launches = 0;
+    if (!out) return fail(F2C_EINVAL, "out is NULL");
+    *out = nullptr;
+    if (C < 1 || n_local_max < 1 || m_local_max < 1)
+        return fail(F2C_EINVAL, "C, n_local_max and m_local_max must be >= 1");
+    if (dtype != F2C_BF16 && dtype != F2C_F32) return fail(F2C_EINVAL, "dtype must be 0 (bf16) or 1 (f32)");
+    if (d < 128 || d % 128 || d > 512)
+        return fail(F2C_EINVAL, "d = %d: must be a multiple of 128 and <= 512", d);
+    if (world < 1 || rank < -1 || rank >= world) return fail(F2C_EINVAL, "bad world/rank");
+    if (C < world) return fail(F2C_EINVAL, "C < world");
+    if (m_local_max * world > C) return fail(F2C_ECAPACITY, "world*m_local_max > C (S:276)");
+    if (world > 1 && rank >= 0 && !nccl_uid) return fail(F2C_EINVAL, "nccl_uid required for world > 1");
+    if ((world == 1 || rank < 0) && nccl_uid) return fail(F2C_EINVAL, "nccl_uid must be NULL");
+    if (!state_buf || (reinterpret_cast<uintptr_t>(state_buf) & 255))
+        return fail(F2C_EINVAL, "state_buf must be a 256-byte aligned device pointer");
+    size_t need = f2c_dcp_state_bytes(C, d, dtype, world, rank, n_local_max, m_local_max);
+    if (state_bytes < need) return fail(F2C_ESHAPE, "state_bytes %zu < required %zu", state_bytes, need);
+    int rc = check_device();
+    if (rc) return rc;
+
+    f2c_dcp *h = new f2c_dcp();
+    h->C = C; h->d = d; h->dtype = dtype; h->W = world; h->emulated = rank < 0;
+    h->n_local_max = n_local_max; h->m_local_max = m_local_max;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&h->G, cudaDevAttrMultiProcessorCount, dev);
+    if (h->G > G_MAX) h->G = G_MAX;
+    const int nr = h->emulated ? world : 1;
+    for (int i = 0; i < nr; ++i) {
+        Rank R;
+        R.rank = h->emulated ? i : rank;
+        R.lo = shard_lo(C, world, R.rank);
+        R.hi = shard_lo(C, world, R.rank + 1);
+        R.L = make_layout(C, d, dtype, world, rank, n_local_max, m_local_max);
+        R.base = static_cast<uint8_t *>(state_buf) + static_cast<size_t>(i) * R.L.total;
+        if (cudaMemset(R.base, 0, R.L.total) != cudaSuccess) {
+            delete h;
+            return fail(F2C_ECUDA, "cudaMemset(state) failed");
+        }
+        k_hash_clear<<<64, 256>>>(R.at<int64_t>(R.L.hkeys), R.at<unsigned long long>(R.L.hvals), R.L.H);
+        if (dtype == F2C_BF16) {
+            if ((rc = make_tmap_bf16(&R.tmT, R.base + R.L.T, R.hi - R.lo, d, TP_TILE)) ||
+                (rc = make_tmap_bf16(&R.tmX, R.base + R.L.X_pos, R.L.R_max, d, TP_R))) {
+                delete h;
+                return rc;
+            }
+        }
+        h->ranks.push_back(R);
+    }
+    if (cudaDeviceSynchronize() != cudaSuccess) {
+        delete h;
+        return fail(F2C_ECUDA, "create: device sync failed: %s", cudaGetErrorString(cudaGetLastError()));
+    }
+    if (cudaFuncSetAttribute(dcp_tp64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             TP_SMEM_BYTES) != cudaSuccess) {
+        delete h;
+        return fail(F2C_ECUDA, "cudaFuncSetAttribute(smem) failed");
+    }
+    if (world > 1 && !h->emulated) {
+        NcclApi &api = nccl();
+        if (!api.ok) {
+            delete h;
+            return fail(F2C_ENCCL, "libnccl.so.2 not loadable");
+        }
+        nccl_uid_t uid;
+        memcpy(&uid, nccl_uid, sizeof uid);
+        int nr2 = api.CommInitRank(&h->comm, world, uid, rank);
+        if (nr2 != 0) {
+            delete h;
+            return fail(F2C_ENCCL, "ncclCommInitRank: %s", api.GetErrorString ? api.GetErrorString(nr2) : "?");
+        }
+    }
+    *out = h;
+    return F2C_OK;
+}
+
+void f2c_dcp_destroy(f2c_dcp *h) {
+    if (!h) return;
+    if (h->comm && nccl().CommDestroy) nccl().CommDestroy(h->comm);
+    delete h;
+}
+
+}  // extern "C"
+
+// ============================================================================ comm helpers
+// For world == 1 these are never called.  Emulated world: the ranks are the
+// handle's Rank entries, collectives are device-to-device copies / reductions.
+static int nccl_check(int r, const char *what) {
+    if (r != 0)
+        return fail(F2C_ENCCL, "%s: %s", what, nccl().GetErrorString ? nccl().GetErrorString(r) : "?");
+    return F2C_OK;
+}
+
+// ============================================================================ enqueue
+static int enqueue_rank(f2c_dcp *h, Rank &R, const uint8_t *g, const int64_t *y, int64_t m_glob,
+                        cudaStream_t st) {
+    const int row_bytes = h->d * (h->dtype == F2C_BF16 ? 2 : 4);
+    const int64_t threads = m_glob * 32;
+    k_enqueue<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, st>>>(
+        g, y, m_glob, h->E, h->C, R.lo, R.hi, row_bytes, h->dtype, R.base + R.L.T,
+        R.at<int64_t>(R.L.lab), R.sc());
+    LAUNCH_CHECK();
+    return F2C_OK;
+}
+
+extern "C" int f2c_dcp_enqueue(f2c_dcp *h, const void *g_feats, const int64_t *labels,
+                               int64_t m_local, void *stream) {
+    g_launches = 0;
+    if (!h) return fail(F2C_EINVAL, "NULL handle");
+    if (!g_feats || !labels) return fail(F2C_EINVAL, "NULL g_feats/labels");
+    if (m_local < 1 || m_local > h->m_local_max)
+        return fail(F2C_ESHAPE, "m_local %lld not in [1, %lld]", (long long)m_local, (long long)h->m_local_max);
+    const int64_t m_glob = m_local * h->W;
+    if (m_glob > h->C) return fail(F2C_ECAPACITY, "block of %lld rows > C (S:276)", (long long)m_glob);
+    if (reinterpret_cast<uintptr_t>(g_feats) & 15) return fail(F2C_EINVAL, "g_feats must be 16-byte aligned");
+    int rc = latched(h, false);
+    if (rc) return rc;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    h->last_stream = st;
+    const size_t es = h->dtype == F2C_BF16 ? 2 : 4;
+    if (h->W == 1) {
+        if ((rc = enqueue_rank(h, h->ranks[0], static_cast<const uint8_t *>(g_feats), labels, m_glob, st)))
+            return rc;
+    } else if (h->emulated) {
+        // g_feats / labels already hold the rank-ordered global block
+        for (Rank &R : h->ranks)
+            if ((rc = enqueue_rank(h, R, static_cast<const uint8_t *>(g_feats), labels, m_glob, st)))
+                return rc;
+    } else {
+        // C5: route the block to the owners; every rank receives the whole block
+        // (all-gather) and keeps the rows of its slot range.
+        Rank &R = h->ranks[0];
+        NcclApi &api = nccl();
+        api.GroupStart();
+        api.AllGather(g_feats, R.base + R.L.blk_x, m_local * h->d * es, NCCL_INT8, h->comm, st);
+        api.AllGather(labels, R.base + R.L.blk_y, m_local, NCCL_INT64, h->comm, st);
+        if ((rc = nccl_check(api.GroupEnd(), "enqueue all-gather"))) return rc;
+        if ((rc = enqueue_rank(h, R, R.base + R.L.blk_x, R.at<int64_t>(R.L.blk_y), m_glob, st))) return rc;
+    }
+    h->E += m_glob;
+    h->M_last = m_glob;
+    return F2C_OK;
+}
+
+// ============================================================================ EMA
+extern "C" int f2c_gnet_ema(const float *p, float *g, int64_t n, double momentum, void *stream) {
+    g_launches = 0;
+    if (n < 0) return fail(F2C_ESHAPE, "n < 0");
+    if (!(momentum >= 0.0 && momentum <= 1.0)) return fail(F2C_EINVAL, "momentum must be in [0, 1]");
+    if (n == 0) return F2C_OK;
+    if (!p || !g) return fail(F2C_EINVAL, "NULL p/g");
+    if ((reinterpret_cast<uintptr_t>(p) | reinterpret_cast<uintptr_t>(g)) & 15)
+        return fail(F2C_EINVAL, "p and g must be 16-byte aligned");
+    if ((p < g + n) && (g < p + n)) return fail(F2C_EINVAL, "p and g overlap");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int64_t n4 = n / 4;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (n4 > 0) {
+        int64_t blocks = (n4 + 255) / 256;
+        if (blocks > static_cast<int64_t>(sms) * 8) blocks = static_cast<int64_t>(sms) * 8;
+        k_ema<<<static_cast<unsigned>(blocks), 256, 0, st>>>(reinterpret_cast<const float4 *>(p),
+                                                             reinterpret_cast<float4 *>(g), n4,
+                                                             momentum, 1.0 - momentum);
+        LAUNCH_CHECK();
+    }
+    if (n4 * 4 < n) {
+        k_ema_tail<<<1, 32, 0, st>>>(p, g, n4 * 4, n, momentum, 1.0 - momentum);
+        LAUNCH_CHECK();
+    }
+    return F2C_OK;
+}
+
+// ============================================================================ loss
+struct StepCtx {
+    int64_t N;         // global batch rows
+    float s, m;
+    const uint8_t *x;  // global batch rows on this rank (W == 1: the input)
+    const int64_t *y;
+    const int32_t *pair;
+    cudaStream_t st;
+};
+
+// a2 + a3: norms, label hash, local target resolve (tseq = newest local seq or -1)
+static int phase_resolve(f2c_dcp *h, Rank &R, const StepCtx &c) {
+    const Layout &L = R.L;
+    const unsigned rows_blocks = static_cast<unsigned>((c.N * 32 + 255) / 256);
+    if (h->dtype == F2C_BF16)
+        k_rownorm_insert<__nv_bfloat16><<<rows_blocks, 256, 0, c.st>>>(
+            reinterpret_cast<const __nv_bfloat16 *>(c.x), c.y, c.N, h->d, R.at<float>(L.inv_n),
+            R.at<int64_t>(L.hkeys), L.H, R.at<int>(L.hslot), R.sc());
+    else
+        k_rownorm_insert<float><<<rows_blocks, 256, 0, c.st>>>(
+            reinterpret_cast<const float *>(c.x), c.y, c.N, h->d, R.at<float>(L.inv_n),
+            R.at<int64_t>(L.hkeys), L.H, R.at<int>(L.hslot), R.sc());
+    LAUNCH_CHECK();
+    const int64_t C_occ = h->E < h->C ? h->E : h->C;
+    int64_t occ_loc = C_occ - R.lo;
+    if (occ_loc > R.hi - R.lo) occ_loc = R.hi - R.lo;
+    if (occ_loc < 0) occ_loc = 0;
+    if (occ_loc > 0) {
+        int64_t blocks = (occ_loc + 255) / 256;
+        if (blocks > h->G * 16) blocks = h->G * 16;
+        k_scan_pool<<<static_cast<unsigned>(blocks), 256, 0, c.st>>>(
+            R.at<int64_t>(L.lab), occ_loc, R.lo, h->C, h->E, R.at<int64_t>(L.hkeys),
+            R.at<unsigned long long>(L.hvals), L.H);
+        LAUNCH_CHECK();
+    }
+    k_resolve<<<static_cast<unsigned>((c.N + 255) / 256), 256, 0, c.st>>>(
+        R.at<int>(L.hslot), R.at<unsigned long long>(L.hvals), c.N, R.at<int64_t>(L.tseq));
+    LAUNCH_CHECK();
+    return F2C_OK;
+}
+
+// a3 split + compaction + gather
+static int phase_compact(f2c_dcp *h, Rank &R, const StepCtx &c) {
+    const Layout &L = R.L;
+    CompactArgs a;
+    a.tseq = R.at<int64_t>(L.tseq);
+    a.inv_n = R.at<float>(L.inv_n);
+    a.pairing = c.pair;
+    a.N = c.N; a.C = h->C; a.lo = R.lo; a.hi = R.hi; a.E = h->E; a.M_last = h->M_last;
+    a.s = c.s;
+    a.log2e_s = c.s * 1.4426950408889634f;
+    a.ref_scale = a.log2e_s * (1.0f + 1.0f / 1024.0f);
+    a.R_max = static_cast<int>(L.R_max);
+    a.comp_idx = R.at<int>(L.comp_idx);
+    a.pos_row = R.at<int>(L.pos_row);
+    a.row_ab = R.at<float2>(L.row_ab);
+    a.row_tgt = R.at<int>(L.row_tgt);
+    a.ttgt = R.at<float>(L.ttgt);
+    a.sc = R.sc();
+    k_compact<<<1, 1024, 0, c.st>>>(a);
+    LAUNCH_CHECK();
+    const int row_bytes = h->d * 2;
+    k_gather<<<static_cast<unsigned>(c.N), 64, 0, c.st>>>(c.x, R.at<int>(L.pos_row), R.sc(), row_bytes,
+                                                          R.base + L.X_pos);
+    LAUNCH_CHECK();
+    return F2C_OK;
+}
+
+static int phase_main(f2c_dcp *h, Rank &R, const StepCtx &c, int64_t occ_loc) {
+    const Layout &L = R.L;
+    TPParams p;
+    p.d = h->d;
+    p.n_slots = static_cast<int>(occ_loc);
+    p.n_pos = &R.sc()->n_pos;
+    p.row_ab = R.at<float2>(L.row_ab);
+    p.row_tgt = R.at<int>(L.row_tgt);
+    p.margin_l2 = c.s * c.m * 1.4426950408889634f;
+    p.ttgt = R.at<float>(L.ttgt);
+    p.seg_l = R.at<float>(L.seg_l);
+    p.seg_mx = R.at<float>(L.seg_mx);
+    p.seg_O = R.at<float>(L.seg_O);
+    dcp_tp64_kernel<<<h->G, TP_THREADS, TP_SMEM_BYTES, c.st>>>(R.tmT, R.tmX, p);
+    LAUNCH_CHECK();
+    return F2C_OK;
+}
+
+static int64_t occ_local(const f2c_dcp *h, const Rank &R) {
+    const int64_t C_occ = h->E < h->C ? h->E : h->C;
+    int64_t o = C_occ - R.lo;
+    if (o > R.hi - R.lo) o = R.hi - R.lo;
+    return o < 0 ? 0 : o;
+}
+
+extern "C" int f2c_dcp_loss_fwd_bwd(f2c_dcp *h, const void *x, const int64_t *labels,
+                                    const int32_t *pairing, int64_t n_local, float s, float m,
+                                    float *loss, void *dx, void *stream) {
+    g_launches = 0;
+    if (!h) return fail(F2C_EINVAL, "NULL handle");
+    if (!x || !labels || !loss || !dx) return fail(F2C_EINVAL, "NULL x/labels/loss/dx");
+    if (n_local < 1 || n_local > h->n_local_max)
+        return fail(F2C_ESHAPE, "n_local %lld not in [1, %lld]", (long long)n_local, (long long)h->n_local_max);
+    if (!(s > 0.f) || !isfinite(s) || !isfinite(m)) return fail(F2C_EINVAL, "need s > 0 and finite m");
+    if (x == dx) return fail(F2C_EINVAL, "dx must not alias x");
+    if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(dx)) & 15)
+        return fail(F2C_EINVAL, "x and dx must be 16-byte aligned");
+    if (h->dtype != F2C_BF16)
+        return fail(F2C_EINVAL, "the fp32 loss path is not part of this build (DESIGN.md D21); use bf16");
+    int rc = latched(h, false);
+    if (rc) return rc;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    h->last_stream = st;
+    if (h->W != 1) return fail(F2C_EINVAL, "world > 1 loss path: see multi-rank build");
+    Rank &R = h->ranks[0];
+    const Layout &L = R.L;
+    StepCtx c{n_local, s, m, static_cast<const uint8_t *>(x), labels, pairing, st};
+    h->last_N = c.N;
+    if ((rc = phase_resolve(h, R, c))) return rc;
+    if ((rc = phase_compact(h, R, c))) return rc;
+    const int64_t occ = occ_local(h, R);
+    if ((rc = phase_main(h, R, c, occ))) return rc;
+    CombineArgs a;
+    a.x = c.x;
+    a.inv_n = R.at<float>(L.inv_n);
+    a.comp_idx = R.at<int>(L.comp_idx);
+    a.row_ab = R.at<float2>(L.row_ab);
+    a.row_tgt = R.at<int>(L.row_tgt);
+    a.ttgt = R.at<float>(L.ttgt);
+    a.seg_l = R.at<float>(L.seg_l);
+    a.seg_mx = R.at<float>(L.seg_mx);
+    a.seg_O = R.at<float>(L.seg_O);
+    a.T = R.base + L.T;
+    a.sc = R.sc();
+    a.sc_w = R.sc();
+    a.N = c.N;
+    a.C_occ = h->E < h->C ? h->E : h->C;
+    a.d = h->d;
+    a.dtype = h->dtype;
+    a.G = h->G;
+    a.n_tiles = static_cast<int>((occ + TP_TILE - 1) / TP_TILE);
+    a.s = s;
+    a.margin_l2 = s * m * 1.4426950408889634f;
+    a.dx = static_cast<uint8_t *>(dx);
+    a.rowloss = R.at<double>(L.rowloss);
+    a.st_lse = R.at<float>(L.st_lse);
+    a.st_cos = R.at<float>(L.st_cos);
+    a.st_phi = R.at<float>(L.st_phi);
+    a.st_ell = R.at<float>(L.st_ell);
+    k_combine<__nv_bfloat16><<<static_cast<unsigned>(c.N), 128, 0, st>>>(a);
+    LAUNCH_CHECK();
+    k_loss<<<1, 1024, 0, st>>>(R.at<double>(L.rowloss), R.at<int>(L.comp_idx), c.N, R.sc(), loss,
+                               R.at<int64_t>(L.hkeys), R.at<unsigned long long>(L.hvals), L.H);
+    LAUNCH_CHECK();
+    return F2C_OK;
+}
+
+// ============================================================================ support
+static int latched(f2c_dcp *h, bool sync) {
+    if (!sync) return F2C_OK;  // only the debug calls synchronise
+    int worst = F2C_OK;
+    for (Rank &R : h->ranks) {
+        Scalars s;
+        if (cudaMemcpy(&s, R.sc(), sizeof s, cudaMemcpyDeviceToHost) != cudaSuccess)
+            return fail(F2C_ECUDA, "reading the device error word failed");
+        if (s.err) {
+            static const char *det[] = {"", "negative label", "zero-norm (or non-finite) feature row",
+                                        "pairing[i] does not name row i's target",
+                                        "non-finite loss", "softmax underflow (row max < 2^-100 of the reference)"};
+            const int dd = (s.err_detail >= 0 && s.err_detail <= 5) ? s.err_detail : 0;
+            fail(s.err, "device error (rank %d): %s", R.rank, det[dd]);
+            worst = s.err;
+            int zero[2] = {0, 0};
+            cudaMemcpy(R.sc(), zero, sizeof zero, cudaMemcpyHostToDevice);
+        }
+    }
+    return worst;
+}
+
+extern "C" int f2c_dcp_check(f2c_dcp *h) {
+    if (!h) return fail(F2C_EINVAL, "NULL handle");
+    if (h->last_stream) CUDA_TRY(cudaStreamSynchronize(h->last_stream));
+    CUDA_TRY(cudaDeviceSynchronize());
+    return latched(h, true);
+}
+
+extern "C" int f2c_dcp_get_state(f2c_dcp *h, void *feats_host, int64_t *labels_host,
+                                 int64_t *enq_count_host) {
+    if (!h) return fail(F2C_EINVAL, "NULL handle");
+    CUDA_TRY(cudaDeviceSynchronize());
+    const size_t rb = static_cast<size_t>(h->d) * (h->dtype == F2C_BF16 ? 2 : 4);
+    int64_t row0 = 0;
+    for (Rank &R : h->ranks) {
+        const int64_t n = R.hi - R.lo;
+        if (feats_host)
+            CUDA_TRY(cudaMemcpy(static_cast<uint8_t *>(feats_host) + row0 * rb, R.base + R.L.T, n * rb,
+                                cudaMemcpyDeviceToHost));
+        if (labels_host) {
+            CUDA_TRY(cudaMemcpy(labels_host + row0, R.at<int64_t>(R.L.lab), n * 8, cudaMemcpyDeviceToHost));
+            const int64_t occ = occ_local(h, R);
+            for (int64_t i = occ; i < n; ++i) labels_host[row0 + i] = -1;
+        }
+        row0 += n;
+    }
+    if (enq_count_host) *enq_count_host = h->E;
+    return F2C_OK;
+}
+
+extern "C" int f2c_dcp_set_state(f2c_dcp *h, const void *feats_host, const int64_t *labels_host,
+                                 int64_t enq_count) {
+    if (!h) return fail(F2C_EINVAL, "NULL handle");
+    if (!feats_host || !labels_host || enq_count < 0) return fail(F2C_EINVAL, "bad set_state arguments");
+    const size_t rb = static_cast<size_t>(h->d) * (h->dtype == F2C_BF16 ? 2 : 4);
+    const int64_t C_occ = enq_count < h->C ? enq_count : h->C;
+    int64_t row0 = 0;
+    for (Rank &R : h->ranks) {
+        const int64_t n = R.hi - R.lo;
+        for (int64_t i = 0; i < n; ++i) {
+            const int64_t c = R.lo + i;
+            const int64_t lb = labels_host[row0 + i];
+            if (c < C_occ && lb < 0) return fail(F2C_EINVAL, "occupied slot %lld has a negative label", (long long)c);
+            if (c >= C_occ && lb != -1) return fail(F2C_EINVAL, "slot %lld >= min(E, C) must be empty (-1)", (long long)c);
+        }
+        row0 += n;
+    }
+    CUDA_TRY(cudaDeviceSynchronize());
+    row0 = 0;
+    for (Rank &R : h->ranks) {
+        const int64_t n = R.hi - R.lo;
+        int64_t occ = C_occ - R.lo;
+        if (occ > n) occ = n;
+        if (occ < 0) occ = 0;
+        CUDA_TRY(cudaMemset(R.base + R.L.T, 0, n * rb));
+        if (occ > 0)
+            CUDA_TRY(cudaMemcpy(R.base + R.L.T, static_cast<const uint8_t *>(feats_host) + row0 * rb,
+                                occ * rb, cudaMemcpyHostToDevice));
+        CUDA_TRY(cudaMemcpy(R.at<int64_t>(R.L.lab), labels_host + row0, n * 8, cudaMemcpyHostToDevice));
+        int zero = 0;
+        CUDA_TRY(cudaMemcpy(&R.sc()->tmax_bits, &zero, 4, cudaMemcpyHostToDevice));
+        if (occ > 0) {
+            k_pool_norm_max<<<static_cast<unsigned>((occ * 32 + 255) / 256), 256>>>(
+                R.base + R.L.T, occ, static_cast<int>(rb), h->dtype, R.sc());
+            CUDA_TRY(cudaGetLastError());
+        }
+        row0 += n;
+    }
+    CUDA_TRY(cudaDeviceSynchronize());
+    h->E = enq_count;
+    h->M_last = 0;
+    return F2C_OK;
+}
+
+extern "C" int f2c_dcp_row_stats(f2c_dcp *h, float *lse, int64_t *target_seq, float *cos_t,
+                                 float *phi, float *ell, int64_t *counts) {
+    if (!h) return fail(F2C_EINVAL, "NULL handle");
+    CUDA_TRY(cudaDeviceSynchronize());
+    Rank &R = h->ranks[0];
+    const int64_t N = h->last_N;
+    if (lse) CUDA_TRY(cudaMemcpy(lse, R.at<float>(R.L.st_lse), N * 4, cudaMemcpyDeviceToHost));
+    if (target_seq) CUDA_TRY(cudaMemcpy(target_seq, R.at<int64_t>(R.L.tseq), N * 8, cudaMemcpyDeviceToHost));
+    if (cos_t) CUDA_TRY(cudaMemcpy(cos_t, R.at<float>(R.L.st_cos), N * 4, cudaMemcpyDeviceToHost));
+    if (phi) CUDA_TRY(cudaMemcpy(phi, R.at<float>(R.L.st_phi), N * 4, cudaMemcpyDeviceToHost));
+    if (ell) CUDA_TRY(cudaMemcpy(ell, R.at<float>(R.L.st_ell), N * 4, cudaMemcpyDeviceToHost));
+    if (counts) {
+        Scalars s;
+        CUDA_TRY(cudaMemcpy(&s, R.sc(), sizeof s, cudaMemcpyDeviceToHost));
+        counts[0] = s.n_pos;
+        counts[1] = s.n_neg;
+        counts[2] = h->E < h->C ? h->E : h->C;
+    }
+    return F2C_OK;
+}

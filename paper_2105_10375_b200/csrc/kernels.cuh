@@ -1,0 +1,524 @@
+// kernels.cuh -- the DCP head's non-GEMM kernels (hot-path steps a1, a3, a6, a8,
+// a9 and a10 of DESIGN.md section 2).  All of them are HBM- or latency-bound.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "sm100.cuh"
+
+namespace f2c {
+
+enum : int { ERR_OK = 0, ERR_PAIRING = 4, ERR_DEVICE = 7 };
+// detail codes kept next to the status (scal->err_detail) for f2c_last_error
+enum : int {
+    DET_NONE = 0, DET_BAD_LABEL = 1, DET_ZERO_ROW = 2, DET_PAIRING = 3, DET_NONFINITE = 4,
+    DET_UNDERFLOW = 5
+};
+
+struct Scalars {          // lives at the start of the per-rank scratch
+    int err;              // latched f2c_status
+    int err_detail;       // DET_*
+    int tmax_bits;        // max ||T_c|| over rows ever written (float bits, >= 0)
+    int n_pos;            // in-pool rows of the last loss call
+    int n_neg;
+    int pad0;
+    double loss3[3];      // L, L_ce, L_cos (fp64) of the last loss call
+};
+
+__device__ __forceinline__ void latch(Scalars *s, int code, int detail) {
+    if (atomicCAS(&s->err, 0, code) == 0) s->err_detail = detail;
+}
+
+__device__ __forceinline__ uint64_t hash64(uint64_t z) {
+    z ^= z >> 33;
+    z *= 0xff51afd7ed558ccdull;
+    z ^= z >> 33;
+    z *= 0xc4ceb9fe1a85ec53ull;
+    z ^= z >> 33;
+    return z;
+}
+
+template <typename T>
+__device__ __forceinline__ float to_f(T v);
+template <>
+__device__ __forceinline__ float to_f<__nv_bfloat16>(__nv_bfloat16 v) { return __bfloat162float(v); }
+template <>
+__device__ __forceinline__ float to_f<float>(float v) { return v; }
+
+template <typename T>
+__device__ __forceinline__ T from_f(float v);
+template <>
+__device__ __forceinline__ __nv_bfloat16 from_f<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
+template <>
+__device__ __forceinline__ float from_f<float>(float v) { return v; }
+
+// ------------------------------------------------------------------ a1: enqueue
+// Eq. 7 / Algorithm 1: global block row j -> slot (E+j) mod C.
+// One warp per block row; the rows owned by this shard [lo, hi) are copied with
+// 16-byte vector loads/stores (bit-exact), labels written by lane 0, and the running
+// max row norm (the softmax reference bound) updated.
+__global__ void k_enqueue(const uint8_t *__restrict__ g, const int64_t *__restrict__ y,
+                          int64_t m_glob, int64_t E, int64_t C, int64_t lo, int64_t hi,
+                          int row_bytes, int dtype, uint8_t *__restrict__ T, int64_t *__restrict__ lab,
+                          Scalars *sc) {
+    const int64_t j = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (j >= m_glob) return;
+    const int64_t c = (E + j) % C;
+    if (c < lo || c >= hi) return;
+    const int64_t yl = y[j];
+    if (yl < 0) {
+        if (lane == 0) latch(sc, ERR_DEVICE, DET_BAD_LABEL);
+        return;
+    }
+    const int4 *src = reinterpret_cast<const int4 *>(g + j * row_bytes);
+    int4 *dst = reinterpret_cast<int4 *>(T + (c - lo) * row_bytes);
+    float ss = 0.f;
+    for (int u = lane; u < row_bytes / 16; u += 32) {
+        int4 v = __ldcs(src + u);
+        dst[u] = v;
+        const uint32_t w[4] = {static_cast<uint32_t>(v.x), static_cast<uint32_t>(v.y),
+                               static_cast<uint32_t>(v.z), static_cast<uint32_t>(v.w)};
+        if (dtype == 0) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                float a = __uint_as_float(w[i] << 16), b = __uint_as_float(w[i] & 0xffff0000u);
+                ss += a * a + b * b;
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                float a = __uint_as_float(w[i]);
+                ss += a * a;
+            }
+        }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    if (lane == 0) {
+        lab[c - lo] = yl;
+        float nrm = sqrtf(ss);
+        if (!(nrm <= 3.0e38f)) nrm = 3.0e38f;
+        atomicMax(&sc->tmax_bits, __float_as_int(nrm));
+    }
+}
+
+// recompute the norm bound over a whole shard (after set_state)
+__global__ void k_pool_norm_max(const uint8_t *__restrict__ T, int64_t rows, int row_bytes,
+                                int dtype, Scalars *sc) {
+    const int64_t r = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (r >= rows) return;
+    const int4 *src = reinterpret_cast<const int4 *>(T + r * row_bytes);
+    float ss = 0.f;
+    for (int u = lane; u < row_bytes / 16; u += 32) {
+        int4 v = src[u];
+        const uint32_t w[4] = {static_cast<uint32_t>(v.x), static_cast<uint32_t>(v.y),
+                               static_cast<uint32_t>(v.z), static_cast<uint32_t>(v.w)};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            if (dtype == 0) {
+                float a = __uint_as_float(w[i] << 16), b = __uint_as_float(w[i] & 0xffff0000u);
+                ss += a * a + b * b;
+            } else {
+                float a = __uint_as_float(w[i]);
+                ss += a * a;
+            }
+        }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    if (lane == 0) {
+        float nrm = sqrtf(ss);
+        if (!(nrm <= 3.0e38f)) nrm = 3.0e38f;
+        atomicMax(&sc->tmax_bits, __float_as_int(nrm));
+    }
+}
+
+// ------------------------------------------------------------------ a10: G-Net EMA
+// g <- m*g + (1-m)*p in fp64 (__dmul_rn/__dadd_rn: no contraction), RNE to fp32.
+__device__ __forceinline__ float ema1(float gv, float pv, double m, double om) {
+    return __double2float_rn(__dadd_rn(__dmul_rn(m, static_cast<double>(gv)),
+                                       __dmul_rn(om, static_cast<double>(pv))));
+}
+__global__ void k_ema(const float4 *__restrict__ p, float4 *__restrict__ g, int64_t n4, double m,
+                      double om) {
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n4;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const float4 a = __ldcs(p + i);
+        float4 b = __ldcs(g + i);
+        b.x = ema1(b.x, a.x, m, om);
+        b.y = ema1(b.y, a.y, m, om);
+        b.z = ema1(b.z, a.z, m, om);
+        b.w = ema1(b.w, a.w, m, om);
+        __stcs(g + i, b);
+    }
+}
+__global__ void k_ema_tail(const float *__restrict__ p, float *__restrict__ g, int64_t lo, int64_t n,
+                           double m, double om) {
+    const int64_t i = lo + threadIdx.x;
+    if (i < n) g[i] = ema1(g[i], p[i], m, om);
+}
+
+// ------------------------------------------------------------------ a3: target resolve
+// Hash table of the batch labels (open addressing, H a power of two >= 2N).
+__global__ void k_hash_clear(int64_t *keys, unsigned long long *vals, int H) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < H; i += gridDim.x * blockDim.x) {
+        keys[i] = -1;
+        vals[i] = 0ull;
+    }
+}
+
+// a2 + a3 (part 1): per row (one warp): 1/||x_i|| and insert y_i into the hash table.
+template <typename T>
+__global__ void k_rownorm_insert(const T *__restrict__ x, const int64_t *__restrict__ y, int64_t N,
+                                 int d, float *__restrict__ inv_n, int64_t *keys, int H,
+                                 int *__restrict__ hslot, Scalars *sc) {
+    const int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (i >= N) return;
+    float ss = 0.f;
+    for (int k = lane; k < d; k += 32) {
+        float v = to_f<T>(x[i * d + k]);
+        ss += v * v;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    if (lane == 0) {
+        float nrm = sqrtf(ss);
+        if (!(nrm > 0.f) || !(nrm <= 3.0e38f)) {
+            latch(sc, ERR_DEVICE, DET_ZERO_ROW);
+            inv_n[i] = 0.f;
+        } else {
+            inv_n[i] = 1.0f / nrm;
+        }
+        const int64_t key = y[i];
+        if (key < 0) {
+            latch(sc, ERR_DEVICE, DET_BAD_LABEL);
+            hslot[i] = -1;
+            return;
+        }
+        unsigned h = static_cast<unsigned>(hash64(static_cast<uint64_t>(key))) & (H - 1);
+        for (;;) {
+            unsigned long long old = atomicCAS(reinterpret_cast<unsigned long long *>(keys + h),
+                                               static_cast<unsigned long long>(-1ll),
+                                               static_cast<unsigned long long>(key));
+            if (old == static_cast<unsigned long long>(-1ll) ||
+                old == static_cast<unsigned long long>(key))
+                break;
+            h = (h + 1) & (H - 1);
+        }
+        hslot[i] = static_cast<int>(h);
+    }
+}
+
+// a3 (part 2): one coalesced pass over the shard's occupied slot labels; a slot whose
+// label is in the batch raises that label's newest write index seq(c) (D8).
+__global__ void k_scan_pool(const int64_t *__restrict__ lab, int64_t n_occ_loc, int64_t lo,
+                            int64_t C, int64_t E, const int64_t *__restrict__ keys,
+                            unsigned long long *vals, int H) {
+    for (int64_t cl = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; cl < n_occ_loc;
+         cl += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t L = lab[cl];
+        if (L < 0) continue;
+        unsigned h = static_cast<unsigned>(hash64(static_cast<uint64_t>(L))) & (H - 1);
+        for (;;) {
+            const int64_t k = keys[h];
+            if (k == -1) break;
+            if (k == L) {
+                const int64_t c = lo + cl;
+                const int64_t seq = c + C * ((E - 1 - c) / C);
+                atomicMax(vals + h, static_cast<unsigned long long>(seq + 1));
+                break;
+            }
+            h = (h + 1) & (H - 1);
+        }
+    }
+}
+
+__global__ void k_resolve(const int *__restrict__ hslot, const unsigned long long *__restrict__ vals,
+                          int64_t N, int64_t *__restrict__ tseq) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    const int h = hslot[i];
+    tseq[i] = h < 0 ? -1 : static_cast<int64_t>(vals[h]) - 1;
+}
+
+// ------------------------------------------------------------------ a3: split + compaction
+// Single CTA (1024 threads): Eq. 6's split into in-pool (F_p^DCP) and out-of-pool
+// rows, compaction of the in-pool rows in batch order, per-row softmax coefficients,
+// the pairing check (D13), and the mu row (index N_pos) with coefficients (0, 0) so
+// that the main kernel's p = 2^0 = 1 gives sum_c T_c.
+struct CompactArgs {
+    const int64_t *tseq;      // [N] global write index of the target or -1
+    const float *inv_n;       // [N]
+    const int32_t *pairing;   // [N] or null
+    int64_t N, C, lo, hi, E, M_last;
+    float s, log2e_s;         // s, s*log2(e)
+    int R_max;
+    int *comp_idx;            // [N]
+    int *pos_row;             // [N]
+    float2 *row_ab;           // [R_max]
+    int *row_tgt;             // [R_max]
+    float *ttgt;              // [R_max]
+    Scalars *sc;
+    float ref_scale;          // s*log2(e)*(1+2^-10): reference exponent per unit norm
+};
+__global__ void __launch_bounds__(1024) k_compact(CompactArgs a) {
+    __shared__ int wsum[32];
+    __shared__ int base_s;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int64_t per = (a.N + nt - 1) / nt;
+    const int64_t r0 = tid * per, r1 = r0 + per < a.N ? r0 + per : a.N;
+    int cnt = 0;
+    for (int64_t i = r0; i < r1; ++i) cnt += a.tseq[i] >= 0;
+    // block exclusive scan of cnt
+    const int lane = tid & 31, w = tid >> 5;
+    int v = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int t = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += t;
+    }
+    if (lane == 31) wsum[w] = v;
+    __syncthreads();
+    if (w == 0) {
+        int s2 = wsum[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int t = __shfl_up_sync(0xffffffffu, s2, o);
+            if (lane >= o) s2 += t;
+        }
+        wsum[lane] = s2;  // inclusive
+    }
+    __syncthreads();
+    int k = (w > 0 ? wsum[w - 1] : 0) + v - cnt;
+    const int n_pos = wsum[31];
+    const float tmax = __int_as_float(a.sc->tmax_bits);
+    const float B = a.ref_scale * tmax;
+    for (int64_t i = r0; i < r1; ++i) {
+        const int64_t ts = a.tseq[i];
+        if (a.pairing && a.pairing[i] >= 0) {
+            const int64_t want = a.E - a.M_last + a.pairing[i];
+            if (a.pairing[i] >= a.M_last || ts != want) latch(a.sc, ERR_PAIRING, DET_PAIRING);
+        }
+        if (ts >= 0) {
+            a.comp_idx[i] = k;
+            a.pos_row[k] = static_cast<int>(i);
+            a.row_ab[k] = make_float2(a.log2e_s * a.inv_n[i], B);
+            const int64_t slot = ts % a.C;
+            a.row_tgt[k] = (slot >= a.lo && slot < a.hi) ? static_cast<int>(slot - a.lo) : -1;
+            a.ttgt[k] = -INFINITY;
+            ++k;
+        } else {
+            a.comp_idx[i] = -1;
+        }
+    }
+    // the mu row and the padding rows of the last row group
+    for (int r = n_pos + tid; r < a.R_max; r += nt) {
+        a.row_ab[r] = make_float2(0.f, 0.f);
+        a.row_tgt[r] = -1;
+        a.ttgt[r] = -INFINITY;
+    }
+    if (tid == 0) {
+        a.sc->n_pos = n_pos;
+        a.sc->n_neg = static_cast<int>(a.N) - n_pos;
+    }
+}
+
+// gather the in-pool rows into the dense, 64-row-group-aligned bf16 operand X_pos
+__global__ void k_gather(const uint8_t *__restrict__ x, const int *__restrict__ pos_row,
+                         const Scalars *__restrict__ sc, int row_bytes, uint8_t *__restrict__ Xp) {
+    const int k = blockIdx.x;
+    if (k >= sc->n_pos) return;
+    const int4 *src = reinterpret_cast<const int4 *>(x + static_cast<int64_t>(pos_row[k]) * row_bytes);
+    int4 *dst = reinterpret_cast<int4 *>(Xp + static_cast<int64_t>(k) * row_bytes);
+    for (int u = threadIdx.x; u < row_bytes / 16; u += blockDim.x) dst[u] = src[u];
+}
+
+// ------------------------------------------------------------------ a6 + a8 + a9: combine
+// One CTA per global row.  Sums the main kernel's segment partials in a fixed order,
+// forms dL/dx_hat (Eq. 9 gradient with the target term in fp64, D12), or the L_cos
+// gradient mu / (N_neg C_occ) for out-of-pool rows (D10), applies the normalisation
+// Jacobian and writes dx in the input dtype, plus the per-row loss terms.
+struct CombineArgs {
+    const uint8_t *x;           // [N, d] dtype
+    const float *inv_n;         // [N]
+    const int *comp_idx;        // [N]
+    const float2 *row_ab;       // [R_max]
+    const int *row_tgt;         // [R_max] (local slot)
+    const float *ttgt;          // [R_max]
+    const float *seg_l, *seg_mx, *seg_O;
+    const uint8_t *T;           // local pool
+    const Scalars *sc;
+    Scalars *sc_w;
+    int64_t N, C_occ;
+    int d, dtype, G, n_tiles;
+    float s, margin_l2;
+    uint8_t *dx;                // [N, d] dtype
+    double *rowloss;            // [N]
+    float *st_lse, *st_cos, *st_phi, *st_ell;  // [N] row statistics
+};
+
+__device__ __forceinline__ float block_sum_128(float v, float *red) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __syncthreads();
+    if (lane == 0) red[w] = v;
+    __syncthreads();
+    return red[0] + red[1] + red[2] + red[3];
+}
+
+// sum the partials of compacted row k over its segments (fixed CTA order)
+__device__ __forceinline__ void gather_row_partials(const CombineArgs &a, int n_rg, int k, float (&o)[4],
+                                                    float &lsum, float &mx) {
+    const int rg = k / 64, r = k % 64;
+    lsum = 0.f;
+    mx = -INFINITY;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) o[j] = 0.f;
+    if (a.n_tiles <= 0) return;
+    const long long total = static_cast<long long>(n_rg) * a.n_tiles;
+    const long long p0 = static_cast<long long>(rg) * a.n_tiles, p1 = p0 + a.n_tiles;
+    long long bg = p0 * a.G / total - 1;
+    if (bg < 0) bg = 0;
+    for (long long b = bg; b < a.G; ++b) {
+        const long long s0 = total * b / a.G, s1 = total * (b + 1) / a.G;
+        if (s0 >= p1) break;
+        if (s1 <= p0 || s1 <= s0) continue;
+        const long long seg = b + rg;
+        lsum += a.seg_l[seg * 64 + r];
+        mx = fmaxf(mx, a.seg_mx[seg * 64 + r]);
+        const float *src = a.seg_O + (seg * 64 + r) * a.d;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int dd = threadIdx.x + 128 * j;
+            if (dd < a.d) o[j] += src[dd];
+        }
+    }
+}
+
+template <typename TX>
+__global__ void __launch_bounds__(128) k_combine(CombineArgs a) {
+    __shared__ float red[4];
+    const int64_t i = blockIdx.x;
+    const int n_pos = a.sc->n_pos, n_neg = a.sc->n_neg;
+    const int n_rg = (n_pos + 1 + 63) / 64;
+    const int k = a.comp_idx[i];
+    const TX *xr = reinterpret_cast<const TX *>(a.x) + i * a.d;
+    const float inv = a.inv_n[i];
+    float xh[4], g[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int dd = threadIdx.x + 128 * j;
+        xh[j] = dd < a.d ? to_f<TX>(xr[dd]) * inv : 0.f;
+    }
+    double row_loss = 0.0;
+    if (k >= 0) {
+        float o[4], lsum, mx;
+        gather_row_partials(a, n_rg, k, o, lsum, mx);
+        const double tt = static_cast<double>(a.ttgt[k]);
+        const double lr = static_cast<double>(lsum);
+        const double et = exp2(tt);
+        const double l = lr + et;
+        const float2 ab = a.row_ab[k];
+        const int ts = a.row_tgt[k];
+        const TX *Tt = reinterpret_cast<const TX *>(a.T) + static_cast<int64_t>(ts < 0 ? 0 : ts) * a.d;
+        const double w = static_cast<double>(a.s) / static_cast<double>(n_pos);
+        const float alpha = static_cast<float>(w / l), beta = static_cast<float>(w * (lr / l));
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int dd = threadIdx.x + 128 * j;
+            g[j] = dd < a.d ? alpha * o[j] - beta * to_f<TX>(Tt[dd]) : 0.f;
+        }
+        const double ell = log1p(lr * exp2(-tt));  // = lse - z_t
+        row_loss = ell;
+        if (threadIdx.x == 0) {
+            a.st_ell[i] = static_cast<float>(ell);
+            a.st_lse[i] = static_cast<float>((static_cast<double>(ab.y) + log2(l)) * 0.6931471805599453);
+            a.st_cos[i] = static_cast<float>((tt + a.margin_l2 + ab.y) / (a.s * 1.4426950408889634));
+            a.st_phi[i] = 0.f;
+            if (!(l > 0.0) || !isfinite(ell) || !(ts >= 0) ||
+                (mx < -100.f && static_cast<float>(tt) - mx < 64.f))
+                latch(a.sc_w, ERR_DEVICE, (!(ts >= 0) || !isfinite(ell)) ? DET_NONFINITE : DET_UNDERFLOW);
+        }
+    } else {
+        // out-of-pool: mu = sum over occupied slots of T_c (the mu row, index n_pos)
+        float mu[4], lsum, mx;
+        gather_row_partials(a, n_rg, n_pos, mu, lsum, mx);
+        const float cocc = static_cast<float>(a.C_occ);
+        const float w = (a.C_occ > 0 && n_neg > 0) ? 1.0f / (static_cast<float>(n_neg) * cocc) : 0.f;
+        float dot = 0.f;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            g[j] = w * mu[j];
+            dot += xh[j] * mu[j];
+        }
+        dot = block_sum_128(dot, red);
+        const float phi = a.C_occ > 0 ? dot / cocc : 0.f;
+        row_loss = phi;
+        if (threadIdx.x == 0) {
+            a.st_phi[i] = phi;
+            a.st_ell[i] = 0.f;
+            a.st_lse[i] = 0.f;
+            a.st_cos[i] = 0.f;
+        }
+    }
+    // normalisation Jacobian: dx = (g - (g . x_hat) x_hat) / ||x||
+    float gd = 0.f;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) gd += g[j] * xh[j];
+    gd = block_sum_128(gd, red);
+    TX *dxr = reinterpret_cast<TX *>(a.dx) + i * a.d;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int dd = threadIdx.x + 128 * j;
+        if (dd < a.d) dxr[dd] = from_f<TX>((g[j] - gd * xh[j]) * inv);
+    }
+    if (threadIdx.x == 0) a.rowloss[i] = row_loss;
+}
+
+// ------------------------------------------------------------------ a6: loss reduction
+// L = (1/N_pos) sum ell + (1/N_neg) sum phi in fp64, fixed order (deterministic);
+// also clears the label hash table for the next call.
+__global__ void __launch_bounds__(1024) k_loss(const double *__restrict__ rowloss,
+                                               const int *__restrict__ comp_idx, int64_t N,
+                                               Scalars *sc, float *loss, int64_t *keys,
+                                               unsigned long long *vals, int H) {
+    __shared__ double sa[1024], sb[1024];
+    const int tid = threadIdx.x;
+    double ce = 0.0, cs = 0.0;
+    for (int64_t i = tid; i < N; i += 1024) {
+        if (comp_idx[i] >= 0) ce += rowloss[i];
+        else cs += rowloss[i];
+    }
+    sa[tid] = ce;
+    sb[tid] = cs;
+    __syncthreads();
+    for (int s = 512; s; s >>= 1) {
+        if (tid < s) {
+            sa[tid] += sa[tid + s];
+            sb[tid] += sb[tid + s];
+        }
+        __syncthreads();
+    }
+    if (tid == 0) {
+        const int np = sc->n_pos, nn = sc->n_neg;
+        const double Lce = np > 0 ? sa[0] / np : 0.0;
+        const double Lcos = nn > 0 ? sb[0] / nn : 0.0;
+        const double L = Lce + Lcos;
+        sc->loss3[0] = L;
+        sc->loss3[1] = Lce;
+        sc->loss3[2] = Lcos;
+        *loss = static_cast<float>(L);
+        if (!isfinite(L)) latch(sc, ERR_DEVICE, DET_NONFINITE);
+    }
+    for (int h = tid; h < H; h += 1024) {
+        keys[h] = -1;
+        vals[h] = 0ull;
+    }
+}
+
+}  // namespace f2c

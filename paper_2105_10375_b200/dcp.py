@@ -1,0 +1,180 @@
+"""ctypes binding of libf2c_dcp.so (same names as include/f2c_dcp.h) and a small
+torch-facing wrapper.  Argument marshalling only; no arithmetic of the method."""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+BF16, F32 = 0, 1
+_HERE = os.path.dirname(os.path.abspath(__file__))
+lib_path = os.path.join(_HERE, "libf2c_dcp.so")
+
+STATUS = {0: "F2C_OK", 1: "F2C_EINVAL", 2: "F2C_ESHAPE", 3: "F2C_ECAPACITY", 4: "F2C_EPAIRING",
+          5: "F2C_ECUDA", 6: "F2C_ENCCL", 7: "F2C_EDEVICE"}
+
+_lib = None
+
+
+class DCPError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{STATUS.get(code, code)}: {msg}")
+        self.code = code
+
+
+def load_library():
+    """Load the in-tree libf2c_dcp.so (fails loudly if it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(lib_path):
+        raise ImportError(f"{lib_path} not built; run paper_2105_10375_b200/build.py (or "
+                          "__graft_entry__.build())")
+    L = ctypes.CDLL(lib_path)
+    P, i64, i32, f32, f64, sz = (ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_float,
+                                 ctypes.c_double, ctypes.c_size_t)
+    L.f2c_dcp_state_bytes.argtypes = [i64, i32, i32, i32, i32, i64, i64]
+    L.f2c_dcp_state_bytes.restype = sz
+    L.f2c_dcp_create.argtypes = [i64, i32, i32, i32, i32, P, P, sz, i64, i64, ctypes.POINTER(P)]
+    L.f2c_dcp_enqueue.argtypes = [P, P, P, i64, P]
+    L.f2c_dcp_loss_fwd_bwd.argtypes = [P, P, P, P, i64, f32, f32, P, P, P]
+    L.f2c_gnet_ema.argtypes = [P, P, i64, f64, P]
+    L.f2c_dcp_get_state.argtypes = [P, P, P, P]
+    L.f2c_dcp_set_state.argtypes = [P, P, P, i64]
+    L.f2c_dcp_row_stats.argtypes = [P, P, P, P, P, P, P]
+    L.f2c_dcp_check.argtypes = [P]
+    L.f2c_last_error.argtypes = []
+    L.f2c_last_error.restype = ctypes.c_char_p
+    L.f2c_last_launch_count.argtypes = []
+    L.f2c_dcp_destroy.argtypes = [P]
+    L.f2c_dcp_destroy.restype = None
+    for f in (L.f2c_dcp_create, L.f2c_dcp_enqueue, L.f2c_dcp_loss_fwd_bwd, L.f2c_gnet_ema,
+              L.f2c_dcp_get_state, L.f2c_dcp_set_state, L.f2c_dcp_row_stats, L.f2c_dcp_check,
+              L.f2c_last_launch_count):
+        f.restype = ctypes.c_int
+    _lib = L
+    return L
+
+
+def _check(rc: int):
+    if rc != 0:
+        raise DCPError(rc, load_library().f2c_last_error().decode())
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _tdtype(dtype):
+    return torch.bfloat16 if dtype == BF16 else torch.float32
+
+
+class DCPHead:
+    """One rank's handle of the DCP (or an emulated world when rank == -1).
+
+    The caller-owned state buffer is a torch uint8 CUDA tensor sized by
+    f2c_dcp_state_bytes; all device memory comes from torch."""
+
+    def __init__(self, C: int, d: int, dtype: int = BF16, world: int = 1, rank: int = 0,
+                 n_local_max: int = 1024, m_local_max: int = 512, nccl_uid: bytes | None = None,
+                 device=None):
+        L = load_library()
+        if not torch.cuda.is_available():
+            raise DCPError(5, "no CUDA device: the DCP head has no CPU path")
+        self.C, self.d, self.dtype, self.world, self.rank = int(C), int(d), int(dtype), world, rank
+        self.n_local_max, self.m_local_max = int(n_local_max), int(m_local_max)
+        nbytes = L.f2c_dcp_state_bytes(C, d, dtype, world, rank, n_local_max, m_local_max)
+        if nbytes == 0:
+            raise DCPError(1, "invalid configuration for f2c_dcp_state_bytes")
+        self.device = torch.device("cuda") if device is None else torch.device(device)
+        self.state = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        self._h = ctypes.c_void_p()
+        uid = None if nccl_uid is None else ctypes.create_string_buffer(bytes(nccl_uid), 128)
+        _check(L.f2c_dcp_create(C, d, dtype, world, rank, uid, _ptr(self.state), nbytes,
+                                n_local_max, m_local_max, ctypes.byref(self._h)))
+        self.loss_buf = torch.zeros((), dtype=torch.float32, device=self.device)
+
+    # -- the hot path -----------------------------------------------------------------
+    def enqueue(self, g_feats: torch.Tensor, labels: torch.Tensor, stream=None):
+        assert g_feats.is_contiguous() and labels.is_contiguous() and labels.dtype == torch.int64
+        _check(load_library().f2c_dcp_enqueue(self._h, _ptr(g_feats), _ptr(labels),
+                                              labels.shape[0] // (self.world if self.rank < 0 else 1),
+                                              _stream(stream)))
+
+    def loss_fwd_bwd(self, x: torch.Tensor, labels: torch.Tensor, pairing: torch.Tensor | None,
+                     s: float, m: float, dx: torch.Tensor | None = None, loss: torch.Tensor | None = None,
+                     stream=None):
+        """Returns (loss [fp32 device scalar], dx [same shape/dtype as x])."""
+        assert x.is_contiguous() and labels.dtype == torch.int64
+        if pairing is not None:
+            assert pairing.dtype == torch.int32 and pairing.is_contiguous()
+        dx = torch.empty_like(x) if dx is None else dx
+        loss = self.loss_buf if loss is None else loss
+        n_local = x.shape[0] // (self.world if self.rank < 0 else 1)
+        _check(load_library().f2c_dcp_loss_fwd_bwd(self._h, _ptr(x), _ptr(labels), _ptr(pairing),
+                                                   n_local, float(s), float(m), _ptr(loss), _ptr(dx),
+                                                   _stream(stream)))
+        return loss, dx
+
+    # -- support ----------------------------------------------------------------------
+    def check(self):
+        _check(load_library().f2c_dcp_check(self._h))
+
+    def get_state(self):
+        import numpy as np
+        rows = self.C if (self.rank < 0 or self.world == 1) else None
+        if rows is None:
+            lo = self.C * self.rank // self.world
+            hi = self.C * (self.rank + 1) // self.world
+            rows = hi - lo
+        feats = np.empty((rows, self.d), dtype=np.uint16 if self.dtype == BF16 else np.float32)
+        labs = np.empty(rows, dtype=np.int64)
+        E = ctypes.c_int64()
+        _check(load_library().f2c_dcp_get_state(self._h, feats.ctypes.data_as(ctypes.c_void_p),
+                                                labs.ctypes.data_as(ctypes.c_void_p), ctypes.byref(E)))
+        return feats, labs, E.value
+
+    def set_state(self, feats, labels, E: int):
+        import numpy as np
+        feats = np.ascontiguousarray(feats)
+        labels = np.ascontiguousarray(labels, dtype=np.int64)
+        _check(load_library().f2c_dcp_set_state(self._h, feats.ctypes.data_as(ctypes.c_void_p),
+                                                labels.ctypes.data_as(ctypes.c_void_p), int(E)))
+
+    def row_stats(self, n_global: int):
+        import numpy as np
+        lse, cos, phi, ell = (np.empty(n_global, np.float32) for _ in range(4))
+        tseq = np.empty(n_global, np.int64)
+        counts = np.empty(3, np.int64)
+        P = lambda a: a.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+        _check(load_library().f2c_dcp_row_stats(self._h, P(lse), P(tseq), P(cos), P(phi), P(ell),
+                                                P(counts)))
+        return dict(lse=lse, target_seq=tseq, cos_t=cos, phi=phi, ell=ell, N_pos=int(counts[0]),
+                    N_neg=int(counts[1]), C_occ=int(counts[2]))
+
+    @staticmethod
+    def last_launch_count() -> int:
+        return load_library().f2c_last_launch_count()
+
+    def close(self):
+        if self._h:
+            load_library().f2c_dcp_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def gnet_ema(p: torch.Tensor, g: torch.Tensor, momentum: float, stream=None):
+    """In-place g <- m g + (1-m) p (fp32, fp64 arithmetic, bit-exact)."""
+    assert p.dtype == torch.float32 and g.dtype == torch.float32 and p.numel() == g.numel()
+    _check(load_library().f2c_gnet_ema(_ptr(p), _ptr(g), g.numel(), float(momentum), _stream(stream)))

@@ -1,0 +1,244 @@
+"""GPU parity: the CUDA path through the C ABI vs the fp64 oracle on the same
+seeded inputs.  Enqueue state and EMA bit-exact; loss
+relative error <= 2e-3; max|dx err| <= 1e-2 max|dx| (BJ:5), also applied to the
+in-pool and out-of-pool rows separately and to L_ce / L_cos separately."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from helpers import (assert_dx_close, assert_dx_rows_close, assert_loss_close, from_dev, it, lt,
+                     to_dev)
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def dcp():
+    import paper_2105_10375_b200 as m
+    m.load_library()
+    return m
+
+
+def _head(dcp, C, d, n_max, m_max, dtype=synth.BF16):
+    return dcp.DCPHead(C, d, dtype, 1, 0, n_local_max=n_max, m_local_max=m_max)
+
+
+def _enqueue_both(head, pool, G, y, dtype=synth.BF16):
+    head.enqueue(to_dev(G, dtype), lt(y))
+    pool.enqueue(G, y)
+
+
+def _compare_state(head, pool):
+    feats, labs, E = head.get_state()
+    assert E == int(pool.E[0])
+    np.testing.assert_array_equal(labs, pool.lab)
+    occ = pool.C_occ
+    np.testing.assert_array_equal(feats[:occ], pool.T[:occ])  # bit-exact bytes
+
+
+# ----------------------------------------------------------------------------- a1 enqueue
+@pytest.mark.parametrize("C,M", [(1000, 64), (777, 100), (4096, 512), (130, 130)])
+def test_enqueue_bit_exact_with_wrap(dcp, C, M):
+    d = 128
+    head = _head(dcp, C, d, 64, M)
+    pool = oracle.Pool(C, d, oracle.BF16)
+    rng = np.random.default_rng(C + M)
+    for b in range(2 * C // M + 3):  # fill, then wrap several times (M need not divide C)
+        m = int(rng.integers(1, M + 1))
+        G = synth.unit_rows(1, synth.S_PRE, b, 0, m, d)
+        _enqueue_both(head, pool, G, rng.integers(0, 10**9, m))
+        if b % 5 == 0:
+            _compare_state(head, pool)
+    _compare_state(head, pool)
+    head.check()
+
+
+def test_enqueue_rejects_bad_args(dcp):
+    head = _head(dcp, 100, 128, 64, 64)
+    with pytest.raises(dcp.DCPError) as e:
+        head.enqueue(to_dev(synth.unit_rows(1, 1, 0, 0, 65, 128), synth.BF16), lt(np.arange(65)))
+    assert e.value.code == 2
+    head.enqueue(to_dev(synth.unit_rows(1, 1, 0, 0, 4, 128), synth.BF16), lt([1, 2, -5, 3]))
+    with pytest.raises(dcp.DCPError) as e:
+        head.check()
+    assert e.value.code == 7
+
+
+# ----------------------------------------------------------------------------- a10 EMA
+@pytest.mark.parametrize("n", [1, 7, 4096 + 3, 1_000_003])
+@pytest.mark.parametrize("m", [0.0, 0.999, 1.0, 0.37])
+def test_ema_bit_exact(dcp, n, m):
+    p = synth.f32_normal(3, synth.S_EMA_P, n, 0.05)
+    g = synth.f32_normal(3, synth.S_EMA_G, n, 0.05)
+    ref = oracle.ema(p, g, m)
+    gd = torch.from_numpy(g.copy()).cuda()
+    dcp.gnet_ema(torch.from_numpy(p).cuda(), gd, m)
+    np.testing.assert_array_equal(gd.cpu().numpy(), ref)
+
+
+# ----------------------------------------------------------------------------- loss
+def _run_case(dcp, C, d, blocks, X, y, pairing, s, m, rows_check=True):
+    """blocks: list of (G, y) enqueued in order; then one loss call on (X, y)."""
+    N = len(y)
+    head = _head(dcp, C, d, max(N, 1), max(len(b[1]) for b in blocks))
+    pool = oracle.Pool(C, d, oracle.BF16)
+    for G, yy in blocks:
+        _enqueue_both(head, pool, G, yy)
+    loss, dx = head.loss_fwd_bwd(to_dev(X, synth.BF16), lt(y),
+                                 None if pairing is None else it(pairing), s, m)
+    torch.cuda.synchronize()
+    head.check()
+    ref = pool.loss(X, y, pairing, s, m)
+    st = head.row_stats(N)
+    assert st["N_pos"] == ref.N_pos and st["N_neg"] == ref.N_neg
+    np.testing.assert_array_equal(np.where(st["target_seq"] >= 0, st["target_seq"] % C, -1), ref.tslot)
+    assert_loss_close(float(loss.item()), ref.L)
+    gdx = from_dev(dx)
+    assert_dx_close(gdx, ref.dx)
+    pos, neg = np.where(ref.tslot >= 0)[0], np.where(ref.tslot < 0)[0]
+    if rows_check:
+        assert_dx_rows_close(gdx, ref.dx, pos, what="dx in-pool rows")
+        assert_dx_rows_close(gdx, ref.dx, neg, what="dx out-of-pool rows")
+        if len(pos):
+            assert_loss_close(float(np.mean(st["ell"][pos])), ref.L_ce, what="L_ce")
+            np.testing.assert_allclose(st["lse"][pos], ref.lse[pos], rtol=1e-3, atol=2e-3)
+        if len(neg):
+            assert_loss_close(float(np.mean(st["phi"][neg])), ref.L_cos, rtol=5e-3, atol=1e-5,
+                              what="L_cos")
+    return head, pool, ref
+
+
+def _random_pool_blocks(C, d, M, nblk, n_id, seed):
+    out = []
+    for b in range(nblk):
+        out.append((synth.unit_rows(seed, synth.S_PRE, b, 0, M, d),
+                    synth.uniform_labels(seed, synth.S_PRE_LAB, b, 0, M, n_id)))
+    return out
+
+
+@pytest.mark.parametrize("d", [128, 256, 512])
+def test_loss_small_ragged(dcp, d):
+    """C not a multiple of the 128-slot tile, N_pos not a multiple of 64, wrap."""
+    C, M, n_id = 333, 50, 400
+    blocks = _random_pool_blocks(C, d, M, 9, n_id, 5)
+    Xi = synth.unit_rows(6, synth.S_INST, 0, 0, 30, d)
+    yi = synth.uniform_labels(6, synth.S_INST_LAB, 0, 0, 30, n_id)
+    _run_case(dcp, C, d, blocks, Xi, yi, None, 64.0, 0.35)
+
+
+@pytest.mark.parametrize("s,m", [(64.0, 0.35), (30.0, 0.0), (1.0, 0.0)])
+def test_loss_c0_shape_steps(dcp, s, m):
+    """c0 (BJ:7) geometry in bf16 (D21): d=128, C=1024 = 16 x 64, 128-row mixed batches,
+    fwd+bwd+enqueue for several steps with pairing checked."""
+    cfg = synth.scaled(synth.CONFIGS["c0"], dtype=synth.BF16)
+    head = _head(dcp, cfg.C, cfg.d, cfg.N_loc(), cfg.M_loc)
+    pool = oracle.Pool(cfg.C, cfg.d, oracle.BF16)
+    for b in range(cfg.prefill_blocks()):
+        G, yy = synth.prefill_block(cfg, b)
+        _enqueue_both(head, pool, G, yy)
+    for t in range(4):
+        stp = synth.step_inputs(cfg, t)
+        _enqueue_both(head, pool, stp.g, stp.gy)           # enqueue first (D4)
+        loss, dx = head.loss_fwd_bwd(to_dev(stp.x, synth.BF16), lt(stp.y), it(stp.pairing), s, m)
+        head.check()
+        ref = pool.loss(stp.x, stp.y, stp.pairing, s, m)
+        assert ref.N_pos >= cfg.M_loc
+        assert_loss_close(float(loss.item()), ref.L)
+        gdx = from_dev(dx)
+        assert_dx_close(gdx, ref.dx)
+        assert_dx_rows_close(gdx, ref.dx, np.where(ref.tslot < 0)[0], what="dx out-of-pool")
+    _compare_state(head, pool)
+
+
+@pytest.mark.parametrize("regime", ["literal", "balanced", "peaked"])
+def test_loss_noise_regimes(dcp, regime):
+    cfg = synth.scaled(synth.CONFIGS["c1"], C=4000, M_loc=256, prefill=16)
+    d = cfg.d
+    sig = synth.sigma_regime(regime, d)
+    blocks = [synth.prefill_block(cfg, b) for b in range(cfg.prefill_blocks())]
+    stp = synth.step_inputs(cfg, 0, sigma=sig)
+    blocks.append((stp.g, stp.gy))
+    _run_case(dcp, cfg.C, d, blocks, stp.x, stp.y, stp.pairing, 64.0, 0.35)
+
+
+def test_loss_edge_no_inpool_rows(dcp):
+    d = 128
+    blocks = _random_pool_blocks(200, d, 40, 3, 1000, 7)
+    X = synth.unit_rows(8, synth.S_INST, 0, 0, 10, d)
+    _run_case(dcp, 200, d, blocks, X, np.arange(5000, 5010), None, 64.0, 0.35)
+
+
+def test_loss_edge_all_inpool_and_duplicates(dcp):
+    """N_neg = 0; duplicate labels in the pool (target = newest, D8) and in the batch."""
+    d, C = 256, 150
+    rng = np.random.default_rng(2)
+    blocks = []
+    for b in range(5):
+        blocks.append((synth.unit_rows(9, synth.S_PRE, b, 0, 40, d), rng.integers(0, 30, 40)))
+    X = synth.unit_rows(9, synth.S_INST, 0, 0, 70, d)
+    labs = np.concatenate([blk[1] for blk in blocks])[-C:]
+    y = rng.choice(labs, 70)
+    _run_case(dcp, C, d, blocks, X, y, None, 64.0, 0.35)
+
+
+def test_loss_edge_partial_pool_and_unnormalised_rows(dcp):
+    d, C = 512, 5000
+    blocks = _random_pool_blocks(C, d, 300, 2, 3000, 11)   # 600 of 5000 slots occupied
+    X = synth.unit_rows(12, synth.S_INST, 0, 0, 90, d)
+    Xf = oracle.bf16_to_f64(X) * np.linspace(0.2, 7.0, 90)[:, None]  # ||x|| != 1
+    X = oracle.f64_to_bf16(Xf)
+    y = np.concatenate([blocks[1][1][:45], 10**6 + np.arange(45)])
+    _run_case(dcp, C, d, blocks, X, y, None, 30.0, 0.2)
+
+
+def test_pairing_mismatch_is_reported(dcp):
+    d, C = 128, 256
+    head = _head(dcp, C, d, 8, 8)
+    G = synth.unit_rows(1, 1, 0, 0, 8, d)
+    head.enqueue(to_dev(G, synth.BF16), lt(np.arange(8)))
+    X = synth.unit_rows(1, 2, 0, 0, 8, d)
+    head.loss_fwd_bwd(to_dev(X, synth.BF16), lt(np.arange(8)), it(np.arange(8)), 64, 0.35)
+    head.check()  # consistent pairing
+    head.loss_fwd_bwd(to_dev(X, synth.BF16), lt(np.arange(8)), it(np.roll(np.arange(8), 1)), 64, 0.35)
+    with pytest.raises(dcp.DCPError) as e:
+        head.check()
+    assert e.value.code == 4
+
+
+def test_set_state_roundtrip(dcp):
+    d, C = 128, 300
+    head = _head(dcp, C, d, 16, 64)
+    pool = oracle.Pool(C, d, oracle.BF16)
+    for G, yy in _random_pool_blocks(C, d, 64, 7, 500, 13):
+        _enqueue_both(head, pool, G, yy)
+    feats, labs, E = head.get_state()
+    h2 = _head(dcp, C, d, 16, 64)
+    h2.set_state(feats, labs, E)
+    f2, l2, E2 = h2.get_state()
+    np.testing.assert_array_equal(f2, feats)
+    np.testing.assert_array_equal(l2, labs)
+    X = synth.unit_rows(14, 3, 0, 0, 16, d)
+    y = np.concatenate([labs[:8], np.arange(10**6, 10**6 + 8)])
+    l1, d1 = head.loss_fwd_bwd(to_dev(X, synth.BF16), lt(y), None, 64, 0.35)
+    l1 = float(l1.item())
+    lb, db = h2.loss_fwd_bwd(to_dev(X, synth.BF16), lt(y), None, 64, 0.35)
+    assert l1 == float(lb.item())
+    assert torch.equal(d1, db)
+
+
+def test_determinism(dcp):
+    cfg = synth.scaled(synth.CONFIGS["c1"], C=20000, M_loc=512, prefill=40)
+    head = _head(dcp, cfg.C, cfg.d, cfg.N_loc(), cfg.M_loc)
+    for b in range(cfg.prefill_blocks()):
+        G, yy = synth.prefill_block(cfg, b)
+        head.enqueue(to_dev(G, synth.BF16), lt(yy))
+    stp = synth.step_inputs(cfg, 0)
+    x, y, pr = to_dev(stp.x, synth.BF16), lt(stp.y), it(stp.pairing)
+    outs = []
+    for _ in range(3):
+        l, d = head.loss_fwd_bwd(x, y, pr, 64, 0.35)
+        outs.append((l.clone(), d.clone()))
+    for l, d in outs[1:]:
+        assert torch.equal(l, outs[0][0]) and torch.equal(d, outs[0][1])
