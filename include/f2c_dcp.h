@@ -157,6 +157,14 @@ const char *f2c_last_error(void);
  * thread (for the bench's gpu_launches accounting). */
 int f2c_last_launch_count(void);
 
+/* Kernel timing for the bench (CUDA events recorded on the launching stream around
+ * the fused loss kernel of every loss call while enabled).  enable=1 starts (and
+ * resets) accumulation, enable=0 stops.  f2c_dcp_profile_read synchronises and
+ * returns the summed device time of the fused kernel (ms), the number of timed
+ * launches, and the sum of N_pos over those calls. */
+int f2c_dcp_profile(f2c_dcp *h, int enable);
+int f2c_dcp_profile_read(f2c_dcp *h, double *main_ms, int64_t *launches, int64_t *n_pos_sum);
+
 /* Release host resources and the NCCL communicator.  The caller frees state_buf. */
 void f2c_dcp_destroy(f2c_dcp *h);
 

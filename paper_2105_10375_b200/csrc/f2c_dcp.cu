@@ -178,6 +178,14 @@ struct f2c_dcp {
     cudaStream_t last_stream = nullptr;
     nccl_comm_t comm = nullptr;
     int64_t last_N = 0;
+    // bench instrumentation
+    bool prof = false;
+    std::vector<cudaEvent_t> ev;
+    size_t ev_used = 0;
+    unsigned long long npos_base = 0;
+    ~f2c_dcp() {
+        for (cudaEvent_t e : ev) cudaEventDestroy(e);
+    }
 };
 
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -493,8 +501,21 @@ static int phase_main(f2c_dcp *h, Rank &R, const StepCtx &c, int64_t occ_loc) {
     p.seg_l = R.at<float>(L.seg_l);
     p.seg_mx = R.at<float>(L.seg_mx);
     p.seg_O = R.at<float>(L.seg_O);
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (h->prof) {
+        while (h->ev.size() < h->ev_used + 2) {
+            cudaEvent_t e;
+            CUDA_TRY(cudaEventCreate(&e));
+            h->ev.push_back(e);
+        }
+        e0 = h->ev[h->ev_used];
+        e1 = h->ev[h->ev_used + 1];
+        h->ev_used += 2;
+        CUDA_TRY(cudaEventRecord(e0, c.st));
+    }
     dcp_tp64_kernel<<<h->G, TP_THREADS, TP_SMEM_BYTES, c.st>>>(R.tmT, R.tmX, p);
     LAUNCH_CHECK();
+    if (e1) CUDA_TRY(cudaEventRecord(e1, c.st));
     return F2C_OK;
 }
 
@@ -659,6 +680,38 @@ extern "C" int f2c_dcp_set_state(f2c_dcp *h, const void *feats_host, const int64
     CUDA_TRY(cudaDeviceSynchronize());
     h->E = enq_count;
     h->M_last = 0;
+    return F2C_OK;
+}
+
+extern "C" int f2c_dcp_profile(f2c_dcp *h, int enable) {
+    if (!h) return fail(F2C_EINVAL, "NULL handle");
+    if (enable) {
+        CUDA_TRY(cudaDeviceSynchronize());
+        h->ev_used = 0;
+        Scalars s;
+        CUDA_TRY(cudaMemcpy(&s, h->ranks[0].sc(), sizeof s, cudaMemcpyDeviceToHost));
+        h->npos_base = s.n_pos_sum;
+    }
+    h->prof = enable != 0;
+    return F2C_OK;
+}
+
+extern "C" int f2c_dcp_profile_read(f2c_dcp *h, double *main_ms, int64_t *launches, int64_t *n_pos_sum) {
+    if (!h) return fail(F2C_EINVAL, "NULL handle");
+    CUDA_TRY(cudaDeviceSynchronize());
+    double tot = 0.0;
+    for (size_t i = 0; i + 1 < h->ev_used; i += 2) {
+        float ms = 0.f;
+        CUDA_TRY(cudaEventElapsedTime(&ms, h->ev[i], h->ev[i + 1]));
+        tot += ms;
+    }
+    if (main_ms) *main_ms = tot;
+    if (launches) *launches = static_cast<int64_t>(h->ev_used / 2);
+    if (n_pos_sum) {
+        Scalars s;
+        CUDA_TRY(cudaMemcpy(&s, h->ranks[0].sc(), sizeof s, cudaMemcpyDeviceToHost));
+        *n_pos_sum = static_cast<int64_t>(s.n_pos_sum - h->npos_base);
+    }
     return F2C_OK;
 }
 

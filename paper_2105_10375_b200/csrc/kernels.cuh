@@ -24,6 +24,7 @@ struct Scalars {          // lives at the start of the per-rank scratch
     int n_neg;
     int pad0;
     double loss3[3];      // L, L_ce, L_cos (fp64) of the last loss call
+    unsigned long long n_pos_sum;  // sum of n_pos over loss calls (bench accounting)
 };
 
 __device__ __forceinline__ void latch(Scalars *s, int code, int detail) {
@@ -267,7 +268,6 @@ struct CompactArgs {
 };
 __global__ void __launch_bounds__(1024) k_compact(CompactArgs a) {
     __shared__ int wsum[32];
-    __shared__ int base_s;
     const int tid = threadIdx.x, nt = blockDim.x;
     const int64_t per = (a.N + nt - 1) / nt;
     const int64_t r0 = tid * per, r1 = r0 + per < a.N ? r0 + per : a.N;
@@ -324,6 +324,7 @@ __global__ void __launch_bounds__(1024) k_compact(CompactArgs a) {
     if (tid == 0) {
         a.sc->n_pos = n_pos;
         a.sc->n_neg = static_cast<int>(a.N) - n_pos;
+        a.sc->n_pos_sum += static_cast<unsigned long long>(n_pos);
     }
 }
 

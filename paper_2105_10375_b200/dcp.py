@@ -47,11 +47,13 @@ def load_library():
     L.f2c_last_error.argtypes = []
     L.f2c_last_error.restype = ctypes.c_char_p
     L.f2c_last_launch_count.argtypes = []
+    L.f2c_dcp_profile.argtypes = [P, i32]
+    L.f2c_dcp_profile_read.argtypes = [P, P, P, P]
     L.f2c_dcp_destroy.argtypes = [P]
     L.f2c_dcp_destroy.restype = None
     for f in (L.f2c_dcp_create, L.f2c_dcp_enqueue, L.f2c_dcp_loss_fwd_bwd, L.f2c_gnet_ema,
               L.f2c_dcp_get_state, L.f2c_dcp_set_state, L.f2c_dcp_row_stats, L.f2c_dcp_check,
-              L.f2c_last_launch_count):
+              L.f2c_last_launch_count, L.f2c_dcp_profile, L.f2c_dcp_profile_read):
         f.restype = ctypes.c_int
     _lib = L
     return L
@@ -157,6 +159,15 @@ class DCPHead:
                                                 P(counts)))
         return dict(lse=lse, target_seq=tseq, cos_t=cos, phi=phi, ell=ell, N_pos=int(counts[0]),
                     N_neg=int(counts[1]), C_occ=int(counts[2]))
+
+    def profile(self, enable: bool):
+        _check(load_library().f2c_dcp_profile(self._h, 1 if enable else 0))
+
+    def profile_read(self):
+        ms, n, npos = ctypes.c_double(), ctypes.c_int64(), ctypes.c_int64()
+        _check(load_library().f2c_dcp_profile_read(self._h, ctypes.byref(ms), ctypes.byref(n),
+                                                   ctypes.byref(npos)))
+        return ms.value, n.value, npos.value
 
     @staticmethod
     def last_launch_count() -> int:
