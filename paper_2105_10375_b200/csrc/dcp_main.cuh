@@ -54,6 +54,7 @@ struct TPParams {
     float *seg_l;          // [S][64]   sum of p over the segment's slots (target excluded)
     float *seg_mx;         // [S][64]   max exponent over the segment's slots (target excluded)
     float *seg_O;          // [S][64][d] sum_c p[c, r] T_c (target excluded)
+    unsigned long long *dbg;  // optional per-tile timestamps of CTA 0 (null in production)
 };
 
 struct TPAux {
@@ -68,26 +69,57 @@ struct TPAux {
     float red_mx[4][TP_R];
 };
 
-// Flattened schedule: work item w in [0, n_rg * n_tiles) is (row group w / n_tiles,
-// tile w % n_tiles).  CTA b owns [b*total/G, (b+1)*total/G); each maximal run inside
-// one row group is a "segment" with id b + rg (unique, < n_rg + G).
-struct TPSched {
-    long long pos, end;
-    int n_tiles;
-    __device__ void init(int b, int G, int n_rg, int nt) {
-        n_tiles = nt;
-        long long total = static_cast<long long>(n_rg) * nt;
-        pos = total * b / G;
-        end = total * (b + 1) / G;
+// Work schedule.  The occupied tiles are cut into S contiguous ranges; a unit is
+// (range s, row group rg) with id u = s * R + rg (R = row groups).  CTA b runs units
+// b, b + G, b + 2G, ...  Units that run concurrently share their range across all
+// row groups, so every pool tile is read from HBM about once and served to the R
+// row groups from L2.  S balances R*S units over G CTAs (waves) while keeping
+// ranges long; the combine kernel recomputes the same S.  Unit id = segment id.
+__host__ __device__ inline int tp_choose_S(int R, int G, int n_tiles) {
+    if (n_tiles <= 0 || R <= 0) return 1;
+    int s_lo = G / R;
+    if (s_lo < 1) s_lo = 1;
+    int s_hi = (2 * G) / R + 1;
+    if (s_hi > n_tiles) s_hi = n_tiles;
+    if (s_lo > s_hi) s_lo = s_hi;
+    int best = s_lo;
+    double best_eff = -1.0;
+    for (int S = s_lo; S <= s_hi; ++S) {
+        const long long U = static_cast<long long>(R) * S;
+        const long long waves = (U + G - 1) / G;
+        // time ~ waves * ceil(n_tiles / S); work ~ n_tiles * R / G per CTA
+        const double t = static_cast<double>(waves) * ((n_tiles + S - 1) / S);
+        const double eff = (static_cast<double>(n_tiles) * R / G) / t;
+        if (eff > best_eff + 0.01) {
+            best_eff = eff;
+            best = S;
+        }
     }
-    __device__ bool next(int &rg, int &t0, int &t1) {
-        if (pos >= end) return false;
-        rg = static_cast<int>(pos / n_tiles);
-        t0 = static_cast<int>(pos % n_tiles);
-        long long rem = end - pos;
-        t1 = static_cast<int>(t0 + rem < n_tiles ? t0 + rem : n_tiles);
-        pos += t1 - t0;
-        return true;
+    return best;
+}
+
+struct TPSched {
+    int R, S, n_tiles, G;
+    long long u, U;
+    __device__ void init(int b, int G_, int R_, int nt) {
+        R = R_;
+        G = G_;
+        n_tiles = nt;
+        S = tp_choose_S(R, G, nt);
+        U = nt > 0 ? static_cast<long long>(R) * S : 0;
+        u = b;
+    }
+    __device__ bool next(int &rg, int &t0, int &t1, int &seg) {
+        while (u < U) {
+            const int s = static_cast<int>(u / R);
+            rg = static_cast<int>(u % R);
+            seg = static_cast<int>(u);
+            t0 = static_cast<int>(static_cast<long long>(s) * n_tiles / S);
+            t1 = static_cast<int>(static_cast<long long>(s + 1) * n_tiles / S);
+            u += G;
+            if (t1 > t0) return true;
+        }
+        return false;
     }
 };
 
@@ -154,19 +186,21 @@ __global__ void __launch_bounds__(TP_THREADS, 1)
 
     TPSched sch;
     sch.init(blockIdx.x, gridDim.x, n_rg, n_tiles);
-    int rg, t0, t1;
+    int rg, t0, t1, seg;
 
     if (warp == 8) {
         // ------------------------------------------------------------ TMA producer
         if (lane == 0) {
             uint32_t pc = 0, sg = 0;
-            while (n_tiles > 0 && sch.next(rg, t0, t1)) {
+            while (sch.next(rg, t0, t1, seg)) {
                 mbar_wait(&aux->xempty, (sg & 1) ^ 1);
                 mbar_arrive_expect_tx(&aux->xfull, static_cast<uint32_t>(TP_R * d * 2));
                 for (int c = 0; c < (d >> 6); ++c)
                     tma_load_2d(sX + c * TP_XCHUNK_BYTES, &tmX, &aux->xfull, c * 64, rg * TP_R);
                 for (int t = t0; t < t1; ++t) {
+                    const uint32_t jt_p = pc / npair;
                     for (int q = 0; q < npair; ++q, ++pc) {
+                        if (p.dbg && blockIdx.x == 0 && jt_p < 64 && q == npair - 1) p.dbg[jt_p * 8 + 7] = clock64();
                         const uint32_t st = pc % TP_NSTAGE, ph = (pc / TP_NSTAGE) & 1;
                         mbar_wait(&aux->tempty[st], ph ^ 1);
                         mbar_arrive_expect_tx(&aux->tfull[st], TP_PAIR_BYTES);
@@ -186,11 +220,13 @@ __global__ void __launch_bounds__(TP_THREADS, 1)
             constexpr uint32_t idesc2 = umma_idesc_bf16(128, TP_R, 1, 1);  // MN-major A and B
             const uint32_t sTa = smem_u32(sT), sXa = smem_u32(sX), sPa = smem_u32(sP);
             uint32_t pc = 0, sg = 0, jt = 0;
-            while (n_tiles > 0 && sch.next(rg, t0, t1)) {
+            while (sch.next(rg, t0, t1, seg)) {
                 mbar_wait(&aux->xfull, sg & 1);
                 tc_fence_after();
                 for (int t = t0; t < t1; ++t, ++jt) {
                     const bool first = (t == t0), last = (t == t1 - 1);
+                    unsigned long long *dbg = (p.dbg && blockIdx.x == 0 && jt < 64) ? p.dbg + jt * 8 : nullptr;
+                    if (dbg) dbg[0] = clock64();
                     // GEMM 1: S^T[slot, row] = sum_d T[slot, d] * x[row, d]
                     for (int q = 0; q < npair; ++q) {
                         const uint32_t pq = pc + q;
@@ -209,9 +245,11 @@ __global__ void __launch_bounds__(TP_THREADS, 1)
                     }
                     umma_commit(&aux->sfull);
                     if (last) umma_commit(&aux->xempty);
+                    if (dbg) dbg[1] = clock64();
                     // wait for the softmax warps to publish P^T for this tile
                     mbar_wait(&aux->pfull, jt & 1);
                     tc_fence_after();
+                    if (dbg) dbg[2] = clock64();
                     if (first && sg > 0) {
                         mbar_wait(&aux->oempty, (sg - 1) & 1);
                         tc_fence_after();
@@ -231,6 +269,7 @@ __global__ void __launch_bounds__(TP_THREADS, 1)
                     }
                     pc += npair;
                     if (last) umma_commit(&aux->ofull);
+                    if (dbg) dbg[3] = clock64();
                 }
                 ++sg;
             }
@@ -245,8 +284,7 @@ __global__ void __launch_bounds__(TP_THREADS, 1)
         const int sr = qw * 32 + lane;  // slot row within the tile
         const uint32_t prow = sPa + (sr >> 3) * 1024 + (sr & 7) * 128;
         uint32_t sg = 0, jt = 0;
-        while (n_tiles > 0 && sch.next(rg, t0, t1)) {
-            const int seg = blockIdx.x + rg;
+        while (sch.next(rg, t0, t1, seg)) {
             named_bar_sync(1, TP_EPI_THREADS);
             if (tid < TP_R) {
                 aux->ab[tid] = p.row_ab[rg * TP_R + tid];
@@ -262,8 +300,11 @@ __global__ void __launch_bounds__(TP_THREADS, 1)
                 mxacc[k] = -INFINITY;
             }
             for (int t = t0; t < t1; ++t, ++jt) {
+                unsigned long long *dbg = (p.dbg && blockIdx.x == 0 && jt < 64 && tid == 0) ? p.dbg + jt * 8 : nullptr;
+                if (dbg) dbg[4] = clock64();
                 mbar_wait(&aux->sfull, jt & 1);
                 tc_fence_after();
+                if (dbg) dbg[5] = clock64();
                 float e[32];
                 tmem_ld32(tmem + lane_base + TP_S_COL + hw * 32, e);
                 tmem_wait_ld();
@@ -314,6 +355,7 @@ __global__ void __launch_bounds__(TP_THREADS, 1)
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&aux->pfull);
+                if (dbg) dbg[6] = clock64();
             }
             // ---- segment end: reduce l and max over the 128 slot lanes
             const float lsum = warp_transpose_reduce<false>(lacc, lane);

@@ -1,0 +1,455 @@
+// dcp_pc.cuh -- the fused DCP loss kernel, producer/consumer CTA-pair version
+// (hot-path steps a2, a4, a5, a7, a9).
+//
+// A cluster of two CTAs owns one group of 128 compacted rows and a range of pool tiles
+// (128 slots each):
+//   producer (cluster rank 0): x_hat rows live in TMEM as the UMMA A operand (bf16);
+//     GEMM 1  S[r, c] = <x_r, T_c>        M = 128 rows, N = 128 slots, K = d
+//     (A from TMEM, B = pool chunk from smem), double-buffered S in TMEM so the softmax
+//     of tile j overlaps GEMM 1 of tile j+1.  Softmax warps (rows on TMEM lanes):
+//     e = S*a_r - b_r, margin on the target column (recorded apart, excluded),
+//     p = 2^e -> running l_r, max_r in registers; P (bf16) is written in the
+//     consumer's A-operand layout and shipped to the consumer's smem by a DSMEM bulk
+//     copy (cp.async.bulk shared::cta -> shared::cluster, complete_tx on the
+//     consumer's mbarrier).
+//   consumer (cluster rank 1): O[128 rows x d] fp32 occupies all 512 TMEM columns;
+//     GEMM 2  O[r, :] += sum_c P[r, c] T[c, :]   M = 128, N = 256 (d block), K = slots
+//     (A = P from smem, B = pool chunk MN-major from smem).
+// The N x C logit matrix only exists as one 128x128 tile at a time (TMEM, then smem).
+// The softmax reference b_r is an upper bound of every logit, identical across
+// slots, so partials of different clusters / tiles / ranks add without rescaling.
+#pragma once
+#include "dcp_main.cuh"
+#include "sm100.cuh"
+
+namespace f2c {
+
+constexpr int PC_R = 128;                // rows per group (TMEM lanes)
+constexpr int PC_TILE = 128;             // slots per tile (GEMM-1 N, GEMM-2 K)
+constexpr int PC_THREADS = 352;          // 11 warps
+constexpr int PC_P_NSTAGE = 4;           // producer pool-chunk ring ([128 slots x 64 d] = 16 KB)
+constexpr int PC_Q_NSTAGE = 3;           // consumer pool-chunk ring ([32 slots x 512 d] = 32 KB)
+constexpr int PC_PBYTES = PC_R * PC_TILE * 2;  // one P tile, bf16 = 32 KB
+
+// producer smem
+constexpr int PCP_OFF_T = 0;                              // 4 x 16 KB
+constexpr int PCP_OFF_PS = PCP_OFF_T + PC_P_NSTAGE * 16384;  // 2 x 32 KB P staging
+constexpr int PCP_OFF_AUX = PCP_OFF_PS + 2 * PC_PBYTES;
+// consumer smem
+constexpr int PCQ_OFF_P = 0;                              // 2 x 32 KB P slots
+constexpr int PCQ_OFF_T = PCQ_OFF_P + 2 * PC_PBYTES;      // 3 x 32 KB pool stages
+constexpr int PCQ_OFF_AUX = PCQ_OFF_T + PC_Q_NSTAGE * 32768;
+constexpr int PC_OFF_AUX = PCP_OFF_AUX > PCQ_OFF_AUX ? PCP_OFF_AUX : PCQ_OFF_AUX;
+constexpr int PC_SMEM_BYTES = PC_OFF_AUX + 4096 + 1024;
+
+// the same struct (same offsets) in both CTAs, so multicast commits can target a
+// barrier of the peer by its local offset
+struct PCAux {
+    // producer
+    uint64_t tfull[PC_P_NSTAGE], tempty[PC_P_NSTAGE];
+    uint64_t sfull[2], sempty[2];
+    uint64_t xready, xfree;
+    uint64_t pready[2], pstage_free[2];
+    uint64_t pslot_free[2];            // arrived by the consumer's multicast commit
+    // consumer
+    uint64_t qfull[PC_Q_NSTAGE], qempty[PC_Q_NSTAGE];
+    uint64_t pfull[2];                 // complete_tx by the producer's bulk copy
+    uint64_t ofull, oempty;
+    uint32_t tmem_base;
+    uint32_t pad;
+    float red_l[2][PC_R];
+    float red_mx[2][PC_R];
+};
+
+struct PCParams {
+    int d;                 // feature dim (multiple of 128, <= 512)
+    int n_slots;           // occupied slots of this shard
+    const int *n_pos;      // device: in-pool rows; the mu row is row *n_pos
+    const float2 *row_ab;  // [R_max] (a_r, b_r)
+    const int *row_tgt;    // [R_max] local target slot or -1
+    const uint8_t *X_pos;  // [R_max, d] bf16 compacted rows
+    float margin_l2;       // s * m * log2(e)
+    float *ttgt;           // [R_max]
+    float *seg_l;          // [S][128]
+    float *seg_mx;         // [S][128]
+    float *seg_O;          // [S][128][d]
+    unsigned long long *dbg;
+};
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t cta) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(cta));
+    return r;
+}
+// D[tmem] (+)= A[tmem] * B[smem]  (A operand from tensor memory)
+__device__ __forceinline__ void umma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc,
+                                             uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+// arrive on the barrier at the same smem offset in every CTA of `mask`
+__device__ __forceinline__ void umma_commit_mc(uint64_t *bar, uint16_t mask) {
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"(mask)
+        : "memory");
+}
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+        "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+        "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+        "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+        "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]),
+        "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]),
+        "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]),
+        "r"(v[29]), "r"(v[30]), "r"(v[31])
+        : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() {
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
+    dcp_pc_kernel(const __grid_constant__ CUtensorMap tmT, const __grid_constant__ CUtensorMap tmT32,
+                  const PCParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                                ~static_cast<uintptr_t>(1023));
+    PCAux *aux = reinterpret_cast<PCAux *>(smem + PC_OFF_AUX);
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const uint32_t crank = cluster_ctarank();
+    const int d = p.d;
+    const int nchunk = d >> 6;  // 64-wide d chunks
+    const int n_pos = *p.n_pos;
+    const int n_rg = (n_pos + 1 + PC_R - 1) / PC_R;
+    const int n_tiles = (p.n_slots + PC_TILE - 1) / PC_TILE;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < PC_P_NSTAGE; ++i) {
+            mbar_init(&aux->tfull[i], 1);
+            mbar_init(&aux->tempty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&aux->sfull[i], 1);
+            mbar_init(&aux->sempty[i], 8);
+            mbar_init(&aux->pready[i], 8);
+            mbar_init(&aux->pstage_free[i], 1);
+            mbar_init(&aux->pslot_free[i], 1);
+            mbar_init(&aux->pfull[i], 1);
+        }
+        mbar_init(&aux->xready, 8);
+        mbar_init(&aux->xfree, 1);
+        for (int i = 0; i < PC_Q_NSTAGE; ++i) {
+            mbar_init(&aux->qfull[i], 1);
+            mbar_init(&aux->qempty[i], 1);
+        }
+        mbar_init(&aux->ofull, 1);
+        mbar_init(&aux->oempty, 4);
+        if (crank == 1) {  // arm both P slots before the producer can copy into them
+            mbar_arrive_expect_tx(&aux->pfull[0], PC_PBYTES);
+            mbar_arrive_expect_tx(&aux->pfull[1], PC_PBYTES);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 9) {
+        tma_prefetch_desc(crank == 0 ? &tmT : &tmT32);
+        tmem_alloc(&aux->tmem_base, 512);
+        tmem_relinquish();
+    }
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync_all();
+    tc_fence_after();
+    const uint32_t tmem = aux->tmem_base;
+
+    TPSched sch;
+    sch.init(blockIdx.x >> 1, gridDim.x >> 1, n_rg, n_tiles);
+    int rg, t0, t1, seg;
+
+    if (crank == 0) {
+        // ================================================================= PRODUCER
+        uint8_t *sT = smem + PCP_OFF_T;
+        uint8_t *sPS = smem + PCP_OFF_PS;
+        constexpr uint32_t X_COL = 0, S_COL = 256;  // x_hat (A operand) | two S buffers
+        if (warp == 8) {
+            // -------- TMA: pool chunks [128 slots x 64 d]
+            if (lane == 0) {
+                uint32_t pc = 0;
+                while (sch.next(rg, t0, t1, seg)) {
+                    for (int t = t0; t < t1; ++t)
+                        for (int kc = 0; kc < nchunk; ++kc, ++pc) {
+                            const uint32_t st = pc % PC_P_NSTAGE, ph = (pc / PC_P_NSTAGE) & 1;
+                            mbar_wait(&aux->tempty[st], ph ^ 1);
+                            mbar_arrive_expect_tx(&aux->tfull[st], 16384);
+                            tma_load_2d(sT + st * 16384, &tmT, &aux->tfull[st], kc * 64, t * PC_TILE);
+                        }
+                }
+            }
+        } else if (warp == 9) {
+            // -------- UMMA issuer: GEMM 1 (A = x_hat from TMEM, B = pool chunk K-major)
+            if (lane == 0) {
+                constexpr uint32_t idesc = umma_idesc_bf16(128, PC_TILE, 0, 0);
+                const uint32_t sTa = smem_u32(sT);
+                uint32_t pc = 0, jt = 0, sg = 0;
+                while (sch.next(rg, t0, t1, seg)) {
+                    mbar_wait(&aux->xready, sg & 1);
+                    tc_fence_after();
+                    for (int t = t0; t < t1; ++t, ++jt) {
+                        const uint32_t sb = jt & 1, sph = (jt >> 1) & 1;
+                        mbar_wait(&aux->sempty[sb], sph ^ 1);
+                        tc_fence_after();
+                        const uint32_t dcol = tmem + S_COL + sb * PC_TILE;
+                        for (int kc = 0; kc < nchunk; ++kc, ++pc) {
+                            const uint32_t st = pc % PC_P_NSTAGE, ph = (pc / PC_P_NSTAGE) & 1;
+                            mbar_wait(&aux->tfull[st], ph);
+                            tc_fence_after();
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) {
+                                const uint64_t b = umma_desc_sw128(sTa + st * 16384 + k * 32, 16, 1024);
+                                umma_bf16_ts(dcol, tmem + X_COL + kc * 32 + k * 8, b, idesc,
+                                             (kc | k) != 0);
+                            }
+                            umma_commit(&aux->tempty[st]);
+                        }
+                        umma_commit(&aux->sfull[sb]);
+                        if (t == t1 - 1) umma_commit(&aux->xfree);
+                    }
+                    ++sg;
+                }
+            }
+        } else if (warp == 10) {
+            // -------- P mover: staging buffer -> consumer's P slot (DSMEM bulk copy)
+            if (lane == 0) {
+                uint32_t jt = 0;
+                while (sch.next(rg, t0, t1, seg)) {
+                    for (int t = t0; t < t1; ++t, ++jt) {
+                        const uint32_t b = jt & 1, ph = (jt >> 1) & 1;
+                        mbar_wait(&aux->pready[b], ph);
+                        mbar_wait(&aux->pslot_free[b], ph ^ 1);
+                        const uint32_t dst = mapa_shared(smem_u32(smem + PCQ_OFF_P + b * PC_PBYTES), 1);
+                        const uint32_t rbar = mapa_shared(smem_u32(&aux->pfull[b]), 1);
+                        asm volatile(
+                            "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes"
+                            " [%0], [%1], %2, [%3];" ::"r"(dst),
+                            "r"(smem_u32(sPS + b * PC_PBYTES)), "r"(PC_PBYTES), "r"(rbar)
+                            : "memory");
+                        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                        mbar_arrive(&aux->pstage_free[b]);
+                    }
+                }
+                asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+            }
+        } else {
+            // -------- softmax warps 0-7: warp w -> rows 32*(w%4)+lane, slot half w/4
+            const int q = warp & 3, h = warp >> 2;
+            const int r = q * 32 + lane;
+            const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
+            uint32_t jt = 0, sg = 0;
+            while (sch.next(rg, t0, t1, seg)) {
+                const int row = rg * PC_R + r;
+                const float2 ab = p.row_ab[row];
+                const int tg = p.row_tgt[row];
+                // x_hat (this thread's row, d half h) -> TMEM A operand columns
+                mbar_wait(&aux->xfree, (sg & 1) ^ 1);
+                tc_fence_after();
+                {
+                    const uint4 *src = reinterpret_cast<const uint4 *>(p.X_pos + static_cast<size_t>(row) * d * 2) +
+                                       h * (d / 16);
+                    const int ncol = d / 4;  // 32-bit columns per half row (d/2 bf16)
+                    for (int c0 = 0; c0 < ncol; c0 += 32) {
+                        uint32_t w[32];
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            const uint4 v = src[c0 / 4 + u];
+                            w[4 * u] = v.x; w[4 * u + 1] = v.y; w[4 * u + 2] = v.z; w[4 * u + 3] = v.w;
+                        }
+                        tmem_st32(tmem + lane_base + X_COL + h * ncol + c0, w);
+                    }
+                    tmem_wait_st();
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&aux->xready);
+                float lacc = 0.f, mx = -INFINITY;
+                for (int t = t0; t < t1; ++t, ++jt) {
+                    const uint32_t sb = jt & 1, sph = (jt >> 1) & 1;
+                    mbar_wait(&aux->sfull[sb], sph);
+                    tc_fence_after();
+                    float e[64];
+                    {
+                        float v0[32], v1[32];
+                        const uint32_t ta = tmem + lane_base + S_COL + sb * PC_TILE + h * 64;
+                        tmem_ld32(ta, v0);
+                        tmem_ld32(ta + 32, v1);
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int k = 0; k < 32; ++k) {
+                            e[k] = v0[k];
+                            e[32 + k] = v1[k];
+                        }
+                    }
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&aux->sempty[sb]);
+                    const int base = t * PC_TILE + h * 64;
+                    const int nval = p.n_slots - base;  // valid slots in my 64-wide half
+#pragma unroll
+                    for (int k = 0; k < 64; ++k) e[k] = k < nval ? fmaf(e[k], ab.x, -ab.y) : -INFINITY;
+                    const bool hit = tg >= base && tg < base + 64;
+                    if (__any_sync(0xffffffffu, hit)) {
+                        if (hit) {
+                            const int kt = tg - base;
+#pragma unroll
+                            for (int k = 0; k < 64; ++k)
+                                if (k == kt) {
+                                    p.ttgt[row] = e[k] - p.margin_l2;
+                                    e[k] = -INFINITY;
+                                }
+                        }
+                    }
+                    uint32_t w[32];
+#pragma unroll
+                    for (int k = 0; k < 64; k += 2) {
+                        const float p0 = ex2_approx(e[k]), p1 = ex2_approx(e[k + 1]);
+                        lacc += p0 + p1;
+                        mx = fmaxf(mx, fmaxf(e[k], e[k + 1]));
+                        w[k >> 1] = pack_bf16x2(p0, p1);
+                    }
+                    // P -> staging buffer in the consumer's K-major SW128 A layout:
+                    // chunk h = slots [64h, 64h+64), row r: 128 B, 16-B unit u at u ^ (r & 7)
+                    const uint32_t b = jt & 1, ph = (jt >> 1) & 1;
+                    mbar_wait(&aux->pstage_free[b], ph ^ 1);
+                    const uint32_t rowa = smem_u32(sPS + b * PC_PBYTES + h * 16384 + (r >> 3) * 1024 + (r & 7) * 128);
+#pragma unroll
+                    for (int u = 0; u < 8; ++u)
+                        st_shared_v4(rowa + ((u ^ (r & 7)) << 4), w[4 * u], w[4 * u + 1], w[4 * u + 2],
+                                     w[4 * u + 3]);
+                    fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&aux->pready[b]);
+                }
+                // segment end: l and max over both slot halves
+                aux->red_l[h][r] = lacc;
+                aux->red_mx[h][r] = mx;
+                named_bar_sync(1, 256);
+                if (h == 0) {
+                    p.seg_l[static_cast<size_t>(seg) * PC_R + r] = aux->red_l[0][r] + aux->red_l[1][r];
+                    p.seg_mx[static_cast<size_t>(seg) * PC_R + r] = fmaxf(aux->red_mx[0][r], aux->red_mx[1][r]);
+                }
+                named_bar_sync(1, 256);
+                ++sg;
+            }
+        }
+    } else {
+        // ================================================================= CONSUMER
+        uint8_t *sP = smem + PCQ_OFF_P;
+        uint8_t *sT = smem + PCQ_OFF_T;
+        const int nq = PC_TILE / 32;  // 32-slot pool stages per tile
+        if (warp == 8) {
+            // -------- TMA: pool stages [32 slots x d] as d/64 boxes of [32 slots x 64 d]
+            if (lane == 0) {
+                uint32_t qc = 0;
+                while (sch.next(rg, t0, t1, seg)) {
+                    for (int t = t0; t < t1; ++t)
+                        for (int s = 0; s < nq; ++s, ++qc) {
+                            const uint32_t st = qc % PC_Q_NSTAGE, ph = (qc / PC_Q_NSTAGE) & 1;
+                            mbar_wait(&aux->qempty[st], ph ^ 1);
+                            mbar_arrive_expect_tx(&aux->qfull[st], static_cast<uint32_t>(32 * d * 2));
+                            for (int c = 0; c < nchunk; ++c)
+                                tma_load_2d(sT + st * 32768 + c * 4096, &tmT32, &aux->qfull[st], c * 64,
+                                            t * PC_TILE + s * 32);
+                        }
+                }
+            }
+        } else if (warp == 9) {
+            // -------- UMMA issuer: GEMM 2 (A = P K-major, B = pool MN-major, N = 256 d)
+            if (lane == 0) {
+                const uint32_t sPa = smem_u32(sP), sTa = smem_u32(sT);
+                const int nblk = (d + 255) >> 8;  // d blocks of <= 256 columns
+                uint32_t qc = 0, jt = 0, sg = 0;
+                while (sch.next(rg, t0, t1, seg)) {
+                    for (int t = t0; t < t1; ++t, ++jt) {
+                        const bool first = (t == t0);
+                        const uint32_t b = jt & 1, ph = (jt >> 1) & 1;
+                        mbar_wait(&aux->pfull[b], ph);
+                        mbar_arrive_expect_tx(&aux->pfull[b], PC_PBYTES);  // arm the next use
+                        tc_fence_after();
+                        if (first && sg > 0) {
+                            mbar_wait(&aux->oempty, (sg - 1) & 1);
+                            tc_fence_after();
+                        }
+                        for (int s = 0; s < nq; ++s, ++qc) {
+                            const uint32_t st = qc % PC_Q_NSTAGE, qph = (qc / PC_Q_NSTAGE) & 1;
+                            mbar_wait(&aux->qfull[st], qph);
+                            tc_fence_after();
+#pragma unroll
+                            for (int kk = 0; kk < 2; ++kk) {
+                                const int ks = s * 2 + kk;  // 16-slot K step within the tile
+                                const uint64_t a = umma_desc_sw128(
+                                    sPa + b * PC_PBYTES + (ks >> 2) * 16384 + (ks & 3) * 32, 16, 1024);
+                                for (int bb = 0; bb < nblk; ++bb) {
+                                    const int bN = d - bb * 256 >= 256 ? 256 : d - bb * 256;
+                                    const uint32_t idesc = bN == 256 ? umma_idesc_bf16(128, 256, 0, 1)
+                                                                     : umma_idesc_bf16(128, 128, 0, 1);
+                                    const uint64_t bd = umma_desc_sw128(
+                                        sTa + st * 32768 + bb * 4 * 4096 + kk * 2048, 4096, 1024);
+                                    umma_bf16(tmem + bb * 256, a, bd, idesc, !(first && s == 0 && kk == 0));
+                                }
+                            }
+                            umma_commit(&aux->qempty[st]);
+                        }
+                        umma_commit_mc(&aux->pslot_free[b], 0x1);  // tell the producer slot b is free
+                        if (t == t1 - 1) umma_commit(&aux->ofull);
+                    }
+                    ++sg;
+                }
+            }
+        } else if (warp < 4) {
+            // -------- O drain at segment end: warp w -> rows 32w..32w+31 (TMEM lanes)
+            const uint32_t lane_base = static_cast<uint32_t>(warp * 32) << 16;
+            const int r = warp * 32 + lane;
+            uint32_t sg = 0;
+            while (sch.next(rg, t0, t1, seg)) {
+                mbar_wait(&aux->ofull, sg & 1);
+                tc_fence_after();
+                float4 *dst = reinterpret_cast<float4 *>(p.seg_O + (static_cast<size_t>(seg) * PC_R + r) * d);
+                for (int c0 = 0; c0 < d; c0 += 32) {
+                    float o[32];
+                    tmem_ld32(tmem + lane_base + c0, o);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int u = 0; u < 8; ++u)
+                        dst[c0 / 4 + u] = make_float4(o[4 * u], o[4 * u + 1], o[4 * u + 2], o[4 * u + 3]);
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&aux->oempty);
+                ++sg;
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync_all();
+    if (warp == 9) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
+}  // namespace f2c

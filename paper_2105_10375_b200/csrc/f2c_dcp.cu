@@ -8,6 +8,7 @@
 #include <dlfcn.h>
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <string>
@@ -106,8 +107,8 @@ static Layout make_layout(int64_t C, int d, int dtype, int W, int rank, int64_t 
     if (rank < 0) L.C_loc = (C + W - 1) / W;
     L.N = n_loc * W;
     L.Mg = m_loc * W;
-    L.R_max = (L.N + 1 + 63) / 64 * 64;
-    L.S_max = L.R_max / 64 + G_MAX;
+    L.R_max = (L.N + 1 + 127) / 128 * 128;   // row groups of 64 (TP64) or 128 (PC)
+    L.S_max = L.R_max / 64 + 2 * G_MAX + 1;  // units R*S <= 2G + R (tp_choose_S)
     int H = 64;
     while (H < 2 * L.N) H <<= 1;
     L.H = H;
@@ -138,9 +139,9 @@ static Layout make_layout(int64_t C, int d, int dtype, int W, int rank, int64_t 
     L.row_ab = take(static_cast<size_t>(L.R_max) * 8);
     L.row_tgt = take(static_cast<size_t>(L.R_max) * 4);
     L.ttgt = take(static_cast<size_t>(L.R_max) * 4);
-    L.seg_l = take(static_cast<size_t>(L.S_max) * 64 * 4);
-    L.seg_mx = take(static_cast<size_t>(L.S_max) * 64 * 4);
-    L.seg_O = take(static_cast<size_t>(L.S_max) * 64 * d * 4);
+    L.seg_l = take(static_cast<size_t>(L.S_max) * 128 * 4);
+    L.seg_mx = take(static_cast<size_t>(L.S_max) * 128 * 4);
+    L.seg_O = take(static_cast<size_t>(L.S_max) * 128 * d * 4);
     L.rowloss = take(static_cast<size_t>(L.N) * 8);
     L.st_lse = take(static_cast<size_t>(L.N) * 4);
     L.st_cos = take(static_cast<size_t>(L.N) * 4);
@@ -161,7 +162,7 @@ struct Rank {
     int64_t lo, hi;
     Layout L;
     uint8_t *base;
-    CUtensorMap tmT, tmX;
+    CUtensorMap tmT, tmX, tmT32;
     template <typename P>
     P *at(size_t off) const { return reinterpret_cast<P *>(base + off); }
     Scalars *sc() const { return at<Scalars>(L.sc); }
@@ -183,6 +184,8 @@ struct f2c_dcp {
     std::vector<cudaEvent_t> ev;
     size_t ev_used = 0;
     unsigned long long npos_base = 0;
+    unsigned long long *dbg = nullptr;  // debug timestamps (f2c_dcp_debug_timestamps)
+    bool use_tp64 = false;              // F2C_KERNEL=tp64 selects the single-CTA kernel
     ~f2c_dcp() {
         for (cudaEvent_t e : ev) cudaEventDestroy(e);
     }
@@ -288,6 +291,7 @@ int f2c_dcp_create(int64_t C, int32_t d, int32_t dtype, int32_t world, int32_t r
         k_hash_clear<<<64, 256>>>(R.at<int64_t>(R.L.hkeys), R.at<unsigned long long>(R.L.hvals), R.L.H);
         if (dtype == F2C_BF16) {
             if ((rc = make_tmap_bf16(&R.tmT, R.base + R.L.T, R.hi - R.lo, d, TP_TILE)) ||
+                (rc = make_tmap_bf16(&R.tmT32, R.base + R.L.T, R.hi - R.lo, d, 32)) ||
                 (rc = make_tmap_bf16(&R.tmX, R.base + R.L.X_pos, R.L.R_max, d, TP_R))) {
                 delete h;
                 return rc;
@@ -299,8 +303,14 @@ int f2c_dcp_create(int64_t C, int32_t d, int32_t dtype, int32_t world, int32_t r
         delete h;
         return fail(F2C_ECUDA, "create: device sync failed: %s", cudaGetErrorString(cudaGetLastError()));
     }
+    {
+        const char *kv = getenv("F2C_KERNEL");
+        h->use_tp64 = kv && strcmp(kv, "tp64") == 0;
+    }
     if (cudaFuncSetAttribute(dcp_tp64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             TP_SMEM_BYTES) != cudaSuccess) {
+                             TP_SMEM_BYTES) != cudaSuccess ||
+        cudaFuncSetAttribute(dcp_pc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             PC_SMEM_BYTES) != cudaSuccess) {
         delete h;
         return fail(F2C_ECUDA, "cudaFuncSetAttribute(smem) failed");
     }
@@ -501,6 +511,7 @@ static int phase_main(f2c_dcp *h, Rank &R, const StepCtx &c, int64_t occ_loc) {
     p.seg_l = R.at<float>(L.seg_l);
     p.seg_mx = R.at<float>(L.seg_mx);
     p.seg_O = R.at<float>(L.seg_O);
+    p.dbg = h->dbg;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (h->prof) {
         while (h->ev.size() < h->ev_used + 2) {
@@ -513,7 +524,24 @@ static int phase_main(f2c_dcp *h, Rank &R, const StepCtx &c, int64_t occ_loc) {
         h->ev_used += 2;
         CUDA_TRY(cudaEventRecord(e0, c.st));
     }
-    dcp_tp64_kernel<<<h->G, TP_THREADS, TP_SMEM_BYTES, c.st>>>(R.tmT, R.tmX, p);
+    if (h->use_tp64) {
+        dcp_tp64_kernel<<<h->G, TP_THREADS, TP_SMEM_BYTES, c.st>>>(R.tmT, R.tmX, p);
+    } else {
+        PCParams q;
+        q.d = p.d;
+        q.n_slots = p.n_slots;
+        q.n_pos = p.n_pos;
+        q.row_ab = p.row_ab;
+        q.row_tgt = p.row_tgt;
+        q.X_pos = R.base + L.X_pos;
+        q.margin_l2 = p.margin_l2;
+        q.ttgt = p.ttgt;
+        q.seg_l = p.seg_l;
+        q.seg_mx = p.seg_mx;
+        q.seg_O = p.seg_O;
+        q.dbg = p.dbg;
+        dcp_pc_kernel<<<(h->G / 2) * 2, PC_THREADS, PC_SMEM_BYTES, c.st>>>(R.tmT, R.tmT32, q);
+    }
     LAUNCH_CHECK();
     if (e1) CUDA_TRY(cudaEventRecord(e1, c.st));
     return F2C_OK;
@@ -570,7 +598,8 @@ extern "C" int f2c_dcp_loss_fwd_bwd(f2c_dcp *h, const void *x, const int64_t *la
     a.C_occ = h->E < h->C ? h->E : h->C;
     a.d = h->d;
     a.dtype = h->dtype;
-    a.G = h->G;
+    a.G = h->use_tp64 ? h->G : h->G / 2;
+    a.rows_per_group = h->use_tp64 ? TP_R : PC_R;
     a.n_tiles = static_cast<int>((occ + TP_TILE - 1) / TP_TILE);
     a.s = s;
     a.margin_l2 = s * m * 1.4426950408889634f;
@@ -712,6 +741,13 @@ extern "C" int f2c_dcp_profile_read(f2c_dcp *h, double *main_ms, int64_t *launch
         CUDA_TRY(cudaMemcpy(&s, h->ranks[0].sc(), sizeof s, cudaMemcpyDeviceToHost));
         *n_pos_sum = static_cast<int64_t>(s.n_pos_sum - h->npos_base);
     }
+    return F2C_OK;
+}
+
+// internal debugging aid (not in the public header): per-tile clock64 stamps of CTA 0
+extern "C" int f2c_dcp_debug_timestamps(f2c_dcp *h, unsigned long long *dev_buf) {
+    if (!h) return fail(F2C_EINVAL, "NULL handle");
+    h->dbg = dev_buf;
     return F2C_OK;
 }
 

@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "dcp_main.cuh"
+#include "dcp_pc.cuh"
 #include "sm100.cuh"
 
 namespace f2c {
@@ -356,6 +358,7 @@ struct CombineArgs {
     Scalars *sc_w;
     int64_t N, C_occ;
     int d, dtype, G, n_tiles;
+    int rows_per_group;         // 64 (TP64 kernel) or 128 (producer/consumer kernel)
     float s, margin_l2;
     uint8_t *dx;                // [N, d] dtype
     double *rowloss;            // [N]
@@ -372,27 +375,26 @@ __device__ __forceinline__ float block_sum_128(float v, float *red) {
     return red[0] + red[1] + red[2] + red[3];
 }
 
-// sum the partials of compacted row k over its segments (fixed CTA order)
+// sum the partials of compacted row k over its segments (fixed range order);
+// the schedule (tp_choose_S) is the main kernel's.
 __device__ __forceinline__ void gather_row_partials(const CombineArgs &a, int n_rg, int k, float (&o)[4],
                                                     float &lsum, float &mx) {
-    const int rg = k / 64, r = k % 64;
+    const int RG = a.rows_per_group;
+    const int rg = k / RG, r = k % RG;
     lsum = 0.f;
     mx = -INFINITY;
 #pragma unroll
     for (int j = 0; j < 4; ++j) o[j] = 0.f;
     if (a.n_tiles <= 0) return;
-    const long long total = static_cast<long long>(n_rg) * a.n_tiles;
-    const long long p0 = static_cast<long long>(rg) * a.n_tiles, p1 = p0 + a.n_tiles;
-    long long bg = p0 * a.G / total - 1;
-    if (bg < 0) bg = 0;
-    for (long long b = bg; b < a.G; ++b) {
-        const long long s0 = total * b / a.G, s1 = total * (b + 1) / a.G;
-        if (s0 >= p1) break;
-        if (s1 <= p0 || s1 <= s0) continue;
-        const long long seg = b + rg;
-        lsum += a.seg_l[seg * 64 + r];
-        mx = fmaxf(mx, a.seg_mx[seg * 64 + r]);
-        const float *src = a.seg_O + (seg * 64 + r) * a.d;
+    const int S = tp_choose_S(n_rg, a.G, a.n_tiles);
+    for (int s = 0; s < S; ++s) {
+        const long long t0 = static_cast<long long>(s) * a.n_tiles / S;
+        const long long t1 = static_cast<long long>(s + 1) * a.n_tiles / S;
+        if (t1 <= t0) continue;
+        const long long seg = static_cast<long long>(s) * n_rg + rg;
+        lsum += a.seg_l[seg * RG + r];
+        mx = fmaxf(mx, a.seg_mx[seg * RG + r]);
+        const float *src = a.seg_O + (seg * RG + r) * a.d;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             const int dd = threadIdx.x + 128 * j;
@@ -406,7 +408,7 @@ __global__ void __launch_bounds__(128) k_combine(CombineArgs a) {
     __shared__ float red[4];
     const int64_t i = blockIdx.x;
     const int n_pos = a.sc->n_pos, n_neg = a.sc->n_neg;
-    const int n_rg = (n_pos + 1 + 63) / 64;
+    const int n_rg = (n_pos + 1 + a.rows_per_group - 1) / a.rows_per_group;
     const int k = a.comp_idx[i];
     const TX *xr = reinterpret_cast<const TX *>(a.x) + i * a.d;
     const float inv = a.inv_n[i];
