@@ -27,18 +27,20 @@ namespace f2c {
 constexpr int PC_R = 128;                // rows per group (TMEM lanes)
 constexpr int PC_TILE = 128;             // slots per tile (GEMM-1 N, GEMM-2 K)
 constexpr int PC_THREADS = 352;          // 11 warps
-constexpr int PC_P_NSTAGE = 4;           // producer pool-chunk ring ([128 slots x 64 d] = 16 KB)
-constexpr int PC_Q_NSTAGE = 3;           // consumer pool-chunk ring ([32 slots x 512 d] = 32 KB)
+constexpr int PC_P_NSTAGE = 4;           // producer pool ring: stages of [2 chunks x 128 slots x 64 d]
+constexpr int PC_P_STAGE_BYTES = 32768;
+constexpr int PC_Q_NSTAGE = 2;           // consumer pool ring: same stages (one d block each)
+constexpr int PC_STAGE_BYTES = 65536;    // up to 4 chunks of 16 KB, one 3D TMA box
 constexpr int PC_PBYTES = PC_R * PC_TILE * 2;  // one P tile, bf16 = 32 KB
 
 // producer smem
-constexpr int PCP_OFF_T = 0;                              // 4 x 16 KB
-constexpr int PCP_OFF_PS = PCP_OFF_T + PC_P_NSTAGE * 16384;  // 2 x 32 KB P staging
+constexpr int PCP_OFF_T = 0;                                         // 4 x 32 KB
+constexpr int PCP_OFF_PS = PCP_OFF_T + PC_P_NSTAGE * PC_P_STAGE_BYTES;  // 2 x 32 KB P staging
 constexpr int PCP_OFF_AUX = PCP_OFF_PS + 2 * PC_PBYTES;
 // consumer smem
 constexpr int PCQ_OFF_P = 0;                              // 2 x 32 KB P slots
-constexpr int PCQ_OFF_T = PCQ_OFF_P + 2 * PC_PBYTES;      // 3 x 32 KB pool stages
-constexpr int PCQ_OFF_AUX = PCQ_OFF_T + PC_Q_NSTAGE * 32768;
+constexpr int PCQ_OFF_T = PCQ_OFF_P + 2 * PC_PBYTES;      // 2 x 64 KB pool stages
+constexpr int PCQ_OFF_AUX = PCQ_OFF_T + PC_Q_NSTAGE * PC_STAGE_BYTES;
 constexpr int PC_OFF_AUX = PCP_OFF_AUX > PCQ_OFF_AUX ? PCP_OFF_AUX : PCQ_OFF_AUX;
 constexpr int PC_SMEM_BYTES = PC_OFF_AUX + 4096 + 1024;
 
@@ -118,12 +120,19 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32
         "r"(v[29]), "r"(v[30]), "r"(v[31])
         : "memory");
 }
+__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *m, uint64_t *bar, int x, int y, int z) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(z)
+        : "memory");
+}
 __device__ __forceinline__ void tmem_wait_st() {
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
-    dcp_pc_kernel(const __grid_constant__ CUtensorMap tmT, const __grid_constant__ CUtensorMap tmT32,
+    dcp_pc_kernel(const __grid_constant__ CUtensorMap tm3p, const __grid_constant__ CUtensorMap tm3q,
                   const PCParams p) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -133,7 +142,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
     const int lane = threadIdx.x & 31;
     const uint32_t crank = cluster_ctarank();
     const int d = p.d;
-    const int nchunk = d >> 6;  // 64-wide d chunks
+    const int nchunk = d >> 6;                  // 64-wide d chunks
+    // producer stages: 2 chunks (32 KB); consumer stages: one GEMM-2 d block (2 or 4 chunks)
+    const int cps_p = 2, nstg_p = nchunk / 2;
+    const int cps = (d % 256 == 0) ? 4 : 2;
+    const int nstg = nchunk / cps;
+    const uint32_t stage_bytes = static_cast<uint32_t>(cps) * 16384;
     const int n_pos = *p.n_pos;
     const int n_rg = (n_pos + 1 + PC_R - 1) / PC_R;
     const int n_tiles = (p.n_slots + PC_TILE - 1) / PC_TILE;
@@ -166,7 +180,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
         fence_mbar_init();
     }
     if (warp == 9) {
-        tma_prefetch_desc(crank == 0 ? &tmT : &tmT32);
+        tma_prefetch_desc(&tm3p);
+        tma_prefetch_desc(&tm3q);
         tmem_alloc(&aux->tmem_base, 512);
         tmem_relinquish();
     }
@@ -186,16 +201,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
         uint8_t *sPS = smem + PCP_OFF_PS;
         constexpr uint32_t X_COL = 0, S_COL = 256;  // x_hat (A operand) | two S buffers
         if (warp == 8) {
-            // -------- TMA: pool chunks [128 slots x 64 d]
+            // -------- TMA: pool stages [cps chunks x 128 slots x 64 d] (3D box)
             if (lane == 0) {
                 uint32_t pc = 0;
                 while (sch.next(rg, t0, t1, seg)) {
                     for (int t = t0; t < t1; ++t)
-                        for (int kc = 0; kc < nchunk; ++kc, ++pc) {
+                        for (int g = 0; g < nstg_p; ++g, ++pc) {
                             const uint32_t st = pc % PC_P_NSTAGE, ph = (pc / PC_P_NSTAGE) & 1;
                             mbar_wait(&aux->tempty[st], ph ^ 1);
-                            mbar_arrive_expect_tx(&aux->tfull[st], 16384);
-                            tma_load_2d(sT + st * 16384, &tmT, &aux->tfull[st], kc * 64, t * PC_TILE);
+                            mbar_arrive_expect_tx(&aux->tfull[st], PC_P_STAGE_BYTES);
+                            tma_load_3d(sT + st * PC_P_STAGE_BYTES, &tm3p, &aux->tfull[st], 0, t * PC_TILE, g * cps_p);
                         }
                 }
             }
@@ -209,23 +224,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                     mbar_wait(&aux->xready, sg & 1);
                     tc_fence_after();
                     for (int t = t0; t < t1; ++t, ++jt) {
+                        unsigned long long *dbg = (p.dbg && blockIdx.x == 0 && jt < 64) ? p.dbg + jt * 8 : nullptr;
                         const uint32_t sb = jt & 1, sph = (jt >> 1) & 1;
                         mbar_wait(&aux->sempty[sb], sph ^ 1);
                         tc_fence_after();
+                        if (dbg) dbg[0] = clock64();
                         const uint32_t dcol = tmem + S_COL + sb * PC_TILE;
-                        for (int kc = 0; kc < nchunk; ++kc, ++pc) {
+                        for (int g = 0; g < nstg_p; ++g, ++pc) {
                             const uint32_t st = pc % PC_P_NSTAGE, ph = (pc / PC_P_NSTAGE) & 1;
                             mbar_wait(&aux->tfull[st], ph);
                             tc_fence_after();
 #pragma unroll
-                            for (int k = 0; k < 4; ++k) {
-                                const uint64_t b = umma_desc_sw128(sTa + st * 16384 + k * 32, 16, 1024);
-                                umma_bf16_ts(dcol, tmem + X_COL + kc * 32 + k * 8, b, idesc,
-                                             (kc | k) != 0);
+                            for (int c = 0; c < 2; ++c) {
+                                const int kc = g * 2 + c;
+#pragma unroll
+                                for (int k = 0; k < 4; ++k) {
+                                    const uint64_t b = umma_desc_sw128(
+                                        sTa + st * PC_P_STAGE_BYTES + c * 16384 + k * 32, 16, 1024);
+                                    umma_bf16_ts(dcol, tmem + X_COL + kc * 32 + k * 8, b, idesc,
+                                                 (kc | k) != 0);
+                                }
                             }
                             umma_commit(&aux->tempty[st]);
                         }
                         umma_commit(&aux->sfull[sb]);
+                        if (dbg) dbg[1] = clock64();
                         if (t == t1 - 1) umma_commit(&aux->xfree);
                     }
                     ++sg;
@@ -240,6 +263,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                         const uint32_t b = jt & 1, ph = (jt >> 1) & 1;
                         mbar_wait(&aux->pready[b], ph);
                         mbar_wait(&aux->pslot_free[b], ph ^ 1);
+                        unsigned long long *dbg = (p.dbg && blockIdx.x == 0 && jt < 64) ? p.dbg + jt * 8 : nullptr;
+                        if (dbg) dbg[4] = clock64();
                         const uint32_t dst = mapa_shared(smem_u32(smem + PCQ_OFF_P + b * PC_PBYTES), 1);
                         const uint32_t rbar = mapa_shared(smem_u32(&aux->pfull[b]), 1);
                         asm volatile(
@@ -249,6 +274,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                             : "memory");
                         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                         asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                        if (dbg) dbg[5] = clock64();
                         mbar_arrive(&aux->pstage_free[b]);
                     }
                 }
@@ -290,6 +316,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                     const uint32_t sb = jt & 1, sph = (jt >> 1) & 1;
                     mbar_wait(&aux->sfull[sb], sph);
                     tc_fence_after();
+                    unsigned long long *dbg = (p.dbg && blockIdx.x == 0 && jt < 64 && threadIdx.x == 0) ? p.dbg + jt * 8 : nullptr;
+                    if (dbg) dbg[2] = clock64();
                     float e[64];
                     {
                         float v0[32], v1[32];
@@ -308,8 +336,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                     if (lane == 0) mbar_arrive(&aux->sempty[sb]);
                     const int base = t * PC_TILE + h * 64;
                     const int nval = p.n_slots - base;  // valid slots in my 64-wide half
+                    if (nval >= 64) {
 #pragma unroll
-                    for (int k = 0; k < 64; ++k) e[k] = k < nval ? fmaf(e[k], ab.x, -ab.y) : -INFINITY;
+                        for (int k = 0; k < 64; ++k) e[k] = fmaf(e[k], ab.x, -ab.y);
+                    } else {
+#pragma unroll
+                        for (int k = 0; k < 64; ++k) e[k] = k < nval ? fmaf(e[k], ab.x, -ab.y) : -INFINITY;
+                    }
                     const bool hit = tg >= base && tg < base + 64;
                     if (__any_sync(0xffffffffu, hit)) {
                         if (hit) {
@@ -323,13 +356,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                         }
                     }
                     uint32_t w[32];
+                    float la[4] = {0.f, 0.f, 0.f, 0.f}, ma[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
                     for (int k = 0; k < 64; k += 2) {
                         const float p0 = ex2_approx(e[k]), p1 = ex2_approx(e[k + 1]);
-                        lacc += p0 + p1;
-                        mx = fmaxf(mx, fmaxf(e[k], e[k + 1]));
+                        la[(k >> 1) & 3] += p0 + p1;
+                        ma[(k >> 1) & 3] = fmaxf(ma[(k >> 1) & 3], fmaxf(e[k], e[k + 1]));
                         w[k >> 1] = pack_bf16x2(p0, p1);
                     }
+                    lacc += (la[0] + la[1]) + (la[2] + la[3]);
+                    mx = fmaxf(mx, fmaxf(fmaxf(ma[0], ma[1]), fmaxf(ma[2], ma[3])));
                     // P -> staging buffer in the consumer's K-major SW128 A layout:
                     // chunk h = slots [64h, 64h+64), row r: 128 B, 16-B unit u at u ^ (r & 7)
                     const uint32_t b = jt & 1, ph = (jt >> 1) & 1;
@@ -342,6 +378,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                     fence_proxy_async_smem();
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&aux->pready[b]);
+                    if (dbg) dbg[3] = clock64();
                 }
                 // segment end: l and max over both slot halves
                 aux->red_l[h][r] = lacc;
@@ -361,18 +398,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
         uint8_t *sT = smem + PCQ_OFF_T;
         const int nq = PC_TILE / 32;  // 32-slot pool stages per tile
         if (warp == 8) {
-            // -------- TMA: pool stages [32 slots x d] as d/64 boxes of [32 slots x 64 d]
+            // -------- TMA: pool stages [cps chunks x 128 slots x 64 d] (3D box) = one d block
             if (lane == 0) {
                 uint32_t qc = 0;
                 while (sch.next(rg, t0, t1, seg)) {
                     for (int t = t0; t < t1; ++t)
-                        for (int s = 0; s < nq; ++s, ++qc) {
+                        for (int g = 0; g < nstg; ++g, ++qc) {
                             const uint32_t st = qc % PC_Q_NSTAGE, ph = (qc / PC_Q_NSTAGE) & 1;
                             mbar_wait(&aux->qempty[st], ph ^ 1);
-                            mbar_arrive_expect_tx(&aux->qfull[st], static_cast<uint32_t>(32 * d * 2));
-                            for (int c = 0; c < nchunk; ++c)
-                                tma_load_2d(sT + st * 32768 + c * 4096, &tmT32, &aux->qfull[st], c * 64,
-                                            t * PC_TILE + s * 32);
+                            mbar_arrive_expect_tx(&aux->qfull[st], stage_bytes);
+                            tma_load_3d(sT + st * PC_STAGE_BYTES, &tm3q, &aux->qfull[st], 0, t * PC_TILE, g * cps);
                         }
                 }
             }
@@ -380,40 +415,37 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
             // -------- UMMA issuer: GEMM 2 (A = P K-major, B = pool MN-major, N = 256 d)
             if (lane == 0) {
                 const uint32_t sPa = smem_u32(sP), sTa = smem_u32(sT);
-                const int nblk = (d + 255) >> 8;  // d blocks of <= 256 columns
+                const uint32_t idesc = cps == 4 ? umma_idesc_bf16(128, 256, 0, 1) : umma_idesc_bf16(128, 128, 0, 1);
                 uint32_t qc = 0, jt = 0, sg = 0;
                 while (sch.next(rg, t0, t1, seg)) {
                     for (int t = t0; t < t1; ++t, ++jt) {
                         const bool first = (t == t0);
                         const uint32_t b = jt & 1, ph = (jt >> 1) & 1;
                         mbar_wait(&aux->pfull[b], ph);
+                        unsigned long long *dbg = (p.dbg && blockIdx.x == 1 && jt < 64) ? p.dbg + jt * 8 : nullptr;
+                        if (dbg) dbg[6] = clock64();
                         mbar_arrive_expect_tx(&aux->pfull[b], PC_PBYTES);  // arm the next use
                         tc_fence_after();
                         if (first && sg > 0) {
                             mbar_wait(&aux->oempty, (sg - 1) & 1);
                             tc_fence_after();
                         }
-                        for (int s = 0; s < nq; ++s, ++qc) {
+                        for (int g = 0; g < nstg; ++g, ++qc) {
                             const uint32_t st = qc % PC_Q_NSTAGE, qph = (qc / PC_Q_NSTAGE) & 1;
                             mbar_wait(&aux->qfull[st], qph);
                             tc_fence_after();
 #pragma unroll
-                            for (int kk = 0; kk < 2; ++kk) {
-                                const int ks = s * 2 + kk;  // 16-slot K step within the tile
+                            for (int ks = 0; ks < 8; ++ks) {  // 16-slot K steps over the tile
                                 const uint64_t a = umma_desc_sw128(
                                     sPa + b * PC_PBYTES + (ks >> 2) * 16384 + (ks & 3) * 32, 16, 1024);
-                                for (int bb = 0; bb < nblk; ++bb) {
-                                    const int bN = d - bb * 256 >= 256 ? 256 : d - bb * 256;
-                                    const uint32_t idesc = bN == 256 ? umma_idesc_bf16(128, 256, 0, 1)
-                                                                     : umma_idesc_bf16(128, 128, 0, 1);
-                                    const uint64_t bd = umma_desc_sw128(
-                                        sTa + st * 32768 + bb * 4 * 4096 + kk * 2048, 4096, 1024);
-                                    umma_bf16(tmem + bb * 256, a, bd, idesc, !(first && s == 0 && kk == 0));
-                                }
+                                const uint64_t bd =
+                                    umma_desc_sw128(sTa + st * PC_STAGE_BYTES + ks * 2048, 16384, 1024);
+                                umma_bf16(tmem + g * cps * 64, a, bd, idesc, !(first && ks == 0));
                             }
                             umma_commit(&aux->qempty[st]);
                         }
                         umma_commit_mc(&aux->pslot_free[b], 0x1);  // tell the producer slot b is free
+                        if (dbg) dbg[7] = clock64();
                         if (t == t1 - 1) umma_commit(&aux->ofull);
                     }
                     ++sg;

@@ -162,7 +162,7 @@ struct Rank {
     int64_t lo, hi;
     Layout L;
     uint8_t *base;
-    CUtensorMap tmT, tmX, tmT32;
+    CUtensorMap tmT, tmX, tm3p, tm3q;
     template <typename P>
     P *at(size_t off) const { return reinterpret_cast<P *>(base + off); }
     Scalars *sc() const { return at<Scalars>(L.sc); }
@@ -215,6 +215,22 @@ static int make_tmap_bf16(CUtensorMap *m, void *ptr, int64_t rows, int d, int bo
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(F2C_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return F2C_OK;
+}
+
+// The pool viewed as [d/64 chunks][rows][64] so that one box [64, 128, cps] lands in
+// shared memory chunk-major: cps SW128 blocks of [128 slots x 64 d] (16 KB each).
+static int make_tmap_pool3d(CUtensorMap *m, void *ptr, int64_t rows, int d, cuuint32_t cps) {
+    auto fn = encode_fn();
+    if (!fn) return fail(F2C_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    cuuint64_t dims[3] = {64, static_cast<cuuint64_t>(rows < 1 ? 1 : rows), static_cast<cuuint64_t>(d / 64)};
+    cuuint64_t strides[2] = {static_cast<cuuint64_t>(d) * 2, 128};
+    cuuint32_t box[3] = {64, 128, cps};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, ptr, dims, strides, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(F2C_ECUDA, "cuTensorMapEncodeTiled(3d) failed (%d)", (int)r);
     return F2C_OK;
 }
 
@@ -291,7 +307,8 @@ int f2c_dcp_create(int64_t C, int32_t d, int32_t dtype, int32_t world, int32_t r
         k_hash_clear<<<64, 256>>>(R.at<int64_t>(R.L.hkeys), R.at<unsigned long long>(R.L.hvals), R.L.H);
         if (dtype == F2C_BF16) {
             if ((rc = make_tmap_bf16(&R.tmT, R.base + R.L.T, R.hi - R.lo, d, TP_TILE)) ||
-                (rc = make_tmap_bf16(&R.tmT32, R.base + R.L.T, R.hi - R.lo, d, 32)) ||
+                (rc = make_tmap_pool3d(&R.tm3p, R.base + R.L.T, R.hi - R.lo, d, 2)) ||
+                (rc = make_tmap_pool3d(&R.tm3q, R.base + R.L.T, R.hi - R.lo, d, (d % 256 == 0) ? 4 : 2)) ||
                 (rc = make_tmap_bf16(&R.tmX, R.base + R.L.X_pos, R.L.R_max, d, TP_R))) {
                 delete h;
                 return rc;
@@ -540,7 +557,7 @@ static int phase_main(f2c_dcp *h, Rank &R, const StepCtx &c, int64_t occ_loc) {
         q.seg_mx = p.seg_mx;
         q.seg_O = p.seg_O;
         q.dbg = p.dbg;
-        dcp_pc_kernel<<<(h->G / 2) * 2, PC_THREADS, PC_SMEM_BYTES, c.st>>>(R.tmT, R.tmT32, q);
+        dcp_pc_kernel<<<(h->G / 2) * 2, PC_THREADS, PC_SMEM_BYTES, c.st>>>(R.tm3p, R.tm3q, q);
     }
     LAUNCH_CHECK();
     if (e1) CUDA_TRY(cudaEventRecord(e1, c.st));

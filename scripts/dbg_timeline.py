@@ -26,12 +26,17 @@ head.loss_fwd_bwd(x, y, pr, 64, 0.35)
 torch.cuda.synchronize()
 a = buf.view(64, 8).cpu().numpy().astype(np.int64)
 t0 = a[0, 0]
-print("cols: mma_g1_start g1_issued pfull_done g2_issued | epi_wait_start sfull_done pfull_arrive | prod_lastpair_issue (rel cycles)")
-for j in range(40):
-    r = a[j] - t0
-    print(j, r.tolist(), " tile:", (a[j + 1, 0] - a[j, 0]) if j < 63 else 0)
-d = np.diff(a[:40, 0])
-print("median cycles per tile", np.median(d))
-print("median g1 issue", np.median(a[:40, 1] - a[:40, 0]), "median sfull->pfull(epi)", np.median(a[:40, 6] - a[:40, 5]),
-      "median g1_issued->pfull_done(mma)", np.median(a[:40, 2] - a[:40, 1]), "median g2 issue", np.median(a[:40, 3] - a[:40, 2]),
-      "median epi sfull wait", np.median(a[:40, 5] - a[:40, 4]))
+import os
+if os.environ.get("F2C_KERNEL") == "tp64":
+    for j in range(40):
+        print(j, (a[j] - t0).tolist())
+else:
+    P = a[:, :6] - a[0, 0]; Q = a[:, 6:] - a[0, 6]
+    print("producer cols: g1_start g1_issued sfull_seen pready copy_issue copy_done | consumer: pfull_seen g2_issued")
+    for j in range(24):
+        print(j, P[j].tolist(), Q[j].tolist())
+    n = 40
+    print("producer cadence (g1_start)", np.median(np.diff(a[:n, 0])), "consumer cadence (pfull_seen)", np.median(np.diff(a[:n, 6])))
+    print("g1 issue", np.median(a[:n, 1] - a[:n, 0]), "softmax sfull->pready", np.median(a[:n, 3] - a[:n, 2]),
+          "copy", np.median(a[:n, 5] - a[:n, 4]), "pready->copy issue", np.median(a[:n, 4] - a[:n, 3]),
+          "g2 issue", np.median(a[:n, 7] - a[:n, 6]))
