@@ -76,6 +76,7 @@ struct PCParams {
     float *seg_mx;         // [S][128]
     float *seg_O;          // [S][128][d]
     unsigned long long *dbg;
+    int dbg_flags;         // timing experiments only: 1 = skip P smem writes, 2 = skip DSMEM copy
 };
 
 __device__ __forceinline__ uint32_t cluster_ctarank() {
@@ -98,6 +99,38 @@ __device__ __forceinline__ void umma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, u
         "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
         "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d_tmem),
         "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+// Warp-wide issue helpers: the whole warp runs the issue loop (operands stay in
+// uniform registers) and exactly one elected lane executes the instruction.
+__device__ __forceinline__ void umma_ts_e(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accumulate) {
+    asm volatile(
+        "{\n.reg .pred p, e;\n.reg .b32 r;\nelect.sync r|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void umma_ss_e(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accumulate) {
+    asm volatile(
+        "{\n.reg .pred p, e;\n.reg .b32 r;\nelect.sync r|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void umma_commit_e(uint64_t *bar) {
+    asm volatile(
+        "{\n.reg .pred e;\n.reg .b32 r;\nelect.sync r|e, 0xffffffff;\n"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void umma_commit_mc_e(uint64_t *bar, uint16_t mask) {
+    asm volatile(
+        "{\n.reg .pred e;\n.reg .b32 r;\nelect.sync r|e, 0xffffffff;\n"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n}\n" ::"r"(
+            smem_u32(bar)),
+        "h"(mask)
         : "memory");
 }
 // arrive on the barrier at the same smem offset in every CTA of `mask`
@@ -216,15 +249,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
             }
         } else if (warp == 9) {
             // -------- UMMA issuer: GEMM 1 (A = x_hat from TMEM, B = pool chunk K-major)
-            if (lane == 0) {
+            {  // whole warp; one elected lane issues
                 constexpr uint32_t idesc = umma_idesc_bf16(128, PC_TILE, 0, 0);
-                const uint32_t sTa = smem_u32(sT);
+                // descriptors advance by immediates: the start-address field holds addr >> 4
+                const uint64_t bdesc0 = umma_desc_sw128(smem_u32(sT), 16, 1024);
                 uint32_t pc = 0, jt = 0, sg = 0;
                 while (sch.next(rg, t0, t1, seg)) {
                     mbar_wait(&aux->xready, sg & 1);
                     tc_fence_after();
                     for (int t = t0; t < t1; ++t, ++jt) {
-                        unsigned long long *dbg = (p.dbg && blockIdx.x == 0 && jt < 64) ? p.dbg + jt * 8 : nullptr;
+                        unsigned long long *dbg = (p.dbg && blockIdx.x == 0 && jt < 64 && lane == 0) ? p.dbg + jt * 8 : nullptr;
                         const uint32_t sb = jt & 1, sph = (jt >> 1) & 1;
                         mbar_wait(&aux->sempty[sb], sph ^ 1);
                         tc_fence_after();
@@ -234,22 +268,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                             const uint32_t st = pc % PC_P_NSTAGE, ph = (pc / PC_P_NSTAGE) & 1;
                             mbar_wait(&aux->tfull[st], ph);
                             tc_fence_after();
-#pragma unroll
-                            for (int c = 0; c < 2; ++c) {
-                                const int kc = g * 2 + c;
-#pragma unroll
-                                for (int k = 0; k < 4; ++k) {
-                                    const uint64_t b = umma_desc_sw128(
-                                        sTa + st * PC_P_STAGE_BYTES + c * 16384 + k * 32, 16, 1024);
-                                    umma_bf16_ts(dcol, tmem + X_COL + kc * 32 + k * 8, b, idesc,
-                                                 (kc | k) != 0);
-                                }
+                            const uint64_t bst = bdesc0 + static_cast<uint64_t>(st * (PC_P_STAGE_BYTES >> 4));
+                            const uint32_t ast = tmem + X_COL + g * 64;
+                            if (g == 0) {
+                                umma_ts_e(dcol, ast, bst, idesc, 0);
+                            } else {
+                                umma_ts_e(dcol, ast, bst, idesc, 1);
                             }
-                            umma_commit(&aux->tempty[st]);
+#pragma unroll
+                            for (int i = 1; i < 8; ++i)  // i = c*4 + k: chunk c (16 KB), K step k (32 B)
+                                umma_ts_e(dcol, ast + (i >> 2) * 32 + (i & 3) * 8,
+                                             bst + static_cast<uint64_t>(((i >> 2) * 16384 + (i & 3) * 32) >> 4),
+                                             idesc, 1);
+                            umma_commit_e(&aux->tempty[st]);
                         }
-                        umma_commit(&aux->sfull[sb]);
+                        umma_commit_e(&aux->sfull[sb]);
                         if (dbg) dbg[1] = clock64();
-                        if (t == t1 - 1) umma_commit(&aux->xfree);
+                        if (t == t1 - 1) umma_commit_e(&aux->xfree);
                     }
                     ++sg;
                 }
@@ -267,6 +302,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                         if (dbg) dbg[4] = clock64();
                         const uint32_t dst = mapa_shared(smem_u32(smem + PCQ_OFF_P + b * PC_PBYTES), 1);
                         const uint32_t rbar = mapa_shared(smem_u32(&aux->pfull[b]), 1);
+                        if (p.dbg_flags & 2) {
+                            asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(rbar), "r"(0) : "memory");
+                            asm volatile("mbarrier.complete_tx.shared::cluster.b64 [%0], %1;" :: "r"(rbar), "r"(PC_PBYTES) : "memory");
+                        } else
                         asm volatile(
                             "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes"
                             " [%0], [%1], %2, [%3];" ::"r"(dst),
@@ -371,6 +410,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                     const uint32_t b = jt & 1, ph = (jt >> 1) & 1;
                     mbar_wait(&aux->pstage_free[b], ph ^ 1);
                     const uint32_t rowa = smem_u32(sPS + b * PC_PBYTES + h * 16384 + (r >> 3) * 1024 + (r & 7) * 128);
+                    if (!(p.dbg_flags & 1))
 #pragma unroll
                     for (int u = 0; u < 8; ++u)
                         st_shared_v4(rowa + ((u ^ (r & 7)) << 4), w[4 * u], w[4 * u + 1], w[4 * u + 2],
@@ -413,7 +453,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
             }
         } else if (warp == 9) {
             // -------- UMMA issuer: GEMM 2 (A = P K-major, B = pool MN-major, N = 256 d)
-            if (lane == 0) {
+            {  // whole warp; one elected lane issues
                 const uint32_t sPa = smem_u32(sP), sTa = smem_u32(sT);
                 const uint32_t idesc = cps == 4 ? umma_idesc_bf16(128, 256, 0, 1) : umma_idesc_bf16(128, 128, 0, 1);
                 uint32_t qc = 0, jt = 0, sg = 0;
@@ -422,9 +462,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                         const bool first = (t == t0);
                         const uint32_t b = jt & 1, ph = (jt >> 1) & 1;
                         mbar_wait(&aux->pfull[b], ph);
-                        unsigned long long *dbg = (p.dbg && blockIdx.x == 1 && jt < 64) ? p.dbg + jt * 8 : nullptr;
+                        unsigned long long *dbg = (p.dbg && blockIdx.x == 1 && jt < 64 && lane == 0) ? p.dbg + jt * 8 : nullptr;
                         if (dbg) dbg[6] = clock64();
-                        mbar_arrive_expect_tx(&aux->pfull[b], PC_PBYTES);  // arm the next use
+                        if (lane == 0) mbar_arrive_expect_tx(&aux->pfull[b], PC_PBYTES);  // arm the next use
+                        __syncwarp();
                         tc_fence_after();
                         if (first && sg > 0) {
                             mbar_wait(&aux->oempty, (sg - 1) & 1);
@@ -440,13 +481,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                                     sPa + b * PC_PBYTES + (ks >> 2) * 16384 + (ks & 3) * 32, 16, 1024);
                                 const uint64_t bd =
                                     umma_desc_sw128(sTa + st * PC_STAGE_BYTES + ks * 2048, 16384, 1024);
-                                umma_bf16(tmem + g * cps * 64, a, bd, idesc, !(first && ks == 0));
+                                umma_ss_e(tmem + g * cps * 64, a, bd, idesc, !(first && ks == 0));
                             }
-                            umma_commit(&aux->qempty[st]);
+                            umma_commit_e(&aux->qempty[st]);
                         }
-                        umma_commit_mc(&aux->pslot_free[b], 0x1);  // tell the producer slot b is free
+                        umma_commit_mc_e(&aux->pslot_free[b], 0x1);  // tell the producer slot b is free
                         if (dbg) dbg[7] = clock64();
-                        if (t == t1 - 1) umma_commit(&aux->ofull);
+                        if (t == t1 - 1) umma_commit_e(&aux->ofull);
                     }
                     ++sg;
                 }

@@ -185,7 +185,8 @@ struct f2c_dcp {
     size_t ev_used = 0;
     unsigned long long npos_base = 0;
     unsigned long long *dbg = nullptr;  // debug timestamps (f2c_dcp_debug_timestamps)
-    bool use_tp64 = false;              // F2C_KERNEL=tp64 selects the single-CTA kernel
+    bool use_tp64 = false;
+    int dbg_flags = 0;              // F2C_KERNEL=tp64 selects the single-CTA kernel
     ~f2c_dcp() {
         for (cudaEvent_t e : ev) cudaEventDestroy(e);
     }
@@ -557,6 +558,7 @@ static int phase_main(f2c_dcp *h, Rank &R, const StepCtx &c, int64_t occ_loc) {
         q.seg_mx = p.seg_mx;
         q.seg_O = p.seg_O;
         q.dbg = p.dbg;
+        q.dbg_flags = h->dbg_flags;
         dcp_pc_kernel<<<(h->G / 2) * 2, PC_THREADS, PC_SMEM_BYTES, c.st>>>(R.tm3p, R.tm3q, q);
     }
     LAUNCH_CHECK();
@@ -765,6 +767,8 @@ extern "C" int f2c_dcp_profile_read(f2c_dcp *h, double *main_ms, int64_t *launch
 extern "C" int f2c_dcp_debug_timestamps(f2c_dcp *h, unsigned long long *dev_buf) {
     if (!h) return fail(F2C_EINVAL, "NULL handle");
     h->dbg = dev_buf;
+    const char *fl = getenv("F2C_DBG_FLAGS");
+    h->dbg_flags = fl ? atoi(fl) : 0;
     return F2C_OK;
 }
 

@@ -17,14 +17,16 @@ st = synth.step_inputs(cfg, 0)
 x = torch.from_numpy(st.x.view(np.int16)).view(torch.bfloat16).cuda()
 y = torch.from_numpy(st.y).cuda(); pr = torch.from_numpy(st.pairing).cuda()
 head.enqueue(torch.from_numpy(st.g.view(np.int16)).view(torch.bfloat16).cuda(), torch.from_numpy(st.gy).cuda())
-buf = torch.zeros(64 * 8, dtype=torch.int64, device="cuda")
+buf = torch.zeros(64 * 8 + 64, dtype=torch.int64, device="cuda")
 L.f2c_dcp_debug_timestamps.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
 for it in range(3):
     head.loss_fwd_bwd(x, y, pr, 64, 0.35)
 L.f2c_dcp_debug_timestamps(head._h, ctypes.c_void_p(buf.data_ptr()))
 head.loss_fwd_bwd(x, y, pr, 64, 0.35)
 torch.cuda.synchronize()
-a = buf.view(64, 8).cpu().numpy().astype(np.int64)
+bb = buf.cpu().numpy().astype(np.int64)
+a = bb[:512].reshape(64, 8)
+st = bb[512:].reshape(8, 8)
 t0 = a[0, 0]
 import os
 if os.environ.get("F2C_KERNEL") == "tp64":
@@ -36,6 +38,9 @@ else:
     for j in range(24):
         print(j, P[j].tolist(), Q[j].tolist())
     n = 40
+    for j in range(8):
+        r = st[j] - a[16 + j, 0]
+        print("tile", 16 + j, "stage (wait_start, wait_done) rel g1_start:", r.tolist(), " g1_issued", a[16 + j, 1] - a[16 + j, 0])
     print("producer cadence (g1_start)", np.median(np.diff(a[:n, 0])), "consumer cadence (pfull_seen)", np.median(np.diff(a[:n, 6])))
     print("g1 issue", np.median(a[:n, 1] - a[:n, 0]), "softmax sfull->pready", np.median(a[:n, 3] - a[:n, 2]),
           "copy", np.median(a[:n, 5] - a[:n, 4]), "pready->copy issue", np.median(a[:n, 4] - a[:n, 3]),

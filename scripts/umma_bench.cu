@@ -14,8 +14,9 @@ __device__ __forceinline__ void umma_ts(uint32_t d, uint32_t a_tmem, uint64_t bd
                  :: "r"(d), "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(acc) : "memory");
 }
 
-template <int N, bool TS, int AMN, int BMN>
-__global__ void __launch_bounds__(128, 1) bench(unsigned long long *out, int iters) {
+__device__ volatile int g_stop;
+template <int N, bool TS, int AMN, int BMN, int LDW = 0>
+__global__ void __launch_bounds__(256, 1) bench(unsigned long long *out, int iters) {
     extern __shared__ __align__(1024) uint8_t sm[];
     __shared__ uint64_t bar;
     __shared__ uint32_t tbase;
@@ -23,7 +24,7 @@ __global__ void __launch_bounds__(128, 1) bench(unsigned long long *out, int ite
     const int warp = threadIdx.x >> 5;
     if (warp == 0) { tmem_alloc(&tbase, 512); tmem_relinquish(); }
     if (threadIdx.x == 32) { mbar_init(&bar, 1); fence_mbar_init(); }
-    for (int i = threadIdx.x; i < 196608 / 4; i += 128) reinterpret_cast<uint32_t *>(s)[i] = 0;
+    for (int i = threadIdx.x; i < 196608 / 4; i += 256) reinterpret_cast<uint32_t *>(s)[i] = 0;
     fence_proxy_async_smem();
     tc_fence_before(); __syncthreads(); tc_fence_after();
     const uint32_t tm = tbase;
@@ -46,24 +47,37 @@ __global__ void __launch_bounds__(128, 1) bench(unsigned long long *out, int ite
         mbar_wait(&bar, 0);
         unsigned long long t1 = clock64();
         out[blockIdx.x] = t1 - t0;
+        g_stop = 1;
+    } else if (LDW && warp >= 4 && warp < 4 + LDW) {
+        // concurrent TMEM readers: tcgen05.ld of 32 columns at the S region (cols 384..)
+        float v[32];
+        float acc = 0.f;
+        for (int it = 0; it < iters * 4 && !g_stop; ++it) {
+            tmem_ld32(tm + ((uint32_t)((warp & 3) * 32) << 16) + 384 + (it & 1) * 32, v);
+            tmem_wait_ld();
+            acc += v[it & 31];
+        }
+        if (acc == 12345.f) out[0] = 0;
     }
     tc_fence_before(); __syncthreads(); tc_fence_after();
     if (warp == 0) tmem_dealloc(tm, 512);
 }
 
-template <int N, bool TS, int AMN, int BMN>
+template <int N, bool TS, int AMN, int BMN, int LDW = 0>
 void run(const char *name) {
     const int G = 148, iters = 2048;
     unsigned long long *d;
     cudaMalloc(&d, G * 8);
-    auto k = bench<N, TS, AMN, BMN>;
+    auto k = bench<N, TS, AMN, BMN, LDW>;
+    int zero = 0; cudaMemcpyToSymbol(g_stop, &zero, sizeof(int));
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200000);
-    k<<<G, 128, 200000>>>(d, 64);
+    k<<<G, 256, 200000>>>(d, 64);
     cudaDeviceSynchronize();
+    cudaMemcpyToSymbol(g_stop, &zero, sizeof(int));
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0); cudaEventCreate(&e1);
     cudaEventRecord(e0);
-    k<<<G, 128, 200000>>>(d, iters);
+    k<<<G, 256, 200000>>>(d, iters);
     cudaEventRecord(e1);
     cudaError_t err = cudaDeviceSynchronize();
     float ms; cudaEventElapsedTime(&ms, e0, e1);
@@ -115,27 +129,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1) dsmem_bench(
 }
 
 int main() {
-    {
-        unsigned long long *d; cudaMalloc(&d, 148 * 8);
-        cudaFuncSetAttribute(dsmem_bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 200000);
-        for (int bytes : {16384, 32768}) {
-            const int iters = 2000;
-            dsmem_bench<<<148, 128, 200000>>>(d, iters, bytes);
-            cudaError_t e = cudaDeviceSynchronize();
-            unsigned long long h[148]; cudaMemcpy(h, d, sizeof h, cudaMemcpyDeviceToHost);
-            printf("DSMEM bulk copy %d B chunks: err=%d  %.1f B/cycle (rank0 view)\n", bytes, (int)e, (double)bytes * iters / h[0]);
-        }
-        cudaFree(d);
-    }
-    run<64, false, 0, 0>("SS  N=64  A:K  B:K");
-    run<128, false, 0, 0>("SS  N=128 A:K  B:K");
-    run<256, false, 0, 0>("SS  N=256 A:K  B:K");
-    run<64, false, 1, 1>("SS  N=64  A:MN B:MN");
-    run<256, false, 1, 1>("SS  N=256 A:MN B:MN");
-    run<256, false, 0, 1>("SS  N=256 A:K  B:MN");
-    run<64, true, 0, 0>("TS  N=64  B:K");
     run<128, true, 0, 0>("TS  N=128 B:K");
-    run<256, true, 0, 0>("TS  N=256 B:K");
-    run<256, true, 0, 1>("TS  N=256 B:MN");
+    run<128, true, 0, 0, 1>("TS  N=128 B:K +1 LDTM warp");
+    run<128, true, 0, 0, 4>("TS  N=128 B:K +4 LDTM warps");
+    run<128, false, 0, 0>("SS  N=128");
+    run<128, false, 0, 0, 4>("SS  N=128 +4 LDTM warps");
+    run<256, false, 0, 1>("SS  N=256 A:K B:MN");
+    run<256, false, 0, 1, 4>("SS  N=256 +4 LDTM warps");
     return 0;
 }
