@@ -93,7 +93,7 @@ constexpr int G_MAX = 256;  // upper bound of the persistent grid (SM count)
 struct Layout {
     size_t T, lab, sc, x_all, y_all, pair_all, blk_x, blk_y, inv_n, hslot, hkeys, hvals, tseq,
         comp_idx, pos_row, X_pos, row_ab, row_tgt, ttgt, seg_l, seg_mx, seg_O, rowloss, st_lse,
-        st_cos, st_phi, st_ell, rs_buf, rs_all, dx_part, mu_buf, total;
+        st_cos, st_phi, st_ell, rs_buf, rs_all, dx_part, tseq_ext, dx32, tmax_glob, mu_buf, total;
     int64_t C_loc, N, Mg, R_max, S_max;
     int H;
 };
@@ -147,10 +147,14 @@ static Layout make_layout(int64_t C, int d, int dtype, int W, int rank, int64_t 
     L.st_cos = take(static_cast<size_t>(L.N) * 4);
     L.st_phi = take(static_cast<size_t>(L.N) * 4);
     L.st_ell = take(static_cast<size_t>(L.N) * 4);
-    // multi-rank exchange buffers: per compacted row (l_rest, max, ttgt) + tmax
-    L.rs_buf = take(multi ? static_cast<size_t>(L.R_max) * 4 * 4 : 0);
-    L.rs_all = take(multi ? static_cast<size_t>(W) * L.R_max * 4 * 4 : 0);
+    // multi-rank exchange buffers: per global row 4 floats (C3), the packed (tseq, tmax)
+    // MAX all-reduce buffer (C2), the linear dx share (C4) and its reduce-scatter output
+    L.rs_buf = take(multi ? static_cast<size_t>(L.N) * 16 : 0);
+    L.rs_all = take(multi ? static_cast<size_t>(W) * L.N * 16 : 0);
     L.dx_part = take(multi ? static_cast<size_t>(L.N) * d * 4 : 0);
+    L.tseq_ext = take(multi ? static_cast<size_t>(L.N + 1) * 8 : 0);
+    L.dx32 = take(multi ? static_cast<size_t>(n_loc) * d * 4 : 0);
+    L.tmax_glob = take(64);
     L.mu_buf = take(static_cast<size_t>(d) * 4);
     L.total = align_up(o, 1024);
     return L;
@@ -490,7 +494,7 @@ static int phase_resolve(f2c_dcp *h, Rank &R, const StepCtx &c) {
 }
 
 // a3 split + compaction + gather
-static int phase_compact(f2c_dcp *h, Rank &R, const StepCtx &c) {
+static int phase_compact(f2c_dcp *h, Rank &R, const StepCtx &c, const int *tmax_bits) {
     const Layout &L = R.L;
     CompactArgs a;
     a.tseq = R.at<int64_t>(L.tseq);
@@ -507,6 +511,7 @@ static int phase_compact(f2c_dcp *h, Rank &R, const StepCtx &c) {
     a.row_tgt = R.at<int>(L.row_tgt);
     a.ttgt = R.at<float>(L.ttgt);
     a.sc = R.sc();
+    a.tmax_bits = tmax_bits;
     k_compact<<<1, 1024, 0, c.st>>>(a);
     LAUNCH_CHECK();
     const int row_bytes = h->d * 2;
@@ -573,33 +578,8 @@ static int64_t occ_local(const f2c_dcp *h, const Rank &R) {
     return o < 0 ? 0 : o;
 }
 
-extern "C" int f2c_dcp_loss_fwd_bwd(f2c_dcp *h, const void *x, const int64_t *labels,
-                                    const int32_t *pairing, int64_t n_local, float s, float m,
-                                    float *loss, void *dx, void *stream) {
-    g_launches = 0;
-    if (!h) return fail(F2C_EINVAL, "NULL handle");
-    if (!x || !labels || !loss || !dx) return fail(F2C_EINVAL, "NULL x/labels/loss/dx");
-    if (n_local < 1 || n_local > h->n_local_max)
-        return fail(F2C_ESHAPE, "n_local %lld not in [1, %lld]", (long long)n_local, (long long)h->n_local_max);
-    if (!(s > 0.f) || !isfinite(s) || !isfinite(m)) return fail(F2C_EINVAL, "need s > 0 and finite m");
-    if (x == dx) return fail(F2C_EINVAL, "dx must not alias x");
-    if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(dx)) & 15)
-        return fail(F2C_EINVAL, "x and dx must be 16-byte aligned");
-    if (h->dtype != F2C_BF16)
-        return fail(F2C_EINVAL, "the fp32 loss path is not part of this build (DESIGN.md D21); use bf16");
-    int rc = latched(h, false);
-    if (rc) return rc;
-    cudaStream_t st = static_cast<cudaStream_t>(stream);
-    h->last_stream = st;
-    if (h->W != 1) return fail(F2C_EINVAL, "world > 1 loss path: see multi-rank build");
-    Rank &R = h->ranks[0];
+static CombineArgs combine_args(f2c_dcp *h, Rank &R, const StepCtx &c, int64_t occ, uint8_t *dx) {
     const Layout &L = R.L;
-    StepCtx c{n_local, s, m, static_cast<const uint8_t *>(x), labels, pairing, st};
-    h->last_N = c.N;
-    if ((rc = phase_resolve(h, R, c))) return rc;
-    if ((rc = phase_compact(h, R, c))) return rc;
-    const int64_t occ = occ_local(h, R);
-    if ((rc = phase_main(h, R, c, occ))) return rc;
     CombineArgs a;
     a.x = c.x;
     a.inv_n = R.at<float>(L.inv_n);
@@ -620,14 +600,161 @@ extern "C" int f2c_dcp_loss_fwd_bwd(f2c_dcp *h, const void *x, const int64_t *la
     a.G = h->use_tp64 ? h->G : h->G / 2;
     a.rows_per_group = h->use_tp64 ? TP_R : PC_R;
     a.n_tiles = static_cast<int>((occ + TP_TILE - 1) / TP_TILE);
-    a.s = s;
-    a.margin_l2 = s * m * 1.4426950408889634f;
-    a.dx = static_cast<uint8_t *>(dx);
+    a.s = c.s;
+    a.margin_l2 = c.s * c.m * 1.4426950408889634f;
+    a.dx = dx;
     a.rowloss = R.at<double>(L.rowloss);
     a.st_lse = R.at<float>(L.st_lse);
     a.st_cos = R.at<float>(L.st_cos);
     a.st_phi = R.at<float>(L.st_phi);
     a.st_ell = R.at<float>(L.st_ell);
+    return a;
+}
+
+static unsigned grid_for(int64_t n) {
+    int64_t b = (n + 255) / 256;
+    if (b > 4096) b = 4096;
+    return static_cast<unsigned>(b < 1 ? 1 : b);
+}
+
+// world > 1: slot-range sharding, SURVEY 8(e) / DESIGN.md section 7.
+//   C1 all-gather x, labels, pairing | local resolve | C2 MAX all-reduce (target seq, norm
+//   bound) | compaction + fused kernel on the local shard | local row partials | C3
+//   all-gather of the partials | identical finalisation + linear dx share | C4
+//   reduce-scatter of dx.  Emulated world: the same steps, collectives as device copies.
+static int loss_multi(f2c_dcp *h, const uint8_t *x, const int64_t *labels, const int32_t *pairing,
+                      int64_t n_local, float s, float m, float *loss, uint8_t *dx, cudaStream_t st) {
+    const int W = h->W;
+    const int64_t N = n_local * W;
+    const size_t rb = static_cast<size_t>(h->d) * 2;
+    int rc;
+    h->last_N = N;
+    std::vector<StepCtx> ctx(h->ranks.size());
+    // ---- C1
+    if (h->emulated) {
+        for (size_t q = 0; q < h->ranks.size(); ++q) ctx[q] = StepCtx{N, s, m, x, labels, pairing, st};
+    } else {
+        Rank &R = h->ranks[0];
+        NcclApi &api = nccl();
+        api.GroupStart();
+        api.AllGather(x, R.base + R.L.x_all, n_local * rb, NCCL_INT8, h->comm, st);
+        api.AllGather(labels, R.base + R.L.y_all, n_local, NCCL_INT64, h->comm, st);
+        if (pairing) api.AllGather(pairing, R.base + R.L.pair_all, n_local * 4, NCCL_INT8, h->comm, st);
+        if ((rc = nccl_check(api.GroupEnd(), "C1 all-gather"))) return rc;
+        ctx[0] = StepCtx{N, s, m, R.base + R.L.x_all, R.at<int64_t>(R.L.y_all),
+                         pairing ? R.at<int32_t>(R.L.pair_all) : nullptr, st};
+    }
+    // ---- local resolve, then C2 (MAX of target write index and of the norm bound)
+    for (size_t q = 0; q < h->ranks.size(); ++q) {
+        Rank &R = h->ranks[q];
+        if ((rc = phase_resolve(h, R, ctx[q]))) return rc;
+        k_pack_tseq<<<grid_for(N + 1), 256, 0, st>>>(R.at<int64_t>(R.L.tseq), R.sc(), N, R.at<int64_t>(R.L.tseq_ext));
+        LAUNCH_CHECK();
+    }
+    if (h->emulated) {
+        Rank &R0 = h->ranks[0];
+        for (size_t q = 1; q < h->ranks.size(); ++q) {
+            k_max_i64_into<<<grid_for(N + 1), 256, 0, st>>>(R0.at<int64_t>(R0.L.tseq_ext),
+                                                            h->ranks[q].at<int64_t>(h->ranks[q].L.tseq_ext), N + 1);
+            LAUNCH_CHECK();
+        }
+        for (size_t q = 1; q < h->ranks.size(); ++q)
+            CUDA_TRY(cudaMemcpyAsync(h->ranks[q].at<int64_t>(h->ranks[q].L.tseq_ext), R0.at<int64_t>(R0.L.tseq_ext),
+                                     (N + 1) * 8, cudaMemcpyDeviceToDevice, st));
+    } else {
+        Rank &R = h->ranks[0];
+        if ((rc = nccl_check(nccl().AllReduce(R.at<int64_t>(R.L.tseq_ext), R.at<int64_t>(R.L.tseq_ext), N + 1,
+                                              NCCL_INT64, NCCL_MAX, h->comm, st), "C2 all-reduce")))
+            return rc;
+    }
+    // ---- compaction, fused kernel on the local shard, local row partials
+    for (size_t q = 0; q < h->ranks.size(); ++q) {
+        Rank &R = h->ranks[q];
+        k_unpack_tseq<<<grid_for(N + 1), 256, 0, st>>>(R.at<int64_t>(R.L.tseq_ext), N, R.at<int64_t>(R.L.tseq),
+                                                       R.at<int>(R.L.tmax_glob));
+        LAUNCH_CHECK();
+        if ((rc = phase_compact(h, R, ctx[q], R.at<int>(R.L.tmax_glob)))) return rc;
+        const int64_t occ = occ_local(h, R);
+        if ((rc = phase_main(h, R, ctx[q], occ))) return rc;
+        CombineArgs a = combine_args(h, R, ctx[q], occ, nullptr);
+        k_local_rows<<<static_cast<unsigned>(N), 128, 0, st>>>(a, R.at<float4>(R.L.rs_buf));
+        LAUNCH_CHECK();
+    }
+    // ---- C3: all-gather of the per-row partials
+    if (h->emulated) {
+        for (size_t q = 0; q < h->ranks.size(); ++q)
+            for (size_t r = 0; r < h->ranks.size(); ++r)
+                CUDA_TRY(cudaMemcpyAsync(h->ranks[q].at<float4>(h->ranks[q].L.rs_all) + r * N,
+                                         h->ranks[r].at<float4>(h->ranks[r].L.rs_buf), N * 16,
+                                         cudaMemcpyDeviceToDevice, st));
+    } else {
+        Rank &R = h->ranks[0];
+        if ((rc = nccl_check(nccl().AllGather(R.at<float4>(R.L.rs_buf), R.at<float4>(R.L.rs_all), N * 4, NCCL_FLOAT32,
+                                              h->comm, st), "C3 all-gather")))
+            return rc;
+    }
+    // ---- finalisation (identical on every rank) + linear dx share, then C4
+    for (size_t q = 0; q < h->ranks.size(); ++q) {
+        Rank &R = h->ranks[q];
+        CombineArgs a = combine_args(h, R, ctx[q], occ_local(h, R), nullptr);
+        k_finalize_multi<<<static_cast<unsigned>(N), 128, 0, st>>>(a, R.at<float4>(R.L.rs_all), W, N,
+                                                                   R.at<float>(R.L.dx_part));
+        LAUNCH_CHECK();
+        k_loss<<<1, 1024, 0, st>>>(R.at<double>(R.L.rowloss), R.at<int>(R.L.comp_idx), N, R.sc(), loss,
+                                   R.at<int64_t>(R.L.hkeys), R.at<unsigned long long>(R.L.hvals), R.L.H);
+        LAUNCH_CHECK();
+    }
+    if (h->emulated) {
+        Rank &R0 = h->ranks[0];
+        for (size_t q = 1; q < h->ranks.size(); ++q) {
+            k_add_f32_into<<<grid_for(N * h->d), 256, 0, st>>>(R0.at<float>(R0.L.dx_part),
+                                                               h->ranks[q].at<float>(h->ranks[q].L.dx_part), N * h->d);
+            LAUNCH_CHECK();
+        }
+        k_cast_bf16<<<grid_for(N * h->d), 256, 0, st>>>(R0.at<float>(R0.L.dx_part), reinterpret_cast<__nv_bfloat16 *>(dx),
+                                                        N * h->d);
+        LAUNCH_CHECK();
+    } else {
+        Rank &R = h->ranks[0];
+        if ((rc = nccl_check(nccl().ReduceScatter(R.at<float>(R.L.dx_part), R.at<float>(R.L.dx32), n_local * h->d,
+                                                  NCCL_FLOAT32, NCCL_SUM, h->comm, st), "C4 reduce-scatter")))
+            return rc;
+        k_cast_bf16<<<grid_for(n_local * h->d), 256, 0, st>>>(R.at<float>(R.L.dx32), reinterpret_cast<__nv_bfloat16 *>(dx),
+                                                              n_local * h->d);
+        LAUNCH_CHECK();
+    }
+    return F2C_OK;
+}
+
+extern "C" int f2c_dcp_loss_fwd_bwd(f2c_dcp *h, const void *x, const int64_t *labels,
+                                    const int32_t *pairing, int64_t n_local, float s, float m,
+                                    float *loss, void *dx, void *stream) {
+    g_launches = 0;
+    if (!h) return fail(F2C_EINVAL, "NULL handle");
+    if (!x || !labels || !loss || !dx) return fail(F2C_EINVAL, "NULL x/labels/loss/dx");
+    if (n_local < 1 || n_local > h->n_local_max)
+        return fail(F2C_ESHAPE, "n_local %lld not in [1, %lld]", (long long)n_local, (long long)h->n_local_max);
+    if (!(s > 0.f) || !isfinite(s) || !isfinite(m)) return fail(F2C_EINVAL, "need s > 0 and finite m");
+    if (x == dx) return fail(F2C_EINVAL, "dx must not alias x");
+    if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(dx)) & 15)
+        return fail(F2C_EINVAL, "x and dx must be 16-byte aligned");
+    if (h->dtype != F2C_BF16)
+        return fail(F2C_EINVAL, "the fp32 loss path is not part of this build (DESIGN.md D21); use bf16");
+    int rc = latched(h, false);
+    if (rc) return rc;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    h->last_stream = st;
+    if (h->W != 1) return loss_multi(h, static_cast<const uint8_t *>(x), labels, pairing, n_local, s, m, loss,
+                                     static_cast<uint8_t *>(dx), st);
+    Rank &R = h->ranks[0];
+    const Layout &L = R.L;
+    StepCtx c{n_local, s, m, static_cast<const uint8_t *>(x), labels, pairing, st};
+    h->last_N = c.N;
+    if ((rc = phase_resolve(h, R, c))) return rc;
+    if ((rc = phase_compact(h, R, c, &R.sc()->tmax_bits))) return rc;
+    const int64_t occ = occ_local(h, R);
+    if ((rc = phase_main(h, R, c, occ))) return rc;
+    CombineArgs a = combine_args(h, R, c, occ, static_cast<uint8_t *>(dx));
     k_combine<__nv_bfloat16><<<static_cast<unsigned>(c.N), 128, 0, st>>>(a);
     LAUNCH_CHECK();
     k_loss<<<1, 1024, 0, st>>>(R.at<double>(L.rowloss), R.at<int>(L.comp_idx), c.N, R.sc(), loss,

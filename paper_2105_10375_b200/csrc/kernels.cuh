@@ -266,6 +266,7 @@ struct CompactArgs {
     int *row_tgt;             // [R_max]
     float *ttgt;              // [R_max]
     Scalars *sc;
+    const int *tmax_bits;     // max ||T_c|| over the whole pool (all shards)
     float ref_scale;          // s*log2(e)*(1+2^-10): reference exponent per unit norm
 };
 __global__ void __launch_bounds__(1024) k_compact(CompactArgs a) {
@@ -297,7 +298,7 @@ __global__ void __launch_bounds__(1024) k_compact(CompactArgs a) {
     __syncthreads();
     int k = (w > 0 ? wsum[w - 1] : 0) + v - cnt;
     const int n_pos = wsum[31];
-    const float tmax = __int_as_float(a.sc->tmax_bits);
+    const float tmax = __int_as_float(*a.tmax_bits);
     const float B = a.ref_scale * tmax;
     for (int64_t i = r0; i < r1; ++i) {
         const int64_t ts = a.tseq[i];
@@ -481,6 +482,153 @@ __global__ void __launch_bounds__(128) k_combine(CombineArgs a) {
         if (dd < a.d) dxr[dd] = from_f<TX>((g[j] - gd * xh[j]) * inv);
     }
     if (threadIdx.x == 0) a.rowloss[i] = row_loss;
+}
+
+// ------------------------------------------------------------------ multi-rank combine
+// Per global row i, this rank's partial of the softmax statistics over its slot shard:
+//   in-pool rows:     (l_rest_r, max_r, ttgt_r, 0)   (ttgt_r = -inf unless rank r owns t_i)
+//   out-of-pool rows: (phi_r, 0, 0, 0)               phi_r = x_hat_i . mu_r / C_occ
+// These are all-gathered (C3); every rank then finalises identically (k_finalize_multi).
+__global__ void __launch_bounds__(128) k_local_rows(CombineArgs a, float4 *__restrict__ scal) {
+    __shared__ float red[4];
+    const int64_t i = blockIdx.x;
+    const int n_pos = a.sc->n_pos;
+    const int n_rg = (n_pos + 1 + a.rows_per_group - 1) / a.rows_per_group;
+    const int k = a.comp_idx[i];
+    if (k >= 0) {
+        float o[4], lsum, mx;
+        gather_row_partials(a, n_rg, k, o, lsum, mx);  // (o unused here)
+        if (threadIdx.x == 0) scal[i] = make_float4(lsum, mx, a.ttgt[k], 0.f);
+    } else {
+        float mu[4], lsum, mx;
+        gather_row_partials(a, n_rg, n_pos, mu, lsum, mx);
+        const __nv_bfloat16 *xr = reinterpret_cast<const __nv_bfloat16 *>(a.x) + i * a.d;
+        const float inv = a.inv_n[i];
+        float dot = 0.f;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int dd = threadIdx.x + 128 * j;
+            if (dd < a.d) dot += __bfloat162float(xr[dd]) * inv * mu[j];
+        }
+        dot = block_sum_128(dot, red);
+        if (threadIdx.x == 0) scal[i] = make_float4(a.C_occ > 0 ? dot / static_cast<float>(a.C_occ) : 0.f, 0.f, 0.f, 0.f);
+    }
+}
+
+// Global finalisation from the gathered partials (rank order => deterministic), and this
+// rank's LINEAR share of dL/dx (projection applied), summed over ranks by the
+// reduce-scatter (C4):
+//   in-pool:     g_r = (s/N_pos) (O_r / l - [r owns t] (l_rest / l) T_t)
+//   out-of-pool: g_r = mu_r / (N_neg C_occ)
+__global__ void __launch_bounds__(128) k_finalize_multi(CombineArgs a, const float4 *__restrict__ scal_all,
+                                                        int W, int64_t N, float *__restrict__ dx_part) {
+    __shared__ float red[4];
+    const int64_t i = blockIdx.x;
+    const int n_pos = a.sc->n_pos, n_neg = a.sc->n_neg;
+    const int n_rg = (n_pos + 1 + a.rows_per_group - 1) / a.rows_per_group;
+    const int k = a.comp_idx[i];
+    const __nv_bfloat16 *xr = reinterpret_cast<const __nv_bfloat16 *>(a.x) + i * a.d;
+    const float inv = a.inv_n[i];
+    float xh[4], g[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int dd = threadIdx.x + 128 * j;
+        xh[j] = dd < a.d ? __bfloat162float(xr[dd]) * inv : 0.f;
+    }
+    double row_loss = 0.0;
+    if (k >= 0) {
+        double lr = 0.0;
+        float mx = -INFINITY, tt = -INFINITY;
+        for (int r = 0; r < W; ++r) {
+            const float4 v = scal_all[static_cast<int64_t>(r) * N + i];
+            lr += static_cast<double>(v.x);
+            mx = fmaxf(mx, v.y);
+            tt = fmaxf(tt, v.z);
+        }
+        float o[4], lsum, mxl;
+        gather_row_partials(a, n_rg, k, o, lsum, mxl);
+        const double l = lr + exp2(static_cast<double>(tt));
+        const double w = static_cast<double>(a.s) / static_cast<double>(n_pos);
+        const int ts = a.row_tgt[k];  // >= 0 iff this rank owns the target slot
+        const float alpha = static_cast<float>(w / l);
+        const float beta = ts >= 0 ? static_cast<float>(w * (lr / l)) : 0.f;
+        const __nv_bfloat16 *Tt = reinterpret_cast<const __nv_bfloat16 *>(a.T) + static_cast<int64_t>(ts < 0 ? 0 : ts) * a.d;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int dd = threadIdx.x + 128 * j;
+            g[j] = dd < a.d ? alpha * o[j] - beta * __bfloat162float(Tt[dd]) : 0.f;
+        }
+        const double ell = log1p(lr * exp2(-static_cast<double>(tt)));
+        row_loss = ell;
+        if (threadIdx.x == 0) {
+            const float2 ab = a.row_ab[k];
+            a.st_ell[i] = static_cast<float>(ell);
+            a.st_lse[i] = static_cast<float>((static_cast<double>(ab.y) + log2(l)) * 0.6931471805599453);
+            a.st_cos[i] = static_cast<float>((static_cast<double>(tt) + a.margin_l2 + ab.y) / (a.s * 1.4426950408889634));
+            a.st_phi[i] = 0.f;
+            if (!(l > 0.0) || !isfinite(ell) || (mx < -100.f && tt - mx < 64.f))
+                latch(a.sc_w, ERR_DEVICE, !isfinite(ell) ? DET_NONFINITE : DET_UNDERFLOW);
+        }
+    } else {
+        float mu[4], lsum, mxl;
+        gather_row_partials(a, n_rg, n_pos, mu, lsum, mxl);
+        const float w = (a.C_occ > 0 && n_neg > 0) ? 1.0f / (static_cast<float>(n_neg) * static_cast<float>(a.C_occ)) : 0.f;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) g[j] = w * mu[j];
+        double phi = 0.0;
+        for (int r = 0; r < W; ++r) phi += static_cast<double>(scal_all[static_cast<int64_t>(r) * N + i].x);
+        row_loss = phi;
+        if (threadIdx.x == 0) {
+            a.st_phi[i] = static_cast<float>(phi);
+            a.st_ell[i] = 0.f;
+            a.st_lse[i] = 0.f;
+            a.st_cos[i] = 0.f;
+        }
+    }
+    float gd = 0.f;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) gd += g[j] * xh[j];
+    gd = block_sum_128(gd, red);
+    float *dst = dx_part + i * a.d;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int dd = threadIdx.x + 128 * j;
+        if (dd < a.d) dst[dd] = (g[j] - gd * xh[j]) * inv;
+    }
+    if (threadIdx.x == 0) a.rowloss[i] = row_loss;
+}
+
+__global__ void k_cast_bf16(const float *__restrict__ src, __nv_bfloat16 *__restrict__ dst, int64_t n) {
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        dst[i] = __float2bfloat16_rn(src[i]);
+}
+
+// emulated-world collectives (one device): fixed rank order
+__global__ void k_max_i64_into(int64_t *__restrict__ acc, const int64_t *__restrict__ src, int64_t n) {
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        if (src[i] > acc[i]) acc[i] = src[i];
+}
+__global__ void k_add_f32_into(float *__restrict__ acc, const float *__restrict__ src, int64_t n) {
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        acc[i] += src[i];
+}
+// pack (tseq, tmax bits) for the MAX all-reduce (C2)
+__global__ void k_pack_tseq(const int64_t *__restrict__ tseq, const Scalars *__restrict__ sc, int64_t N,
+                            int64_t *__restrict__ ext) {
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i <= N;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        ext[i] = i < N ? tseq[i] : static_cast<int64_t>(sc->tmax_bits);
+}
+__global__ void k_unpack_tseq(const int64_t *__restrict__ ext, int64_t N, int64_t *__restrict__ tseq,
+                              int *__restrict__ tmax_glob) {
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i <= N;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        if (i < N) tseq[i] = ext[i];
+        else *tmax_glob = static_cast<int>(ext[N]);
+    }
 }
 
 // ------------------------------------------------------------------ a6: loss reduction
