@@ -104,7 +104,7 @@ def run_reference(args, cfg, world):
     probe = oracle_sample_time(cfg, world, C_s, 2)
     per_row = max(probe["t_rows"] / 2, 1e-6)
     C_s = int(min(cfg.C, max(4096, C_s * budget / max(probe["wall"], 1e-3) / 2)))
-    C_s = max(4096, min(C_s, cfg.C))
+    C_s = max(4096, min(C_s, cfg.C, 262144))
     times = []
     for i in range(W + K):
         r = oracle_sample_time(cfg, world, C_s, 2, step=i % 4)
@@ -179,7 +179,7 @@ class Clocks:
 
 
 # --------------------------------------------------------------------------- GPU arm
-def run_ours(args, cfg, world, rank, local_rank):
+def run_ours(args, cfg, world, rank, local_rank, device_only=False):
     import torch
     import torch.distributed as dist
     import paper_2105_10375_b200 as dcp
@@ -189,12 +189,11 @@ def run_ours(args, cfg, world, rank, local_rank):
     M, N_loc, d = cfg.M_loc, cfg.N_loc(), cfg.d
     uid = None
     if world > 1:
-        import ctypes
+        # the library's NCCL communicator is bootstrapped from a unique id made by rank 0
+        # and broadcast over the torch process group (torch only for plumbing)
         if rank == 0:
-            nccl_lib = ctypes.CDLL("libnccl.so.2")
-            buf = ctypes.create_string_buffer(128)
-            assert nccl_lib.ncclGetUniqueId(buf) == 0
-            t = torch.tensor(list(buf.raw), dtype=torch.uint8, device=dev)
+            raw = bytes(torch.cuda.nccl.unique_id())
+            t = torch.tensor(list(raw), dtype=torch.uint8, device=dev)
         else:
             t = torch.zeros(128, dtype=torch.uint8, device=dev)
         dist.broadcast(t, 0)
@@ -279,6 +278,21 @@ def run_ours(args, cfg, world, rank, local_rank):
     head.check()
     value = K * N_loc * world / (ms / 1e3)
 
+    if device_only:
+        if rank != 0:
+            return None
+        pk = _peaks()
+        C_loc = cfg.C // world
+        npos_avg = npos_sum / max(1, main_n)
+        t_launch = main_ms / max(1, main_n) / 1e3
+        achieved = 4.0 * npos_avg * C_loc * d / t_launch / 1e12
+        peak = pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
+        head.close()
+        return {"workload": cfg.name, "value": value, "unit": UNIT, "ms_per_step": ms / K,
+                "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                             "frac": achieved / peak, "avg_launch_ms": t_launch * 1e3, "N_pos_avg": npos_avg},
+                "clocks": clocks, "config": _config(cfg, world)}
+
     # ---- end-to-end through the public API with host buffers (e2e)
     loss_host = torch.zeros((), dtype=torch.float32).pin_memory()
     bufs = tuple(torch.empty_like(a) for a in devin[0])
@@ -296,7 +310,8 @@ def run_ours(args, cfg, world, rank, local_rank):
     value_e2e = K * N_loc * world / (ms_e2e / 1e3)
 
     if rank != 0:
-        return
+        head.close()
+        return None
     pk = _peaks()
     C_loc = cfg.C // world
     npos_avg = npos_sum / max(1, main_n)
@@ -304,7 +319,7 @@ def run_ours(args, cfg, world, rank, local_rank):
     t_launch = main_ms / max(1, main_n) / 1e3
     achieved = flops_alg / t_launch / 1e12
     peak = pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
-    rows_exec = math.ceil((npos_avg + 1) / 64) * 64
+    rows_exec = math.ceil((npos_avg + 1) / 128) * 128   # 128-row groups (TMEM lanes)
     flops_exec = 4.0 * rows_exec * C_loc * d
     traffic = None
     prof_file = os.path.join(ROOT, "profiles", f"ncu_main_{cfg.name}.json")
@@ -319,7 +334,7 @@ def run_ours(args, cfg, world, rank, local_rank):
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic", "config": _config(cfg, world),
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": "dcp_tp64_kernel (fused logits GEMM + softmax + pool-sum GEMM)",
+                     "kernel": "dcp_pc_kernel (producer: TMEM-A logits GEMM + softmax -> DSMEM P; consumer: P x pool GEMM, O in TMEM)",
                      "algorithmic_flops_per_launch": flops_alg,
                      "executed_mma_flops_per_launch": flops_exec,
                      "tensor_pipe_frac": flops_exec / t_launch / 1e12 / peak,
@@ -333,18 +348,20 @@ def run_ours(args, cfg, world, rank, local_rank):
     }
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(cfg, world)
-    print(json.dumps(line), flush=True)
+    return line
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c3", choices=["c1", "c2", "c3"])
     ap.add_argument("--ring", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--also", default="c2", help="extra single-GPU workloads measured device-resident "
+                    "(the north-star 1M-slot config c2 by default); '' to skip")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -359,7 +376,15 @@ def main():
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    run_ours(args, cfg, world, rank, local_rank)
+    line = run_ours(args, cfg, world, rank, local_rank)
+    extras = [w for w in args.also.split(",") if w and w != args.workload] if world == 1 else []
+    if extras:
+        import torch
+        torch.cuda.empty_cache()
+        line["also"] = [run_ours(args, synth.CONFIGS[w], world, rank, local_rank, device_only=True)
+                        for w in extras]
+    if rank == 0 and line is not None:
+        print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()

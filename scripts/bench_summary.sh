@@ -1,7 +1,7 @@
 #!/bin/bash
 # usage: scripts/bench_summary.sh <workload> [extra bench args]
 w=$1; shift
-timeout 400 python bench.py --workload $w --steps 10 --warmup 3 --no-cpu-baseline "$@" 2>&1 | python -c "
+timeout 400 python bench.py --workload $w --steps 10 --warmup 3 --no-cpu-baseline --also "" "$@" 2>&1 | python -c "
 import json,sys
 lines=sys.stdin.read().strip().splitlines()
 try:
