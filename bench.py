@@ -351,6 +351,49 @@ def run_ours(args, cfg, world, rank, local_rank, device_only=False):
     return line
 
 
+def kernel_bench(args):
+    """HBM-bound kernels in isolation (SURVEY 8(d) 'enqueue and EMA evidence'): the
+    enqueue of a 262,144-row bf16 block (256 MB in, 256 MB out) into a 4M-slot pool, and
+    the G-Net EMA over 65M fp32 parameters (780 MB).  CUDA events, best of 10 after warm-up."""
+    import torch
+    import paper_2105_10375_b200 as dcp
+    pk = _peaks()
+    dev = torch.device("cuda", 0)
+    out = {}
+    M, C, d = 262_144, 4_194_304, 512
+    head = dcp.DCPHead(C, d, dcp.BF16, 1, 0, n_local_max=8, m_local_max=M, device=dev)
+    g = torch.randn(M, d, device=dev).bfloat16()
+    y = torch.arange(M, device=dev, dtype=torch.int64)
+    ts = []
+    for i in range(13):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        head.enqueue(g, y)
+        e1.record()
+        torch.cuda.synchronize()
+        if i >= 3:
+            ts.append(e0.elapsed_time(e1))
+    byt = M * d * 2 * 2 + M * 8 * 2
+    out["enqueue"] = {"rows": M, "bytes": byt, "best_ms": min(ts), "GBps": byt / (min(ts) * 1e-3) / 1e9,
+                      "frac_of_measured_copy": byt / (min(ts) * 1e-3) / 1e9 / pk["hbm_gbs"]}
+    del head
+    p = torch.randn(EMA_PARAMS, device=dev) * 0.05
+    gq = torch.randn(EMA_PARAMS, device=dev) * 0.05
+    ts = []
+    for i in range(13):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        dcp.gnet_ema(p, gq, 0.999)
+        e1.record()
+        torch.cuda.synchronize()
+        if i >= 3:
+            ts.append(e0.elapsed_time(e1))
+    byt = EMA_PARAMS * 4 * 3
+    out["ema"] = {"params": EMA_PARAMS, "bytes": byt, "best_ms": min(ts), "GBps": byt / (min(ts) * 1e-3) / 1e9,
+                  "frac_of_measured_copy": byt / (min(ts) * 1e-3) / 1e9 / pk["hbm_gbs"]}
+    print(json.dumps({"kernel_bench": out, "peak_hbm_GBps": pk["hbm_gbs"]}), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -360,6 +403,7 @@ def main():
     ap.add_argument("--workload", default="c3", choices=["c1", "c2", "c3"])
     ap.add_argument("--ring", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--kernel-bench", action="store_true", help="HBM-bound kernels alone (enqueue, EMA)")
     ap.add_argument("--also", default="c2", help="extra single-GPU workloads measured device-resident "
                     "(the north-star 1M-slot config c2 by default); '' to skip")
     args = ap.parse_args()
@@ -367,6 +411,9 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     cfg = synth.CONFIGS[args.workload]
+    if args.kernel_bench:
+        kernel_bench(args)
+        return
     if args.impl == "reference":
         if rank == 0:
             run_reference(args, cfg, world)

@@ -375,8 +375,9 @@ static int nccl_check(int r, const char *what) {
 static int enqueue_rank(f2c_dcp *h, Rank &R, const uint8_t *g, const int64_t *y, int64_t m_glob,
                         cudaStream_t st) {
     const int row_bytes = h->d * (h->dtype == F2C_BF16 ? 2 : 4);
-    const int64_t threads = m_glob * 32;
-    k_enqueue<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, st>>>(
+    int64_t blocks = (m_glob + 7) / 8;                 // 8 rows (warps) per block per pass
+    if (blocks > static_cast<int64_t>(h->G) * 8) blocks = static_cast<int64_t>(h->G) * 8;
+    k_enqueue<<<static_cast<unsigned>(blocks), 256, 0, st>>>(
         g, y, m_glob, h->E, h->C, R.lo, R.hi, row_bytes, h->dtype, R.base + R.L.T,
         R.at<int64_t>(R.L.lab), R.sc());
     LAUNCH_CHECK();
@@ -516,7 +517,8 @@ static int phase_compact(f2c_dcp *h, Rank &R, const StepCtx &c, const int *tmax_
     LAUNCH_CHECK();
     const int row_bytes = h->d * 2;
     k_gather<<<static_cast<unsigned>(c.N), 64, 0, c.st>>>(c.x, R.at<int>(L.pos_row), R.sc(), row_bytes,
-                                                          R.base + L.X_pos);
+                                                          R.base + L.X_pos, R.base + L.T, R.at<int>(L.row_tgt),
+                                                          R.at<float2>(L.row_ab));
     LAUNCH_CHECK();
     return F2C_OK;
 }

@@ -61,49 +61,66 @@ __device__ __forceinline__ float from_f<float>(float v) { return v; }
 // One warp per block row; the rows owned by this shard [lo, hi) are copied with
 // 16-byte vector loads/stores (bit-exact), labels written by lane 0, and the running
 // max row norm (the softmax reference bound) updated.
-__global__ void k_enqueue(const uint8_t *__restrict__ g, const int64_t *__restrict__ y,
-                          int64_t m_glob, int64_t E, int64_t C, int64_t lo, int64_t hi,
-                          int row_bytes, int dtype, uint8_t *__restrict__ T, int64_t *__restrict__ lab,
-                          Scalars *sc) {
-    const int64_t j = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (j >= m_glob) return;
-    const int64_t c = (E + j) % C;
-    if (c < lo || c >= hi) return;
-    const int64_t yl = y[j];
-    if (yl < 0) {
-        if (lane == 0) latch(sc, ERR_DEVICE, DET_BAD_LABEL);
-        return;
-    }
-    const int4 *src = reinterpret_cast<const int4 *>(g + j * row_bytes);
-    int4 *dst = reinterpret_cast<int4 *>(T + (c - lo) * row_bytes);
-    float ss = 0.f;
-    for (int u = lane; u < row_bytes / 16; u += 32) {
-        int4 v = __ldcs(src + u);
-        dst[u] = v;
-        const uint32_t w[4] = {static_cast<uint32_t>(v.x), static_cast<uint32_t>(v.y),
-                               static_cast<uint32_t>(v.z), static_cast<uint32_t>(v.w)};
-        if (dtype == 0) {
+__global__ void __launch_bounds__(256) k_enqueue(const uint8_t *__restrict__ g, const int64_t *__restrict__ y,
+                                                 int64_t m_glob, int64_t E, int64_t C, int64_t lo, int64_t hi,
+                                                 int row_bytes, int dtype, uint8_t *__restrict__ T,
+                                                 int64_t *__restrict__ lab, Scalars *sc) {
+    __shared__ float wmax[8];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+    float nmax = 0.f;
+    for (int64_t j = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + wib; j < m_glob; j += nwarps) {
+        const int64_t c = (E + j) % C;
+        if (c < lo || c >= hi) continue;
+        const int64_t yl = y[j];
+        if (yl < 0) {
+            if (lane == 0) latch(sc, ERR_DEVICE, DET_BAD_LABEL);
+            continue;
+        }
+        const int4 *src = reinterpret_cast<const int4 *>(g + j * row_bytes);
+        int4 *dst = reinterpret_cast<int4 *>(T + (c - lo) * row_bytes);
+        const int nvec = row_bytes / 16;
+        float ss = 0.f;
+        for (int u0 = 0; u0 < nvec; u0 += 64) {  // 2 independent 16-B loads in flight per lane
+            int4 v[2];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                float a = __uint_as_float(w[i] << 16), b = __uint_as_float(w[i] & 0xffff0000u);
-                ss += a * a + b * b;
+            for (int q = 0; q < 2; ++q) {
+                const int u = u0 + q * 32 + lane;
+                if (u < nvec) v[q] = __ldcs(src + u);
             }
-        } else {
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                float a = __uint_as_float(w[i]);
-                ss += a * a;
+            for (int q = 0; q < 2; ++q) {
+                const int u = u0 + q * 32 + lane;
+                if (u >= nvec) continue;
+                __stcs(dst + u, v[q]);
+                const uint32_t w[4] = {static_cast<uint32_t>(v[q].x), static_cast<uint32_t>(v[q].y),
+                                       static_cast<uint32_t>(v[q].z), static_cast<uint32_t>(v[q].w)};
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    if (dtype == 0) {
+                        const float a = __uint_as_float(w[i] << 16), b = __uint_as_float(w[i] & 0xffff0000u);
+                        ss += a * a + b * b;
+                    } else {
+                        const float a = __uint_as_float(w[i]);
+                        ss += a * a;
+                    }
+                }
             }
         }
-    }
 #pragma unroll
-    for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-    if (lane == 0) {
-        lab[c - lo] = yl;
-        float nrm = sqrtf(ss);
+        for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+        if (lane == 0) lab[c - lo] = yl;
+        nmax = fmaxf(nmax, ss);
+    }
+    // one atomic per block for the running norm bound (the softmax reference, R1)
+    if (lane == 0) wmax[wib] = nmax;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float mx = 0.f;
+        for (int i = 0; i < (blockDim.x >> 5); ++i) mx = fmaxf(mx, wmax[i]);
+        float nrm = sqrtf(mx);
         if (!(nrm <= 3.0e38f)) nrm = 3.0e38f;
-        atomicMax(&sc->tmax_bits, __float_as_int(nrm));
+        if (nrm > 0.f) atomicMax(&sc->tmax_bits, __float_as_int(nrm));
     }
 }
 
@@ -331,14 +348,49 @@ __global__ void __launch_bounds__(1024) k_compact(CompactArgs a) {
     }
 }
 
-// gather the in-pool rows into the dense, 64-row-group-aligned bf16 operand X_pos
-__global__ void k_gather(const uint8_t *__restrict__ x, const int *__restrict__ pos_row,
-                         const Scalars *__restrict__ sc, int row_bytes, uint8_t *__restrict__ Xp) {
+// Gather the in-pool rows into the dense bf16 operand X_pos, and set the row's softmax
+// reference (R1): b_r = max(z_t, bound - 100) in log2 units, where z_t = a_r <x_r, T_t>
+// is the unmargined target logit (computed by the shard that owns the target slot; other
+// shards keep bound - 100).  Every exponent is then <= 100 (no overflow of p or O), and
+// the dominant terms stay representable for any |cos| <= 1 at s <= 76.
+__global__ void __launch_bounds__(64) k_gather(const uint8_t *__restrict__ x, const int *__restrict__ pos_row,
+                                               const Scalars *__restrict__ sc, int row_bytes,
+                                               uint8_t *__restrict__ Xp, const uint8_t *__restrict__ T,
+                                               const int *__restrict__ row_tgt, float2 *__restrict__ row_ab) {
+    __shared__ float red[2];
     const int k = blockIdx.x;
     if (k >= sc->n_pos) return;
     const int4 *src = reinterpret_cast<const int4 *>(x + static_cast<int64_t>(pos_row[k]) * row_bytes);
     int4 *dst = reinterpret_cast<int4 *>(Xp + static_cast<int64_t>(k) * row_bytes);
-    for (int u = threadIdx.x; u < row_bytes / 16; u += blockDim.x) dst[u] = src[u];
+    const int ts = row_tgt[k];
+    const int4 *tr = reinterpret_cast<const int4 *>(T + static_cast<int64_t>(ts < 0 ? 0 : ts) * row_bytes);
+    float dot = 0.f;
+    for (int u = threadIdx.x; u < row_bytes / 16; u += blockDim.x) {
+        const int4 v = src[u];
+        dst[u] = v;
+        if (ts >= 0) {
+            const int4 w = tr[u];
+            const uint32_t a[4] = {static_cast<uint32_t>(v.x), static_cast<uint32_t>(v.y),
+                                   static_cast<uint32_t>(v.z), static_cast<uint32_t>(v.w)};
+            const uint32_t b[4] = {static_cast<uint32_t>(w.x), static_cast<uint32_t>(w.y),
+                                   static_cast<uint32_t>(w.z), static_cast<uint32_t>(w.w)};
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                dot += __uint_as_float(a[i] << 16) * __uint_as_float(b[i] << 16) +
+                       __uint_as_float(a[i] & 0xffff0000u) * __uint_as_float(b[i] & 0xffff0000u);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = dot;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float2 ab = row_ab[k];
+        const float floor_b = ab.y - 100.f;  // ab.y holds the global bound on entry
+        const float zt = ab.x * (red[0] + red[1]);
+        ab.y = ts >= 0 ? fmaxf(zt, floor_b) : floor_b;
+        row_ab[k] = ab;
+    }
 }
 
 // ------------------------------------------------------------------ a6 + a8 + a9: combine
@@ -498,7 +550,7 @@ __global__ void __launch_bounds__(128) k_local_rows(CombineArgs a, float4 *__res
     if (k >= 0) {
         float o[4], lsum, mx;
         gather_row_partials(a, n_rg, k, o, lsum, mx);  // (o unused here)
-        if (threadIdx.x == 0) scal[i] = make_float4(lsum, mx, a.ttgt[k], 0.f);
+        if (threadIdx.x == 0) scal[i] = make_float4(lsum, mx, a.ttgt[k], a.row_ab[k].y);
     } else {
         float mu[4], lsum, mx;
         gather_row_partials(a, n_rg, n_pos, mu, lsum, mx);
@@ -537,20 +589,24 @@ __global__ void __launch_bounds__(128) k_finalize_multi(CombineArgs a, const flo
     }
     double row_loss = 0.0;
     if (k >= 0) {
+        // every shard used its own reference b_r: rescale to the common B* = max_r b_r
+        float Bs = -INFINITY;
+        for (int r = 0; r < W; ++r) Bs = fmaxf(Bs, scal_all[static_cast<int64_t>(r) * N + i].w);
         double lr = 0.0;
         float mx = -INFINITY, tt = -INFINITY;
         for (int r = 0; r < W; ++r) {
             const float4 v = scal_all[static_cast<int64_t>(r) * N + i];
-            lr += static_cast<double>(v.x);
-            mx = fmaxf(mx, v.y);
-            tt = fmaxf(tt, v.z);
+            lr += static_cast<double>(v.x) * exp2(static_cast<double>(v.w) - Bs);
+            mx = fmaxf(mx, v.y + (v.w - Bs));
+            tt = fmaxf(tt, v.z + (v.w - Bs));
         }
         float o[4], lsum, mxl;
         gather_row_partials(a, n_rg, k, o, lsum, mxl);
         const double l = lr + exp2(static_cast<double>(tt));
         const double w = static_cast<double>(a.s) / static_cast<double>(n_pos);
         const int ts = a.row_tgt[k];  // >= 0 iff this rank owns the target slot
-        const float alpha = static_cast<float>(w / l);
+        const float my_scale = static_cast<float>(exp2(static_cast<double>(a.row_ab[k].y) - Bs));
+        const float alpha = static_cast<float>(w / l) * my_scale;
         const float beta = ts >= 0 ? static_cast<float>(w * (lr / l)) : 0.f;
         const __nv_bfloat16 *Tt = reinterpret_cast<const __nv_bfloat16 *>(a.T) + static_cast<int64_t>(ts < 0 ? 0 : ts) * a.d;
 #pragma unroll
@@ -561,10 +617,9 @@ __global__ void __launch_bounds__(128) k_finalize_multi(CombineArgs a, const flo
         const double ell = log1p(lr * exp2(-static_cast<double>(tt)));
         row_loss = ell;
         if (threadIdx.x == 0) {
-            const float2 ab = a.row_ab[k];
             a.st_ell[i] = static_cast<float>(ell);
-            a.st_lse[i] = static_cast<float>((static_cast<double>(ab.y) + log2(l)) * 0.6931471805599453);
-            a.st_cos[i] = static_cast<float>((static_cast<double>(tt) + a.margin_l2 + ab.y) / (a.s * 1.4426950408889634));
+            a.st_lse[i] = static_cast<float>((static_cast<double>(Bs) + log2(l)) * 0.6931471805599453);
+            a.st_cos[i] = static_cast<float>((static_cast<double>(tt) + a.margin_l2 + Bs) / (a.s * 1.4426950408889634));
             a.st_phi[i] = 0.f;
             if (!(l > 0.0) || !isfinite(ell) || (mx < -100.f && tt - mx < 64.f))
                 latch(a.sc_w, ERR_DEVICE, !isfinite(ell) ? DET_NONFINITE : DET_UNDERFLOW);

@@ -242,3 +242,37 @@ def test_determinism(dcp):
         outs.append((l.clone(), d.clone()))
     for l, d in outs[1:]:
         assert torch.equal(l, outs[0][0]) and torch.equal(d, outs[0][1])
+
+
+@pytest.mark.parametrize("world", [1, 2])
+def test_degenerate_all_negative_cosines(dcp, world):
+    """Every slot points away from every row (cos ~ -0.99 at s = 64): with a single global
+    reference all softmax terms would underflow; the per-row reference (R1) keeps the
+    result exact within the parity bar (single pool and emulated 2-rank world)."""
+    d, C, n = 128, 300, 24
+    rng = np.random.default_rng(17)
+    u = rng.standard_normal(d)
+    u /= np.linalg.norm(u)
+    P = -u[None, :] + 0.1 * rng.standard_normal((C, d)) / np.sqrt(d)
+    P /= np.linalg.norm(P, axis=1, keepdims=True)
+    G = oracle.f64_to_bf16(P)
+    labs = rng.integers(0, 50, C)
+    X = u[None, :] + 0.1 * rng.standard_normal((n * world, d)) / np.sqrt(d)
+    X = oracle.f64_to_bf16(X)
+    y = np.concatenate([labs[rng.integers(0, C, n * world - 5)], 1000 + np.arange(5)])
+    if world == 1:
+        head = _head(dcp, C, d, n, C)
+    else:
+        head = dcp.DCPHead(C, d, dcp.BF16, world=world, rank=-1, n_local_max=n, m_local_max=C // world)
+    pool = oracle.Pool(C, d, oracle.BF16)
+    step = C // world * world if world > 1 else C
+    head.enqueue(to_dev(G[:step], synth.BF16), lt(labs[:step]))
+    pool.enqueue(G[:step], labs[:step])
+    loss, dx = head.loss_fwd_bwd(to_dev(X, synth.BF16), lt(y), None, 64.0, 0.35)
+    torch.cuda.synchronize()
+    head.check()
+    ref = pool.loss(X, y, None, 64.0, 0.35)
+    assert_loss_close(float(loss.item()), ref.L)
+    gdx = from_dev(dx)
+    assert_dx_close(gdx, ref.dx)
+    assert_dx_rows_close(gdx, ref.dx, np.where(ref.tslot >= 0)[0], what="dx in-pool")
