@@ -56,6 +56,7 @@ struct NcclApi {
     int (*AllGather)(const void *, void *, size_t, int, nccl_comm_t, cudaStream_t) = nullptr;
     int (*AllReduce)(const void *, void *, size_t, int, int, nccl_comm_t, cudaStream_t) = nullptr;
     int (*ReduceScatter)(const void *, void *, size_t, int, int, nccl_comm_t, cudaStream_t) = nullptr;
+    int (*GetUniqueId)(nccl_uid_t *) = nullptr;
     int (*GroupStart)() = nullptr;
     int (*GroupEnd)() = nullptr;
     const char *(*GetErrorString)(int) = nullptr;
@@ -75,6 +76,7 @@ static NcclApi &nccl() {
             api.AllReduce = (decltype(api.AllReduce))dlsym(h, "ncclAllReduce");
             api.ReduceScatter = (decltype(api.ReduceScatter))dlsym(h, "ncclReduceScatter");
             api.GroupStart = (decltype(api.GroupStart))dlsym(h, "ncclGroupStart");
+            api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(h, "ncclGetUniqueId");
             api.GroupEnd = (decltype(api.GroupEnd))dlsym(h, "ncclGroupEnd");
             api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
             api.ok = api.CommInitRank && api.AllGather && api.AllReduce && api.ReduceScatter &&
@@ -89,6 +91,13 @@ static inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; 
 static inline int64_t shard_lo(int64_t C, int W, int r) { return C * r / W; }
 
 constexpr int G_MAX = 256;  // upper bound of the persistent grid (SM count)
+
+// Test hook: F2C_FORCE_MULTI=1 routes a world-1 handle through the multi-rank protocol
+// with a real 1-rank NCCL communicator (exercises the NCCL transport on one GPU).
+static bool force_multi() {
+    const char *v = getenv("F2C_FORCE_MULTI");
+    return v && v[0] == '1';
+}
 
 struct Layout {
     size_t T, lab, sc, x_all, y_all, pair_all, blk_x, blk_y, inv_n, hslot, hkeys, hvals, tseq,
@@ -122,7 +131,7 @@ static Layout make_layout(int64_t C, int d, int dtype, int W, int rank, int64_t 
     L.T = take(static_cast<size_t>(L.C_loc) * d * es, 1024);
     L.lab = take(static_cast<size_t>(L.C_loc) * 8);
     L.sc = take(sizeof(Scalars));
-    const bool multi = W > 1;
+    const bool multi = W > 1 || (W == 1 && rank == 0 && force_multi());
     L.x_all = take(multi ? static_cast<size_t>(L.N) * d * es : 0);
     L.y_all = take(multi ? static_cast<size_t>(L.N) * 8 : 0);
     L.pair_all = take(multi ? static_cast<size_t>(L.N) * 4 : 0);
@@ -183,6 +192,7 @@ struct f2c_dcp {
     cudaStream_t last_stream = nullptr;
     nccl_comm_t comm = nullptr;
     int64_t last_N = 0;
+    bool multi = false;  // multi-rank protocol (world > 1, or the F2C_FORCE_MULTI test hook)
     // bench instrumentation
     bool prof = false;
     std::vector<cudaEvent_t> ev;
@@ -336,14 +346,20 @@ int f2c_dcp_create(int64_t C, int32_t d, int32_t dtype, int32_t world, int32_t r
         delete h;
         return fail(F2C_ECUDA, "cudaFuncSetAttribute(smem) failed");
     }
-    if (world > 1 && !h->emulated) {
+    h->multi = world > 1 || (rank == 0 && force_multi());
+    if (h->multi && !h->emulated) {
         NcclApi &api = nccl();
         if (!api.ok) {
             delete h;
             return fail(F2C_ENCCL, "libnccl.so.2 not loadable");
         }
         nccl_uid_t uid;
-        memcpy(&uid, nccl_uid, sizeof uid);
+        if (nccl_uid) {
+            memcpy(&uid, nccl_uid, sizeof uid);
+        } else if (!api.GetUniqueId || api.GetUniqueId(&uid) != 0) {
+            delete h;
+            return fail(F2C_ENCCL, "ncclGetUniqueId failed");
+        }
         int nr2 = api.CommInitRank(&h->comm, world, uid, rank);
         if (nr2 != 0) {
             delete h;
@@ -399,7 +415,7 @@ extern "C" int f2c_dcp_enqueue(f2c_dcp *h, const void *g_feats, const int64_t *l
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     h->last_stream = st;
     const size_t es = h->dtype == F2C_BF16 ? 2 : 4;
-    if (h->W == 1) {
+    if (!h->multi) {
         if ((rc = enqueue_rank(h, h->ranks[0], static_cast<const uint8_t *>(g_feats), labels, m_glob, st)))
             return rc;
     } else if (h->emulated) {
@@ -746,7 +762,7 @@ extern "C" int f2c_dcp_loss_fwd_bwd(f2c_dcp *h, const void *x, const int64_t *la
     if (rc) return rc;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     h->last_stream = st;
-    if (h->W != 1) return loss_multi(h, static_cast<const uint8_t *>(x), labels, pairing, n_local, s, m, loss,
+    if (h->multi) return loss_multi(h, static_cast<const uint8_t *>(x), labels, pairing, n_local, s, m, loss,
                                      static_cast<uint8_t *>(dx), st);
     Rank &R = h->ranks[0];
     const Layout &L = R.L;

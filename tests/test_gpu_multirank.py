@@ -83,3 +83,29 @@ def test_emulated_world_c0_steps_with_pairing(dcp):
         ref = pool.loss(X, y, pr, cfg.s, cfg.m)
         assert_loss_close(float(loss.item()), ref.L)
         assert_dx_close(from_dev(dx), ref.dx)
+
+
+def test_nccl_transport_single_rank(dcp, monkeypatch):
+    """The NCCL transport of the multi-rank protocol (C1 all-gather, C2 MAX all-reduce,
+    C3 all-gather, C4 reduce-scatter, C5 enqueue all-gather) on a real 1-rank NCCL
+    communicator (test hook F2C_FORCE_MULTI=1): results must equal the single-pool oracle."""
+    monkeypatch.setenv("F2C_FORCE_MULTI", "1")
+    C, d, m_loc, n = 700, 256, 50, 40
+    head = dcp.DCPHead(C, d, dcp.BF16, world=1, rank=0, n_local_max=n, m_local_max=m_loc)
+    monkeypatch.delenv("F2C_FORCE_MULTI")
+    pool = oracle.Pool(C, d, oracle.BF16)
+    for b in range(16):
+        G = synth.unit_rows(31, synth.S_PRE, b, 0, m_loc, d)
+        y = synth.uniform_labels(31, synth.S_PRE_LAB, b, 0, m_loc, 300)
+        head.enqueue(to_dev(G, synth.BF16), lt(y))
+        pool.enqueue(G, y)
+    X = synth.unit_rows(32, synth.S_INST, 0, 0, n, d)
+    y = synth.uniform_labels(32, synth.S_INST_LAB, 0, 0, n, 300)
+    loss, dx = head.loss_fwd_bwd(to_dev(X, synth.BF16), lt(y), None, 64.0, 0.35)
+    torch.cuda.synchronize()
+    head.check()
+    ref = pool.loss(X, y, None, 64.0, 0.35)
+    assert_loss_close(float(loss.item()), ref.L)
+    assert_dx_close(from_dev(dx), ref.dx)
+    feats, labs, E = head.get_state()
+    np.testing.assert_array_equal(labs, pool.lab)
