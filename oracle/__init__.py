@@ -48,7 +48,12 @@ def lib():
         L.orc_loss_rows.argtypes = [i64, i32, i32, P, P, i64, i64, i64, P, P, P, f64, f64,
                                     i64, P, P, P, P, P, P, P, P]
         L.orc_ema.argtypes = [P, P, i64, f64]
-        for f in (L.orc_enqueue, L.orc_loss, L.orc_loss_rows, L.orc_ema):
+        L.orc_loss_k.argtypes = [i64, i32, i32, i32, P, P, i64, i64, i64, P, P, P, f64, f64,
+                                 P, P, P, P, P, P, P, P, P]
+        L.orc_loss_rows_k.argtypes = [i64, i32, i32, i32, P, P, i64, i64, i64, P, P, P, f64, f64,
+                                      i64, P, P, P, P, P, P, P, P]
+        for f in (L.orc_enqueue, L.orc_loss, L.orc_loss_rows, L.orc_ema, L.orc_loss_k,
+                  L.orc_loss_rows_k):
             f.restype = ctypes.c_int
         _lib = L
     return _lib
@@ -90,11 +95,13 @@ class LossResult:
 
 
 class Pool:
-    """The DCP state of the oracle: T [C, d] (raw dtype), lab [C], E, M_last."""
+    """The DCP state of the oracle: T [C, d] (K = 1) or [C, K, d] (raw dtype), lab [C], E,
+    M_last.  An enqueued identity carries K features."""
 
-    def __init__(self, C: int, d: int, dtype: int = BF16):
-        self.C, self.d, self.dtype = int(C), int(d), int(dtype)
-        self.T = np.zeros((C, d), dtype=np.uint16 if dtype == BF16 else np.float32)
+    def __init__(self, C: int, d: int, dtype: int = BF16, K: int = 1):
+        self.C, self.d, self.dtype, self.K = int(C), int(d), int(dtype), int(K)
+        shape = (C, d) if K == 1 else (C, K, d)
+        self.T = np.zeros(shape, dtype=np.uint16 if dtype == BF16 else np.float32)
         self.lab = np.full(C, -1, dtype=np.int64)
         self.E = np.zeros(1, dtype=np.int64)
         self.M_last = np.zeros(1, dtype=np.int64)
@@ -106,9 +113,11 @@ class Pool:
     def enqueue(self, G: np.ndarray, y: np.ndarray) -> None:
         G = np.ascontiguousarray(G)
         y = np.ascontiguousarray(y, dtype=np.int64)
-        if _raw_dtype(G) != self.dtype or G.shape != (len(y), self.d):
+        want = (len(y), self.d) if self.K == 1 else (len(y), self.K, self.d)
+        if _raw_dtype(G) != self.dtype or G.shape != want:
             raise OracleError(2, "enqueue shape/dtype")
-        rc = lib().orc_enqueue(self.C, self.d, self.dtype, _p(self.T), _p(self.lab), _p(self.E),
+        # a slot holds K consecutive feature rows: the ring copy is the same with rows of K*d
+        rc = lib().orc_enqueue(self.C, self.K * self.d, self.dtype, _p(self.T), _p(self.lab), _p(self.E),
                                _p(self.M_last), _p(G), _p(y), len(y))
         if rc:
             raise OracleError(rc, "orc_enqueue")
@@ -128,10 +137,10 @@ class Pool:
         counts = np.zeros(3, dtype=np.int64)
         P = np.zeros((N, self.C_occ)) if want_P else None
         dT = np.zeros((self.C, d)) if want_dT else None
-        rc = lib().orc_loss(self.C, d, self.dtype, _p(self.T), _p(self.lab), int(self.E[0]),
-                            int(self.M_last[0]), N, _p(X), _p(y), _p(pr), float(s), float(m),
-                            _p(out3), _p(dx), _p(lse), _p(ts), _p(phi), _p(ell), _p(counts),
-                            _p(P), _p(dT))
+        rc = lib().orc_loss_k(self.C, self.K, d, self.dtype, _p(self.T), _p(self.lab),
+                              int(self.E[0]), int(self.M_last[0]), N, _p(X), _p(y), _p(pr),
+                              float(s), float(m), _p(out3), _p(dx), _p(lse), _p(ts), _p(phi),
+                              _p(ell), _p(counts), _p(P), _p(dT))
         if rc:
             raise OracleError(rc, "orc_loss")
         return LossResult(out3[0], out3[1], out3[2], dx, lse, ts, phi, ell,
@@ -148,10 +157,10 @@ class Pool:
         ts = np.zeros(k, dtype=np.int64)
         counts = np.zeros(3, dtype=np.int64)
         mu = np.zeros(d)
-        rc = lib().orc_loss_rows(self.C, d, self.dtype, _p(self.T), _p(self.lab), int(self.E[0]),
-                                 int(self.M_last[0]), N, _p(X), _p(y), _p(pr), float(s), float(m),
-                                 k, _p(rows), _p(dx), _p(lse), _p(ts), _p(phi), _p(ell),
-                                 _p(counts), _p(mu))
+        rc = lib().orc_loss_rows_k(self.C, self.K, d, self.dtype, _p(self.T), _p(self.lab),
+                                   int(self.E[0]), int(self.M_last[0]), N, _p(X), _p(y), _p(pr),
+                                   float(s), float(m), k, _p(rows), _p(dx), _p(lse), _p(ts),
+                                   _p(phi), _p(ell), _p(counts), _p(mu))
         if rc:
             raise OracleError(rc, "orc_loss_rows")
         return dict(dx=dx, lse=lse, tslot=ts, phi=phi, ell=ell, N_pos=int(counts[0]),

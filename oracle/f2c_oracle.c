@@ -22,6 +22,13 @@
  *                    (the global normalisers N_pos, N_neg, C_occ and mu are still
  *                    computed from the whole batch / pool).
  *   orc_ema          G-Net moving average phi <- m*phi + (1-m)*theta.
+ *   orc_loss_k / orc_loss_rows_k
+ *                    the pool with K features per slot ("C x K x D"):
+ *                    logits use T_bar_c = (1/K) sum_k T[c,k] (Eq. 8 "(1/K) sum_k <F_p, T[:,k,:]>",
+ *                    P:155-159); for K >= 2 the L_cos term uses the true cosine
+ *                    <x_hat, T_bar_c> / ||T_bar_c|| ("phi ... cosine similarity",
+ *                    "T_bar ... average along the axis of K"; reading R4), a zero-norm
+ *                    center contributing 0.  K = 1 is exactly orc_loss.
  *
  * Parity status: every function here is pinned by tests/test_oracle_pins.py
  * (pins P1-P8 of DESIGN.md section 4).  The semantics choices D3 (margin form),
@@ -83,7 +90,7 @@ static int64_t orc_seq(int64_t c, int64_t C, int64_t E) { return c + C * ((E - 1
 /* ---- shared pieces of the loss definition ------------------------------------ */
 typedef struct {
     int64_t C, N, E, M_last, C_occ;
-    int32_t d, dtype;
+    int32_t d, dtype, K;
     const void *T;
     const int64_t *lab;
     const void *X;
@@ -95,6 +102,25 @@ typedef struct {
     int64_t N_pos, N_neg;
     double *mu;    /* [d] sum over occupied slots of T_c */
 } orc_ctx;
+
+/* T_bar[c][k] = (1/K) sum_kk T[c][kk][k]  (Eq. 8's average over the K axis) */
+static double orc_tbar(const orc_ctx *q, int64_t c, int32_t k) {
+    if (q->K == 1) return orc_elem(q->T, q->dtype, c * q->d + k);
+    double acc = 0.0;
+    for (int32_t kk = 0; kk < q->K; ++kk) acc += orc_elem(q->T, q->dtype, (c * q->K + kk) * q->d + k);
+    return acc / (double)q->K;
+}
+
+/* ||T_bar_c|| for the true cosine of L_cos (K >= 2); 1 for K = 1 (rows as stored, D2) */
+static double orc_tbar_norm(const orc_ctx *q, int64_t c) {
+    if (q->K == 1) return 1.0;
+    double ss = 0.0;
+    for (int32_t k = 0; k < q->d; ++k) {
+        double v = orc_tbar(q, c, k);
+        ss += v * v;
+    }
+    return sqrt(ss);
+}
 
 /* step 1-4 of the definition: norms, targets, split, mu */
 static int orc_prepare(orc_ctx *q, const int32_t *pairing) {
@@ -128,7 +154,7 @@ static int orc_prepare(orc_ctx *q, const int32_t *pairing) {
     q->N_neg = N - q->N_pos;
     for (int32_t k = 0; k < d; ++k) q->mu[k] = 0.0;
     for (int64_t c = 0; c < q->C_occ; ++c)
-        for (int32_t k = 0; k < d; ++k) q->mu[k] += orc_elem(q->T, q->dtype, c * d + k);
+        for (int32_t k = 0; k < d; ++k) q->mu[k] += orc_tbar(q, c, k);
     return ORC_OK;
 }
 
@@ -145,8 +171,8 @@ static void orc_row(const orc_ctx *q, int64_t i, double *ell, double *phi, doubl
     for (int64_t c = 0; c < Co; ++c) {
         double dot = 0.0;
         for (int32_t k = 0; k < d; ++k)
-            dot += orc_elem(q->X, q->dtype, i * d + k) * inv_n * orc_elem(q->T, q->dtype, c * d + k);
-        cos_buf[c] = dot; /* Eq. 8 with K = 1: <F_p, T[c]> on the normalised feature */
+            dot += orc_elem(q->X, q->dtype, i * d + k) * inv_n * orc_tbar(q, c, k);
+        cos_buf[c] = dot; /* Eq. 8: (1/K) sum_k <F_p, T[c,k]> on the normalised feature */
     }
     *ell = 0.0;
     *phi = 0.0;
@@ -173,20 +199,25 @@ static void orc_row(const orc_ctx *q, int64_t i, double *ell, double *phi, doubl
             double p = exp(z - L);
             if (prow) prow[c] = p;
             double gc = w * (p - (c == t ? 1.0 : 0.0)); /* dL/dz * dz/dcos */
-            for (int32_t k = 0; k < d; ++k) g[k] += gc * orc_elem(q->T, q->dtype, c * d + k);
+            for (int32_t k = 0; k < d; ++k) g[k] += gc * orc_tbar(q, c, k);
             if (dT)
                 for (int32_t k = 0; k < d; ++k)
                     dT[c * d + k] += gc * orc_elem(q->X, q->dtype, i * d + k) * inv_n;
         }
     } else {
-        /* L_cos: phi_i = mean over occupied slots of cos(x_i, T_c)  (D10) */
+        /* L_cos: phi_i = mean over occupied slots of cos(x_i, T_bar_c)  (D10, R4) */
         if (Co > 0) {
             double acc = 0.0;
-            for (int64_t c = 0; c < Co; ++c) acc += cos_buf[c];
+            for (int64_t c = 0; c < Co; ++c) {
+                double tn = orc_tbar_norm(q, c);
+                if (tn > 0.0) acc += cos_buf[c] / tn;
+            }
             *phi = acc / (double)Co;
             double w = 1.0 / ((double)q->N_neg * (double)Co);
             for (int64_t c = 0; c < Co; ++c) {
-                for (int32_t k = 0; k < d; ++k) g[k] += w * orc_elem(q->T, q->dtype, c * d + k);
+                double tn = orc_tbar_norm(q, c);
+                double wc = tn > 0.0 ? w / tn : 0.0;
+                for (int32_t k = 0; k < d; ++k) g[k] += wc * orc_tbar(q, c, k);
                 if (dT)
                     for (int32_t k = 0; k < d; ++k)
                         dT[c * d + k] += w * orc_elem(q->X, q->dtype, i * d + k) * inv_n;
@@ -206,14 +237,15 @@ static void orc_row(const orc_ctx *q, int64_t i, double *ell, double *phi, doubl
  * out3 = {L, L_ce, L_cos}; dx [N*d]; lse [N] (0 for out-of-pool rows); tslot [N];
  * phi [N] (0 for in-pool rows); ell [N] (0 for out-of-pool rows);
  * counts = {N_pos, N_neg, C_occ}; P [N * C_occ] or NULL; dT [C * d] or NULL. */
-int orc_loss(int64_t C, int32_t d, int32_t dtype, const void *T, const int64_t *lab, int64_t E,
-             int64_t M_last, int64_t N, const void *X, const int64_t *y, const int32_t *pairing,
-             double s, double m, double *out3, double *dx, double *lse, int64_t *tslot, double *phi,
-             double *ell, int64_t *counts, double *P, double *dT) {
-    if (C < 1 || d < 1 || N < 0 || (dtype != 0 && dtype != 1)) return ORC_EINVAL;
+int orc_loss_k(int64_t C, int32_t K, int32_t d, int32_t dtype, const void *T, const int64_t *lab,
+               int64_t E, int64_t M_last, int64_t N, const void *X, const int64_t *y,
+               const int32_t *pairing, double s, double m, double *out3, double *dx, double *lse,
+               int64_t *tslot, double *phi, double *ell, int64_t *counts, double *P, double *dT) {
+    if (C < 1 || d < 1 || K < 1 || N < 0 || (dtype != 0 && dtype != 1)) return ORC_EINVAL;
     if (!(s > 0.0) || !isfinite(m)) return ORC_EINVAL;
+    if (dT && K != 1) return ORC_EINVAL;
     orc_ctx q = {0};
-    q.C = C; q.N = N; q.E = E; q.M_last = M_last; q.d = d; q.dtype = dtype;
+    q.C = C; q.N = N; q.E = E; q.M_last = M_last; q.d = d; q.dtype = dtype; q.K = K;
     q.T = T; q.lab = lab; q.X = X; q.y = y; q.s = s; q.m = m;
     q.n = (double *)calloc((size_t)(N > 0 ? N : 1), sizeof(double));
     q.t = (int64_t *)calloc((size_t)(N > 0 ? N : 1), sizeof(int64_t));
@@ -243,17 +275,25 @@ int orc_loss(int64_t C, int32_t d, int32_t dtype, const void *T, const int64_t *
     return rc;
 }
 
+int orc_loss(int64_t C, int32_t d, int32_t dtype, const void *T, const int64_t *lab, int64_t E,
+             int64_t M_last, int64_t N, const void *X, const int64_t *y, const int32_t *pairing,
+             double s, double m, double *out3, double *dx, double *lse, int64_t *tslot, double *phi,
+             double *ell, int64_t *counts, double *P, double *dT) {
+    return orc_loss_k(C, 1, d, dtype, T, lab, E, M_last, N, X, y, pairing, s, m, out3, dx, lse, tslot,
+                      phi, ell, counts, P, dT);
+}
+
 /* Same definition for a subset of rows (for configurations too large for the
  * full O(N*C*d) evaluation).  Normalisers are global.  Outputs are per selected
  * row: dx [nsel*d], lse, tslot, phi, ell. counts = {N_pos, N_neg, C_occ}. */
-int orc_loss_rows(int64_t C, int32_t d, int32_t dtype, const void *T, const int64_t *lab,
-                  int64_t E, int64_t M_last, int64_t N, const void *X, const int64_t *y,
-                  const int32_t *pairing, double s, double m, int64_t nsel, const int64_t *rows,
-                  double *dx, double *lse, int64_t *tslot, double *phi, double *ell,
-                  int64_t *counts, double *mu_out) {
-    if (C < 1 || d < 1 || N < 0 || (dtype != 0 && dtype != 1)) return ORC_EINVAL;
+int orc_loss_rows_k(int64_t C, int32_t K, int32_t d, int32_t dtype, const void *T,
+                    const int64_t *lab, int64_t E, int64_t M_last, int64_t N, const void *X,
+                    const int64_t *y, const int32_t *pairing, double s, double m, int64_t nsel,
+                    const int64_t *rows, double *dx, double *lse, int64_t *tslot, double *phi,
+                    double *ell, int64_t *counts, double *mu_out) {
+    if (C < 1 || d < 1 || K < 1 || N < 0 || (dtype != 0 && dtype != 1)) return ORC_EINVAL;
     orc_ctx q = {0};
-    q.C = C; q.N = N; q.E = E; q.M_last = M_last; q.d = d; q.dtype = dtype;
+    q.C = C; q.N = N; q.E = E; q.M_last = M_last; q.d = d; q.dtype = dtype; q.K = K;
     q.T = T; q.lab = lab; q.X = X; q.y = y; q.s = s; q.m = m;
     q.n = (double *)calloc((size_t)(N > 0 ? N : 1), sizeof(double));
     q.t = (int64_t *)calloc((size_t)(N > 0 ? N : 1), sizeof(int64_t));
@@ -273,6 +313,15 @@ int orc_loss_rows(int64_t C, int32_t d, int32_t dtype, const void *T, const int6
     }
     free(q.n); free(q.t); free(q.mu); free(cos_buf); free(g);
     return rc;
+}
+
+int orc_loss_rows(int64_t C, int32_t d, int32_t dtype, const void *T, const int64_t *lab,
+                  int64_t E, int64_t M_last, int64_t N, const void *X, const int64_t *y,
+                  const int32_t *pairing, double s, double m, int64_t nsel, const int64_t *rows,
+                  double *dx, double *lse, int64_t *tslot, double *phi, double *ell,
+                  int64_t *counts, double *mu_out) {
+    return orc_loss_rows_k(C, 1, d, dtype, T, lab, E, M_last, N, X, y, pairing, s, m, nsel, rows, dx,
+                           lse, tslot, phi, ell, counts, mu_out);
 }
 
 /* G-Net moving average: g <- m*g + (1-m)*p, evaluated in fp64

@@ -353,3 +353,101 @@ def test_ema_boundaries_and_closed_form():
     g1 = oracle.ema(th, ph, 0.7)
     np.testing.assert_allclose(np.abs(g1.astype(np.float64) - th),
                                0.7 * np.abs(ph.astype(np.float64) - th), rtol=1e-6, atol=1e-6)
+
+
+# ----------------------------------------------------------------------------- K = 2 (NEXT-1)
+def _pool_k(slots, K=2):
+    """slots: list of (K feature vectors, label), oldest first."""
+    d = len(slots[0][0][0])
+    p = Pool(len(slots), d, F32, K=K)
+    for feats, lab in slots:
+        p.enqueue(np.array([feats], np.float32), np.array([lab]))
+    return p
+
+
+def test_k2_spec_example_closed_form():
+    """K=2 features with cosines 0.8 and 0.6 to the probe give the logit 0.7 (s=1).
+    With a second slot orthogonal to x the CE is ln(1+e^-0.7) (Eq. 8 average + Eq. 9)."""
+    p = _pool_k([([[0.8, 0.6, 0.0], [0.6, 0.0, 0.8]], 0), ([[0.0, 1.0, 0.0], [0.0, 0.0, 1.0]], 1)])
+    r = p.loss(np.array([[1.0, 0.0, 0.0]], np.float32), np.array([0]), None, 1.0, 0.0)
+    assert r.L == pytest.approx(math.log1p(math.exp(-0.7)), rel=1e-6)
+
+
+def test_k2_true_cosine_for_lcos():
+    """R4: for K >= 2 L_cos uses cos(x, T_bar) = <x, T_bar>/||T_bar|| (P:165-169);
+    T_bar_0 = (0.7, 0.3, 0.4), T_bar_1 = (0, .5, .5) -> phi = 0.7/||T_bar_0|| / 2."""
+    p = _pool_k([([[0.8, 0.6, 0.0], [0.6, 0.0, 0.8]], 0), ([[0.0, 1.0, 0.0], [0.0, 0.0, 1.0]], 1)])
+    r = p.loss(np.array([[1.0, 0.0, 0.0]], np.float32), np.array([9]), None, 64.0, 0.35)
+    assert r.L == pytest.approx(0.7 / math.sqrt(0.49 + 0.09 + 0.16) / 2.0, rel=1e-6)
+
+
+def test_k2_cancelling_features_and_zero_center():
+    """T[c,0] = -T[c,1] gives T_bar_c = 0: logit 0 for every row (uniform softmax
+    with the margined target), and the zero-norm center contributes 0 to L_cos."""
+    p = _pool_k([([[1.0, 0.0], [-1.0, 0.0]], 3), ([[0.0, 1.0], [0.0, -1.0]], 4)])
+    r = p.loss(np.array([[0.6, 0.8]], np.float32), np.array([3]), None, 10.0, 0.0)
+    assert r.L == pytest.approx(math.log(2.0), rel=1e-12)
+    r = p.loss(np.array([[0.6, 0.8]], np.float32), np.array([7]), None, 10.0, 0.0)
+    assert r.L == 0.0 and np.all(r.dx == 0.0)
+
+
+def test_k2_duplicated_features_equal_k1():
+    """Paper-literal insertion (one G-Net feature duplicated over K) reduces the
+    K=2 pool to the K=1 pool (unit rows: true cosine == stored inner product)."""
+    rng = np.random.default_rng(21)
+    C, d = 20, 8
+    T = rng.standard_normal((C, d))
+    T /= np.linalg.norm(T, axis=1, keepdims=True)
+    T = T.astype(np.float32)
+    lab = rng.integers(0, 6, C)
+    p1 = Pool(C, d, F32)
+    p1.enqueue(T, lab)
+    p2 = Pool(C, d, F32, K=2)
+    p2.enqueue(np.stack([T, T], axis=1), lab)
+    X = rng.standard_normal((9, d)).astype(np.float32)
+    y = np.concatenate([rng.integers(0, 6, 6), [50, 51, 52]])
+    a, b = p1.loss(X, y, None, 30.0, 0.2), p2.loss(X, y, None, 30.0, 0.2)
+    assert b.L == pytest.approx(a.L, rel=1e-6)
+    np.testing.assert_allclose(b.dx, a.dx, rtol=1e-5, atol=1e-8)
+
+
+def test_k2_autograd_and_finite_differences():
+    """K=2 gradient: oracle dx == torch autograd of an independent formulation (T_bar mean,
+    margined CE on the newest duplicate, true-cosine L_cos) and == Richardson differences."""
+    rng = np.random.default_rng(23)
+    C, d, K = 11, 6, 2
+    T = (rng.integers(-128, 128, (C, K, d)) / 128.0).astype(np.float32)
+    lab = rng.integers(0, 5, C)
+    p = Pool(C, d, F32, K=K)
+    p.enqueue(T, lab)
+    X = (rng.integers(-256, 256, (6, d)) / 128.0).astype(np.float32)
+    y = np.array([0, 1, 2, 3, 8, 9])
+    s, m = 16.0, 0.3
+    r = p.loss(X, y, None, s, m)
+    Tb = torch.tensor(T.astype(np.float64)).mean(dim=1)
+    xt = torch.tensor(X.astype(np.float64), requires_grad=True)
+    cos = (xt / xt.norm(dim=1, keepdim=True)) @ Tb.T
+    tgt = [max([c for c in range(C) if lab[c] == y[i]], default=-1) for i in range(len(y))]
+    pos = [i for i in range(len(y)) if tgt[i] >= 0]
+    neg = [i for i in range(len(y)) if tgt[i] < 0]
+    ce = 0
+    for i in pos:
+        zi = s * cos[i].clone()
+        zi[tgt[i]] = zi[tgt[i]] - s * m
+        ce = ce + torch.logsumexp(zi, 0) - zi[tgt[i]]
+    tcos = cos / Tb.norm(dim=1)[None, :]
+    loss = ce / len(pos) + sum(tcos[i].mean() for i in neg) / len(neg)
+    loss.backward()
+    assert r.L == pytest.approx(loss.item(), rel=1e-12)
+    np.testing.assert_allclose(r.dx, xt.grad.numpy(), rtol=1e-9, atol=1e-12)
+    h = 2.0 ** -8
+    num = np.zeros_like(r.dx)
+    for i in range(len(y)):
+        for k in range(d):
+            def D(hh):
+                Xa, Xb = X.copy(), X.copy()
+                Xa[i, k] += hh
+                Xb[i, k] -= hh
+                return (p.loss(Xa, y, None, s, m).L - p.loss(Xb, y, None, s, m).L) / (2 * hh)
+            num[i, k] = (4 * D(h / 2) - D(h)) / 3
+    np.testing.assert_allclose(r.dx, num, rtol=1e-6, atol=1e-8)
