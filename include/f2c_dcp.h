@@ -78,6 +78,19 @@ int f2c_dcp_create(int64_t C, int32_t d, int32_t dtype, int32_t world, int32_t r
                    const void *nccl_uid, void *state_buf, size_t state_bytes,
                    int64_t n_local_max, int64_t m_local_max, f2c_dcp **out);
 
+/* K features per slot (NEXT-1; the paper's default K = 2): the pool is
+ * T [C][K][d] bf16.  Eq. 8's logits use T_bar_c = (1/K) sum_k T[c,k]; for K >= 2
+ * L_cos uses the true cosine <x_hat, T_bar_c>/||T_bar_c|| (reading R4; a zero
+ * center contributes 0).  Enqueue then takes g_feats [m_local][K][d] (k-fill mode;
+ * the paper-literal mode duplicates one feature over K on the caller's side);
+ * get_state / set_state exchange [C_loc][K][d].  K in [1, 8]; K > 1 requires bf16.
+ * f2c_dcp_create / f2c_dcp_state_bytes are these with K = 1. */
+size_t f2c_dcp_state_bytes_k(int64_t C, int32_t K, int32_t d, int32_t dtype, int32_t world,
+                             int32_t rank, int64_t n_local_max, int64_t m_local_max);
+int f2c_dcp_create_k(int64_t C, int32_t K, int32_t d, int32_t dtype, int32_t world, int32_t rank,
+                     const void *nccl_uid, void *state_buf, size_t state_bytes,
+                     int64_t n_local_max, int64_t m_local_max, f2c_dcp **out);
+
 /* Enqueue one identity block (Eq. 7 + Algorithm 1):
  * the global block is the concatenation of every rank's g_feats in rank order
  * (emulated world: g_feats already holds the concatenation, world*m_local rows).

@@ -70,6 +70,7 @@ struct PCParams {
     const float2 *row_ab;  // [R_max] (a_r, b_r)
     const int *row_tgt;    // [R_max] local target slot or -1
     const uint8_t *X_pos;  // [R_max, d] bf16 compacted rows
+    const float *wslot;    // K >= 2: per-slot 1/||T_bar_c|| weights of the mu row (else null)
     float margin_l2;       // s * m * log2(e)
     float *ttgt;           // [R_max]
     float *seg_l;          // [S][128]
@@ -393,6 +394,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                                     e[k] = -INFINITY;
                                 }
                         }
+                    }
+                    if (p.wslot && row == n_pos) {  // mu row with K >= 2: p_c = 1/||T_bar_c||
+#pragma unroll
+                        for (int k = 0; k < 64; ++k)
+                            e[k] = k < nval ? __log2f(fmaxf(p.wslot[base + k], 1e-30f)) : -INFINITY;
                     }
                     uint32_t w[32];
                     float la[4] = {0.f, 0.f, 0.f, 0.f}, ma[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};

@@ -102,12 +102,14 @@ static bool force_multi() {
 struct Layout {
     size_t T, lab, sc, x_all, y_all, pair_all, blk_x, blk_y, inv_n, hslot, hkeys, hvals, tseq,
         comp_idx, pos_row, X_pos, row_ab, row_tgt, ttgt, seg_l, seg_mx, seg_O, rowloss, st_lse,
-        st_cos, st_phi, st_ell, rs_buf, rs_all, dx_part, tseq_ext, dx32, tmax_glob, mu_buf, total;
+        st_cos, st_phi, st_ell, rs_buf, rs_all, dx_part, tseq_ext, dx32, tmax_glob, mu_buf, Traw, wslot,
+        total;
     int64_t C_loc, N, Mg, R_max, S_max;
     int H;
 };
 
-static Layout make_layout(int64_t C, int d, int dtype, int W, int rank, int64_t n_loc, int64_t m_loc) {
+static Layout make_layout(int64_t C, int d, int dtype, int W, int rank, int64_t n_loc, int64_t m_loc,
+                          int K = 1) {
     Layout L{};
     const size_t es = dtype == F2C_BF16 ? 2 : 4;
     const int r = rank < 0 ? 0 : rank;
@@ -135,7 +137,7 @@ static Layout make_layout(int64_t C, int d, int dtype, int W, int rank, int64_t 
     L.x_all = take(multi ? static_cast<size_t>(L.N) * d * es : 0);
     L.y_all = take(multi ? static_cast<size_t>(L.N) * 8 : 0);
     L.pair_all = take(multi ? static_cast<size_t>(L.N) * 4 : 0);
-    L.blk_x = take(multi ? static_cast<size_t>(L.Mg) * d * es : 0);
+    L.blk_x = take(multi ? static_cast<size_t>(L.Mg) * K * d * es : 0);
     L.blk_y = take(multi ? static_cast<size_t>(L.Mg) * 8 : 0);
     L.inv_n = take(static_cast<size_t>(L.N) * 4);
     L.hslot = take(static_cast<size_t>(L.N) * 4);
@@ -165,6 +167,9 @@ static Layout make_layout(int64_t C, int d, int dtype, int W, int rank, int64_t 
     L.dx32 = take(multi ? static_cast<size_t>(n_loc) * d * 4 : 0);
     L.tmax_glob = take(64);
     L.mu_buf = take(static_cast<size_t>(d) * 4);
+    // K >= 2: raw features [C_loc][K][d] (state) and 1/||T_bar_c|| (the T region holds T_bar)
+    L.Traw = take(K > 1 ? static_cast<size_t>(L.C_loc) * K * d * es : 0, 1024);
+    L.wslot = take(K > 1 ? static_cast<size_t>(L.C_loc) * 4 : 0);
     L.total = align_up(o, 1024);
     return L;
 }
@@ -184,6 +189,7 @@ struct Rank {
 struct f2c_dcp {
     int64_t C;
     int d, dtype, W;
+    int K = 1;  // features per slot (NEXT-1)
     bool emulated;
     int64_t n_local_max, m_local_max;
     int64_t E = 0, M_last = 0;
@@ -267,19 +273,31 @@ extern "C" {
 const char *f2c_last_error(void) { return g_err.c_str(); }
 int f2c_last_launch_count(void) { return g_launches; }
 
-size_t f2c_dcp_state_bytes(int64_t C, int32_t d, int32_t dtype, int32_t world, int32_t rank,
-                           int64_t n_local_max, int64_t m_local_max) {
+size_t f2c_dcp_state_bytes_k(int64_t C, int32_t K, int32_t d, int32_t dtype, int32_t world, int32_t rank,
+                             int64_t n_local_max, int64_t m_local_max) {
     if (C < 1 || d < 128 || d % 128 || d > 512 || (dtype != F2C_BF16 && dtype != F2C_F32) ||
         world < 1 || rank < -1 || rank >= world || n_local_max < 1 || m_local_max < 1 ||
-        C < world)
+        C < world || K < 1 || K > 8 || (K > 1 && dtype != F2C_BF16))
         return 0;
-    Layout L = make_layout(C, d, dtype, world, rank, n_local_max, m_local_max);
+    Layout L = make_layout(C, d, dtype, world, rank, n_local_max, m_local_max, K);
     return rank < 0 ? L.total * static_cast<size_t>(world) : L.total;
+}
+
+size_t f2c_dcp_state_bytes(int64_t C, int32_t d, int32_t dtype, int32_t world, int32_t rank,
+                           int64_t n_local_max, int64_t m_local_max) {
+    return f2c_dcp_state_bytes_k(C, 1, d, dtype, world, rank, n_local_max, m_local_max);
 }
 
 int f2c_dcp_create(int64_t C, int32_t d, int32_t dtype, int32_t world, int32_t rank,
                    const void *nccl_uid, void *state_buf, size_t state_bytes, int64_t n_local_max,
                    int64_t m_local_max, f2c_dcp **out) {
+    return f2c_dcp_create_k(C, 1, d, dtype, world, rank, nccl_uid, state_buf, state_bytes, n_local_max,
+                            m_local_max, out);
+}
+
+int f2c_dcp_create_k(int64_t C, int32_t K, int32_t d, int32_t dtype, int32_t world, int32_t rank,
+                     const void *nccl_uid, void *state_buf, size_t state_bytes, int64_t n_local_max,
+                     int64_t m_local_max, f2c_dcp **out) {
     g_launches = 0;
     if (!out) return fail(F2C_EINVAL, "out is NULL");
     *out = nullptr;
@@ -289,19 +307,21 @@ int f2c_dcp_create(int64_t C, int32_t d, int32_t dtype, int32_t world, int32_t r
     if (d < 128 || d % 128 || d > 512)
         return fail(F2C_EINVAL, "d = %d: must be a multiple of 128 and <= 512", d);
     if (world < 1 || rank < -1 || rank >= world) return fail(F2C_EINVAL, "bad world/rank");
+    if (K < 1 || K > 8) return fail(F2C_EINVAL, "K = %d: must be in [1, 8]", K);
+    if (K > 1 && dtype != F2C_BF16) return fail(F2C_EINVAL, "K > 1 requires bf16 features");
     if (C < world) return fail(F2C_EINVAL, "C < world");
     if (m_local_max * world > C) return fail(F2C_ECAPACITY, "world*m_local_max > C (S:276)");
     if (world > 1 && rank >= 0 && !nccl_uid) return fail(F2C_EINVAL, "nccl_uid required for world > 1");
     if ((world == 1 || rank < 0) && nccl_uid) return fail(F2C_EINVAL, "nccl_uid must be NULL");
     if (!state_buf || (reinterpret_cast<uintptr_t>(state_buf) & 255))
         return fail(F2C_EINVAL, "state_buf must be a 256-byte aligned device pointer");
-    size_t need = f2c_dcp_state_bytes(C, d, dtype, world, rank, n_local_max, m_local_max);
+    size_t need = f2c_dcp_state_bytes_k(C, K, d, dtype, world, rank, n_local_max, m_local_max);
     if (state_bytes < need) return fail(F2C_ESHAPE, "state_bytes %zu < required %zu", state_bytes, need);
     int rc = check_device();
     if (rc) return rc;
 
     f2c_dcp *h = new f2c_dcp();
-    h->C = C; h->d = d; h->dtype = dtype; h->W = world; h->emulated = rank < 0;
+    h->C = C; h->d = d; h->dtype = dtype; h->W = world; h->emulated = rank < 0; h->K = K;
     h->n_local_max = n_local_max; h->m_local_max = m_local_max;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -313,7 +333,7 @@ int f2c_dcp_create(int64_t C, int32_t d, int32_t dtype, int32_t world, int32_t r
         R.rank = h->emulated ? i : rank;
         R.lo = shard_lo(C, world, R.rank);
         R.hi = shard_lo(C, world, R.rank + 1);
-        R.L = make_layout(C, d, dtype, world, rank, n_local_max, m_local_max);
+        R.L = make_layout(C, d, dtype, world, rank, n_local_max, m_local_max, K);
         R.base = static_cast<uint8_t *>(state_buf) + static_cast<size_t>(i) * R.L.total;
         if (cudaMemset(R.base, 0, R.L.total) != cudaSuccess) {
             delete h;
@@ -337,7 +357,7 @@ int f2c_dcp_create(int64_t C, int32_t d, int32_t dtype, int32_t world, int32_t r
     }
     {
         const char *kv = getenv("F2C_KERNEL");
-        h->use_tp64 = kv && strcmp(kv, "tp64") == 0;
+        h->use_tp64 = kv && strcmp(kv, "tp64") == 0 && K == 1;
     }
     if (cudaFuncSetAttribute(dcp_tp64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              TP_SMEM_BYTES) != cudaSuccess ||
@@ -390,6 +410,16 @@ static int nccl_check(int r, const char *what) {
 // ============================================================================ enqueue
 static int enqueue_rank(f2c_dcp *h, Rank &R, const uint8_t *g, const int64_t *y, int64_t m_glob,
                         cudaStream_t st) {
+    if (h->K > 1) {
+        int64_t blocks = (m_glob + 7) / 8;
+        if (blocks > static_cast<int64_t>(h->G) * 8) blocks = static_cast<int64_t>(h->G) * 8;
+        k_enqueue_k<<<static_cast<unsigned>(blocks), 256, 0, st>>>(
+            reinterpret_cast<const __nv_bfloat16 *>(g), y, m_glob, h->K, h->d, h->E, h->C, R.lo, R.hi,
+            R.at<__nv_bfloat16>(R.L.Traw), R.at<__nv_bfloat16>(R.L.T), R.at<float>(R.L.wslot),
+            R.at<int64_t>(R.L.lab), R.sc());
+        LAUNCH_CHECK();
+        return F2C_OK;
+    }
     const int row_bytes = h->d * (h->dtype == F2C_BF16 ? 2 : 4);
     int64_t blocks = (m_glob + 7) / 8;                 // 8 rows (warps) per block per pass
     if (blocks > static_cast<int64_t>(h->G) * 8) blocks = static_cast<int64_t>(h->G) * 8;
@@ -429,7 +459,7 @@ extern "C" int f2c_dcp_enqueue(f2c_dcp *h, const void *g_feats, const int64_t *l
         Rank &R = h->ranks[0];
         NcclApi &api = nccl();
         api.GroupStart();
-        api.AllGather(g_feats, R.base + R.L.blk_x, m_local * h->d * es, NCCL_INT8, h->comm, st);
+        api.AllGather(g_feats, R.base + R.L.blk_x, m_local * h->K * h->d * es, NCCL_INT8, h->comm, st);
         api.AllGather(labels, R.base + R.L.blk_y, m_local, NCCL_INT64, h->comm, st);
         if ((rc = nccl_check(api.GroupEnd(), "enqueue all-gather"))) return rc;
         if ((rc = enqueue_rank(h, R, R.base + R.L.blk_x, R.at<int64_t>(R.L.blk_y), m_glob, st))) return rc;
@@ -575,6 +605,7 @@ static int phase_main(f2c_dcp *h, Rank &R, const StepCtx &c, int64_t occ_loc) {
         q.row_ab = p.row_ab;
         q.row_tgt = p.row_tgt;
         q.X_pos = R.base + L.X_pos;
+        q.wslot = h->K > 1 ? R.at<float>(L.wslot) : nullptr;
         q.margin_l2 = p.margin_l2;
         q.ttgt = p.ttgt;
         q.seg_l = p.seg_l;
@@ -814,13 +845,13 @@ extern "C" int f2c_dcp_get_state(f2c_dcp *h, void *feats_host, int64_t *labels_h
                                  int64_t *enq_count_host) {
     if (!h) return fail(F2C_EINVAL, "NULL handle");
     CUDA_TRY(cudaDeviceSynchronize());
-    const size_t rb = static_cast<size_t>(h->d) * (h->dtype == F2C_BF16 ? 2 : 4);
+    const size_t rb = static_cast<size_t>(h->d) * h->K * (h->dtype == F2C_BF16 ? 2 : 4);
     int64_t row0 = 0;
     for (Rank &R : h->ranks) {
         const int64_t n = R.hi - R.lo;
         if (feats_host)
-            CUDA_TRY(cudaMemcpy(static_cast<uint8_t *>(feats_host) + row0 * rb, R.base + R.L.T, n * rb,
-                                cudaMemcpyDeviceToHost));
+            CUDA_TRY(cudaMemcpy(static_cast<uint8_t *>(feats_host) + row0 * rb, R.base + (h->K > 1 ? R.L.Traw : R.L.T),
+                                n * rb, cudaMemcpyDeviceToHost));
         if (labels_host) {
             CUDA_TRY(cudaMemcpy(labels_host + row0, R.at<int64_t>(R.L.lab), n * 8, cudaMemcpyDeviceToHost));
             const int64_t occ = occ_local(h, R);
@@ -836,7 +867,7 @@ extern "C" int f2c_dcp_set_state(f2c_dcp *h, const void *feats_host, const int64
                                  int64_t enq_count) {
     if (!h) return fail(F2C_EINVAL, "NULL handle");
     if (!feats_host || !labels_host || enq_count < 0) return fail(F2C_EINVAL, "bad set_state arguments");
-    const size_t rb = static_cast<size_t>(h->d) * (h->dtype == F2C_BF16 ? 2 : 4);
+    const size_t rb = static_cast<size_t>(h->d) * h->K * (h->dtype == F2C_BF16 ? 2 : 4);
     const int64_t C_occ = enq_count < h->C ? enq_count : h->C;
     int64_t row0 = 0;
     for (Rank &R : h->ranks) {
@@ -856,14 +887,21 @@ extern "C" int f2c_dcp_set_state(f2c_dcp *h, const void *feats_host, const int64
         int64_t occ = C_occ - R.lo;
         if (occ > n) occ = n;
         if (occ < 0) occ = 0;
-        CUDA_TRY(cudaMemset(R.base + R.L.T, 0, n * rb));
+        uint8_t *dstT = R.base + (h->K > 1 ? R.L.Traw : R.L.T);
+        CUDA_TRY(cudaMemset(dstT, 0, n * rb));
+        if (h->K > 1) CUDA_TRY(cudaMemset(R.base + R.L.T, 0, n * static_cast<size_t>(h->d) * 2));
         if (occ > 0)
-            CUDA_TRY(cudaMemcpy(R.base + R.L.T, static_cast<const uint8_t *>(feats_host) + row0 * rb,
+            CUDA_TRY(cudaMemcpy(dstT, static_cast<const uint8_t *>(feats_host) + row0 * rb,
                                 occ * rb, cudaMemcpyHostToDevice));
         CUDA_TRY(cudaMemcpy(R.at<int64_t>(R.L.lab), labels_host + row0, n * 8, cudaMemcpyHostToDevice));
         int zero = 0;
         CUDA_TRY(cudaMemcpy(&R.sc()->tmax_bits, &zero, 4, cudaMemcpyHostToDevice));
-        if (occ > 0) {
+        if (occ > 0 && h->K > 1) {
+            k_rebuild_k<<<static_cast<unsigned>((occ * 32 + 255) / 256), 256>>>(
+                R.at<__nv_bfloat16>(R.L.Traw), occ, h->K, h->d, R.at<__nv_bfloat16>(R.L.T),
+                R.at<float>(R.L.wslot), R.sc());
+            CUDA_TRY(cudaGetLastError());
+        } else if (occ > 0) {
             k_pool_norm_max<<<static_cast<unsigned>((occ * 32 + 255) / 256), 256>>>(
                 R.base + R.L.T, occ, static_cast<int>(rb), h->dtype, R.sc());
             CUDA_TRY(cudaGetLastError());

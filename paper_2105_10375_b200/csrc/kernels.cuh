@@ -124,6 +124,99 @@ __global__ void __launch_bounds__(256) k_enqueue(const uint8_t *__restrict__ g, 
     }
 }
 
+// K >= 2 features per slot (NEXT-1): block row j carries K bf16 feature rows.
+// The raw rows are copied bit-exactly (state / checkpoint); the derived operand of every
+// kernel is T_bar = (1/K) sum_k T[c,k] (Eq. 8), fp32 mean rounded to bf16, plus
+// w_c = 1/||T_bar_c|| (0 for a zero center) for the true-cosine L_cos (reading R4).
+// One warp per row, d <= 512 (16 elements per lane).
+__global__ void __launch_bounds__(256) k_enqueue_k(const __nv_bfloat16 *__restrict__ g, const int64_t *__restrict__ y,
+                                                   int64_t m_glob, int K, int d, int64_t E, int64_t C,
+                                                   int64_t lo, int64_t hi, __nv_bfloat16 *__restrict__ Traw,
+                                                   __nv_bfloat16 *__restrict__ Tbar, float *__restrict__ wslot,
+                                                   int64_t *__restrict__ lab, Scalars *sc) {
+    __shared__ float wmax[8];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+    float nmax = 0.f;
+    for (int64_t j = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + wib; j < m_glob; j += nwarps) {
+        const int64_t c = (E + j) % C;
+        if (c < lo || c >= hi) continue;
+        const int64_t yl = y[j];
+        if (yl < 0) {
+            if (lane == 0) latch(sc, ERR_DEVICE, DET_BAD_LABEL);
+            continue;
+        }
+        float acc[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) acc[e] = 0.f;
+        for (int kk = 0; kk < K; ++kk) {
+            const __nv_bfloat16 *src = g + (j * K + kk) * d;
+            __nv_bfloat16 *dst = Traw + ((c - lo) * K + kk) * d;
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+                const int col = e * 32 + lane;
+                if (col < d) {
+                    const __nv_bfloat16 v = src[col];
+                    dst[col] = v;
+                    acc[e] += __bfloat162float(v);
+                }
+            }
+        }
+        float ss = 0.f;
+        const float invK = 1.0f / static_cast<float>(K);
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+            const int col = e * 32 + lane;
+            if (col < d) {
+                const __nv_bfloat16 m = __float2bfloat16_rn(acc[e] * invK);
+                Tbar[(c - lo) * d + col] = m;
+                const float mf = __bfloat162float(m);
+                ss += mf * mf;
+            }
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+        if (lane == 0) {
+            lab[c - lo] = yl;
+            wslot[c - lo] = ss > 0.f ? rsqrtf(ss) : 0.f;
+        }
+        nmax = fmaxf(nmax, ss);
+    }
+    if (lane == 0) wmax[wib] = nmax;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float mx = 0.f;
+        for (int i = 0; i < (blockDim.x >> 5); ++i) mx = fmaxf(mx, wmax[i]);
+        float nrm = sqrtf(mx);
+        if (!(nrm <= 3.0e38f)) nrm = 3.0e38f;
+        if (nrm > 0.f) atomicMax(&sc->tmax_bits, __float_as_int(nrm));
+    }
+}
+
+// set_state with K >= 2: rebuild T_bar, w and the norm bound from the raw features
+__global__ void __launch_bounds__(256) k_rebuild_k(const __nv_bfloat16 *__restrict__ Traw, int64_t rows, int K, int d,
+                                                   __nv_bfloat16 *__restrict__ Tbar, float *__restrict__ wslot,
+                                                   Scalars *sc) {
+    const int lane = threadIdx.x & 31;
+    const int64_t r = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    if (r >= rows) return;
+    float ss = 0.f;
+    for (int col = lane; col < d; col += 32) {
+        float acc = 0.f;
+        for (int kk = 0; kk < K; ++kk) acc += __bfloat162float(Traw[(r * K + kk) * d + col]);
+        const __nv_bfloat16 m = __float2bfloat16_rn(acc * (1.0f / static_cast<float>(K)));
+        Tbar[r * d + col] = m;
+        ss += __bfloat162float(m) * __bfloat162float(m);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    if (lane == 0) {
+        wslot[r] = ss > 0.f ? rsqrtf(ss) : 0.f;
+        float nrm = sqrtf(ss);
+        if (nrm > 0.f) atomicMax(&sc->tmax_bits, __float_as_int(nrm));
+    }
+}
+
 // recompute the norm bound over a whole shard (after set_state)
 __global__ void k_pool_norm_max(const uint8_t *__restrict__ T, int64_t rows, int row_bytes,
                                 int dtype, Scalars *sc) {

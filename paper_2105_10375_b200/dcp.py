@@ -37,6 +37,9 @@ def load_library():
     L.f2c_dcp_state_bytes.argtypes = [i64, i32, i32, i32, i32, i64, i64]
     L.f2c_dcp_state_bytes.restype = sz
     L.f2c_dcp_create.argtypes = [i64, i32, i32, i32, i32, P, P, sz, i64, i64, ctypes.POINTER(P)]
+    L.f2c_dcp_state_bytes_k.argtypes = [i64, i32, i32, i32, i32, i32, i64, i64]
+    L.f2c_dcp_state_bytes_k.restype = sz
+    L.f2c_dcp_create_k.argtypes = [i64, i32, i32, i32, i32, i32, P, P, sz, i64, i64, ctypes.POINTER(P)]
     L.f2c_dcp_enqueue.argtypes = [P, P, P, i64, P]
     L.f2c_dcp_loss_fwd_bwd.argtypes = [P, P, P, P, i64, f32, f32, P, P, P]
     L.f2c_gnet_ema.argtypes = [P, P, i64, f64, P]
@@ -51,7 +54,7 @@ def load_library():
     L.f2c_dcp_profile_read.argtypes = [P, P, P, P]
     L.f2c_dcp_destroy.argtypes = [P]
     L.f2c_dcp_destroy.restype = None
-    for f in (L.f2c_dcp_create, L.f2c_dcp_enqueue, L.f2c_dcp_loss_fwd_bwd, L.f2c_gnet_ema,
+    for f in (L.f2c_dcp_create, L.f2c_dcp_create_k, L.f2c_dcp_enqueue, L.f2c_dcp_loss_fwd_bwd, L.f2c_gnet_ema,
               L.f2c_dcp_get_state, L.f2c_dcp_set_state, L.f2c_dcp_row_stats, L.f2c_dcp_check,
               L.f2c_last_launch_count, L.f2c_dcp_profile, L.f2c_dcp_profile_read):
         f.restype = ctypes.c_int
@@ -85,21 +88,21 @@ class DCPHead:
 
     def __init__(self, C: int, d: int, dtype: int = BF16, world: int = 1, rank: int = 0,
                  n_local_max: int = 1024, m_local_max: int = 512, nccl_uid: bytes | None = None,
-                 device=None):
+                 device=None, K: int = 1):
         L = load_library()
         if not torch.cuda.is_available():
             raise DCPError(5, "no CUDA device: the DCP head has no CPU path")
         self.C, self.d, self.dtype, self.world, self.rank = int(C), int(d), int(dtype), world, rank
-        self.n_local_max, self.m_local_max = int(n_local_max), int(m_local_max)
-        nbytes = L.f2c_dcp_state_bytes(C, d, dtype, world, rank, n_local_max, m_local_max)
+        self.n_local_max, self.m_local_max, self.K = int(n_local_max), int(m_local_max), int(K)
+        nbytes = L.f2c_dcp_state_bytes_k(C, K, d, dtype, world, rank, n_local_max, m_local_max)
         if nbytes == 0:
             raise DCPError(1, "invalid configuration for f2c_dcp_state_bytes")
         self.device = torch.device("cuda") if device is None else torch.device(device)
         self.state = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
         self._h = ctypes.c_void_p()
         uid = None if nccl_uid is None else ctypes.create_string_buffer(bytes(nccl_uid), 128)
-        _check(L.f2c_dcp_create(C, d, dtype, world, rank, uid, _ptr(self.state), nbytes,
-                                n_local_max, m_local_max, ctypes.byref(self._h)))
+        _check(L.f2c_dcp_create_k(C, K, d, dtype, world, rank, uid, _ptr(self.state), nbytes,
+                                  n_local_max, m_local_max, ctypes.byref(self._h)))
         self.loss_buf = torch.zeros((), dtype=torch.float32, device=self.device)
 
     # -- the hot path -----------------------------------------------------------------
@@ -135,7 +138,8 @@ class DCPHead:
             lo = self.C * self.rank // self.world
             hi = self.C * (self.rank + 1) // self.world
             rows = hi - lo
-        feats = np.empty((rows, self.d), dtype=np.uint16 if self.dtype == BF16 else np.float32)
+        shape = (rows, self.d) if self.K == 1 else (rows, self.K, self.d)
+        feats = np.empty(shape, dtype=np.uint16 if self.dtype == BF16 else np.float32)
         labs = np.empty(rows, dtype=np.int64)
         E = ctypes.c_int64()
         _check(load_library().f2c_dcp_get_state(self._h, feats.ctypes.data_as(ctypes.c_void_p),
