@@ -22,6 +22,7 @@ _SRC = os.path.join(_HERE, "f2c_oracle.c")
 _LIB = os.path.join(_HERE, "libf2c_oracle.so")
 
 BF16, F32 = 0, 1
+PHI_MEAN, PHI_SUM, PHI_MAX = 0, 1, 2   # NEXT-3 reductions of phi over the pool
 
 _lib = None
 
@@ -52,8 +53,12 @@ def lib():
                                  P, P, P, P, P, P, P, P, P]
         L.orc_loss_rows_k.argtypes = [i64, i32, i32, i32, P, P, i64, i64, i64, P, P, P, f64, f64,
                                       i64, P, P, P, P, P, P, P, P]
+        L.orc_loss_v.argtypes = [i64, i32, i32, i32, P, P, i64, i64, i64, P, P, P, f64, f64,
+                                 i32, i32, f64, P, P, P, P, P, P, P, P, P]
+        L.orc_loss_rows_v.argtypes = [i64, i32, i32, i32, P, P, i64, i64, i64, P, P, P, f64, f64,
+                                      i32, i32, f64, i64, P, P, P, P, P, P, P, P]
         for f in (L.orc_enqueue, L.orc_loss, L.orc_loss_rows, L.orc_ema, L.orc_loss_k,
-                  L.orc_loss_rows_k):
+                  L.orc_loss_rows_k, L.orc_loss_v, L.orc_loss_rows_v):
             f.restype = ctypes.c_int
         _lib = L
     return _lib
@@ -123,7 +128,8 @@ class Pool:
             raise OracleError(rc, "orc_enqueue")
 
     def loss(self, X: np.ndarray, y: np.ndarray, pairing: np.ndarray | None, s: float, m: float,
-             want_P: bool = False, want_dT: bool = False) -> LossResult:
+             want_P: bool = False, want_dT: bool = False, phi_mode: int = PHI_MEAN,
+             hinge: bool = False, lam: float = 1.0) -> LossResult:
         X = np.ascontiguousarray(X)
         y = np.ascontiguousarray(y, dtype=np.int64)
         N, d = len(y), self.d
@@ -137,16 +143,18 @@ class Pool:
         counts = np.zeros(3, dtype=np.int64)
         P = np.zeros((N, self.C_occ)) if want_P else None
         dT = np.zeros((self.C, d)) if want_dT else None
-        rc = lib().orc_loss_k(self.C, self.K, d, self.dtype, _p(self.T), _p(self.lab),
+        rc = lib().orc_loss_v(self.C, self.K, d, self.dtype, _p(self.T), _p(self.lab),
                               int(self.E[0]), int(self.M_last[0]), N, _p(X), _p(y), _p(pr),
-                              float(s), float(m), _p(out3), _p(dx), _p(lse), _p(ts), _p(phi),
-                              _p(ell), _p(counts), _p(P), _p(dT))
+                              float(s), float(m), int(phi_mode), int(bool(hinge)), float(lam),
+                              _p(out3), _p(dx), _p(lse), _p(ts), _p(phi), _p(ell), _p(counts),
+                              _p(P), _p(dT))
         if rc:
             raise OracleError(rc, "orc_loss")
         return LossResult(out3[0], out3[1], out3[2], dx, lse, ts, phi, ell,
                           int(counts[0]), int(counts[1]), int(counts[2]), P, dT)
 
-    def loss_rows(self, X, y, pairing, s, m, rows):
+    def loss_rows(self, X, y, pairing, s, m, rows, phi_mode: int = PHI_MEAN, hinge: bool = False,
+                  lam: float = 1.0):
         X = np.ascontiguousarray(X)
         y = np.ascontiguousarray(y, dtype=np.int64)
         rows = np.ascontiguousarray(rows, dtype=np.int64)
@@ -157,9 +165,10 @@ class Pool:
         ts = np.zeros(k, dtype=np.int64)
         counts = np.zeros(3, dtype=np.int64)
         mu = np.zeros(d)
-        rc = lib().orc_loss_rows_k(self.C, self.K, d, self.dtype, _p(self.T), _p(self.lab),
+        rc = lib().orc_loss_rows_v(self.C, self.K, d, self.dtype, _p(self.T), _p(self.lab),
                                    int(self.E[0]), int(self.M_last[0]), N, _p(X), _p(y), _p(pr),
-                                   float(s), float(m), k, _p(rows), _p(dx), _p(lse), _p(ts),
+                                   float(s), float(m), int(phi_mode), int(bool(hinge)), float(lam),
+                                   k, _p(rows), _p(dx), _p(lse), _p(ts),
                                    _p(phi), _p(ell), _p(counts), _p(mu))
         if rc:
             raise OracleError(rc, "orc_loss_rows")

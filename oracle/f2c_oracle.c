@@ -29,6 +29,14 @@
  *                    <x_hat, T_bar_c> / ||T_bar_c|| ("phi ... cosine similarity",
  *                    "T_bar ... average along the axis of K"; reading R4), a zero-norm
  *                    center contributing 0.  K = 1 is exactly orc_loss.
+ *   orc_loss_v / orc_loss_rows_v
+ *                    NEXT-3 variants of the L_cos term (the paper leaves the reduction of
+ *                    phi over the pool unstated; SPEC's open questions S:399,
+ *                    S:426): phi_mode 0 = mean over the occupied centers (D10,
+ *                    default), 1 = sum, 2 = max (hardest negative, first slot on ties);
+ *                    hinge = 1 penalises only positive similarity, max(0, cos); and the
+ *                    weight lambda on L_cos (L_total = L_ce + lambda L_cos).
+ *                    orc_loss_k is orc_loss_v with (mean, no hinge, lambda = 1).
  *
  * Parity status: every function here is pinned by tests/test_oracle_pins.py
  * (pins P1-P8 of DESIGN.md section 4).  The semantics choices D3 (margin form),
@@ -101,6 +109,9 @@ typedef struct {
     int64_t *t;    /* [N] target slot or -1 (Eq. 6 split) */
     int64_t N_pos, N_neg;
     double *mu;    /* [d] sum over occupied slots of T_c */
+    /* NEXT-3 variants of L_cos */
+    int32_t phi_mode, hinge;
+    double lam;
 } orc_ctx;
 
 /* T_bar[c][k] = (1/K) sum_kk T[c][kk][k]  (Eq. 8's average over the K axis) */
@@ -205,22 +216,40 @@ static void orc_row(const orc_ctx *q, int64_t i, double *ell, double *phi, doubl
                     dT[c * d + k] += gc * orc_elem(q->X, q->dtype, i * d + k) * inv_n;
         }
     } else {
-        /* L_cos: phi_i = mean over occupied slots of cos(x_i, T_bar_c)  (D10, R4) */
+        /* L_cos: phi_i = R_c h(cos(x_i, T_bar_c)) over the occupied centers with a
+         * nonzero T_bar, R = mean (D10) / sum / max, h = identity or the hinge
+         * max(0, .) (NEXT-3); cos is the true cosine <x_hat, T_bar_c>/||T_bar_c|| (R4).
+         * Gradient: (lambda / N_neg) dphi/dx_hat (P:167 normaliser 1/(M-I)). */
         if (Co > 0) {
-            double acc = 0.0;
+            double acc = 0.0, best = -INFINITY;
+            int64_t cbest = -1;
             for (int64_t c = 0; c < Co; ++c) {
                 double tn = orc_tbar_norm(q, c);
-                if (tn > 0.0) acc += cos_buf[c] / tn;
+                if (!(tn > 0.0)) continue;
+                double cs = cos_buf[c] / tn;
+                if (q->phi_mode == 2) {
+                    if (cs > best) { best = cs; cbest = c; }
+                } else {
+                    acc += q->hinge ? (cs > 0.0 ? cs : 0.0) : cs;
+                }
             }
-            *phi = acc / (double)Co;
-            double w = 1.0 / ((double)q->N_neg * (double)Co);
+            double w = q->lam / (double)q->N_neg;  /* dL/dphi_i */
+            if (q->phi_mode == 0) { *phi = acc / (double)Co; w /= (double)Co; }
+            else if (q->phi_mode == 1) { *phi = acc; }
+            else { *phi = cbest < 0 ? 0.0 : (q->hinge && best <= 0.0 ? 0.0 : best); }
             for (int64_t c = 0; c < Co; ++c) {
                 double tn = orc_tbar_norm(q, c);
-                double wc = tn > 0.0 ? w / tn : 0.0;
+                if (!(tn > 0.0)) continue;
+                double cs = cos_buf[c] / tn;
+                double hp;  /* dphi_i / dcos_c (before the reduction weight w) */
+                if (q->phi_mode == 2) hp = (c == cbest && !(q->hinge && cs <= 0.0)) ? 1.0 : 0.0;
+                else hp = q->hinge ? (cs > 0.0 ? 1.0 : 0.0) : 1.0;
+                if (hp == 0.0) continue;
+                double wc = w * hp / tn;
                 for (int32_t k = 0; k < d; ++k) g[k] += wc * orc_tbar(q, c, k);
                 if (dT)
                     for (int32_t k = 0; k < d; ++k)
-                        dT[c * d + k] += w * orc_elem(q->X, q->dtype, i * d + k) * inv_n;
+                        dT[c * d + k] += wc * orc_elem(q->X, q->dtype, i * d + k) * inv_n;
             }
         }
     }
@@ -237,16 +266,19 @@ static void orc_row(const orc_ctx *q, int64_t i, double *ell, double *phi, doubl
  * out3 = {L, L_ce, L_cos}; dx [N*d]; lse [N] (0 for out-of-pool rows); tslot [N];
  * phi [N] (0 for in-pool rows); ell [N] (0 for out-of-pool rows);
  * counts = {N_pos, N_neg, C_occ}; P [N * C_occ] or NULL; dT [C * d] or NULL. */
-int orc_loss_k(int64_t C, int32_t K, int32_t d, int32_t dtype, const void *T, const int64_t *lab,
+int orc_loss_v(int64_t C, int32_t K, int32_t d, int32_t dtype, const void *T, const int64_t *lab,
                int64_t E, int64_t M_last, int64_t N, const void *X, const int64_t *y,
-               const int32_t *pairing, double s, double m, double *out3, double *dx, double *lse,
-               int64_t *tslot, double *phi, double *ell, int64_t *counts, double *P, double *dT) {
+               const int32_t *pairing, double s, double m, int32_t phi_mode, int32_t hinge,
+               double lam, double *out3, double *dx, double *lse, int64_t *tslot, double *phi,
+               double *ell, int64_t *counts, double *P, double *dT) {
     if (C < 1 || d < 1 || K < 1 || N < 0 || (dtype != 0 && dtype != 1)) return ORC_EINVAL;
     if (!(s > 0.0) || !isfinite(m)) return ORC_EINVAL;
+    if (phi_mode < 0 || phi_mode > 2 || hinge < 0 || hinge > 1 || !isfinite(lam)) return ORC_EINVAL;
     if (dT && K != 1) return ORC_EINVAL;
     orc_ctx q = {0};
     q.C = C; q.N = N; q.E = E; q.M_last = M_last; q.d = d; q.dtype = dtype; q.K = K;
     q.T = T; q.lab = lab; q.X = X; q.y = y; q.s = s; q.m = m;
+    q.phi_mode = phi_mode; q.hinge = hinge; q.lam = lam;
     q.n = (double *)calloc((size_t)(N > 0 ? N : 1), sizeof(double));
     q.t = (int64_t *)calloc((size_t)(N > 0 ? N : 1), sizeof(int64_t));
     q.mu = (double *)calloc((size_t)d, sizeof(double));
@@ -266,13 +298,21 @@ int orc_loss_k(int64_t C, int32_t K, int32_t d, int32_t dtype, const void *T, co
         }
         double Lce = q.N_pos > 0 ? sce / (double)q.N_pos : 0.0;  /* 1/I */
         double Lcos = q.N_neg > 0 ? scos / (double)q.N_neg : 0.0; /* 1/(M-I) */
-        out3[0] = Lce + Lcos; /* L_total = L_ce + L_cos */
+        out3[0] = Lce + lam * Lcos; /* L_total = L_ce + L_cos; lambda: S:408 */
         out3[1] = Lce;
         out3[2] = Lcos;
         counts[0] = q.N_pos; counts[1] = q.N_neg; counts[2] = q.C_occ;
     }
     free(q.n); free(q.t); free(q.mu); free(cos_buf); free(g);
     return rc;
+}
+
+int orc_loss_k(int64_t C, int32_t K, int32_t d, int32_t dtype, const void *T, const int64_t *lab,
+               int64_t E, int64_t M_last, int64_t N, const void *X, const int64_t *y,
+               const int32_t *pairing, double s, double m, double *out3, double *dx, double *lse,
+               int64_t *tslot, double *phi, double *ell, int64_t *counts, double *P, double *dT) {
+    return orc_loss_v(C, K, d, dtype, T, lab, E, M_last, N, X, y, pairing, s, m, 0, 0, 1.0, out3, dx,
+                      lse, tslot, phi, ell, counts, P, dT);
 }
 
 int orc_loss(int64_t C, int32_t d, int32_t dtype, const void *T, const int64_t *lab, int64_t E,
@@ -286,15 +326,18 @@ int orc_loss(int64_t C, int32_t d, int32_t dtype, const void *T, const int64_t *
 /* Same definition for a subset of rows (for configurations too large for the
  * full O(N*C*d) evaluation).  Normalisers are global.  Outputs are per selected
  * row: dx [nsel*d], lse, tslot, phi, ell. counts = {N_pos, N_neg, C_occ}. */
-int orc_loss_rows_k(int64_t C, int32_t K, int32_t d, int32_t dtype, const void *T,
+int orc_loss_rows_v(int64_t C, int32_t K, int32_t d, int32_t dtype, const void *T,
                     const int64_t *lab, int64_t E, int64_t M_last, int64_t N, const void *X,
-                    const int64_t *y, const int32_t *pairing, double s, double m, int64_t nsel,
-                    const int64_t *rows, double *dx, double *lse, int64_t *tslot, double *phi,
-                    double *ell, int64_t *counts, double *mu_out) {
+                    const int64_t *y, const int32_t *pairing, double s, double m, int32_t phi_mode,
+                    int32_t hinge, double lam, int64_t nsel, const int64_t *rows, double *dx,
+                    double *lse, int64_t *tslot, double *phi, double *ell, int64_t *counts,
+                    double *mu_out) {
     if (C < 1 || d < 1 || K < 1 || N < 0 || (dtype != 0 && dtype != 1)) return ORC_EINVAL;
+    if (phi_mode < 0 || phi_mode > 2 || hinge < 0 || hinge > 1 || !isfinite(lam)) return ORC_EINVAL;
     orc_ctx q = {0};
     q.C = C; q.N = N; q.E = E; q.M_last = M_last; q.d = d; q.dtype = dtype; q.K = K;
     q.T = T; q.lab = lab; q.X = X; q.y = y; q.s = s; q.m = m;
+    q.phi_mode = phi_mode; q.hinge = hinge; q.lam = lam;
     q.n = (double *)calloc((size_t)(N > 0 ? N : 1), sizeof(double));
     q.t = (int64_t *)calloc((size_t)(N > 0 ? N : 1), sizeof(int64_t));
     q.mu = (double *)calloc((size_t)d, sizeof(double));
@@ -313,6 +356,15 @@ int orc_loss_rows_k(int64_t C, int32_t K, int32_t d, int32_t dtype, const void *
     }
     free(q.n); free(q.t); free(q.mu); free(cos_buf); free(g);
     return rc;
+}
+
+int orc_loss_rows_k(int64_t C, int32_t K, int32_t d, int32_t dtype, const void *T,
+                    const int64_t *lab, int64_t E, int64_t M_last, int64_t N, const void *X,
+                    const int64_t *y, const int32_t *pairing, double s, double m, int64_t nsel,
+                    const int64_t *rows, double *dx, double *lse, int64_t *tslot, double *phi,
+                    double *ell, int64_t *counts, double *mu_out) {
+    return orc_loss_rows_v(C, K, d, dtype, T, lab, E, M_last, N, X, y, pairing, s, m, 0, 0, 1.0, nsel,
+                           rows, dx, lse, tslot, phi, ell, counts, mu_out);
 }
 
 int orc_loss_rows(int64_t C, int32_t d, int32_t dtype, const void *T, const int64_t *lab,

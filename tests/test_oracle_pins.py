@@ -451,3 +451,121 @@ def test_k2_autograd_and_finite_differences():
                 return (p.loss(Xa, y, None, s, m).L - p.loss(Xb, y, None, s, m).L) / (2 * hh)
             num[i, k] = (4 * D(h / 2) - D(h)) / 3
     np.testing.assert_allclose(r.dx, num, rtol=1e-6, atol=1e-8)
+
+
+# ----------------------------------------------------------------------------- NEXT-3 phi variants
+from oracle import PHI_MAX, PHI_MEAN, PHI_SUM  # noqa: E402
+
+
+def test_phi_variants_spec_example():
+    """C=2, F = T_bar_0 (unit), T_bar_1 orthogonal -> mean L_cos = 0.5; the sum is
+    1.0 and the hardest negative (max) is 1.0.  With T_bar_1 = -F: mean 0, hinged mean 0.5,
+    max 1, sum 0 (closed forms of the NEXT-3 reductions)."""
+    F = [0.6, 0.8, 0.0]
+    for other, want in (([0.0, 0.0, 1.0], {(PHI_MEAN, 0): 0.5, (PHI_SUM, 0): 1.0, (PHI_MAX, 0): 1.0,
+                                             (PHI_MEAN, 1): 0.5, (PHI_MAX, 1): 1.0}),
+                        ([-0.6, -0.8, 0.0], {(PHI_MEAN, 0): 0.0, (PHI_SUM, 0): 0.0, (PHI_MAX, 0): 1.0,
+                                               (PHI_MEAN, 1): 0.5, (PHI_SUM, 1): 1.0})):
+        p = _pool_from([(F, 0), (other, 1)])
+        for (mode, hinge), L in want.items():
+            r = p.loss(np.array([F], np.float32), np.array([5]), None, 64.0, 0.35, phi_mode=mode,
+                       hinge=bool(hinge))
+            assert r.L == pytest.approx(L, abs=1e-7), (other, mode, hinge)
+
+
+def test_phi_max_hinge_all_negative_is_zero():
+    """Hardest negative with the hinge: every cosine <= 0 -> phi = 0 and zero gradient."""
+    p = _pool_from([([-1.0, 0.0], 0), ([0.0, -1.0], 1)])
+    r = p.loss(np.array([[0.6, 0.8]], np.float32), np.array([9]), None, 64.0, 0.0, phi_mode=PHI_MAX,
+               hinge=True)
+    assert r.L == 0.0 and np.all(r.dx == 0.0)
+    r = p.loss(np.array([[0.6, 0.8]], np.float32), np.array([9]), None, 64.0, 0.0, phi_mode=PHI_MAX)
+    assert r.L == pytest.approx(-0.6, abs=1e-7)
+
+
+def test_lambda_zero_is_ce_only():
+    """S:408: lambda = 0 gives L_total = L_ce and zero gradient on out-of-pool rows;
+    lambda scales L_cos and its gradient linearly."""
+    rng = np.random.default_rng(31)
+    C, d = 16, 8
+    T = rng.standard_normal((C, d)); T /= np.linalg.norm(T, axis=1, keepdims=True)
+    p = Pool(C, d, F32)
+    p.enqueue(T.astype(np.float32), rng.integers(0, 5, C))
+    X = rng.standard_normal((6, d)).astype(np.float32)
+    y = np.array([0, 1, 2, 40, 41, 42])
+    r1 = p.loss(X, y, None, 20.0, 0.3)
+    r0 = p.loss(X, y, None, 20.0, 0.3, lam=0.0)
+    r3 = p.loss(X, y, None, 20.0, 0.3, lam=3.0)
+    neg = r1.tslot < 0
+    assert r0.L == pytest.approx(r1.L_ce, rel=1e-14)
+    assert np.all(r0.dx[neg] == 0.0)
+    assert r3.L == pytest.approx(r1.L_ce + 3.0 * r1.L_cos, rel=1e-13)
+    np.testing.assert_allclose(r3.dx[neg], 3.0 * r1.dx[neg], rtol=1e-13)
+    np.testing.assert_array_equal(r3.dx[~neg], r1.dx[~neg])
+
+
+@pytest.mark.parametrize("mode,hinge", [(PHI_SUM, False), (PHI_MAX, False), (PHI_MEAN, True),
+                                        (PHI_SUM, True), (PHI_MAX, True)])
+@pytest.mark.parametrize("K", [1, 2])
+def test_phi_variants_autograd_and_finite_differences(mode, hinge, K):
+    """Each variant's oracle gradient == torch autograd of an independent formulation
+    (torch.max / relu over the true cosines) and == Richardson differences of the oracle's
+    own loss value (inputs away from ties and from cos = 0)."""
+    rng = np.random.default_rng(40 + mode * 2 + int(hinge) + 10 * K)
+    C, d = 9, 5
+    T = (rng.integers(-128, 128, (C, K, d)) / 128.0).astype(np.float32)
+    lab = rng.integers(0, 4, C)
+    p = Pool(C, d, F32, K=K)
+    p.enqueue(T if K > 1 else T[:, 0], lab)
+    X = (rng.integers(-256, 256, (6, d)) / 128.0).astype(np.float32)
+    y = np.array([0, 1, 2, 7, 8, 9])
+    s, m, lam = 12.0, 0.25, 0.7
+    kw = dict(phi_mode=mode, hinge=hinge, lam=lam)
+    r = p.loss(X, y, None, s, m, **kw)
+    Tb = torch.tensor(T.astype(np.float64)).mean(dim=1)
+    xt = torch.tensor(X.astype(np.float64), requires_grad=True)
+    cos = (xt / xt.norm(dim=1, keepdim=True)) @ Tb.T
+    tgt = [max([c for c in range(C) if lab[c] == y[i]], default=-1) for i in range(len(y))]
+    pos = [i for i in range(len(y)) if tgt[i] >= 0]
+    neg = [i for i in range(len(y)) if tgt[i] < 0]
+    ce = 0
+    for i in pos:
+        zi = s * cos[i].clone()
+        zi[tgt[i]] = zi[tgt[i]] - s * m
+        ce = ce + torch.logsumexp(zi, 0) - zi[tgt[i]]
+    # K = 1 keeps the stored rows as they are (D2); K >= 2 divides by ||T_bar|| (R4)
+    tcos = cos / Tb.norm(dim=1)[None, :] if K > 1 else cos
+    hc = torch.relu(tcos) if hinge else tcos
+    red = {PHI_SUM: lambda v: v.sum(), PHI_MAX: lambda v: v.max()}[mode] if mode != PHI_MEAN else (lambda v: v.mean())
+    loss = ce / len(pos) + lam * sum(red(hc[i]) for i in neg) / len(neg)
+    loss.backward()
+    assert r.L == pytest.approx(loss.item(), rel=1e-12)
+    np.testing.assert_allclose(r.dx, xt.grad.numpy(), rtol=1e-9, atol=1e-12)
+    h = 2.0 ** -10
+    num = np.zeros_like(r.dx)
+    for i in range(len(y)):
+        for k in range(d):
+            def D(hh):
+                Xa, Xb = X.copy(), X.copy()
+                Xa[i, k] += hh
+                Xb[i, k] -= hh
+                return (p.loss(Xa, y, None, s, m, **kw).L - p.loss(Xb, y, None, s, m, **kw).L) / (2 * hh)
+            num[i, k] = (4 * D(h / 2) - D(h)) / 3
+    np.testing.assert_allclose(r.dx, num, rtol=1e-5, atol=1e-7)
+
+
+def test_phi_sum_is_occupancy_times_mean_and_max_bounds_mean():
+    """Invariants: sum = C_occ * mean (per row); max >= mean; hinge(mean) >= mean."""
+    rng = np.random.default_rng(44)
+    C, d = 30, 16
+    T = rng.standard_normal((C, d)); T /= np.linalg.norm(T, axis=1, keepdims=True)
+    p = Pool(C, d, F32)
+    p.enqueue(T[:20].astype(np.float32), rng.integers(0, 10, 20))   # partially filled
+    X = rng.standard_normal((8, d)).astype(np.float32)
+    y = np.arange(100, 108)
+    mean = p.loss(X, y, None, 30.0, 0.3).phi
+    sm = p.loss(X, y, None, 30.0, 0.3, phi_mode=PHI_SUM).phi
+    mx = p.loss(X, y, None, 30.0, 0.3, phi_mode=PHI_MAX).phi
+    hm = p.loss(X, y, None, 30.0, 0.3, hinge=True).phi
+    np.testing.assert_allclose(sm, 20 * mean, rtol=1e-12)
+    assert np.all(mx >= mean) and np.all(hm >= mean)
