@@ -91,6 +91,19 @@ int f2c_dcp_create_k(int64_t C, int32_t K, int32_t d, int32_t dtype, int32_t wor
                      const void *nccl_uid, void *state_buf, size_t state_bytes,
                      int64_t n_local_max, int64_t m_local_max, f2c_dcp **out);
 
+/* NEXT-3 variants of the L_cos term, applied by every later loss call on this handle.
+ * The paper names phi only as "calculating the cosine similarity" between the out-of-pool
+ * features and T and sums L_ce + L_cos unweighted; SPEC leaves the
+ * reduction over the pool and a hinge open.
+ *   phi_mode 0 = mean over the occupied centers (default, D10), 1 = sum, 2 = max (hardest
+ *            negative; the first slot wins ties);
+ *   hinge    1 replaces cos by max(0, cos) (only positive similarity is penalised);
+ *   lambda   L = L_ce + lambda L_cos (default 1).
+ * Cosines are the true cosines for K >= 2 (R4); zero centers are skipped.  Modes
+ * other than (mean or sum, no hinge) run the out-of-pool rows through the fused kernel
+ * too (their GEMM cost is the in-pool rows').  Errors: F2C_EINVAL for out-of-range values. */
+int f2c_dcp_set_lcos(f2c_dcp *h, int32_t phi_mode, int32_t hinge, double lambda);
+
 /* Enqueue one identity block (Eq. 7 + Algorithm 1):
  * the global block is the concatenation of every rank's g_feats in rank order
  * (emulated world: g_feats already holds the concatenation, world*m_local rows).

@@ -61,12 +61,17 @@ struct PCAux {
     uint32_t pad;
     float red_l[2][PC_R];
     float red_mx[2][PC_R];
+    int red_arg[2][PC_R];
 };
+static_assert(sizeof(PCAux) <= 4096, "PCAux must fit the aux region");
 
 struct PCParams {
     int d;                 // feature dim (multiple of 128, <= 512)
     int n_slots;           // occupied slots of this shard
     const int *n_pos;      // device: in-pool rows; the mu row is row *n_pos
+    const int *n_rows;     // device: rows to process (n_pos + 1, or N + 1 with NEXT-3 neg rows)
+    int neg_mode;          // 0; 1 = hinge (p = [cos > 0] w_c, l = sum relu(cos)); 2 = max cos
+    int *seg_arg;          // [S][128] local argmax slot (neg_mode 2)
     const float2 *row_ab;  // [R_max] (a_r, b_r)
     const int *row_tgt;    // [R_max] local target slot or -1
     const uint8_t *X_pos;  // [R_max, d] bf16 compacted rows
@@ -183,7 +188,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
     const int nstg = nchunk / cps;
     const uint32_t stage_bytes = static_cast<uint32_t>(cps) * 16384;
     const int n_pos = *p.n_pos;
-    const int n_rg = (n_pos + 1 + PC_R - 1) / PC_R;
+    const int n_rows = *p.n_rows;
+    const int n_rg = (n_rows + PC_R - 1) / PC_R;
     const int n_tiles = (p.n_slots + PC_TILE - 1) / PC_TILE;
 
     if (threadIdx.x == 0) {
@@ -352,6 +358,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&aux->xready);
                 float lacc = 0.f, mx = -INFINITY;
+                int barg = -1;
+                // NEXT-3: out-of-pool rows compacted after the mu row (a = 1/||x||, b = 0)
+                const bool negrow = p.neg_mode != 0 && row > n_pos && row < n_rows;
                 for (int t = t0; t < t1; ++t, ++jt) {
                     const uint32_t sb = jt & 1, sph = (jt >> 1) & 1;
                     mbar_wait(&aux->sfull[sb], sph);
@@ -376,41 +385,70 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                     if (lane == 0) mbar_arrive(&aux->sempty[sb]);
                     const int base = t * PC_TILE + h * 64;
                     const int nval = p.n_slots - base;  // valid slots in my 64-wide half
-                    if (nval >= 64) {
+                    uint32_t w[32];
+                    if (!negrow) {
+                        if (nval >= 64) {
 #pragma unroll
-                        for (int k = 0; k < 64; ++k) e[k] = fmaf(e[k], ab.x, -ab.y);
-                    } else {
+                            for (int k = 0; k < 64; ++k) e[k] = fmaf(e[k], ab.x, -ab.y);
+                        } else {
 #pragma unroll
-                        for (int k = 0; k < 64; ++k) e[k] = k < nval ? fmaf(e[k], ab.x, -ab.y) : -INFINITY;
-                    }
-                    const bool hit = tg >= base && tg < base + 64;
-                    if (__any_sync(0xffffffffu, hit)) {
-                        if (hit) {
-                            const int kt = tg - base;
+                            for (int k = 0; k < 64; ++k) e[k] = k < nval ? fmaf(e[k], ab.x, -ab.y) : -INFINITY;
+                        }
+                        const bool hit = tg >= base && tg < base + 64;
+                        if (__any_sync(__activemask(), hit)) {
+                            if (hit) {
+                                const int kt = tg - base;
+#pragma unroll
+                                for (int k = 0; k < 64; ++k)
+                                    if (k == kt) {
+                                        p.ttgt[row] = e[k] - p.margin_l2;
+                                        e[k] = -INFINITY;
+                                    }
+                            }
+                        }
+                        if (p.wslot && row == n_pos) {  // mu row with K >= 2: p_c = 1/||T_bar_c||
 #pragma unroll
                             for (int k = 0; k < 64; ++k)
-                                if (k == kt) {
-                                    p.ttgt[row] = e[k] - p.margin_l2;
-                                    e[k] = -INFINITY;
-                                }
+                                e[k] = k < nval ? __log2f(fmaxf(p.wslot[base + k], 1e-30f)) : -INFINITY;
                         }
-                    }
-                    if (p.wslot && row == n_pos) {  // mu row with K >= 2: p_c = 1/||T_bar_c||
+                        float la[4] = {0.f, 0.f, 0.f, 0.f}, ma[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-                        for (int k = 0; k < 64; ++k)
-                            e[k] = k < nval ? __log2f(fmaxf(p.wslot[base + k], 1e-30f)) : -INFINITY;
-                    }
-                    uint32_t w[32];
-                    float la[4] = {0.f, 0.f, 0.f, 0.f}, ma[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+                        for (int k = 0; k < 64; k += 2) {
+                            const float p0 = ex2_approx(e[k]), p1 = ex2_approx(e[k + 1]);
+                            la[(k >> 1) & 3] += p0 + p1;
+                            ma[(k >> 1) & 3] = fmaxf(ma[(k >> 1) & 3], fmaxf(e[k], e[k + 1]));
+                            w[k >> 1] = pack_bf16x2(p0, p1);
+                        }
+                        lacc += (la[0] + la[1]) + (la[2] + la[3]);
+                        mx = fmaxf(mx, fmaxf(fmaxf(ma[0], ma[1]), fmaxf(ma[2], ma[3])));
+                    } else {
+                        // cosine c = <x_hat, T_bar_c> w_c (w_c = 1 for K = 1; zero centers are
+                        // no candidates for the max and contribute 0 to the hinge)
+                        float pv[64];
 #pragma unroll
-                    for (int k = 0; k < 64; k += 2) {
-                        const float p0 = ex2_approx(e[k]), p1 = ex2_approx(e[k + 1]);
-                        la[(k >> 1) & 3] += p0 + p1;
-                        ma[(k >> 1) & 3] = fmaxf(ma[(k >> 1) & 3], fmaxf(e[k], e[k + 1]));
-                        w[k >> 1] = pack_bf16x2(p0, p1);
+                        for (int k = 0; k < 64; ++k) {
+                            float c = e[k] * ab.x, wc = 1.f;
+                            bool ok = k < nval;
+                            if (p.wslot && ok) {
+                                wc = p.wslot[base + k];
+                                ok = wc > 0.f;
+                                c *= wc;
+                            }
+                            if (p.neg_mode == 1) {
+                                const bool pos = ok && c > 0.f;
+                                lacc += pos ? c : 0.f;
+                                pv[k] = pos ? wc : 0.f;
+                            } else {
+                                if (ok && c > mx) {
+                                    mx = c;
+                                    barg = base + k;
+                                }
+                                pv[k] = 0.f;
+                            }
+                        }
+#pragma unroll
+                        for (int k = 0; k < 64; k += 2) w[k >> 1] = pack_bf16x2(pv[k], pv[k + 1]);
                     }
-                    lacc += (la[0] + la[1]) + (la[2] + la[3]);
-                    mx = fmaxf(mx, fmaxf(fmaxf(ma[0], ma[1]), fmaxf(ma[2], ma[3])));
                     // P -> staging buffer in the consumer's K-major SW128 A layout:
                     // chunk h = slots [64h, 64h+64), row r: 128 B, 16-B unit u at u ^ (r & 7)
                     const uint32_t b = jt & 1, ph = (jt >> 1) & 1;
@@ -429,10 +467,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                 // segment end: l and max over both slot halves
                 aux->red_l[h][r] = lacc;
                 aux->red_mx[h][r] = mx;
+                aux->red_arg[h][r] = barg;
                 named_bar_sync(1, 256);
                 if (h == 0) {
                     p.seg_l[static_cast<size_t>(seg) * PC_R + r] = aux->red_l[0][r] + aux->red_l[1][r];
-                    p.seg_mx[static_cast<size_t>(seg) * PC_R + r] = fmaxf(aux->red_mx[0][r], aux->red_mx[1][r]);
+                    const float m0 = aux->red_mx[0][r], m1 = aux->red_mx[1][r];
+                    p.seg_mx[static_cast<size_t>(seg) * PC_R + r] = fmaxf(m0, m1);
+                    if (negrow && p.neg_mode == 2) {  // first slot on ties
+                        const int a0 = aux->red_arg[0][r], a1 = aux->red_arg[1][r];
+                        const bool take1 = a1 >= 0 && (a0 < 0 || m1 > m0 || (m1 == m0 && a1 < a0));
+                        p.seg_arg[static_cast<size_t>(seg) * PC_R + r] = take1 ? a1 : a0;
+                    }
                 }
                 named_bar_sync(1, 256);
                 ++sg;

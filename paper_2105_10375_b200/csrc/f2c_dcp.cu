@@ -102,7 +102,7 @@ static bool force_multi() {
 struct Layout {
     size_t T, lab, sc, x_all, y_all, pair_all, blk_x, blk_y, inv_n, hslot, hkeys, hvals, tseq,
         comp_idx, pos_row, X_pos, row_ab, row_tgt, ttgt, seg_l, seg_mx, seg_O, rowloss, st_lse,
-        st_cos, st_phi, st_ell, rs_buf, rs_all, dx_part, tseq_ext, dx32, tmax_glob, mu_buf, Traw, wslot,
+        st_cos, st_phi, st_ell, seg_arg, rs_buf, rs_all, dx_part, tseq_ext, dx32, tmax_glob, mu_buf, Traw, wslot,
         total;
     int64_t C_loc, N, Mg, R_max, S_max;
     int H;
@@ -145,13 +145,14 @@ static Layout make_layout(int64_t C, int d, int dtype, int W, int rank, int64_t 
     L.hvals = take(static_cast<size_t>(H) * 8);
     L.tseq = take(static_cast<size_t>(L.N) * 8);
     L.comp_idx = take(static_cast<size_t>(L.N) * 4);
-    L.pos_row = take(static_cast<size_t>(L.N) * 4);
+    L.pos_row = take(static_cast<size_t>(L.R_max) * 4);
     L.X_pos = take(static_cast<size_t>(L.R_max) * d * 2, 1024);
     L.row_ab = take(static_cast<size_t>(L.R_max) * 8);
     L.row_tgt = take(static_cast<size_t>(L.R_max) * 4);
     L.ttgt = take(static_cast<size_t>(L.R_max) * 4);
     L.seg_l = take(static_cast<size_t>(L.S_max) * 128 * 4);
     L.seg_mx = take(static_cast<size_t>(L.S_max) * 128 * 4);
+    L.seg_arg = take(static_cast<size_t>(L.S_max) * 128 * 4);
     L.seg_O = take(static_cast<size_t>(L.S_max) * 128 * d * 4);
     L.rowloss = take(static_cast<size_t>(L.N) * 8);
     L.st_lse = take(static_cast<size_t>(L.N) * 4);
@@ -190,6 +191,10 @@ struct f2c_dcp {
     int64_t C;
     int d, dtype, W;
     int K = 1;  // features per slot (NEXT-1)
+    // NEXT-3 L_cos variant (f2c_dcp_set_lcos): reduction, hinge, weight
+    int phi_mode = 0, hinge = 0;
+    float lam = 1.f;
+    int neg_mode() const { return phi_mode == 2 ? 2 : (hinge ? 1 : 0); }
     bool emulated;
     int64_t n_local_max, m_local_max;
     int64_t E = 0, M_last = 0;
@@ -559,10 +564,11 @@ static int phase_compact(f2c_dcp *h, Rank &R, const StepCtx &c, const int *tmax_
     a.ttgt = R.at<float>(L.ttgt);
     a.sc = R.sc();
     a.tmax_bits = tmax_bits;
+    a.neg_mode = h->neg_mode();
     k_compact<<<1, 1024, 0, c.st>>>(a);
     LAUNCH_CHECK();
     const int row_bytes = h->d * 2;
-    k_gather<<<static_cast<unsigned>(c.N), 64, 0, c.st>>>(c.x, R.at<int>(L.pos_row), R.sc(), row_bytes,
+    k_gather<<<static_cast<unsigned>(c.N + 1), 64, 0, c.st>>>(c.x, R.at<int>(L.pos_row), R.sc(), row_bytes,
                                                           R.base + L.X_pos, R.base + L.T, R.at<int>(L.row_tgt),
                                                           R.at<float2>(L.row_ab));
     LAUNCH_CHECK();
@@ -595,13 +601,16 @@ static int phase_main(f2c_dcp *h, Rank &R, const StepCtx &c, int64_t occ_loc) {
         h->ev_used += 2;
         CUDA_TRY(cudaEventRecord(e0, c.st));
     }
-    if (h->use_tp64) {
+    if (h->use_tp64 && h->neg_mode() == 0) {
         dcp_tp64_kernel<<<h->G, TP_THREADS, TP_SMEM_BYTES, c.st>>>(R.tmT, R.tmX, p);
     } else {
         PCParams q;
         q.d = p.d;
         q.n_slots = p.n_slots;
         q.n_pos = p.n_pos;
+        q.n_rows = &R.sc()->n_rows;
+        q.neg_mode = h->neg_mode();
+        q.seg_arg = R.at<int>(L.seg_arg);
         q.row_ab = p.row_ab;
         q.row_tgt = p.row_tgt;
         q.X_pos = R.base + L.X_pos;
@@ -646,8 +655,9 @@ static CombineArgs combine_args(f2c_dcp *h, Rank &R, const StepCtx &c, int64_t o
     a.C_occ = h->E < h->C ? h->E : h->C;
     a.d = h->d;
     a.dtype = h->dtype;
-    a.G = h->use_tp64 ? h->G : h->G / 2;
-    a.rows_per_group = h->use_tp64 ? TP_R : PC_R;
+    const bool tp64 = h->use_tp64 && h->neg_mode() == 0;
+    a.G = tp64 ? h->G : h->G / 2;
+    a.rows_per_group = tp64 ? TP_R : PC_R;
     a.n_tiles = static_cast<int>((occ + TP_TILE - 1) / TP_TILE);
     a.s = c.s;
     a.margin_l2 = c.s * c.m * 1.4426950408889634f;
@@ -657,6 +667,13 @@ static CombineArgs combine_args(f2c_dcp *h, Rank &R, const StepCtx &c, int64_t o
     a.st_cos = R.at<float>(L.st_cos);
     a.st_phi = R.at<float>(L.st_phi);
     a.st_ell = R.at<float>(L.st_ell);
+    a.neg_mode = h->neg_mode();
+    a.phi_mean = h->phi_mode == 0;
+    a.hinge = h->hinge;
+    a.lam = h->lam;
+    a.my_rank = R.rank < 0 ? 0 : R.rank;
+    a.seg_arg = R.at<int>(L.seg_arg);
+    a.wslot = h->K > 1 ? R.at<float>(L.wslot) : nullptr;
     return a;
 }
 
@@ -750,7 +767,8 @@ static int loss_multi(f2c_dcp *h, const uint8_t *x, const int64_t *labels, const
                                                                    R.at<float>(R.L.dx_part));
         LAUNCH_CHECK();
         k_loss<<<1, 1024, 0, st>>>(R.at<double>(R.L.rowloss), R.at<int>(R.L.comp_idx), N, R.sc(), loss,
-                                   R.at<int64_t>(R.L.hkeys), R.at<unsigned long long>(R.L.hvals), R.L.H);
+                                   R.at<int64_t>(R.L.hkeys), R.at<unsigned long long>(R.L.hvals), R.L.H,
+                                   static_cast<double>(h->lam));
         LAUNCH_CHECK();
     }
     if (h->emulated) {
@@ -807,8 +825,20 @@ extern "C" int f2c_dcp_loss_fwd_bwd(f2c_dcp *h, const void *x, const int64_t *la
     k_combine<__nv_bfloat16><<<static_cast<unsigned>(c.N), 128, 0, st>>>(a);
     LAUNCH_CHECK();
     k_loss<<<1, 1024, 0, st>>>(R.at<double>(L.rowloss), R.at<int>(L.comp_idx), c.N, R.sc(), loss,
-                               R.at<int64_t>(L.hkeys), R.at<unsigned long long>(L.hvals), L.H);
+                               R.at<int64_t>(L.hkeys), R.at<unsigned long long>(L.hvals), L.H,
+                               static_cast<double>(h->lam));
     LAUNCH_CHECK();
+    return F2C_OK;
+}
+
+extern "C" int f2c_dcp_set_lcos(f2c_dcp *h, int32_t phi_mode, int32_t hinge, double lambda) {
+    if (!h) return fail(F2C_EINVAL, "NULL handle");
+    if (phi_mode < 0 || phi_mode > 2) return fail(F2C_EINVAL, "phi_mode %d not in {0 mean, 1 sum, 2 max}", phi_mode);
+    if (hinge != 0 && hinge != 1) return fail(F2C_EINVAL, "hinge must be 0 or 1");
+    if (!isfinite(lambda)) return fail(F2C_EINVAL, "lambda must be finite");
+    h->phi_mode = phi_mode;
+    h->hinge = hinge;
+    h->lam = static_cast<float>(lambda);
     return F2C_OK;
 }
 

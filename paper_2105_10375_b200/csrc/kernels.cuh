@@ -24,7 +24,8 @@ struct Scalars {          // lives at the start of the per-rank scratch
     int tmax_bits;        // max ||T_c|| over rows ever written (float bits, >= 0)
     int n_pos;            // in-pool rows of the last loss call
     int n_neg;
-    int pad0;
+    int n_rows;           // compacted rows the main kernel processes (n_pos + 1, or N + 1
+                          // when the out-of-pool rows go through it: NEXT-3 hinge / max)
     double loss3[3];      // L, L_ce, L_cos (fp64) of the last loss call
     unsigned long long n_pos_sum;  // sum of n_pos over loss calls (bench accounting)
 };
@@ -370,8 +371,11 @@ struct CompactArgs {
     int64_t N, C, lo, hi, E, M_last;
     float s, log2e_s;         // s, s*log2(e)
     int R_max;
-    int *comp_idx;            // [N]
-    int *pos_row;             // [N]
+    int neg_mode;             // 0: mu path; 1 (hinge) / 2 (max): out-of-pool rows are compacted
+                              // after the mu row (index n_pos + 1 + j) and run through the kernel
+    int *comp_idx;            // [N]: k >= 0 in-pool row k; -1 out-of-pool (mu path); -2 - k
+                              // out-of-pool row compacted at k (neg_mode != 0)
+    int *pos_row;             // [R_max]
     float2 *row_ab;           // [R_max]
     int *row_tgt;             // [R_max]
     float *ttgt;              // [R_max]
@@ -416,7 +420,14 @@ __global__ void __launch_bounds__(1024) k_compact(CompactArgs a) {
             const int64_t want = a.E - a.M_last + a.pairing[i];
             if (a.pairing[i] >= a.M_last || ts != want) latch(a.sc, ERR_PAIRING, DET_PAIRING);
         }
-        if (ts >= 0) {
+        if (ts < 0 && a.neg_mode) {
+            const int kn = n_pos + 1 + static_cast<int>(i - k);  // i - k = out-of-pool rows before i
+            a.comp_idx[i] = -2 - kn;
+            a.pos_row[kn] = static_cast<int>(i);
+            a.row_ab[kn] = make_float2(a.inv_n[i], 0.f);  // e = <x, T> / ||x|| = cosine
+            a.row_tgt[kn] = -2;
+            a.ttgt[kn] = -INFINITY;
+        } else if (ts >= 0) {
             a.comp_idx[i] = k;
             a.pos_row[k] = static_cast<int>(i);
             a.row_ab[k] = make_float2(a.log2e_s * a.inv_n[i], B);
@@ -429,12 +440,19 @@ __global__ void __launch_bounds__(1024) k_compact(CompactArgs a) {
         }
     }
     // the mu row and the padding rows of the last row group
-    for (int r = n_pos + tid; r < a.R_max; r += nt) {
+    const int n_rows = a.neg_mode ? static_cast<int>(a.N) + 1 : n_pos + 1;
+    for (int r = (a.neg_mode ? n_rows : n_pos) + tid; r < a.R_max; r += nt) {
         a.row_ab[r] = make_float2(0.f, 0.f);
         a.row_tgt[r] = -1;
         a.ttgt[r] = -INFINITY;
     }
+    if (a.neg_mode && tid == 0) {
+        a.row_ab[n_pos] = make_float2(0.f, 0.f);
+        a.row_tgt[n_pos] = -1;
+        a.ttgt[n_pos] = -INFINITY;
+    }
     if (tid == 0) {
+        a.sc->n_rows = n_rows;
         a.sc->n_pos = n_pos;
         a.sc->n_neg = static_cast<int>(a.N) - n_pos;
         a.sc->n_pos_sum += static_cast<unsigned long long>(n_pos);
@@ -452,10 +470,10 @@ __global__ void __launch_bounds__(64) k_gather(const uint8_t *__restrict__ x, co
                                                const int *__restrict__ row_tgt, float2 *__restrict__ row_ab) {
     __shared__ float red[2];
     const int k = blockIdx.x;
-    if (k >= sc->n_pos) return;
+    if (k >= sc->n_rows || k == sc->n_pos) return;  // (row n_pos is the mu row)
     const int4 *src = reinterpret_cast<const int4 *>(x + static_cast<int64_t>(pos_row[k]) * row_bytes);
     int4 *dst = reinterpret_cast<int4 *>(Xp + static_cast<int64_t>(k) * row_bytes);
-    const int ts = row_tgt[k];
+    const int ts = row_tgt[k];  // local target slot, -1 (not on this shard), -2 (out-of-pool row)
     const int4 *tr = reinterpret_cast<const int4 *>(T + static_cast<int64_t>(ts < 0 ? 0 : ts) * row_bytes);
     float dot = 0.f;
     for (int u = threadIdx.x; u < row_bytes / 16; u += blockDim.x) {
@@ -477,7 +495,7 @@ __global__ void __launch_bounds__(64) k_gather(const uint8_t *__restrict__ x, co
     for (int o = 16; o; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = dot;
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && ts != -2) {  // (-2: out-of-pool row of NEXT-3, (a, b) final)
         float2 ab = row_ab[k];
         const float floor_b = ab.y - 100.f;  // ab.y holds the global bound on entry
         const float zt = ab.x * (red[0] + red[1]);
@@ -509,6 +527,12 @@ struct CombineArgs {
     uint8_t *dx;                // [N, d] dtype
     double *rowloss;            // [N]
     float *st_lse, *st_cos, *st_phi, *st_ell;  // [N] row statistics
+    // NEXT-3 L_cos variants: reduction (mean: 1/C_occ, sum: 1), hinge, weight lambda;
+    // neg_mode 1 (hinge) / 2 (max) reads the out-of-pool rows' own kernel partials
+    int neg_mode, phi_mean, hinge, my_rank;
+    float lam;
+    const int *seg_arg;         // [S][128] local argmax slot of a segment (neg_mode 2)
+    const float *wslot;         // [C_loc] 1/||T_bar_c|| (K >= 2) or null
 };
 
 __device__ __forceinline__ float block_sum_128(float v, float *red) {
@@ -549,12 +573,62 @@ __device__ __forceinline__ void gather_row_partials(const CombineArgs &a, int n_
     }
 }
 
+// max over the segments of compacted row k (first segment on ties = lowest slot) and its
+// local argmax slot (-1 if the shard has no candidate)
+__device__ __forceinline__ void gather_row_max(const CombineArgs &a, int n_rg, int k, float &cmax, int &carg) {
+    const int RG = a.rows_per_group;
+    const int rg = k / RG, r = k % RG;
+    cmax = -INFINITY;
+    carg = -1;
+    if (a.n_tiles <= 0) return;
+    const int S = tp_choose_S(n_rg, a.G, a.n_tiles);
+    for (int s = 0; s < S; ++s) {
+        const long long t0 = static_cast<long long>(s) * a.n_tiles / S;
+        const long long t1 = static_cast<long long>(s + 1) * a.n_tiles / S;
+        if (t1 <= t0) continue;
+        const long long seg = static_cast<long long>(s) * n_rg + rg;
+        const float v = a.seg_mx[seg * RG + r];
+        if (v > cmax) {
+            cmax = v;
+            carg = a.seg_arg[seg * RG + r];
+        }
+    }
+}
+
+// dL_cos/dx_hat of an out-of-pool row handled by the main kernel (neg_mode 1 / 2), before
+// the factor lambda / N_neg; phi_raw = the shard's unreduced phi partial (sum of hinged
+// cosines, or the max cosine).
+__device__ __forceinline__ void neg_row_local(const CombineArgs &a, int n_rg, int kn, float (&g)[4],
+                                              float &phi_raw, int &carg) {
+    carg = -1;
+    if (a.neg_mode == 1) {
+        float lsum, mx;
+        gather_row_partials(a, n_rg, kn, g, lsum, mx);
+        phi_raw = lsum;
+    } else {
+        float cmax;
+        gather_row_max(a, n_rg, kn, cmax, carg);
+        phi_raw = cmax;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) g[j] = 0.f;
+    }
+}
+__device__ __forceinline__ void add_center(const CombineArgs &a, int carg, float coef, float (&g)[4]) {
+    const float wc = a.wslot ? a.wslot[carg] : 1.f;
+    const __nv_bfloat16 *Tc = reinterpret_cast<const __nv_bfloat16 *>(a.T) + static_cast<int64_t>(carg) * a.d;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int dd = threadIdx.x + 128 * j;
+        g[j] = dd < a.d ? coef * wc * __bfloat162float(Tc[dd]) : 0.f;
+    }
+}
+
 template <typename TX>
 __global__ void __launch_bounds__(128) k_combine(CombineArgs a) {
     __shared__ float red[4];
     const int64_t i = blockIdx.x;
     const int n_pos = a.sc->n_pos, n_neg = a.sc->n_neg;
-    const int n_rg = (n_pos + 1 + a.rows_per_group - 1) / a.rows_per_group;
+    const int n_rg = (a.sc->n_rows + a.rows_per_group - 1) / a.rows_per_group;
     const int k = a.comp_idx[i];
     const TX *xr = reinterpret_cast<const TX *>(a.x) + i * a.d;
     const float inv = a.inv_n[i];
@@ -594,19 +668,35 @@ __global__ void __launch_bounds__(128) k_combine(CombineArgs a) {
                 latch(a.sc_w, ERR_DEVICE, (!(ts >= 0) || !isfinite(ell)) ? DET_NONFINITE : DET_UNDERFLOW);
         }
     } else {
-        // out-of-pool: mu = sum over occupied slots of T_c (the mu row, index n_pos)
-        float mu[4], lsum, mx;
-        gather_row_partials(a, n_rg, n_pos, mu, lsum, mx);
-        const float cocc = static_cast<float>(a.C_occ);
-        const float w = (a.C_occ > 0 && n_neg > 0) ? 1.0f / (static_cast<float>(n_neg) * cocc) : 0.f;
-        float dot = 0.f;
+        // out-of-pool (L_cos, D10 / NEXT-3): phi = R_c h(cos_c), gradient (lambda/N_neg) dphi
+        const float rs = a.phi_mean ? (a.C_occ > 0 ? 1.0f / static_cast<float>(a.C_occ) : 0.f) : 1.f;
+        const float w = n_neg > 0 ? a.lam / static_cast<float>(n_neg) : 0.f;
+        float phi;
+        if (k == -1) {
+            // mu path: mu = sum over occupied slots of w_c T_bar_c (the mu row, index n_pos)
+            float mu[4], lsum, mx;
+            gather_row_partials(a, n_rg, n_pos, mu, lsum, mx);
+            float dot = 0.f;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            g[j] = w * mu[j];
-            dot += xh[j] * mu[j];
+            for (int j = 0; j < 4; ++j) {
+                g[j] = w * rs * mu[j];
+                dot += xh[j] * mu[j];
+            }
+            dot = block_sum_128(dot, red);
+            phi = a.C_occ > 0 ? dot * rs : 0.f;
+        } else {
+            float raw;
+            int carg;
+            neg_row_local(a, n_rg, -2 - k, g, raw, carg);
+            if (a.neg_mode == 1) {
+                phi = a.C_occ > 0 ? raw * rs : 0.f;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) g[j] *= w * rs;
+            } else {
+                phi = carg < 0 ? 0.f : (a.hinge ? fmaxf(raw, 0.f) : raw);
+                if (carg >= 0 && !(a.hinge && raw <= 0.f)) add_center(a, carg, w, g);
+            }
         }
-        dot = block_sum_128(dot, red);
-        const float phi = a.C_occ > 0 ? dot / cocc : 0.f;
         row_loss = phi;
         if (threadIdx.x == 0) {
             a.st_phi[i] = phi;
@@ -638,12 +728,17 @@ __global__ void __launch_bounds__(128) k_local_rows(CombineArgs a, float4 *__res
     __shared__ float red[4];
     const int64_t i = blockIdx.x;
     const int n_pos = a.sc->n_pos;
-    const int n_rg = (n_pos + 1 + a.rows_per_group - 1) / a.rows_per_group;
+    const int n_rg = (a.sc->n_rows + a.rows_per_group - 1) / a.rows_per_group;
     const int k = a.comp_idx[i];
     if (k >= 0) {
         float o[4], lsum, mx;
         gather_row_partials(a, n_rg, k, o, lsum, mx);  // (o unused here)
         if (threadIdx.x == 0) scal[i] = make_float4(lsum, mx, a.ttgt[k], a.row_ab[k].y);
+    } else if (k <= -2) {
+        float g[4], raw;
+        int carg;
+        neg_row_local(a, n_rg, -2 - k, g, raw, carg);
+        if (threadIdx.x == 0) scal[i] = make_float4(raw, 0.f, 0.f, 0.f);
     } else {
         float mu[4], lsum, mx;
         gather_row_partials(a, n_rg, n_pos, mu, lsum, mx);
@@ -656,7 +751,7 @@ __global__ void __launch_bounds__(128) k_local_rows(CombineArgs a, float4 *__res
             if (dd < a.d) dot += __bfloat162float(xr[dd]) * inv * mu[j];
         }
         dot = block_sum_128(dot, red);
-        if (threadIdx.x == 0) scal[i] = make_float4(a.C_occ > 0 ? dot / static_cast<float>(a.C_occ) : 0.f, 0.f, 0.f, 0.f);
+        if (threadIdx.x == 0) scal[i] = make_float4(dot, 0.f, 0.f, 0.f);  // x_hat . mu_r (unreduced)
     }
 }
 
@@ -670,7 +765,7 @@ __global__ void __launch_bounds__(128) k_finalize_multi(CombineArgs a, const flo
     __shared__ float red[4];
     const int64_t i = blockIdx.x;
     const int n_pos = a.sc->n_pos, n_neg = a.sc->n_neg;
-    const int n_rg = (n_pos + 1 + a.rows_per_group - 1) / a.rows_per_group;
+    const int n_rg = (a.sc->n_rows + a.rows_per_group - 1) / a.rows_per_group;
     const int k = a.comp_idx[i];
     const __nv_bfloat16 *xr = reinterpret_cast<const __nv_bfloat16 *>(a.x) + i * a.d;
     const float inv = a.inv_n[i];
@@ -718,13 +813,37 @@ __global__ void __launch_bounds__(128) k_finalize_multi(CombineArgs a, const flo
                 latch(a.sc_w, ERR_DEVICE, !isfinite(ell) ? DET_NONFINITE : DET_UNDERFLOW);
         }
     } else {
-        float mu[4], lsum, mxl;
-        gather_row_partials(a, n_rg, n_pos, mu, lsum, mxl);
-        const float w = (a.C_occ > 0 && n_neg > 0) ? 1.0f / (static_cast<float>(n_neg) * static_cast<float>(a.C_occ)) : 0.f;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) g[j] = w * mu[j];
+        const float rs = a.phi_mean ? (a.C_occ > 0 ? 1.0f / static_cast<float>(a.C_occ) : 0.f) : 1.f;
+        const float w = n_neg > 0 ? a.lam / static_cast<float>(n_neg) : 0.f;
         double phi = 0.0;
-        for (int r = 0; r < W; ++r) phi += static_cast<double>(scal_all[static_cast<int64_t>(r) * N + i].x);
+        if (a.neg_mode == 2 && k <= -2) {
+            // hardest negative: global max over the shards (first rank = lowest slot on ties);
+            // only the owning shard contributes the gradient T_bar_c* / ||T_bar_c*||
+            float gmax = -INFINITY;
+            int rw = -1;
+            for (int r = 0; r < W; ++r) {
+                const float v = scal_all[static_cast<int64_t>(r) * N + i].x;
+                if (v > gmax) { gmax = v; rw = r; }
+            }
+            phi = rw < 0 ? 0.0 : static_cast<double>(a.hinge ? fmaxf(gmax, 0.f) : gmax);
+            float raw;
+            int carg;
+            neg_row_local(a, n_rg, -2 - k, g, raw, carg);
+            if (rw == a.my_rank && carg >= 0 && !(a.hinge && gmax <= 0.f)) add_center(a, carg, w, g);
+        } else {
+            if (k <= -2) {
+                float raw;
+                int carg;
+                neg_row_local(a, n_rg, -2 - k, g, raw, carg);
+            } else {
+                float lsum, mxl;
+                gather_row_partials(a, n_rg, n_pos, g, lsum, mxl);
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) g[j] *= w * rs;
+            for (int r = 0; r < W; ++r) phi += static_cast<double>(scal_all[static_cast<int64_t>(r) * N + i].x);
+            phi = a.C_occ > 0 ? phi * rs : 0.0;
+        }
         row_loss = phi;
         if (threadIdx.x == 0) {
             a.st_phi[i] = static_cast<float>(phi);
@@ -780,12 +899,12 @@ __global__ void k_unpack_tseq(const int64_t *__restrict__ ext, int64_t N, int64_
 }
 
 // ------------------------------------------------------------------ a6: loss reduction
-// L = (1/N_pos) sum ell + (1/N_neg) sum phi in fp64, fixed order (deterministic);
+// L = (1/N_pos) sum ell + lambda (1/N_neg) sum phi in fp64, fixed order (deterministic);
 // also clears the label hash table for the next call.
 __global__ void __launch_bounds__(1024) k_loss(const double *__restrict__ rowloss,
                                                const int *__restrict__ comp_idx, int64_t N,
                                                Scalars *sc, float *loss, int64_t *keys,
-                                               unsigned long long *vals, int H) {
+                                               unsigned long long *vals, int H, double lam) {
     __shared__ double sa[1024], sb[1024];
     const int tid = threadIdx.x;
     double ce = 0.0, cs = 0.0;
@@ -807,7 +926,7 @@ __global__ void __launch_bounds__(1024) k_loss(const double *__restrict__ rowlos
         const int np = sc->n_pos, nn = sc->n_neg;
         const double Lce = np > 0 ? sa[0] / np : 0.0;
         const double Lcos = nn > 0 ? sb[0] / nn : 0.0;
-        const double L = Lce + Lcos;
+        const double L = Lce + lam * Lcos;  // lambda = 1: P:170; NEXT-3 weight
         sc->loss3[0] = L;
         sc->loss3[1] = Lce;
         sc->loss3[2] = Lcos;

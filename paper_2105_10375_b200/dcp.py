@@ -8,6 +8,7 @@ import os
 import torch
 
 BF16, F32 = 0, 1
+PHI_MEAN, PHI_SUM, PHI_MAX = 0, 1, 2
 _HERE = os.path.dirname(os.path.abspath(__file__))
 lib_path = os.path.join(_HERE, "libf2c_dcp.so")
 
@@ -54,7 +55,8 @@ def load_library():
     L.f2c_dcp_profile_read.argtypes = [P, P, P, P]
     L.f2c_dcp_destroy.argtypes = [P]
     L.f2c_dcp_destroy.restype = None
-    for f in (L.f2c_dcp_create, L.f2c_dcp_create_k, L.f2c_dcp_enqueue, L.f2c_dcp_loss_fwd_bwd, L.f2c_gnet_ema,
+    L.f2c_dcp_set_lcos.argtypes = [P, i32, i32, ctypes.c_double]
+    for f in (L.f2c_dcp_create, L.f2c_dcp_create_k, L.f2c_dcp_set_lcos, L.f2c_dcp_enqueue, L.f2c_dcp_loss_fwd_bwd, L.f2c_gnet_ema,
               L.f2c_dcp_get_state, L.f2c_dcp_set_state, L.f2c_dcp_row_stats, L.f2c_dcp_check,
               L.f2c_last_launch_count, L.f2c_dcp_profile, L.f2c_dcp_profile_read):
         f.restype = ctypes.c_int
@@ -126,6 +128,11 @@ class DCPHead:
                                                    n_local, float(s), float(m), _ptr(loss), _ptr(dx),
                                                    _stream(stream)))
         return loss, dx
+
+    def set_lcos(self, phi_mode: int = PHI_MEAN, hinge: bool = False, lam: float = 1.0):
+        """NEXT-3 L_cos variant for later loss calls: phi_mode PHI_MEAN / PHI_SUM / PHI_MAX,
+        hinge max(0, cos), L = L_ce + lam * L_cos (include/f2c_dcp.h)."""
+        _check(load_library().f2c_dcp_set_lcos(self._h, int(phi_mode), int(hinge), float(lam)))
 
     # -- support ----------------------------------------------------------------------
     def check(self):
