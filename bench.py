@@ -244,7 +244,9 @@ def run_ours(args, cfg, world, rank, local_rank, device_only=False):
 
     for i in range(args.warmup):
         step(devin[i % R])
-    head.check()
+    timing_experiment = bool(os.environ.get("F2C_DBG_FLAGS"))  # kernel parts disabled: results void
+    if not timing_experiment:
+        head.check()
 
     def barrier():
         if world > 1:
@@ -275,7 +277,8 @@ def run_ours(args, cfg, world, rank, local_rank, device_only=False):
     n_launch = launches[0]
     main_ms, main_n, npos_sum = head.profile_read()
     head.profile(False)
-    head.check()
+    if not timing_experiment:
+        head.check()
     value = K * N_loc * world / (ms / 1e3)
 
     if device_only:

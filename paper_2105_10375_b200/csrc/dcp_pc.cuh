@@ -46,6 +46,26 @@ constexpr int PC_SMEM_BYTES = PC_OFF_AUX + 4096 + 1024;
 
 // the same struct (same offsets) in both CTAs, so multicast commits can target a
 // barrier of the peer by its local offset
+constexpr int PC_MAX_UNITS = 32;
+// (Measured and rejected: the softmax warps storing P straight into the consumer's smem with
+// st.shared::cluster + fence.proxy.async.shared::cluster instead of staging + one bulk copy
+// took 6300 cycles per tile against 2150.)  // host-checked: ceil(R*S/G) <= 32 for every R <= R_max/128
+
+// the cluster's unit list, computed once per CTA (TPSched) and read by every role
+struct PCUnitIt {
+    const int4 *u;
+    int n, i;
+    __device__ bool next(int &rg, int &t0, int &t1, int &seg) {
+        if (i >= n) return false;
+        const int4 v = u[i++];
+        rg = v.x;
+        t0 = v.y;
+        t1 = v.z;
+        seg = v.w;
+        return true;
+    }
+};
+
 struct PCAux {
     // producer
     uint64_t tfull[PC_P_NSTAGE], tempty[PC_P_NSTAGE];
@@ -62,6 +82,8 @@ struct PCAux {
     float red_l[2][PC_R];
     float red_mx[2][PC_R];
     int red_arg[2][PC_R];
+    int4 units[PC_MAX_UNITS];          // this cluster's (row group, t0, t1, segment) list
+    int n_units;
 };
 static_assert(sizeof(PCAux) <= 4096, "PCAux must fit the aux region");
 
@@ -82,7 +104,9 @@ struct PCParams {
     float *seg_mx;         // [S][128]
     float *seg_O;          // [S][128][d]
     unsigned long long *dbg;
-    int dbg_flags;         // timing experiments only: 1 = skip P smem writes, 2 = skip DSMEM copy
+    int dbg_flags;         // timing experiments only: 1 = skip P smem writes, 128 = skip DSMEM copy,
+                           // 4 / 8 = no producer / consumer pool loads, 16 = no softmax arithmetic,
+                           // 64 = softmax warps idle (barrier protocol only), 256 = no GEMM-2 MMAs
 };
 
 __device__ __forceinline__ uint32_t cluster_ctarank() {
@@ -131,6 +155,57 @@ __device__ __forceinline__ void umma_commit_e(uint64_t *bar) {
         "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(smem_u32(bar))
         : "memory");
 }
+
+// One producer stage of GEMM 1 in a single elected issue: 8 TS MMAs (chunk c = i>>2 of the
+// 32 KB stage, K step k = i&3) and the commit that releases the stage.  One asm block, one
+// elect.sync: the operands go to uniform registers once per stage, not once per MMA.
+__device__ __forceinline__ void umma_ts_stage8(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
+                                               uint32_t acc0, uint64_t *bar) {
+    asm volatile(
+        "{\n.reg .pred e, p, t;\n.reg .b32 r;\n"
+        "elect.sync r|e, 0xffffffff;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "setp.eq.b32 t, 0, 0;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+8], %6, %3, t;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+16], %7, %3, t;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+24], %8, %3, t;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+32], %9, %3, t;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+40], %10, %3, t;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+48], %11, %3, t;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+56], %12, %3, t;\n"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%5];\n}\n" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(acc0), "r"(smem_u32(bar)), "l"(bdesc + 2), "l"(bdesc + 4),
+        "l"(bdesc + 6), "l"(bdesc + 1024), "l"(bdesc + 1026), "l"(bdesc + 1028), "l"(bdesc + 1030)
+        : "memory");
+}
+// One consumer stage of GEMM 2: 8 SS MMAs over the tile's 128 slots (K steps of 16) and the
+// commit that releases the pool stage.  a/b descriptors advance by +2 (32 B) / +128 (2 KB)
+// per K step, plus +1024 (16 KB) for the A chunk after 4 steps.
+__device__ __forceinline__ void umma_ss_stage8(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                               uint32_t acc0, uint64_t *bar) {
+    asm volatile(
+        "{\n.reg .pred e, p, t;\n.reg .b32 r;\n"
+        "elect.sync r|e, 0xffffffff;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "setp.eq.b32 t, 0, 0;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %6, %7, %3, t;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %8, %9, %3, t;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %10, %11, %3, t;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %12, %13, %3, t;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %14, %15, %3, t;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %16, %17, %3, t;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %18, %19, %3, t;\n"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%5];\n}\n" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc0), "r"(smem_u32(bar)),
+        "l"(adesc + 2), "l"(bdesc + 128), "l"(adesc + 4), "l"(bdesc + 256), "l"(adesc + 6), "l"(bdesc + 384),
+        "l"(adesc + 1024), "l"(bdesc + 512), "l"(adesc + 1026), "l"(bdesc + 640), "l"(adesc + 1028),
+        "l"(bdesc + 768), "l"(adesc + 1030), "l"(bdesc + 896)
+        : "memory");
+}
+#include "gemm1_tile.inc"
+
 __device__ __forceinline__ void umma_commit_mc_e(uint64_t *bar, uint16_t mask) {
     asm volatile(
         "{\n.reg .pred e;\n.reg .b32 r;\nelect.sync r|e, 0xffffffff;\n"
@@ -191,6 +266,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
     const int n_rows = *p.n_rows;
     const int n_rg = (n_rows + PC_R - 1) / PC_R;
     const int n_tiles = (p.n_slots + PC_TILE - 1) / PC_TILE;
+    if (p.dbg && threadIdx.x == 0 && blockIdx.x < 2) {  // kernel-span clocks (debug hook)
+        unsigned long long gt;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+        p.dbg[1024 + blockIdx.x * 4] = clock64();
+        p.dbg[1025 + blockIdx.x * 4] = gt;
+    }
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < PC_P_NSTAGE; ++i) {
@@ -213,11 +294,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
         }
         mbar_init(&aux->ofull, 1);
         mbar_init(&aux->oempty, 4);
-        if (crank == 1) {  // arm both P slots before the producer can copy into them
+        if (crank == 1 && !(p.dbg_flags & 128)) {  // arm both P slots before the producer can copy into them
             mbar_arrive_expect_tx(&aux->pfull[0], PC_PBYTES);
             mbar_arrive_expect_tx(&aux->pfull[1], PC_PBYTES);
         }
         fence_mbar_init();
+        TPSched ts;
+        ts.init(blockIdx.x >> 1, gridDim.x >> 1, n_rg, n_tiles);
+        int n = 0, a, b, c, s;
+        while (n < PC_MAX_UNITS && ts.next(a, b, c, s)) aux->units[n++] = make_int4(a, b, c, s);
+        aux->n_units = n;
     }
     if (warp == 9) {
         tma_prefetch_desc(&tm3p);
@@ -231,8 +317,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
     tc_fence_after();
     const uint32_t tmem = aux->tmem_base;
 
-    TPSched sch;
-    sch.init(blockIdx.x >> 1, gridDim.x >> 1, n_rg, n_tiles);
+    PCUnitIt sch{aux->units, aux->n_units, 0};
     int rg, t0, t1, seg;
 
     if (crank == 0) {
@@ -249,6 +334,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                         for (int g = 0; g < nstg_p; ++g, ++pc) {
                             const uint32_t st = pc % PC_P_NSTAGE, ph = (pc / PC_P_NSTAGE) & 1;
                             mbar_wait(&aux->tempty[st], ph ^ 1);
+                            if (p.dbg_flags & 4) {  // timing experiment: no pool loads
+                                mbar_arrive(&aux->tfull[st]);
+                                continue;
+                            }
                             mbar_arrive_expect_tx(&aux->tfull[st], PC_P_STAGE_BYTES);
                             tma_load_3d(sT + st * PC_P_STAGE_BYTES, &tm3p, &aux->tfull[st], 0, t * PC_TILE, g * cps_p);
                         }
@@ -265,31 +354,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                     mbar_wait(&aux->xready, sg & 1);
                     tc_fence_after();
                     for (int t = t0; t < t1; ++t, ++jt) {
-                        unsigned long long *dbg = (p.dbg && blockIdx.x == 0 && jt < 64 && lane == 0) ? p.dbg + jt * 8 : nullptr;
+                        unsigned long long *dbg = (p.dbg && blockIdx.x == 0 && jt < 64 && lane == 0) ? p.dbg + jt * 16 : nullptr;
                         const uint32_t sb = jt & 1, sph = (jt >> 1) & 1;
+                        const uint32_t dcol = tmem + S_COL + sb * PC_TILE;
+                        if (nstg_p == 4) {  // d = 512: the whole tile in one elected issue
+                            if (dbg) dbg[0] = clock64();
+                            gemm1_tile_issue(dcol, tmem + X_COL, bdesc0, idesc, smem_u32(&aux->sempty[sb]), sph ^ 1,
+                                             smem_u32(&aux->tfull[0]), smem_u32(&aux->tempty[0]), jt & 1,
+                                             smem_u32(&aux->sfull[sb]));
+                            pc += 4;
+                        } else {
                         mbar_wait(&aux->sempty[sb], sph ^ 1);
                         tc_fence_after();
                         if (dbg) dbg[0] = clock64();
-                        const uint32_t dcol = tmem + S_COL + sb * PC_TILE;
                         for (int g = 0; g < nstg_p; ++g, ++pc) {
                             const uint32_t st = pc % PC_P_NSTAGE, ph = (pc / PC_P_NSTAGE) & 1;
                             mbar_wait(&aux->tfull[st], ph);
                             tc_fence_after();
                             const uint64_t bst = bdesc0 + static_cast<uint64_t>(st * (PC_P_STAGE_BYTES >> 4));
-                            const uint32_t ast = tmem + X_COL + g * 64;
-                            if (g == 0) {
-                                umma_ts_e(dcol, ast, bst, idesc, 0);
-                            } else {
-                                umma_ts_e(dcol, ast, bst, idesc, 1);
-                            }
-#pragma unroll
-                            for (int i = 1; i < 8; ++i)  // i = c*4 + k: chunk c (16 KB), K step k (32 B)
-                                umma_ts_e(dcol, ast + (i >> 2) * 32 + (i & 3) * 8,
-                                             bst + static_cast<uint64_t>(((i >> 2) * 16384 + (i & 3) * 32) >> 4),
-                                             idesc, 1);
-                            umma_commit_e(&aux->tempty[st]);
+                            umma_ts_stage8(dcol, tmem + X_COL + g * 64, bst, idesc, g != 0, &aux->tempty[st]);
                         }
                         umma_commit_e(&aux->sfull[sb]);
+                        }
                         if (dbg) dbg[1] = clock64();
                         if (t == t1 - 1) umma_commit_e(&aux->xfree);
                     }
@@ -298,20 +384,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
             }
         } else if (warp == 10) {
             // -------- P mover: staging buffer -> consumer's P slot (DSMEM bulk copy)
-            if (lane == 0) {
+            if (lane == 0 && !(p.dbg_flags & 4096)) {
                 uint32_t jt = 0;
                 while (sch.next(rg, t0, t1, seg)) {
                     for (int t = t0; t < t1; ++t, ++jt) {
                         const uint32_t b = jt & 1, ph = (jt >> 1) & 1;
                         mbar_wait(&aux->pready[b], ph);
                         mbar_wait(&aux->pslot_free[b], ph ^ 1);
-                        unsigned long long *dbg = (p.dbg && blockIdx.x == 0 && jt < 64) ? p.dbg + jt * 8 : nullptr;
+                        unsigned long long *dbg = (p.dbg && blockIdx.x == 0 && jt < 64) ? p.dbg + jt * 16 : nullptr;
                         if (dbg) dbg[4] = clock64();
                         const uint32_t dst = mapa_shared(smem_u32(smem + PCQ_OFF_P + b * PC_PBYTES), 1);
                         const uint32_t rbar = mapa_shared(smem_u32(&aux->pfull[b]), 1);
-                        if (p.dbg_flags & 2) {
-                            asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(rbar), "r"(0) : "memory");
-                            asm volatile("mbarrier.complete_tx.shared::cluster.b64 [%0], %1;" :: "r"(rbar), "r"(PC_PBYTES) : "memory");
+                        if (p.dbg_flags & 128) {  // timing experiment: no P transfer
+                            asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(rbar) : "memory");
                         } else
                         asm volatile(
                             "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes"
@@ -365,8 +450,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                     const uint32_t sb = jt & 1, sph = (jt >> 1) & 1;
                     mbar_wait(&aux->sfull[sb], sph);
                     tc_fence_after();
-                    unsigned long long *dbg = (p.dbg && blockIdx.x == 0 && jt < 64 && threadIdx.x == 0) ? p.dbg + jt * 8 : nullptr;
+                    unsigned long long *dbg = (p.dbg && blockIdx.x == 0 && jt < 64 && threadIdx.x == 0) ? p.dbg + jt * 16 : nullptr;
                     if (dbg) dbg[2] = clock64();
+                    if (p.dbg_flags & 64) {  // timing experiment: softmax warps only keep the protocol
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&aux->sempty[sb]);
+                        const uint32_t b = jt & 1, ph = (jt >> 1) & 1;
+                        if (!(p.dbg_flags & 4096)) {
+                            mbar_wait(&aux->pstage_free[b], ph ^ 1);
+                            __syncwarp();
+                            if (lane == 0) mbar_arrive(&aux->pready[b]);
+                        }
+                        if (dbg) dbg[3] = clock64();
+                        continue;
+                    }
                     float e[64];
                     {
                         float v0[32], v1[32];
@@ -383,13 +480,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&aux->sempty[sb]);
+                    if (dbg) dbg[8] = clock64();
                     const int base = t * PC_TILE + h * 64;
                     const int nval = p.n_slots - base;  // valid slots in my 64-wide half
                     uint32_t w[32];
-                    if (!negrow) {
+                    if (p.dbg_flags & 16) {  // timing experiment: no softmax arithmetic
+#pragma unroll
+                        for (int k = 0; k < 32; ++k) w[k] = __float_as_uint(e[2 * k]) & 0x3f803f80u;
+                    } else if (!negrow) {
                         if (nval >= 64) {
 #pragma unroll
-                            for (int k = 0; k < 64; ++k) e[k] = fmaf(e[k], ab.x, -ab.y);
+                            for (int k = 0; k < 64; k += 2) ffma2_scalar(e[k], e[k + 1], ab.x, -ab.y);
                         } else {
 #pragma unroll
                             for (int k = 0; k < 64; ++k) e[k] = k < nval ? fmaf(e[k], ab.x, -ab.y) : -INFINITY;
@@ -411,15 +512,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                             for (int k = 0; k < 64; ++k)
                                 e[k] = k < nval ? __log2f(fmaxf(p.wslot[base + k], 1e-30f)) : -INFINITY;
                         }
-                        float la[4] = {0.f, 0.f, 0.f, 0.f}, ma[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+                        // 2-wide packed sums (FADD2) and 3-input max (FMNMX3), 4 chains each for ILP
+                        float la[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+                        float ma[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
                         for (int k = 0; k < 64; k += 2) {
                             const float p0 = ex2_approx(e[k]), p1 = ex2_approx(e[k + 1]);
-                            la[(k >> 1) & 3] += p0 + p1;
-                            ma[(k >> 1) & 3] = fmaxf(ma[(k >> 1) & 3], fmaxf(e[k], e[k + 1]));
+                            const int c = (k >> 1) & 3;
+                            fadd2_acc(la[2 * c], la[2 * c + 1], p0, p1);
+                            fmax3_acc(ma[c], e[k], e[k + 1]);
                             w[k >> 1] = pack_bf16x2(p0, p1);
                         }
-                        lacc += (la[0] + la[1]) + (la[2] + la[3]);
+                        lacc += ((la[0] + la[1]) + (la[2] + la[3])) + ((la[4] + la[5]) + (la[6] + la[7]));
                         mx = fmaxf(mx, fmaxf(fmaxf(ma[0], ma[1]), fmaxf(ma[2], ma[3])));
                     } else {
                         // cosine c = <x_hat, T_bar_c> w_c (w_c = 1 for K = 1; zero centers are
@@ -452,7 +556,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                     // P -> staging buffer in the consumer's K-major SW128 A layout:
                     // chunk h = slots [64h, 64h+64), row r: 128 B, 16-B unit u at u ^ (r & 7)
                     const uint32_t b = jt & 1, ph = (jt >> 1) & 1;
+                    if (dbg) dbg[9] = clock64();
                     mbar_wait(&aux->pstage_free[b], ph ^ 1);
+                    if (dbg) dbg[10] = clock64();
                     const uint32_t rowa = smem_u32(sPS + b * PC_PBYTES + h * 16384 + (r >> 3) * 1024 + (r & 7) * 128);
                     if (!(p.dbg_flags & 1))
 #pragma unroll
@@ -483,7 +589,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                 ++sg;
             }
         }
-    } else {
+    } else if (!(p.dbg_flags & 4096)) {  // (4096: timing experiment, producer alone)
         // ================================================================= CONSUMER
         uint8_t *sP = smem + PCQ_OFF_P;
         uint8_t *sT = smem + PCQ_OFF_T;
@@ -497,6 +603,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                         for (int g = 0; g < nstg; ++g, ++qc) {
                             const uint32_t st = qc % PC_Q_NSTAGE, ph = (qc / PC_Q_NSTAGE) & 1;
                             mbar_wait(&aux->qempty[st], ph ^ 1);
+                            if (p.dbg_flags & 8) {  // timing experiment: no pool loads
+                                mbar_arrive(&aux->qfull[st]);
+                                continue;
+                            }
                             mbar_arrive_expect_tx(&aux->qfull[st], stage_bytes);
                             tma_load_3d(sT + st * PC_STAGE_BYTES, &tm3q, &aux->qfull[st], 0, t * PC_TILE, g * cps);
                         }
@@ -513,9 +623,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                         const bool first = (t == t0);
                         const uint32_t b = jt & 1, ph = (jt >> 1) & 1;
                         mbar_wait(&aux->pfull[b], ph);
-                        unsigned long long *dbg = (p.dbg && blockIdx.x == 1 && jt < 64 && lane == 0) ? p.dbg + jt * 8 : nullptr;
+                        unsigned long long *dbg = (p.dbg && blockIdx.x == 1 && jt < 64 && lane == 0) ? p.dbg + jt * 16 : nullptr;
                         if (dbg) dbg[6] = clock64();
-                        if (lane == 0) mbar_arrive_expect_tx(&aux->pfull[b], PC_PBYTES);  // arm the next use
+                        if (lane == 0 && !(p.dbg_flags & 128)) mbar_arrive_expect_tx(&aux->pfull[b], PC_PBYTES);  // arm the next use
                         __syncwarp();
                         tc_fence_after();
                         if (first && sg > 0) {
@@ -526,15 +636,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                             const uint32_t st = qc % PC_Q_NSTAGE, qph = (qc / PC_Q_NSTAGE) & 1;
                             mbar_wait(&aux->qfull[st], qph);
                             tc_fence_after();
-#pragma unroll
-                            for (int ks = 0; ks < 8; ++ks) {  // 16-slot K steps over the tile
-                                const uint64_t a = umma_desc_sw128(
-                                    sPa + b * PC_PBYTES + (ks >> 2) * 16384 + (ks & 3) * 32, 16, 1024);
-                                const uint64_t bd =
-                                    umma_desc_sw128(sTa + st * PC_STAGE_BYTES + ks * 2048, 16384, 1024);
-                                umma_ss_e(tmem + g * cps * 64, a, bd, idesc, !(first && ks == 0));
-                            }
-                            umma_commit_e(&aux->qempty[st]);
+                            // 8 K steps of 16 slots: A = P (K-major, two 64-slot chunks), B = pool MN-major
+                            umma_ss_stage8(tmem + g * cps * 64, umma_desc_sw128(sPa + b * PC_PBYTES, 16, 1024),
+                                           umma_desc_sw128(sTa + st * PC_STAGE_BYTES, 16384, 1024), idesc,
+                                           !first, &aux->qempty[st]);
                         }
                         umma_commit_mc_e(&aux->pslot_free[b], 0x1);  // tell the producer slot b is free
                         if (dbg) dbg[7] = clock64();
@@ -569,6 +674,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
     }
     tc_fence_before();
     __syncthreads();
+    if (p.dbg && threadIdx.x == 0 && blockIdx.x < 2) {
+        unsigned long long gt;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+        p.dbg[1026 + blockIdx.x * 4] = clock64();
+        p.dbg[1027 + blockIdx.x * 4] = gt;
+    }
     cluster_sync_all();
     if (warp == 9) {
         tc_fence_after();

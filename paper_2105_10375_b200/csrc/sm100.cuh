@@ -152,6 +152,23 @@ __device__ __forceinline__ float ex2_approx(float x) {
     return y;
 }
 
+// packed fp32x2 arithmetic (FFMA2 / FADD2 on sm_100a) and the 3-input max (FMNMX3)
+__device__ __forceinline__ void ffma2_scalar(float &x, float &y, float a, float b) {  // (x, y) = (x, y) * a + b
+    asm("{\n.reg .b64 v, a2, b2;\nmov.b64 v, {%0, %1};\nmov.b64 a2, {%2, %2};\nmov.b64 b2, {%3, %3};\n"
+        "fma.rn.f32x2 v, v, a2, b2;\nmov.b64 {%0, %1}, v;\n}"
+        : "+f"(x), "+f"(y)
+        : "f"(a), "f"(b));
+}
+__device__ __forceinline__ void fadd2_acc(float &s0, float &s1, float x, float y) {  // (s0, s1) += (x, y)
+    asm("{\n.reg .b64 v, s;\nmov.b64 v, {%2, %3};\nmov.b64 s, {%0, %1};\nadd.rn.f32x2 s, s, v;\n"
+        "mov.b64 {%0, %1}, s;\n}"
+        : "+f"(s0), "+f"(s1)
+        : "f"(x), "f"(y));
+}
+__device__ __forceinline__ void fmax3_acc(float &m, float x, float y) {  // m = max(m, x, y)
+    asm("max.f32 %0, %0, %1, %2;" : "+f"(m) : "f"(x), "f"(y));
+}
+
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
     uint32_t r;
     asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));

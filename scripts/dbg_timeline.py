@@ -17,7 +17,7 @@ st = synth.step_inputs(cfg, 0)
 x = torch.from_numpy(st.x.view(np.int16)).view(torch.bfloat16).cuda()
 y = torch.from_numpy(st.y).cuda(); pr = torch.from_numpy(st.pairing).cuda()
 head.enqueue(torch.from_numpy(st.g.view(np.int16)).view(torch.bfloat16).cuda(), torch.from_numpy(st.gy).cuda())
-buf = torch.zeros(64 * 8 + 64, dtype=torch.int64, device="cuda")
+buf = torch.zeros(64 * 16 + 64, dtype=torch.int64, device="cuda")
 L.f2c_dcp_debug_timestamps.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
 for it in range(3):
     head.loss_fwd_bwd(x, y, pr, 64, 0.35)
@@ -25,8 +25,9 @@ L.f2c_dcp_debug_timestamps(head._h, ctypes.c_void_p(buf.data_ptr()))
 head.loss_fwd_bwd(x, y, pr, 64, 0.35)
 torch.cuda.synchronize()
 bb = buf.cpu().numpy().astype(np.int64)
-a = bb[:512].reshape(64, 8)
-st = bb[512:].reshape(8, 8)
+a16 = bb[:1024].reshape(64, 16)
+a = a16[:, :8]
+st = bb[1024:1088].reshape(8, 8)
 t0 = a[0, 0]
 import os
 if os.environ.get("F2C_KERNEL") == "tp64":
@@ -41,6 +42,13 @@ else:
     for j in range(8):
         r = st[j] - a[16 + j, 0]
         print("tile", 16 + j, "stage (wait_start, wait_done) rel g1_start:", r.tolist(), " g1_issued", a[16 + j, 1] - a[16 + j, 0])
+    sp = bb[1024:1032]
+    for c in range(2):
+        cyc, ns = sp[4 * c + 2] - sp[4 * c], sp[4 * c + 3] - sp[4 * c + 1]
+        print("CTA", c, "span: %d cycles, %.3f ms, eff clock %.0f MHz" % (cyc, ns / 1e6, cyc / max(ns, 1) * 1e3))
+    print("softmax: sfull->ld done", np.median(a16[:n, 8] - a16[:n, 2]), "ld->compute done", np.median(a16[:n, 9] - a16[:n, 8]),
+          "pstage wait", np.median(a16[:n, 10] - a16[:n, 9]), "P write+arrive", np.median(a16[:n, 3] - a16[:n, 10]),
+          "pready->next sfull", np.median(a16[1:n, 2] - a16[:n - 1, 3]))
     print("producer cadence (g1_start)", np.median(np.diff(a[:n, 0])), "consumer cadence (pfull_seen)", np.median(np.diff(a[:n, 6])))
     print("g1 issue", np.median(a[:n, 1] - a[:n, 0]), "softmax sfull->pready", np.median(a[:n, 3] - a[:n, 2]),
           "copy", np.median(a[:n, 5] - a[:n, 4]), "pready->copy issue", np.median(a[:n, 4] - a[:n, 3]),
