@@ -47,6 +47,7 @@ constexpr int PC_SMEM_BYTES = PC_OFF_AUX + 4096 + 1024;
 // the same struct (same offsets) in both CTAs, so multicast commits can target a
 // barrier of the peer by its local offset
 constexpr int PC_MAX_UNITS = 32;
+constexpr int PC_P_CHUNKS = 4;     // P transfer pieces (see the mover)
 // (Measured and rejected: the softmax warps storing P straight into the consumer's smem with
 // st.shared::cluster + fence.proxy.async.shared::cluster instead of staging + one bulk copy
 // took 6300 cycles per tile against 2150.)  // host-checked: ceil(R*S/G) <= 32 for every R <= R_max/128
@@ -397,14 +398,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                         const uint32_t rbar = mapa_shared(smem_u32(&aux->pfull[b]), 1);
                         if (p.dbg_flags & 128) {  // timing experiment: no P transfer
                             asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(rbar) : "memory");
-                        } else
-                        asm volatile(
-                            "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes"
-                            " [%0], [%1], %2, [%3];" ::"r"(dst),
-                            "r"(smem_u32(sPS + b * PC_PBYTES)), "r"(PC_PBYTES), "r"(rbar)
-                            : "memory");
-                        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-                        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                        } else {
+                            // in PC_P_CHUNKS pieces, at most two in flight:
+                            // the SM's async-copy unit also serves the pool TMA loads, which would
+                            // otherwise queue behind one long (DSMEM-rate) copy
+                            const int nck = (p.dbg_flags & 8192) ? 1 : PC_P_CHUNKS;  // 8192: one piece (comparison)
+                            const uint32_t ck = PC_PBYTES / nck;
+                            for (int c = 0; c < nck; ++c) {
+                                asm volatile(
+                                    "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes"
+                                    " [%0], [%1], %2, [%3];" ::"r"(dst + c * ck),
+                                    "r"(smem_u32(sPS + b * PC_PBYTES) + c * ck), "r"(ck), "r"(rbar)
+                                    : "memory");
+                                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                                asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");  // two in flight
+                            }
+                            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                        }
                         if (dbg) dbg[5] = clock64();
                         mbar_arrive(&aux->pstage_free[b]);
                     }
