@@ -129,7 +129,7 @@ class Pool:
 
     def loss(self, X: np.ndarray, y: np.ndarray, pairing: np.ndarray | None, s: float, m: float,
              want_P: bool = False, want_dT: bool = False, phi_mode: int = PHI_MEAN,
-             hinge: bool = False, lam: float = 1.0) -> LossResult:
+             hinge: bool = False, lam: float = 1.0, excl_dup: bool = False) -> LossResult:
         X = np.ascontiguousarray(X)
         y = np.ascontiguousarray(y, dtype=np.int64)
         N, d = len(y), self.d
@@ -145,8 +145,8 @@ class Pool:
         dT = np.zeros((self.C, d)) if want_dT else None
         rc = lib().orc_loss_v(self.C, self.K, d, self.dtype, _p(self.T), _p(self.lab),
                               int(self.E[0]), int(self.M_last[0]), N, _p(X), _p(y), _p(pr),
-                              float(s), float(m), int(phi_mode), int(bool(hinge)), float(lam),
-                              _p(out3), _p(dx), _p(lse), _p(ts), _p(phi), _p(ell), _p(counts),
+                              float(s), float(m), int(phi_mode), int(bool(hinge)) | (int(bool(excl_dup)) << 1),
+                              float(lam), _p(out3), _p(dx), _p(lse), _p(ts), _p(phi), _p(ell), _p(counts),
                               _p(P), _p(dT))
         if rc:
             raise OracleError(rc, "orc_loss")
@@ -154,7 +154,7 @@ class Pool:
                           int(counts[0]), int(counts[1]), int(counts[2]), P, dT)
 
     def loss_rows(self, X, y, pairing, s, m, rows, phi_mode: int = PHI_MEAN, hinge: bool = False,
-                  lam: float = 1.0):
+                  lam: float = 1.0, excl_dup: bool = False):
         X = np.ascontiguousarray(X)
         y = np.ascontiguousarray(y, dtype=np.int64)
         rows = np.ascontiguousarray(rows, dtype=np.int64)
@@ -167,7 +167,8 @@ class Pool:
         mu = np.zeros(d)
         rc = lib().orc_loss_rows_v(self.C, self.K, d, self.dtype, _p(self.T), _p(self.lab),
                                    int(self.E[0]), int(self.M_last[0]), N, _p(X), _p(y), _p(pr),
-                                   float(s), float(m), int(phi_mode), int(bool(hinge)), float(lam),
+                                   float(s), float(m), int(phi_mode),
+                                   int(bool(hinge)) | (int(bool(excl_dup)) << 1), float(lam),
                                    k, _p(rows), _p(dx), _p(lse), _p(ts),
                                    _p(phi), _p(ell), _p(counts), _p(mu))
         if rc:

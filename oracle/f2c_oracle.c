@@ -36,6 +36,9 @@
  *                    default), 1 = sum, 2 = max (hardest negative, first slot on ties);
  *                    hinge = 1 penalises only positive similarity, max(0, cos); and the
  *                    weight lambda on L_cos (L_total = L_ce + lambda L_cos).
+ *                    flags bit 0 = hinge; bit 1 = exclude stale self-duplicates: an in-pool
+ *                    row's softmax runs over the occupied slots minus the OLDER slots that
+ *                    carry its own label (D8 keeps them as ordinary denominator terms).
  *                    orc_loss_k is orc_loss_v with (mean, no hinge, lambda = 1).
  *
  * Parity status: every function here is pinned by tests/test_oracle_pins.py
@@ -110,7 +113,7 @@ typedef struct {
     int64_t N_pos, N_neg;
     double *mu;    /* [d] sum over occupied slots of T_c */
     /* NEXT-3 variants of L_cos */
-    int32_t phi_mode, hinge;
+    int32_t phi_mode, hinge, excl_dup;
     double lam;
 } orc_ctx;
 
@@ -193,11 +196,13 @@ static void orc_row(const orc_ctx *q, int64_t i, double *ell, double *phi, doubl
         int64_t t = q->t[i];
         double zmax = -INFINITY;
         for (int64_t c = 0; c < Co; ++c) {
+            if (q->excl_dup && c != t && q->lab[c] == q->y[i]) continue; /* stale self-duplicate */
             double z = q->s * cos_buf[c] - (c == t ? q->s * q->m : 0.0);
             if (z > zmax) zmax = z;
         }
         double sum = 0.0;
         for (int64_t c = 0; c < Co; ++c) {
+            if (q->excl_dup && c != t && q->lab[c] == q->y[i]) continue;
             double z = q->s * cos_buf[c] - (c == t ? q->s * q->m : 0.0);
             sum += exp(z - zmax);
         }
@@ -206,6 +211,10 @@ static void orc_row(const orc_ctx *q, int64_t i, double *ell, double *phi, doubl
         *ell = L - (q->s * cos_buf[t] - q->s * q->m);
         double w = q->s / (double)q->N_pos;
         for (int64_t c = 0; c < Co; ++c) {
+            if (q->excl_dup && c != t && q->lab[c] == q->y[i]) {
+                if (prow) prow[c] = 0.0;
+                continue;
+            }
             double z = q->s * cos_buf[c] - (c == t ? q->s * q->m : 0.0);
             double p = exp(z - L);
             if (prow) prow[c] = p;
@@ -268,17 +277,17 @@ static void orc_row(const orc_ctx *q, int64_t i, double *ell, double *phi, doubl
  * counts = {N_pos, N_neg, C_occ}; P [N * C_occ] or NULL; dT [C * d] or NULL. */
 int orc_loss_v(int64_t C, int32_t K, int32_t d, int32_t dtype, const void *T, const int64_t *lab,
                int64_t E, int64_t M_last, int64_t N, const void *X, const int64_t *y,
-               const int32_t *pairing, double s, double m, int32_t phi_mode, int32_t hinge,
+               const int32_t *pairing, double s, double m, int32_t phi_mode, int32_t flags,
                double lam, double *out3, double *dx, double *lse, int64_t *tslot, double *phi,
                double *ell, int64_t *counts, double *P, double *dT) {
     if (C < 1 || d < 1 || K < 1 || N < 0 || (dtype != 0 && dtype != 1)) return ORC_EINVAL;
     if (!(s > 0.0) || !isfinite(m)) return ORC_EINVAL;
-    if (phi_mode < 0 || phi_mode > 2 || hinge < 0 || hinge > 1 || !isfinite(lam)) return ORC_EINVAL;
+    if (phi_mode < 0 || phi_mode > 2 || flags < 0 || flags > 3 || !isfinite(lam)) return ORC_EINVAL;
     if (dT && K != 1) return ORC_EINVAL;
     orc_ctx q = {0};
     q.C = C; q.N = N; q.E = E; q.M_last = M_last; q.d = d; q.dtype = dtype; q.K = K;
     q.T = T; q.lab = lab; q.X = X; q.y = y; q.s = s; q.m = m;
-    q.phi_mode = phi_mode; q.hinge = hinge; q.lam = lam;
+    q.phi_mode = phi_mode; q.hinge = flags & 1; q.excl_dup = (flags >> 1) & 1; q.lam = lam;
     q.n = (double *)calloc((size_t)(N > 0 ? N : 1), sizeof(double));
     q.t = (int64_t *)calloc((size_t)(N > 0 ? N : 1), sizeof(int64_t));
     q.mu = (double *)calloc((size_t)d, sizeof(double));
@@ -329,15 +338,15 @@ int orc_loss(int64_t C, int32_t d, int32_t dtype, const void *T, const int64_t *
 int orc_loss_rows_v(int64_t C, int32_t K, int32_t d, int32_t dtype, const void *T,
                     const int64_t *lab, int64_t E, int64_t M_last, int64_t N, const void *X,
                     const int64_t *y, const int32_t *pairing, double s, double m, int32_t phi_mode,
-                    int32_t hinge, double lam, int64_t nsel, const int64_t *rows, double *dx,
+                    int32_t flags, double lam, int64_t nsel, const int64_t *rows, double *dx,
                     double *lse, int64_t *tslot, double *phi, double *ell, int64_t *counts,
                     double *mu_out) {
     if (C < 1 || d < 1 || K < 1 || N < 0 || (dtype != 0 && dtype != 1)) return ORC_EINVAL;
-    if (phi_mode < 0 || phi_mode > 2 || hinge < 0 || hinge > 1 || !isfinite(lam)) return ORC_EINVAL;
+    if (phi_mode < 0 || phi_mode > 2 || flags < 0 || flags > 3 || !isfinite(lam)) return ORC_EINVAL;
     orc_ctx q = {0};
     q.C = C; q.N = N; q.E = E; q.M_last = M_last; q.d = d; q.dtype = dtype; q.K = K;
     q.T = T; q.lab = lab; q.X = X; q.y = y; q.s = s; q.m = m;
-    q.phi_mode = phi_mode; q.hinge = hinge; q.lam = lam;
+    q.phi_mode = phi_mode; q.hinge = flags & 1; q.excl_dup = (flags >> 1) & 1; q.lam = lam;
     q.n = (double *)calloc((size_t)(N > 0 ? N : 1), sizeof(double));
     q.t = (int64_t *)calloc((size_t)(N > 0 ? N : 1), sizeof(int64_t));
     q.mu = (double *)calloc((size_t)d, sizeof(double));

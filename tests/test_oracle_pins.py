@@ -569,3 +569,43 @@ def test_phi_sum_is_occupancy_times_mean_and_max_bounds_mean():
     hm = p.loss(X, y, None, 30.0, 0.3, hinge=True).phi
     np.testing.assert_allclose(sm, 20 * mean, rtol=1e-12)
     assert np.all(mx >= mean) and np.all(hm >= mean)
+
+
+# ----------------------------------------------------------------------------- NEXT-3 duplicates
+def test_exclude_stale_duplicates_equals_deleting_them():
+    """Variant 'exclude stale self-duplicates': for in-pool rows it must equal the D8 loss on
+    the pool with the older same-label slots deleted (independent formulation: a smaller pool)."""
+    rng = np.random.default_rng(51)
+    C, d = 24, 8
+    T = rng.standard_normal((C, d)); T /= np.linalg.norm(T, axis=1, keepdims=True)
+    lab = rng.integers(0, 6, C)                     # many duplicates
+    p = Pool(C, d, F32)
+    p.enqueue(T.astype(np.float32), lab)
+    y = np.array([0, 1, 2, 3, 4, 5, 2, 0])
+    X = rng.standard_normal((len(y), d)).astype(np.float32)
+    r = p.loss(X, y, None, 20.0, 0.3, excl_dup=True)
+    assert r.N_neg == 0
+    for i in range(len(y)):
+        keep = [c for c in range(C) if lab[c] != y[i] or c == r.tslot[i]]   # newest one of y_i stays
+        q = Pool(len(keep), d, F32)
+        q.enqueue(T[keep].astype(np.float32), lab[keep])
+        ri = q.loss(X[i:i + 1], y[i:i + 1], None, 20.0, 0.3)
+        assert r.ell[i] == pytest.approx(ri.ell[0], rel=1e-12)
+        # per-row gradient scales with 1/N_pos: compare the row's own gradient
+        np.testing.assert_allclose(r.dx[i] * len(y), ri.dx[0], rtol=1e-10, atol=1e-13)
+
+
+def test_exclude_stale_duplicates_closed_form_and_out_of_pool():
+    """SURVEY case F pool [(.8,.6) lab 7 older, (0,1) lab 3, (1,0) lab 7 newest, (.6,.8) lab 5]:
+    with the stale (.8,.6) excluded the row x=(0,1), y=7 sees {(0,1), (1,0)t, (.6,.8)}:
+    L = log(e^{s*1} + e^{s*(0-m)} + e^{s*.8}) - s*(0-m); out-of-pool rows are unchanged."""
+    p = _pool_from([([0.8, 0.6], 7), ([0.0, 1.0], 3), ([1.0, 0.0], 7), ([0.6, 0.8], 5)])
+    s, m = 64.0, 0.35
+    r = p.loss(np.array([[0.0, 1.0]], np.float32), np.array([7]), None, s, m, excl_dup=True)
+    z = np.array([s * 1.0, s * (0.0 - m), s * np.float64(np.float32(0.8))])
+    want = np.log(np.exp(z - z.max()).sum()) + z.max() - s * (0.0 - m)
+    assert r.L == pytest.approx(want, rel=1e-9)
+    X = np.array([[0.3, 0.7], [0.9, -0.2]], np.float32)
+    a = p.loss(X, np.array([99, 98]), None, s, m, excl_dup=True)
+    b = p.loss(X, np.array([99, 98]), None, s, m)
+    assert a.L == b.L and np.array_equal(a.dx, b.dx)
