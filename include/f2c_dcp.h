@@ -104,6 +104,16 @@ int f2c_dcp_create_k(int64_t C, int32_t K, int32_t d, int32_t dtype, int32_t wor
  * too (their GEMM cost is the in-pool rows').  Errors: F2C_EINVAL for out-of-range values. */
 int f2c_dcp_set_lcos(f2c_dcp *h, int32_t phi_mode, int32_t hinge, double lambda);
 
+/* NEXT-3 variant of Eq. 9's denominator for pools holding several slots with one label
+ * (possible under pure Eq. 7, D7).  The paper sums over every slot j = 1..C, so by
+ * default (exclude_stale = 0, reading D8) an in-pool row's OLDER slots of its own label stay
+ * in the softmax as ordinary, unmargined negatives.  exclude_stale = 1 drops them from the
+ * row's softmax (and hence from p and dx): the row is then scored as if those stale slots
+ * had been deleted.  The target is still the newest slot (D8); out-of-pool rows and L_cos are
+ * unaffected.  Applies to every later loss call on this handle.  Cost: two extra passes over
+ * the shard's slot labels per loss call.  Errors: F2C_EINVAL unless exclude_stale is 0 or 1. */
+int f2c_dcp_set_dup_mode(f2c_dcp *h, int32_t exclude_stale);
+
 /* Enqueue one identity block (Eq. 7 + Algorithm 1):
  * the global block is the concatenation of every rank's g_feats in rank order
  * (emulated world: g_feats already holds the concatenation, world*m_local rows).

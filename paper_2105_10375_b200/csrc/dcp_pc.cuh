@@ -104,6 +104,13 @@ struct PCParams {
     float *seg_l;          // [S][128]
     float *seg_mx;         // [S][128]
     float *seg_O;          // [S][128][d]
+    // NEXT-3 "exclude stale self-duplicates" (excl != 0): per 128-slot tile t, entries
+    // [dup_off[t], dup_off[t+1]) of dup_list = (local slot, label hash entry) of the stale
+    // duplicates in that tile; a row skips the ones of its own hash entry row_hent[r]
+    int excl;
+    const int *dup_off;
+    const int2 *dup_list;
+    const int *row_hent;
     unsigned long long *dbg;
     int dbg_flags;         // timing experiments only: 1 = skip P smem writes, 128 = skip DSMEM copy,
                            // 4 / 8 = no producer / consumer pool loads, 16 = no softmax arithmetic,
@@ -431,6 +438,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                 const int row = rg * PC_R + r;
                 const float2 ab = p.row_ab[row];
                 const int tg = p.row_tgt[row];
+                const int hent = p.excl ? p.row_hent[row] : -1;
                 // x_hat (this thread's row, d half h) -> TMEM A operand columns
                 mbar_wait(&aux->xfree, (sg & 1) ^ 1);
                 tc_fence_after();
@@ -515,6 +523,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                                         p.ttgt[row] = e[k] - p.margin_l2;
                                         e[k] = -INFINITY;
                                     }
+                            }
+                        }
+                        if (p.excl) {  // NEXT-3: drop this row's stale self-duplicates of tile t
+                            const int o1 = p.dup_off[t + 1];
+                            for (int o = p.dup_off[t]; o < o1; ++o) {
+                                const int2 v = p.dup_list[o];
+                                const int kt = v.x - base;
+                                if (v.y == hent && kt >= 0 && kt < 64) {
+#pragma unroll
+                                    for (int k = 0; k < 64; ++k)
+                                        if (k == kt) e[k] = -INFINITY;
+                                }
                             }
                         }
                         if (p.wslot && row == n_pos) {  // mu row with K >= 2: p_c = 1/||T_bar_c||

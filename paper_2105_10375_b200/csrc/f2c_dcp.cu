@@ -103,7 +103,7 @@ struct Layout {
     size_t T, lab, sc, x_all, y_all, pair_all, blk_x, blk_y, inv_n, hslot, hkeys, hvals, tseq,
         comp_idx, pos_row, X_pos, row_ab, row_tgt, ttgt, seg_l, seg_mx, seg_O, rowloss, st_lse,
         st_cos, st_phi, st_ell, seg_arg, rs_buf, rs_all, dx_part, tseq_ext, dx32, tmax_glob, mu_buf, Traw, wslot,
-        total;
+        hgseq, row_hent, dup_cnt, dup_off, dup_list, total;
     int64_t C_loc, N, Mg, R_max, S_max;
     int H;
 };
@@ -171,6 +171,15 @@ static Layout make_layout(int64_t C, int d, int dtype, int W, int rank, int64_t 
     // K >= 2: raw features [C_loc][K][d] (state) and 1/||T_bar_c|| (the T region holds T_bar)
     L.Traw = take(K > 1 ? static_cast<size_t>(L.C_loc) * K * d * es : 0, 1024);
     L.wslot = take(K > 1 ? static_cast<size_t>(L.C_loc) * 4 : 0);
+    // NEXT-3 stale self-duplicate lists (f2c_dcp_set_dup_mode): per hash entry the target
+    // write index, per compacted row its hash entry, per 128-slot tile a count / offset, and
+    // at most one (slot, entry) pair per local slot
+    const int64_t n_tiles = (L.C_loc + 127) / 128;
+    L.hgseq = take(static_cast<size_t>(H) * 8);
+    L.row_hent = take(static_cast<size_t>(L.R_max) * 4);
+    L.dup_cnt = take(static_cast<size_t>(n_tiles) * 4);
+    L.dup_off = take(static_cast<size_t>(n_tiles + 1) * 4);
+    L.dup_list = take(static_cast<size_t>(L.C_loc) * 8);
     L.total = align_up(o, 1024);
     return L;
 }
@@ -194,6 +203,7 @@ struct f2c_dcp {
     // NEXT-3 L_cos variant (f2c_dcp_set_lcos): reduction, hinge, weight
     int phi_mode = 0, hinge = 0;
     float lam = 1.f;
+    int excl_dup = 0;  // NEXT-3: exclude stale self-duplicates (f2c_dcp_set_dup_mode)
     int neg_mode() const { return phi_mode == 2 ? 2 : (hinge ? 1 : 0); }
     bool emulated;
     int64_t n_local_max, m_local_max;
@@ -526,6 +536,13 @@ struct StepCtx {
     cudaStream_t st;
 };
 
+static int64_t occ_local(const f2c_dcp *h, const Rank &R) {
+    const int64_t C_occ = h->E < h->C ? h->E : h->C;
+    int64_t o = C_occ - R.lo;
+    if (o > R.hi - R.lo) o = R.hi - R.lo;
+    return o < 0 ? 0 : o;
+}
+
 // a2 + a3: norms, label hash, local target resolve (tseq = newest local seq or -1)
 static int phase_resolve(f2c_dcp *h, Rank &R, const StepCtx &c) {
     const Layout &L = R.L;
@@ -577,8 +594,29 @@ static int phase_compact(f2c_dcp *h, Rank &R, const StepCtx &c, const int *tmax_
     a.sc = R.sc();
     a.tmax_bits = tmax_bits;
     a.neg_mode = h->neg_mode();
+    a.excl = h->excl_dup;
+    a.hslot = R.at<int>(L.hslot);
+    a.row_hent = R.at<int>(L.row_hent);
+    a.hgseq = R.at<int64_t>(L.hgseq);
     k_compact<<<1, 1024, 0, c.st>>>(a);
     LAUNCH_CHECK();
+    const int64_t occ = occ_local(h, R);
+    if (h->excl_dup && occ > 0) {  // NEXT-3: per-tile lists of the shard's stale self-duplicates
+        const int n_tiles = static_cast<int>((occ + 127) / 128);
+        int64_t blocks = (occ + 255) / 256;
+        if (blocks > h->G * 16) blocks = h->G * 16;
+        CUDA_TRY(cudaMemsetAsync(R.at<int>(L.dup_cnt), 0, static_cast<size_t>(n_tiles) * 4, c.st));
+        k_dup_count<<<static_cast<unsigned>(blocks), 256, 0, c.st>>>(
+            R.at<int64_t>(L.lab), occ, R.lo, h->C, h->E, R.at<int64_t>(L.hkeys), L.H, R.at<int64_t>(L.hgseq),
+            R.at<int>(L.dup_cnt));
+        LAUNCH_CHECK();
+        k_dup_scan<<<1, 1024, 0, c.st>>>(R.at<int>(L.dup_cnt), R.at<int>(L.dup_off), n_tiles);
+        LAUNCH_CHECK();
+        k_dup_fill<<<static_cast<unsigned>(blocks), 256, 0, c.st>>>(
+            R.at<int64_t>(L.lab), occ, R.lo, h->C, h->E, R.at<int64_t>(L.hkeys), L.H, R.at<int64_t>(L.hgseq),
+            R.at<int>(L.dup_cnt), R.at<int>(L.dup_off), R.at<int2>(L.dup_list));
+        LAUNCH_CHECK();
+    }
     const int row_bytes = h->d * 2;
     k_gather<<<static_cast<unsigned>(c.N + 1), 64, 0, c.st>>>(c.x, R.at<int>(L.pos_row), R.sc(), row_bytes,
                                                           R.base + L.X_pos, R.base + L.T, R.at<int>(L.row_tgt),
@@ -613,7 +651,7 @@ static int phase_main(f2c_dcp *h, Rank &R, const StepCtx &c, int64_t occ_loc) {
         h->ev_used += 2;
         CUDA_TRY(cudaEventRecord(e0, c.st));
     }
-    if (h->use_tp64 && h->neg_mode() == 0) {
+    if (h->use_tp64 && h->neg_mode() == 0 && !h->excl_dup) {
         dcp_tp64_kernel<<<h->G, TP_THREADS, TP_SMEM_BYTES, c.st>>>(R.tmT, R.tmX, p);
     } else {
         PCParams q;
@@ -632,6 +670,10 @@ static int phase_main(f2c_dcp *h, Rank &R, const StepCtx &c, int64_t occ_loc) {
         q.seg_l = p.seg_l;
         q.seg_mx = p.seg_mx;
         q.seg_O = p.seg_O;
+        q.excl = h->excl_dup;
+        q.dup_off = R.at<int>(L.dup_off);
+        q.dup_list = R.at<int2>(L.dup_list);
+        q.row_hent = R.at<int>(L.row_hent);
         q.dbg = p.dbg;
         q.dbg_flags = h->dbg_flags;
         dcp_pc_kernel<<<(h->G / 2) * 2, PC_THREADS, PC_SMEM_BYTES, c.st>>>(R.tm3p, R.tm3q, q);
@@ -641,12 +683,6 @@ static int phase_main(f2c_dcp *h, Rank &R, const StepCtx &c, int64_t occ_loc) {
     return F2C_OK;
 }
 
-static int64_t occ_local(const f2c_dcp *h, const Rank &R) {
-    const int64_t C_occ = h->E < h->C ? h->E : h->C;
-    int64_t o = C_occ - R.lo;
-    if (o > R.hi - R.lo) o = R.hi - R.lo;
-    return o < 0 ? 0 : o;
-}
 
 static CombineArgs combine_args(f2c_dcp *h, Rank &R, const StepCtx &c, int64_t occ, uint8_t *dx) {
     const Layout &L = R.L;
@@ -667,7 +703,7 @@ static CombineArgs combine_args(f2c_dcp *h, Rank &R, const StepCtx &c, int64_t o
     a.C_occ = h->E < h->C ? h->E : h->C;
     a.d = h->d;
     a.dtype = h->dtype;
-    const bool tp64 = h->use_tp64 && h->neg_mode() == 0;
+    const bool tp64 = h->use_tp64 && h->neg_mode() == 0 && !h->excl_dup;
     a.G = tp64 ? h->G : h->G / 2;
     a.rows_per_group = tp64 ? TP_R : PC_R;
     a.n_tiles = static_cast<int>((occ + TP_TILE - 1) / TP_TILE);
@@ -851,6 +887,13 @@ extern "C" int f2c_dcp_set_lcos(f2c_dcp *h, int32_t phi_mode, int32_t hinge, dou
     h->phi_mode = phi_mode;
     h->hinge = hinge;
     h->lam = static_cast<float>(lambda);
+    return F2C_OK;
+}
+
+extern "C" int f2c_dcp_set_dup_mode(f2c_dcp *h, int32_t exclude_stale) {
+    if (!h) return fail(F2C_EINVAL, "NULL handle");
+    if (exclude_stale != 0 && exclude_stale != 1) return fail(F2C_EINVAL, "exclude_stale must be 0 or 1");
+    h->excl_dup = exclude_stale;
     return F2C_OK;
 }
 

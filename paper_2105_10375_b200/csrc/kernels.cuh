@@ -359,6 +359,89 @@ __global__ void k_resolve(const int *__restrict__ hslot, const unsigned long lon
     tseq[i] = h < 0 ? -1 : static_cast<int64_t>(vals[h]) - 1;
 }
 
+// ------------------------------------------------------------------ NEXT-3: stale self-duplicates
+// Variant "exclude stale self-duplicates" (D8 keeps them): an in-pool
+// row's softmax skips the occupied slots that carry its own label but are not its target
+// (the newest such slot).  Built after the targets are final (W > 1: after C2): a per-tile
+// list of the shard's stale slots, (local slot, label hash entry), in tile order, which the
+// fused kernel's softmax warps consult once per tile.  Two passes over the shard's labels
+// (count per 128-slot tile, then fill) around an exclusive scan of the tile counts.
+__device__ __forceinline__ int stale_dup_entry(int64_t L, int64_t c, int64_t C, int64_t E,
+                                               const int64_t *__restrict__ keys, int H,
+                                               const int64_t *__restrict__ hgseq) {
+    if (L < 0) return -1;
+    unsigned h = static_cast<unsigned>(hash64(static_cast<uint64_t>(L))) & (H - 1);
+    for (;;) {
+        const int64_t k = keys[h];
+        if (k == -1) return -1;
+        if (k == L) {
+            const int64_t seq = c + C * ((E - 1 - c) / C);
+            return seq != hgseq[h] ? static_cast<int>(h) : -1;
+        }
+        h = (h + 1) & (H - 1);
+    }
+}
+
+__global__ void k_dup_count(const int64_t *__restrict__ lab, int64_t n_occ_loc, int64_t lo, int64_t C,
+                            int64_t E, const int64_t *__restrict__ keys, int H,
+                            const int64_t *__restrict__ hgseq, int *__restrict__ tile_cnt) {
+    for (int64_t cl = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; cl < n_occ_loc;
+         cl += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        if (stale_dup_entry(lab[cl], lo + cl, C, E, keys, H, hgseq) >= 0) atomicAdd(tile_cnt + (cl >> 7), 1);
+}
+
+// single CTA: tile_off[t] = sum of tile_cnt[< t] (n_tiles + 1 entries); tile_cnt reset to 0
+// for use as the fill cursor
+__global__ void __launch_bounds__(1024) k_dup_scan(int *__restrict__ tile_cnt, int *__restrict__ tile_off,
+                                                   int n_tiles) {
+    __shared__ int wsum[32];
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int per = (n_tiles + nt - 1) / nt;
+    const int t0 = tid * per, t1 = min(t0 + per, n_tiles);
+    int cnt = 0;
+    for (int t = t0; t < t1; ++t) cnt += tile_cnt[t];
+    const int lane = tid & 31, w = tid >> 5;
+    int v = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int u = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += u;
+    }
+    if (lane == 31) wsum[w] = v;
+    __syncthreads();
+    if (w == 0) {
+        int s2 = wsum[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int u = __shfl_up_sync(0xffffffffu, s2, o);
+            if (lane >= o) s2 += u;
+        }
+        wsum[lane] = s2;
+    }
+    __syncthreads();
+    int run = (w > 0 ? wsum[w - 1] : 0) + v - cnt;
+    for (int t = t0; t < t1; ++t) {
+        tile_off[t] = run;
+        run += tile_cnt[t];
+        tile_cnt[t] = 0;
+    }
+    if (tid == nt - 1) tile_off[n_tiles] = wsum[31];
+}
+
+__global__ void k_dup_fill(const int64_t *__restrict__ lab, int64_t n_occ_loc, int64_t lo, int64_t C,
+                           int64_t E, const int64_t *__restrict__ keys, int H,
+                           const int64_t *__restrict__ hgseq, int *__restrict__ tile_cur,
+                           const int *__restrict__ tile_off, int2 *__restrict__ list) {
+    for (int64_t cl = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; cl < n_occ_loc;
+         cl += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int he = stale_dup_entry(lab[cl], lo + cl, C, E, keys, H, hgseq);
+        if (he >= 0) {
+            const int t = static_cast<int>(cl >> 7);
+            list[tile_off[t] + atomicAdd(tile_cur + t, 1)] = make_int2(static_cast<int>(cl), he);
+        }
+    }
+}
+
 // ------------------------------------------------------------------ a3: split + compaction
 // Single CTA (1024 threads): Eq. 6's split into in-pool (F_p^DCP) and out-of-pool
 // rows, compaction of the in-pool rows in batch order, per-row softmax coefficients,
@@ -382,6 +465,12 @@ struct CompactArgs {
     Scalars *sc;
     const int *tmax_bits;     // max ||T_c|| over the whole pool (all shards)
     float ref_scale;          // s*log2(e)*(1+2^-10): reference exponent per unit norm
+    // NEXT-3 "exclude stale self-duplicates": the row's label hash entry (-1 = none) and the
+    // target write index per hash entry, read by the duplicate-list kernels below
+    int excl;
+    const int *hslot;         // [N]
+    int *row_hent;            // [R_max]
+    int64_t *hgseq;           // [H]
 };
 __global__ void __launch_bounds__(1024) k_compact(CompactArgs a) {
     __shared__ int wsum[32];
@@ -430,6 +519,11 @@ __global__ void __launch_bounds__(1024) k_compact(CompactArgs a) {
         } else if (ts >= 0) {
             a.comp_idx[i] = k;
             a.pos_row[k] = static_cast<int>(i);
+            if (a.excl) {
+                const int he = a.hslot[i];
+                a.row_hent[k] = he;
+                if (he >= 0) a.hgseq[he] = ts;  // rows sharing a label share the target
+            }
             a.row_ab[k] = make_float2(a.log2e_s * a.inv_n[i], B);
             const int64_t slot = ts % a.C;
             a.row_tgt[k] = (slot >= a.lo && slot < a.hi) ? static_cast<int>(slot - a.lo) : -1;
@@ -441,6 +535,8 @@ __global__ void __launch_bounds__(1024) k_compact(CompactArgs a) {
     }
     // the mu row and the padding rows of the last row group
     const int n_rows = a.neg_mode ? static_cast<int>(a.N) + 1 : n_pos + 1;
+    if (a.excl)
+        for (int r = n_pos + tid; r < a.R_max; r += nt) a.row_hent[r] = -1;  // mu, out-of-pool, padding
     for (int r = (a.neg_mode ? n_rows : n_pos) + tid; r < a.R_max; r += nt) {
         a.row_ab[r] = make_float2(0.f, 0.f);
         a.row_tgt[r] = -1;
