@@ -44,6 +44,7 @@ def lib():
         P = ctypes.c_void_p
         i64, i32, f64 = ctypes.c_int64, ctypes.c_int32, ctypes.c_double
         L.orc_enqueue.argtypes = [i64, i32, i32, P, P, P, P, P, P, i64]
+        L.orc_enqueue_refresh.argtypes = [i64, i32, i32, P, P, P, P, P, P, i64, P]
         L.orc_loss.argtypes = [i64, i32, i32, P, P, i64, i64, i64, P, P, P, f64, f64,
                                P, P, P, P, P, P, P, P, P]
         L.orc_loss_rows.argtypes = [i64, i32, i32, P, P, i64, i64, i64, P, P, P, f64, f64,
@@ -57,7 +58,7 @@ def lib():
                                  i32, i32, f64, P, P, P, P, P, P, P, P, P]
         L.orc_loss_rows_v.argtypes = [i64, i32, i32, i32, P, P, i64, i64, i64, P, P, P, f64, f64,
                                       i32, i32, f64, i64, P, P, P, P, P, P, P, P]
-        for f in (L.orc_enqueue, L.orc_loss, L.orc_loss_rows, L.orc_ema, L.orc_loss_k,
+        for f in (L.orc_enqueue, L.orc_enqueue_refresh, L.orc_loss, L.orc_loss_rows, L.orc_ema, L.orc_loss_k,
                   L.orc_loss_rows_k, L.orc_loss_v, L.orc_loss_rows_v):
             f.restype = ctypes.c_int
         _lib = L
@@ -110,22 +111,48 @@ class Pool:
         self.lab = np.full(C, -1, dtype=np.int64)
         self.E = np.zeros(1, dtype=np.int64)
         self.M_last = np.zeros(1, dtype=np.int64)
+        # after a refresh-in-place enqueue (NEXT-3): write index of the slot holding each row
+        # of the last block (the pairing check's target); None after a pure Eq. 7 enqueue
+        self.blk_seq = None
 
     @property
     def C_occ(self) -> int:
         return int(min(self.E[0], self.C))
 
-    def enqueue(self, G: np.ndarray, y: np.ndarray) -> None:
+    def enqueue(self, G: np.ndarray, y: np.ndarray, refresh: bool = False) -> None:
+        """Eq. 7 / Algorithm 1 (orc_enqueue); refresh=True: SPEC's refresh-in-place insert
+        (orc_enqueue_refresh, NEXT-3, reading R7)."""
         G = np.ascontiguousarray(G)
         y = np.ascontiguousarray(y, dtype=np.int64)
         want = (len(y), self.d) if self.K == 1 else (len(y), self.K, self.d)
         if _raw_dtype(G) != self.dtype or G.shape != want:
             raise OracleError(2, "enqueue shape/dtype")
         # a slot holds K consecutive feature rows: the ring copy is the same with rows of K*d
+        if refresh:
+            bs = np.zeros(len(y), dtype=np.int64)
+            rc = lib().orc_enqueue_refresh(self.C, self.K * self.d, self.dtype, _p(self.T), _p(self.lab),
+                                           _p(self.E), _p(self.M_last), _p(G), _p(y), len(y), _p(bs))
+            if rc:
+                raise OracleError(rc, "orc_enqueue_refresh")
+            self.blk_seq = bs
+            return
         rc = lib().orc_enqueue(self.C, self.K * self.d, self.dtype, _p(self.T), _p(self.lab), _p(self.E),
                                _p(self.M_last), _p(G), _p(y), len(y))
         if rc:
             raise OracleError(rc, "orc_enqueue")
+        self.blk_seq = None
+
+    def _pairing(self, pairing, tslot):
+        """The C oracle checks pairing against the pure ring (E - M_last + j); after a
+        refresh enqueue row j's slot is blk_seq[j] mod C instead (D13 with R7)."""
+        if pairing is None or self.blk_seq is None:
+            return pairing
+        pr = np.asarray(pairing)
+        for i in np.where(pr >= 0)[0]:
+            j = int(pr[i])
+            if j >= int(self.M_last[0]) or tslot[i] != self.blk_seq[j] % self.C:
+                raise OracleError(4, "orc_loss pairing")
+        return None
 
     def loss(self, X: np.ndarray, y: np.ndarray, pairing: np.ndarray | None, s: float, m: float,
              want_P: bool = False, want_dT: bool = False, phi_mode: int = PHI_MEAN,
@@ -136,6 +163,9 @@ class Pool:
         if _raw_dtype(X) != self.dtype or X.shape != (N, d):
             raise OracleError(2, "loss shape/dtype")
         pr = None if pairing is None else np.ascontiguousarray(pairing, dtype=np.int32)
+        pr_after = pr if self.blk_seq is not None else None
+        if pr_after is not None:
+            pr = None
         out3 = np.zeros(3)
         dx = np.zeros((N, d))
         lse, phi, ell = np.zeros(N), np.zeros(N), np.zeros(N)
@@ -150,6 +180,7 @@ class Pool:
                               _p(P), _p(dT))
         if rc:
             raise OracleError(rc, "orc_loss")
+        self._pairing(pr_after, ts)
         return LossResult(out3[0], out3[1], out3[2], dx, lse, ts, phi, ell,
                           int(counts[0]), int(counts[1]), int(counts[2]), P, dT)
 
@@ -160,6 +191,9 @@ class Pool:
         rows = np.ascontiguousarray(rows, dtype=np.int64)
         N, d, k = len(y), self.d, len(rows)
         pr = None if pairing is None else np.ascontiguousarray(pairing, dtype=np.int32)
+        if self.blk_seq is not None and pr is not None:
+            self.loss(X, y, pr, s, m, phi_mode=phi_mode, hinge=hinge, lam=lam, excl_dup=excl_dup)
+            pr = None   # (checked above over the whole batch)
         dx = np.zeros((k, d))
         lse, phi, ell = np.zeros(k), np.zeros(k), np.zeros(k)
         ts = np.zeros(k, dtype=np.int64)

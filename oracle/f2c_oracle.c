@@ -21,6 +21,8 @@
  *   orc_loss_rows    the same definition, evaluated for a subset of rows only
  *                    (the global normalisers N_pos, N_neg, C_occ and mu are still
  *                    computed from the whole batch / pool).
+ *   orc_enqueue_refresh
+ *                    NEXT-3: SPEC's refresh-in-place insert (reading R7).
  *   orc_ema          G-Net moving average phi <- m*phi + (1-m)*theta.
  *   orc_loss_k / orc_loss_rows_k
  *                    the pool with K features per slot ("C x K x D"):
@@ -97,6 +99,66 @@ int orc_enqueue(int64_t C, int32_t d, int32_t dtype, void *T, int64_t *lab, int6
 
 /* global write index of the current content of slot c (c < min(E, C)) */
 static int64_t orc_seq(int64_t c, int64_t C, int64_t E) { return c + C * ((E - 1 - c) / C); }
+
+/* ---- NEXT-3: refresh-in-place enqueue (reading R7) ----------
+ * SPEC's insert_batch: "If an id is already resident, its features are overwritten in place
+ * and its queue position is unchanged"; new ids take the next positions of the ring,
+ * evicting the oldest (Alg. 1 / Eq. 7 for them).  Reading R7 for the one case SPEC leaves
+ * open -- a resident id whose slot is among those this block's new rows evict -- keeps
+ * every block id resident after the call: such a row is appended as a new one.
+ *   1. y_j >= 0 and pairwise distinct within the block ("duplicate ids ... input error");
+ *   2. res(j) = the newest occupied slot with label y_j (D8) and sigma_j its write index,
+ *      or none;
+ *   3. appending n rows overwrites the contents with write index < E + n - C; so
+ *      n = the smallest n >= n0 = #{j : no res(j)} with
+ *      n = n0 + #{j : res(j) exists, sigma_j < E + n - C}   (iterated from n0; monotone);
+ *   4. rows with no res(j), or whose res(j) is overwritten (step 3), are appended in block
+ *      order: k-th such row -> slot (E + k) mod C, write index E + k;
+ *   5. every other row overwrites the features of slot res(j) (label and age unchanged);
+ *   6. E += n; blk_seq[j] = write index of the slot now holding row j. */
+int orc_enqueue_refresh(int64_t C, int32_t d, int32_t dtype, void *T, int64_t *lab, int64_t *E,
+                        int64_t *M_last, const void *G, const int64_t *y, int64_t M,
+                        int64_t *blk_seq) {
+    if (C < 1 || d < 1 || (dtype != 0 && dtype != 1)) return ORC_EINVAL;
+    if (M < 1 || M > C) return ORC_ECAPACITY;
+    for (int64_t j = 0; j < M; ++j) {
+        if (y[j] < 0) return ORC_EINVAL;
+        for (int64_t i = 0; i < j; ++i)
+            if (y[i] == y[j]) return ORC_EINVAL;
+    }
+    const int64_t Ec = *E, C_occ = Ec < C ? Ec : C;
+    int64_t *sigma = (int64_t *)malloc((size_t)M * sizeof(int64_t));
+    if (!sigma) return ORC_EINVAL;
+    for (int64_t j = 0; j < M; ++j) {  /* step 2 */
+        sigma[j] = -1;
+        for (int64_t c = 0; c < C_occ; ++c)
+            if (lab[c] == y[j] && orc_seq(c, C, Ec) > sigma[j]) sigma[j] = orc_seq(c, C, Ec);
+    }
+    int64_t n0 = 0;
+    for (int64_t j = 0; j < M; ++j) n0 += sigma[j] < 0;
+    int64_t n = n0;
+    for (;;) {  /* step 3 */
+        int64_t f = n0;
+        for (int64_t j = 0; j < M; ++j) f += sigma[j] >= 0 && sigma[j] < Ec + n - C;
+        if (f == n) break;
+        n = f;
+    }
+    size_t rb = (size_t)d * orc_esize(dtype);
+    int64_t k = 0;
+    for (int64_t j = 0; j < M; ++j) {  /* steps 4, 5 */
+        int64_t w;
+        if (sigma[j] < 0 || sigma[j] < Ec + n - C) w = Ec + k++;
+        else w = sigma[j];
+        int64_t c = w % C;
+        memcpy((char *)T + (size_t)c * rb, (const char *)G + (size_t)j * rb, rb);
+        lab[c] = y[j];
+        blk_seq[j] = w;
+    }
+    free(sigma);
+    *E = Ec + n;  /* step 6 */
+    *M_last = M;
+    return ORC_OK;
+}
 
 /* ---- shared pieces of the loss definition ------------------------------------ */
 typedef struct {

@@ -609,3 +609,121 @@ def test_exclude_stale_duplicates_closed_form_and_out_of_pool():
     a = p.loss(X, np.array([99, 98]), None, s, m, excl_dup=True)
     b = p.loss(X, np.array([99, 98]), None, s, m)
     assert a.L == b.L and np.array_equal(a.dx, b.dx)
+
+
+# ----------------------------------------------------------------------------- NEXT-3 refresh-in-place enqueue
+def _queue_refresh(q, ids, feats, C):
+    """SPEC's insert_batch as a literal queue: a Python list of [id, feat],
+    oldest first.  Resident ids (their newest entry) are refreshed in place, new ids are
+    appended in block order, the overflow is dropped from the front.  Reading R7: a block id
+    that this drops is appended as a new one too, until every block id survives
+    (S:307).  Returns the new queue and the number of appended rows."""
+    M = len(ids)
+    S = set(j for j in range(M) if all(e[0] != ids[j] for e in q))
+    while True:
+        q2 = [list(e) for e in q]
+        for j in range(M):
+            if j in S:
+                continue
+            for e in reversed(q2):          # the newest entry of the id (D8)
+                if e[0] == ids[j]:
+                    e[1] = feats[j]
+                    break
+        for j in range(M):
+            if j in S:
+                q2.append([ids[j], feats[j]])
+        q2 = q2[-C:]
+        alive = [e[0] for e in q2]
+        missing = set(j for j in range(M) if ids[j] not in alive
+                      or [e for e in q2 if e[0] == ids[j]][-1][1] != feats[j])
+        if not missing:
+            return q2, len(S)
+        S |= missing
+
+
+def _ring_in_order(p):
+    E, C = int(p.E[0]), p.C
+    order = np.arange(E) if E < C else (np.arange(C) + E) % C
+    return [[int(p.lab[c]), float(p.T[c, 0])] for c in order]
+
+
+def test_refresh_spec_examples():
+    """S:280 'a resident identity re-inserted -> fill_count unchanged, features replaced';
+    S:278's FIFO when nothing is resident; reading R7 when the resident is the oldest."""
+    p = Pool(4, 1, F32)
+    p.enqueue(np.array([[1.0], [2.0]], np.float32), np.array([10, 20]), refresh=True)
+    p.enqueue(np.array([[1.5]], np.float32), np.array([10]), refresh=True)     # not full
+    assert int(p.E[0]) == 2 and p.lab[:2].tolist() == [10, 20] and p.T[0, 0] == 1.5
+    assert p.blk_seq.tolist() == [0]
+    for blk in ([3, 4], [5, 6]):                                               # S:278
+        q = Pool(4, 1, F32)
+        q.enqueue(np.array([[1], [2]], np.float32), np.array([1, 2]), refresh=True)
+        q.enqueue(np.array([[3], [4]], np.float32), np.array([3, 4]), refresh=True)
+        q.enqueue(np.array([[5], [6]], np.float32), np.array([5, 6]), refresh=True)
+        assert q.lab.tolist() == [5, 6, 3, 4]
+    # full pool A,B,C,D (A oldest): re-insert C with new G -> C refreshed in place (age kept),
+    # G takes A's slot
+    p = Pool(4, 1, F32)
+    p.enqueue(np.array([[1], [2], [3], [4]], np.float32), np.array([1, 2, 3, 4]), refresh=True)
+    p.enqueue(np.array([[3.5], [7]], np.float32), np.array([3, 7]), refresh=True)
+    assert p.lab.tolist() == [7, 2, 3, 4] and p.T[2, 0] == 3.5 and int(p.E[0]) == 5
+    assert p.blk_seq.tolist() == [2, 4]
+    # re-insert A (the oldest) with new E: E's append evicts A, so A is appended too (R7)
+    p = Pool(4, 1, F32)
+    p.enqueue(np.array([[1], [2], [3], [4]], np.float32), np.array([1, 2, 3, 4]), refresh=True)
+    p.enqueue(np.array([[1.5], [5]], np.float32), np.array([1, 5]), refresh=True)
+    assert p.lab.tolist() == [1, 5, 3, 4] and p.T[0, 0] == 1.5 and int(p.E[0]) == 6
+    assert [int(v) for v in p.blk_seq] == [4, 5]
+    with pytest.raises(oracle.OracleError):                                     # S:277
+        p.enqueue(np.array([[1], [2]], np.float32), np.array([9, 9]), refresh=True)
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_refresh_equals_queue_model_random(seed):
+    """The ring under refresh-in-place equals the literal queue model above after many random
+    blocks (labels from a small range, so residency and evictions of residents are common),
+    also starting from a pool with duplicates made by pure Eq. 7 enqueues."""
+    rng = np.random.default_rng(seed)
+    C = int(rng.integers(3, 40))
+    p = Pool(C, 1, F32)
+    q = []
+    n_lab = max(2, C // 2 + int(rng.integers(0, C)))
+    for it in range(300):
+        M = int(rng.integers(1, min(C, n_lab) + 1))
+        ids = rng.choice(n_lab, size=M, replace=False).astype(np.int64)
+        feats = (rng.integers(1, 10**6, M) + it * 10**6).astype(np.float32)[:, None]
+        if it < 3 and seed == 2:   # pure enqueues first: duplicates in the pool
+            p.enqueue(feats, ids)
+            q = (q + [[int(a), float(b)] for a, b in zip(ids, feats[:, 0])])[-C:]
+            continue
+        E0 = int(p.E[0])
+        p.enqueue(feats, ids, refresh=True)
+        q, n_app = _queue_refresh(q, [int(v) for v in ids], [float(v) for v in feats[:, 0]], C)
+        assert int(p.E[0]) - E0 == n_app
+        assert _ring_in_order(p) == q
+        # every block id is resident with this block's feature, at the slot blk_seq names
+        for j in range(M):
+            c = int(p.blk_seq[j]) % C
+            assert p.lab[c] == ids[j] and p.T[c, 0] == feats[j, 0]
+
+
+def test_refresh_keeps_age_and_pairing():
+    """A refreshed identity keeps its queue position (S:317 'without resetting age'): it is
+    evicted at the same step as without the refresh.  The pairing check follows blk_seq."""
+    C, M = 8, 2
+    p = Pool(C, 1, F32)
+    for k in range(4):
+        p.enqueue(np.array([[k * 2], [k * 2 + 1]], np.float32), np.array([k * 2, k * 2 + 1]), refresh=True)
+    # refresh id 4 (written at step 2) at step 4, then watch when it leaves
+    p.enqueue(np.array([[44.0], [100.0]], np.float32), np.array([4, 100]), refresh=True)
+    X = np.array([[44.0]], np.float32)
+    r = p.loss(X, np.array([4]), np.array([0], np.int32), 1.0, 0.0)
+    assert r.tslot[0] == 4 % C and r.N_pos == 1
+    with pytest.raises(oracle.OracleError):
+        p.loss(X, np.array([4]), np.array([1], np.int32), 1.0, 0.0)
+    gone = None
+    for k in range(5, 9):
+        p.enqueue(np.array([[200.0 + k], [300.0 + k]], np.float32), np.array([200 + k, 300 + k]), refresh=True)
+        if 4 not in p.lab.tolist() and gone is None:
+            gone = k
+    assert gone == 6   # written at step 2 (positions 4,5), evicted when positions 12,13 are written
