@@ -114,6 +114,23 @@ int f2c_dcp_set_lcos(f2c_dcp *h, int32_t phi_mode, int32_t hinge, double lambda)
  * the shard's slot labels per loss call.  Errors: F2C_EINVAL unless exclude_stale is 0 or 1. */
 int f2c_dcp_set_dup_mode(f2c_dcp *h, int32_t exclude_stale);
 
+/* NEXT-3 enqueue variant: SPEC's refresh-in-place insert ("If an id is
+ * already resident, its features are overwritten in place and its queue position is
+ * unchanged"; reading R7 in DESIGN.md).  With refresh_in_place = 1, later enqueues on this
+ * handle do, for the global block (rows j, labels y_j):
+ *   - y_j must be pairwise distinct (a duplicate latches F2C_EDEVICE) and >= 0;
+ *   - sigma_j = write index of the newest occupied slot with label y_j (D8), if any;
+ *   - n = the smallest n >= n0 (rows with no resident slot) with
+ *     n = n0 + #{j : sigma_j exists, sigma_j < E + n - C}: the resident rows whose slot the
+ *     appends overwrite are appended too, so every block id is resident afterwards;
+ *   - appended rows go, in block order, to slots (E + k) mod C, k < n; the other rows
+ *     overwrite the features of their resident slot (label and age unchanged); E += n.
+ * The pairing check of the next loss call follows each row's actual slot.  Because n is
+ * data-dependent, a refresh enqueue synchronises `stream` before it returns (the host
+ * bookkeeping needs E).  refresh_in_place = 0 restores pure Eq. 7 (D7).
+ * Errors: F2C_EINVAL unless refresh_in_place is 0 or 1; F2C_ECUDA if pinned memory fails. */
+int f2c_dcp_set_enqueue_mode(f2c_dcp *h, int32_t refresh_in_place);
+
 /* Enqueue one identity block (Eq. 7 + Algorithm 1):
  * the global block is the concatenation of every rank's g_feats in rank order
  * (emulated world: g_feats already holds the concatenation, world*m_local rows).

@@ -103,9 +103,9 @@ struct Layout {
     size_t T, lab, sc, x_all, y_all, pair_all, blk_x, blk_y, inv_n, hslot, hkeys, hvals, tseq,
         comp_idx, pos_row, X_pos, row_ab, row_tgt, ttgt, seg_l, seg_mx, seg_O, rowloss, st_lse,
         st_cos, st_phi, st_ell, seg_arg, rs_buf, rs_all, dx_part, tseq_ext, dx32, tmax_glob, mu_buf, Traw, wslot,
-        hgseq, row_hent, dup_cnt, dup_off, dup_list, total;
+        hgseq, row_hent, dup_cnt, dup_off, dup_list, ekeys, evals, ehslot, rseq, dst_seq, total;
     int64_t C_loc, N, Mg, R_max, S_max;
-    int H;
+    int H, He;
 };
 
 static Layout make_layout(int64_t C, int d, int dtype, int W, int rank, int64_t n_loc, int64_t m_loc,
@@ -180,6 +180,16 @@ static Layout make_layout(int64_t C, int d, int dtype, int W, int rank, int64_t 
     L.dup_cnt = take(static_cast<size_t>(n_tiles) * 4);
     L.dup_off = take(static_cast<size_t>(n_tiles + 1) * 4);
     L.dup_list = take(static_cast<size_t>(L.C_loc) * 8);
+    // NEXT-3 refresh-in-place enqueue: block-label hash, per block row the resident write
+    // index (MAX all-reduce buffer for W > 1) and the planned destination (blk_seq)
+    int He = 64;
+    while (He < 2 * L.Mg) He <<= 1;
+    L.He = He;
+    L.ekeys = take(static_cast<size_t>(He) * 8);
+    L.evals = take(static_cast<size_t>(He) * 8);
+    L.ehslot = take(static_cast<size_t>(L.Mg) * 4);
+    L.rseq = take(static_cast<size_t>(L.Mg) * 8);
+    L.dst_seq = take(static_cast<size_t>(L.Mg) * 8);
     L.total = align_up(o, 1024);
     return L;
 }
@@ -204,6 +214,9 @@ struct f2c_dcp {
     int phi_mode = 0, hinge = 0;
     float lam = 1.f;
     int excl_dup = 0;  // NEXT-3: exclude stale self-duplicates (f2c_dcp_set_dup_mode)
+    int refresh = 0;   // NEXT-3: refresh-in-place enqueue (f2c_dcp_set_enqueue_mode)
+    bool last_refresh = false;  // the last enqueue was a refresh (pairing checks use blk_seq)
+    long long *n_app_host = nullptr;  // pinned: rows appended by the last refresh enqueue
     int neg_mode() const { return phi_mode == 2 ? 2 : (hinge ? 1 : 0); }
     bool emulated;
     int64_t n_local_max, m_local_max;
@@ -224,8 +237,16 @@ struct f2c_dcp {
     int dbg_flags = 0;              // F2C_KERNEL=tp64 selects the single-CTA kernel
     ~f2c_dcp() {
         for (cudaEvent_t e : ev) cudaEventDestroy(e);
+        if (n_app_host) cudaFreeHost(n_app_host);
     }
 };
+
+static int64_t occ_local(const f2c_dcp *h, const Rank &R) {
+    const int64_t C_occ = h->E < h->C ? h->E : h->C;
+    int64_t o = C_occ - R.lo;
+    if (o > R.hi - R.lo) o = R.hi - R.lo;
+    return o < 0 ? 0 : o;
+}
 
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -367,6 +388,7 @@ int f2c_dcp_create_k(int64_t C, int32_t K, int32_t d, int32_t dtype, int32_t wor
             return fail(F2C_ECUDA, "cudaMemset(state) failed");
         }
         k_hash_clear<<<64, 256>>>(R.at<int64_t>(R.L.hkeys), R.at<unsigned long long>(R.L.hvals), R.L.H);
+        k_hash_clear<<<64, 256>>>(R.at<int64_t>(R.L.ekeys), R.at<unsigned long long>(R.L.evals), R.L.He);
         if (dtype == F2C_BF16) {
             if ((rc = make_tmap_bf16(&R.tmT, R.base + R.L.T, R.hi - R.lo, d, TP_TILE)) ||
                 (rc = make_tmap_pool3d(&R.tm3p, R.base + R.L.T, R.hi - R.lo, d, 2)) ||
@@ -435,6 +457,37 @@ static int nccl_check(int r, const char *what) {
 }
 
 // ============================================================================ enqueue
+// NEXT-3 refresh-in-place (reading R7), part 1 on every shard: block-label hash, scan of the
+// shard's labels -> rseq[j] = newest local write index of label y_j or -1
+static int refresh_resolve(f2c_dcp *h, Rank &R, const int64_t *y, int64_t m_glob, cudaStream_t st) {
+    const Layout &L = R.L;
+    k_blk_insert<<<static_cast<unsigned>((m_glob + 255) / 256), 256, 0, st>>>(y, m_glob, R.at<int64_t>(L.ekeys), L.He,
+                                                                             R.at<int>(L.ehslot), R.sc());
+    LAUNCH_CHECK();
+    const int64_t occ = occ_local(h, R);
+    if (occ > 0) {
+        int64_t blocks = (occ + 255) / 256;
+        if (blocks > h->G * 16) blocks = h->G * 16;
+        k_scan_pool<<<static_cast<unsigned>(blocks), 256, 0, st>>>(R.at<int64_t>(L.lab), occ, R.lo, h->C, h->E,
+                                                                   R.at<int64_t>(L.ekeys),
+                                                                   R.at<unsigned long long>(L.evals), L.He);
+        LAUNCH_CHECK();
+    }
+    k_resolve<<<static_cast<unsigned>((m_glob + 255) / 256), 256, 0, st>>>(
+        R.at<int>(L.ehslot), R.at<unsigned long long>(L.evals), m_glob, R.at<int64_t>(L.rseq));
+    LAUNCH_CHECK();
+    return F2C_OK;
+}
+
+// part 2 (after the global MAX of rseq): destinations, identical on every shard
+static int refresh_plan(f2c_dcp *h, Rank &R, int64_t m_glob, cudaStream_t st) {
+    const Layout &L = R.L;
+    k_refresh_plan<<<1, 1024, 0, st>>>(R.at<int64_t>(L.rseq), m_glob, h->E, h->C, R.at<int64_t>(L.dst_seq), R.sc(),
+                                       R.at<int64_t>(L.ekeys), R.at<unsigned long long>(L.evals), L.He);
+    LAUNCH_CHECK();
+    return F2C_OK;
+}
+
 static int enqueue_rank(f2c_dcp *h, Rank &R, const uint8_t *g, const int64_t *y, int64_t m_glob,
                         cudaStream_t st) {
     if (h->K > 1) {
@@ -443,7 +496,7 @@ static int enqueue_rank(f2c_dcp *h, Rank &R, const uint8_t *g, const int64_t *y,
         k_enqueue_k<<<static_cast<unsigned>(blocks), 256, 0, st>>>(
             reinterpret_cast<const __nv_bfloat16 *>(g), y, m_glob, h->K, h->d, h->E, h->C, R.lo, R.hi,
             R.at<__nv_bfloat16>(R.L.Traw), R.at<__nv_bfloat16>(R.L.T), R.at<float>(R.L.wslot),
-            R.at<int64_t>(R.L.lab), R.sc());
+            R.at<int64_t>(R.L.lab), R.sc(), h->refresh ? R.at<int64_t>(R.L.dst_seq) : nullptr);
         LAUNCH_CHECK();
         return F2C_OK;
     }
@@ -452,7 +505,7 @@ static int enqueue_rank(f2c_dcp *h, Rank &R, const uint8_t *g, const int64_t *y,
     if (blocks > static_cast<int64_t>(h->G) * 8) blocks = static_cast<int64_t>(h->G) * 8;
     k_enqueue<<<static_cast<unsigned>(blocks), 256, 0, st>>>(
         g, y, m_glob, h->E, h->C, R.lo, R.hi, row_bytes, h->dtype, R.base + R.L.T,
-        R.at<int64_t>(R.L.lab), R.sc());
+        R.at<int64_t>(R.L.lab), R.sc(), h->refresh ? R.at<int64_t>(R.L.dst_seq) : nullptr);
     LAUNCH_CHECK();
     return F2C_OK;
 }
@@ -472,15 +525,9 @@ extern "C" int f2c_dcp_enqueue(f2c_dcp *h, const void *g_feats, const int64_t *l
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     h->last_stream = st;
     const size_t es = h->dtype == F2C_BF16 ? 2 : 4;
-    if (!h->multi) {
-        if ((rc = enqueue_rank(h, h->ranks[0], static_cast<const uint8_t *>(g_feats), labels, m_glob, st)))
-            return rc;
-    } else if (h->emulated) {
-        // g_feats / labels already hold the rank-ordered global block
-        for (Rank &R : h->ranks)
-            if ((rc = enqueue_rank(h, R, static_cast<const uint8_t *>(g_feats), labels, m_glob, st)))
-                return rc;
-    } else {
+    const uint8_t *gx = static_cast<const uint8_t *>(g_feats);
+    const int64_t *gy = labels;
+    if (h->multi && !h->emulated) {
         // C5: route the block to the owners; every rank receives the whole block
         // (all-gather) and keeps the rows of its slot range.
         Rank &R = h->ranks[0];
@@ -489,9 +536,45 @@ extern "C" int f2c_dcp_enqueue(f2c_dcp *h, const void *g_feats, const int64_t *l
         api.AllGather(g_feats, R.base + R.L.blk_x, m_local * h->K * h->d * es, NCCL_INT8, h->comm, st);
         api.AllGather(labels, R.base + R.L.blk_y, m_local, NCCL_INT64, h->comm, st);
         if ((rc = nccl_check(api.GroupEnd(), "enqueue all-gather"))) return rc;
-        if ((rc = enqueue_rank(h, R, R.base + R.L.blk_x, R.at<int64_t>(R.L.blk_y), m_glob, st))) return rc;
+        gx = R.base + R.L.blk_x;
+        gy = R.at<int64_t>(R.L.blk_y);
     }
-    h->E += m_glob;
+    // (emulated world: g_feats / labels already hold the rank-ordered global block)
+    if (h->refresh) {
+        // NEXT-3 refresh-in-place: residency over all shards (MAX of the newest write index),
+        // then the same plan on every shard
+        for (Rank &R : h->ranks)
+            if ((rc = refresh_resolve(h, R, gy, m_glob, st))) return rc;
+        if (h->emulated) {
+            Rank &R0 = h->ranks[0];
+            for (size_t q = 1; q < h->ranks.size(); ++q) {
+                k_max_i64_into<<<static_cast<unsigned>((m_glob + 255) / 256), 256, 0, st>>>(
+                    R0.at<int64_t>(R0.L.rseq), h->ranks[q].at<int64_t>(h->ranks[q].L.rseq), m_glob);
+                LAUNCH_CHECK();
+            }
+            for (size_t q = 1; q < h->ranks.size(); ++q)
+                CUDA_TRY(cudaMemcpyAsync(h->ranks[q].at<int64_t>(h->ranks[q].L.rseq), R0.at<int64_t>(R0.L.rseq),
+                                         m_glob * 8, cudaMemcpyDeviceToDevice, st));
+        } else if (h->multi) {
+            Rank &R = h->ranks[0];
+            if ((rc = nccl_check(nccl().AllReduce(R.at<int64_t>(R.L.rseq), R.at<int64_t>(R.L.rseq), m_glob, NCCL_INT64,
+                                                  NCCL_MAX, h->comm, st), "refresh all-reduce")))
+                return rc;
+        }
+        for (Rank &R : h->ranks)
+            if ((rc = refresh_plan(h, R, m_glob, st))) return rc;
+    }
+    for (Rank &R : h->ranks)
+        if ((rc = enqueue_rank(h, R, gx, gy, m_glob, st))) return rc;
+    if (h->refresh) {
+        // the number of appended rows is data-dependent: the host's E waits for it
+        CUDA_TRY(cudaMemcpyAsync(h->n_app_host, &h->ranks[0].sc()->n_app, sizeof(long long), cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+        h->E += *h->n_app_host;
+    } else {
+        h->E += m_glob;
+    }
+    h->last_refresh = h->refresh != 0;
     h->M_last = m_glob;
     return F2C_OK;
 }
@@ -536,12 +619,6 @@ struct StepCtx {
     cudaStream_t st;
 };
 
-static int64_t occ_local(const f2c_dcp *h, const Rank &R) {
-    const int64_t C_occ = h->E < h->C ? h->E : h->C;
-    int64_t o = C_occ - R.lo;
-    if (o > R.hi - R.lo) o = R.hi - R.lo;
-    return o < 0 ? 0 : o;
-}
 
 // a2 + a3: norms, label hash, local target resolve (tseq = newest local seq or -1)
 static int phase_resolve(f2c_dcp *h, Rank &R, const StepCtx &c) {
@@ -594,6 +671,7 @@ static int phase_compact(f2c_dcp *h, Rank &R, const StepCtx &c, const int *tmax_
     a.sc = R.sc();
     a.tmax_bits = tmax_bits;
     a.neg_mode = h->neg_mode();
+    a.blk_seq = h->last_refresh ? R.at<int64_t>(L.dst_seq) : nullptr;
     a.excl = h->excl_dup;
     a.hslot = R.at<int>(L.hslot);
     a.row_hent = R.at<int>(L.row_hent);
@@ -890,6 +968,18 @@ extern "C" int f2c_dcp_set_lcos(f2c_dcp *h, int32_t phi_mode, int32_t hinge, dou
     return F2C_OK;
 }
 
+extern "C" int f2c_dcp_set_enqueue_mode(f2c_dcp *h, int32_t refresh_in_place) {
+    if (!h) return fail(F2C_EINVAL, "NULL handle");
+    if (refresh_in_place != 0 && refresh_in_place != 1) return fail(F2C_EINVAL, "refresh_in_place must be 0 or 1");
+    if (refresh_in_place && !h->n_app_host) {
+        void *p = nullptr;
+        CUDA_TRY(cudaMallocHost(&p, sizeof(long long)));
+        h->n_app_host = static_cast<long long *>(p);
+    }
+    h->refresh = refresh_in_place;
+    return F2C_OK;
+}
+
 extern "C" int f2c_dcp_set_dup_mode(f2c_dcp *h, int32_t exclude_stale) {
     if (!h) return fail(F2C_EINVAL, "NULL handle");
     if (exclude_stale != 0 && exclude_stale != 1) return fail(F2C_EINVAL, "exclude_stale must be 0 or 1");
@@ -908,8 +998,9 @@ static int latched(f2c_dcp *h, bool sync) {
         if (s.err) {
             static const char *det[] = {"", "negative label", "zero-norm (or non-finite) feature row",
                                         "pairing[i] does not name row i's target",
-                                        "non-finite loss", "softmax underflow (row max < 2^-100 of the reference)"};
-            const int dd = (s.err_detail >= 0 && s.err_detail <= 5) ? s.err_detail : 0;
+                                        "non-finite loss", "softmax underflow (row max < 2^-100 of the reference)",
+                                        "duplicate label within a refresh-in-place enqueue block (S:277)"};
+            const int dd = (s.err_detail >= 0 && s.err_detail <= 6) ? s.err_detail : 0;
             fail(s.err, "device error (rank %d): %s", R.rank, det[dd]);
             worst = s.err;
             int zero[2] = {0, 0};

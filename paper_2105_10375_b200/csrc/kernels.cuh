@@ -15,7 +15,7 @@ enum : int { ERR_OK = 0, ERR_PAIRING = 4, ERR_DEVICE = 7 };
 // detail codes kept next to the status (scal->err_detail) for f2c_last_error
 enum : int {
     DET_NONE = 0, DET_BAD_LABEL = 1, DET_ZERO_ROW = 2, DET_PAIRING = 3, DET_NONFINITE = 4,
-    DET_UNDERFLOW = 5
+    DET_UNDERFLOW = 5, DET_DUP_BLOCK = 6
 };
 
 struct Scalars {          // lives at the start of the per-rank scratch
@@ -28,6 +28,7 @@ struct Scalars {          // lives at the start of the per-rank scratch
                           // when the out-of-pool rows go through it: NEXT-3 hinge / max)
     double loss3[3];      // L, L_ce, L_cos (fp64) of the last loss call
     unsigned long long n_pos_sum;  // sum of n_pos over loss calls (bench accounting)
+    long long n_app;      // rows appended by the last refresh-in-place enqueue (NEXT-3)
 };
 
 __device__ __forceinline__ void latch(Scalars *s, int code, int detail) {
@@ -65,13 +66,15 @@ __device__ __forceinline__ float from_f<float>(float v) { return v; }
 __global__ void __launch_bounds__(256) k_enqueue(const uint8_t *__restrict__ g, const int64_t *__restrict__ y,
                                                  int64_t m_glob, int64_t E, int64_t C, int64_t lo, int64_t hi,
                                                  int row_bytes, int dtype, uint8_t *__restrict__ T,
-                                                 int64_t *__restrict__ lab, Scalars *sc) {
+                                                 int64_t *__restrict__ lab, Scalars *sc,
+                                                 const int64_t *__restrict__ dst_seq) {
     __shared__ float wmax[8];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
     float nmax = 0.f;
     for (int64_t j = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + wib; j < m_glob; j += nwarps) {
-        const int64_t c = (E + j) % C;
+        // pure Eq. 7: row j -> slot (E + j) mod C; refresh-in-place (NEXT-3): the planned slot
+        const int64_t c = (dst_seq ? dst_seq[j] : E + j) % C;
         if (c < lo || c >= hi) continue;
         const int64_t yl = y[j];
         if (yl < 0) {
@@ -134,13 +137,14 @@ __global__ void __launch_bounds__(256) k_enqueue_k(const __nv_bfloat16 *__restri
                                                    int64_t m_glob, int K, int d, int64_t E, int64_t C,
                                                    int64_t lo, int64_t hi, __nv_bfloat16 *__restrict__ Traw,
                                                    __nv_bfloat16 *__restrict__ Tbar, float *__restrict__ wslot,
-                                                   int64_t *__restrict__ lab, Scalars *sc) {
+                                                   int64_t *__restrict__ lab, Scalars *sc,
+                                                   const int64_t *__restrict__ dst_seq) {
     __shared__ float wmax[8];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
     float nmax = 0.f;
     for (int64_t j = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + wib; j < m_glob; j += nwarps) {
-        const int64_t c = (E + j) % C;
+        const int64_t c = (dst_seq ? dst_seq[j] : E + j) % C;
         if (c < lo || c >= hi) continue;
         const int64_t yl = y[j];
         if (yl < 0) {
@@ -359,6 +363,103 @@ __global__ void k_resolve(const int *__restrict__ hslot, const unsigned long lon
     tseq[i] = h < 0 ? -1 : static_cast<int64_t>(vals[h]) - 1;
 }
 
+// ------------------------------------------------------------------ NEXT-3: refresh-in-place enqueue
+// SPEC's insert_batch (reading R7): a block row whose label is resident
+// overwrites that slot's features in place (age kept); the other rows are appended at
+// E, E+1, ... in block order -- together with the resident rows whose slot those appends
+// would overwrite (the smallest fixed point n = n0 + #{sigma_j < E + n - C}).  The block's
+// labels go into their own hash (k_blk_insert), the shard's labels are scanned with
+// k_scan_pool / k_resolve (sigma_j = newest write index, -1 = not resident; W > 1: MAX
+// all-reduce), and one CTA plans the destinations (k_refresh_plan).
+__global__ void k_blk_insert(const int64_t *__restrict__ y, int64_t M, int64_t *keys, int H,
+                             int *__restrict__ hslot, Scalars *sc) {
+    const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (j >= M) return;
+    const int64_t key = y[j];
+    if (key < 0) {
+        latch(sc, ERR_DEVICE, DET_BAD_LABEL);
+        hslot[j] = -1;
+        return;
+    }
+    unsigned h = static_cast<unsigned>(hash64(static_cast<uint64_t>(key))) & (H - 1);
+    for (;;) {
+        const unsigned long long old = atomicCAS(reinterpret_cast<unsigned long long *>(keys + h),
+                                                 static_cast<unsigned long long>(-1ll),
+                                                 static_cast<unsigned long long>(key));
+        if (old == static_cast<unsigned long long>(-1ll)) break;
+        if (old == static_cast<unsigned long long>(key)) {  // ids pairwise distinct
+            latch(sc, ERR_DEVICE, DET_DUP_BLOCK);
+            break;
+        }
+        h = (h + 1) & (H - 1);
+    }
+    hslot[j] = static_cast<int>(h);
+}
+
+// single CTA: the fixed point n, then dst_seq[j] (write index of row j's slot) and
+// sc->n_app = n; clears the block hash for the next call
+__global__ void __launch_bounds__(1024) k_refresh_plan(const int64_t *__restrict__ sigma, int64_t M, int64_t E,
+                                                       int64_t C, int64_t *__restrict__ dst_seq, Scalars *sc,
+                                                       int64_t *keys, unsigned long long *vals, int H) {
+    __shared__ int wsum[32];
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, w = tid >> 5;
+    const int64_t per = (M + nt - 1) / nt;
+    const int64_t r0 = tid * per, r1 = r0 + per < M ? r0 + per : M;
+    auto block_sum = [&](int v) {  // all threads get the total
+#pragma unroll
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        __syncthreads();
+        if (lane == 0) wsum[w] = v;
+        __syncthreads();
+        int t = 0;
+        for (int i = 0; i < (nt >> 5); ++i) t += wsum[i];
+        return t;
+    };
+    int c0 = 0;
+    for (int64_t j = r0; j < r1; ++j) c0 += sigma[j] < 0;
+    const int n0 = block_sum(c0);
+    long long n = n0;
+    for (;;) {
+        int c = 0;
+        for (int64_t j = r0; j < r1; ++j) c += sigma[j] >= 0 && sigma[j] < E + n - C;
+        const long long f = n0 + block_sum(c);
+        if (f == n) break;
+        n = f;
+    }
+    // exclusive scan of the appended flags in block order
+    int cnt = 0;
+    for (int64_t j = r0; j < r1; ++j) cnt += sigma[j] < 0 || sigma[j] < E + n - C;
+    int v = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += t;
+    }
+    __syncthreads();
+    if (lane == 31) wsum[w] = v;
+    __syncthreads();
+    if (w == 0) {
+        int s2 = lane < (nt >> 5) ? wsum[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, s2, o);
+            if (lane >= o) s2 += t;
+        }
+        wsum[lane] = s2;
+    }
+    __syncthreads();
+    long long k = (w > 0 ? wsum[w - 1] : 0) + v - cnt;
+    for (int64_t j = r0; j < r1; ++j) {
+        const int64_t sg = sigma[j];
+        dst_seq[j] = (sg < 0 || sg < E + n - C) ? E + k++ : sg;
+    }
+    if (tid == 0) sc->n_app = n;
+    for (int h = tid; h < H; h += nt) {
+        keys[h] = -1;
+        vals[h] = 0ull;
+    }
+}
+
 // ------------------------------------------------------------------ NEXT-3: stale self-duplicates
 // Variant "exclude stale self-duplicates" (D8 keeps them): an in-pool
 // row's softmax skips the occupied slots that carry its own label but are not its target
@@ -467,6 +568,7 @@ struct CompactArgs {
     float ref_scale;          // s*log2(e)*(1+2^-10): reference exponent per unit norm
     // NEXT-3 "exclude stale self-duplicates": the row's label hash entry (-1 = none) and the
     // target write index per hash entry, read by the duplicate-list kernels below
+    const int64_t *blk_seq;   // [M_last] after a refresh-in-place enqueue, else null
     int excl;
     const int *hslot;         // [N]
     int *row_hent;            // [R_max]
@@ -506,8 +608,11 @@ __global__ void __launch_bounds__(1024) k_compact(CompactArgs a) {
     for (int64_t i = r0; i < r1; ++i) {
         const int64_t ts = a.tseq[i];
         if (a.pairing && a.pairing[i] >= 0) {
-            const int64_t want = a.E - a.M_last + a.pairing[i];
-            if (a.pairing[i] >= a.M_last || ts != want) latch(a.sc, ERR_PAIRING, DET_PAIRING);
+            const bool inb = a.pairing[i] < a.M_last;
+            // pure Eq. 7: block row j sits at write index E - M_last + j; after a
+            // refresh-in-place enqueue (NEXT-3) at the planned blk_seq[j]
+            const int64_t want = !inb ? -2 : (a.blk_seq ? a.blk_seq[a.pairing[i]] : a.E - a.M_last + a.pairing[i]);
+            if (!inb || ts != want) latch(a.sc, ERR_PAIRING, DET_PAIRING);
         }
         if (ts < 0 && a.neg_mode) {
             const int kn = n_pos + 1 + static_cast<int>(i - k);  // i - k = out-of-pool rows before i

@@ -57,7 +57,8 @@ def load_library():
     L.f2c_dcp_destroy.restype = None
     L.f2c_dcp_set_lcos.argtypes = [P, i32, i32, ctypes.c_double]
     L.f2c_dcp_set_dup_mode.argtypes = [P, i32]
-    for f in (L.f2c_dcp_create, L.f2c_dcp_create_k, L.f2c_dcp_set_lcos, L.f2c_dcp_set_dup_mode, L.f2c_dcp_enqueue, L.f2c_dcp_loss_fwd_bwd, L.f2c_gnet_ema,
+    L.f2c_dcp_set_enqueue_mode.argtypes = [P, i32]
+    for f in (L.f2c_dcp_create, L.f2c_dcp_create_k, L.f2c_dcp_set_lcos, L.f2c_dcp_set_dup_mode, L.f2c_dcp_set_enqueue_mode, L.f2c_dcp_enqueue, L.f2c_dcp_loss_fwd_bwd, L.f2c_gnet_ema,
               L.f2c_dcp_get_state, L.f2c_dcp_set_state, L.f2c_dcp_row_stats, L.f2c_dcp_check,
               L.f2c_last_launch_count, L.f2c_dcp_profile, L.f2c_dcp_profile_read):
         f.restype = ctypes.c_int
@@ -134,6 +135,11 @@ class DCPHead:
         """NEXT-3 L_cos variant for later loss calls: phi_mode PHI_MEAN / PHI_SUM / PHI_MAX,
         hinge max(0, cos), L = L_ce + lam * L_cos (include/f2c_dcp.h)."""
         _check(load_library().f2c_dcp_set_lcos(self._h, int(phi_mode), int(hinge), float(lam)))
+
+    def set_enqueue_mode(self, refresh_in_place: bool = False):
+        """NEXT-3: SPEC's refresh-in-place enqueue (resident ids overwritten in place, age kept;
+        reading R7) for later enqueues; False restores pure Eq. 7 (include/f2c_dcp.h)."""
+        _check(load_library().f2c_dcp_set_enqueue_mode(self._h, int(bool(refresh_in_place))))
 
     def set_dup_mode(self, exclude_stale: bool = False):
         """NEXT-3: drop each in-pool row's stale self-duplicates (older slots of its own label)
