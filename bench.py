@@ -399,25 +399,69 @@ def kernel_bench(args):
     print(json.dumps({"kernel_bench": out, "peak_hbm_GBps": pk["hbm_gbs"]}), flush=True)
 
 
+def c4_rank_config(frac, n_glob):
+    """One rank of the W=8 c4 point (C = frac * 10M, global batch n_glob) as a 1-GPU workload."""
+    base = synth.c4_point(frac, n_glob, world=8)
+    return synth.scaled(base, name=f"c4r_{int(round(frac * 100))}_{n_glob}", C=base.C // 8,
+                        M_loc=n_glob // 2, n_id=base.n_id // 8)
+
+
+def _workload(name):
+    if name.startswith("c4r_"):  # c4r_<pct>_<global batch>: one rank of a W=8 c4 point
+        _, pct, n = name.split("_")
+        return c4_rank_config(int(pct) / 100, int(n))
+    return synth.CONFIGS[name]
+
+
+def sweep_c4(args):
+    """BJ:11's pool-ratio x batch sweep, per-rank view on ONE GPU: for each point (C = 1/2/5/10 %
+    of 10M ids, global batch N in {2048, 8192, 16384}) run the compute ONE rank of the W=8 job
+    does -- all N global rows against its C/8-slot shard, plus the enqueue of the N/2-row global
+    block and the 65M-parameter EMA -- device-resident (n_ID / 8 keeps the instance rows' in-pool
+    rate C / n_ID of the sharded job).  Collectives (C1-C5) are excluded, so
+    N / t_step is an upper bound of the W=8 job's samples/s; the driver's 8-GPU run measures the
+    real thing.  Prints one JSON line (evidence for profiles/, not the bench contract line)."""
+    import torch
+    pts = []
+    for frac in (0.01, 0.02, 0.05, 0.10):
+        for n_glob in (2048, 8192, 16384):
+            base = synth.c4_point(frac, n_glob, world=8)
+            cfg = c4_rank_config(frac, n_glob)
+            r = run_ours(args, cfg, 1, 0, 0, device_only=True)
+            pts.append({"C_global": base.C, "C_per_rank": cfg.C, "global_batch": n_glob,
+                        "ms_per_step": r["ms_per_step"], "upper_bound_w8_samples_per_s": r["value"],
+                        "fused_kernel_ms": r["roofline"]["avg_launch_ms"],
+                        "fused_kernel_frac": r["roofline"]["frac"], "N_pos_avg": r["roofline"]["N_pos_avg"],
+                        "clocks": r["clocks"]})
+            torch.cuda.empty_cache()
+    print(json.dumps({"sweep": "c4 (BJ:11), one rank of W=8 on one B200, collectives excluded",
+                      "steps": args.steps, "warmup": args.warmup, "points": pts}), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c3", choices=["c1", "c2", "c3"])
+    ap.add_argument("--workload", default="c3",
+                    help="c1 | c2 | c3 | c4r_<pct>_<global batch> (one rank of a W=8 c4 point)")
     ap.add_argument("--ring", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--kernel-bench", action="store_true", help="HBM-bound kernels alone (enqueue, EMA)")
+    ap.add_argument("--sweep-c4", action="store_true", help="BJ:11 sweep, one rank of W=8 per point (evidence)")
     ap.add_argument("--also", default="c2", help="extra single-GPU workloads measured device-resident "
                     "(the north-star 1M-slot config c2 by default); 'none' to skip")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    cfg = synth.CONFIGS[args.workload]
+    cfg = _workload(args.workload)
     if args.kernel_bench:
         kernel_bench(args)
+        return
+    if args.sweep_c4:
+        sweep_c4(args)
         return
     if args.impl == "reference":
         if rank == 0:
@@ -434,7 +478,7 @@ def main():
     if extras:
         import torch
         torch.cuda.empty_cache()
-        line["also"] = [run_ours(args, synth.CONFIGS[w], world, rank, local_rank, device_only=True)
+        line["also"] = [run_ours(args, _workload(w), world, rank, local_rank, device_only=True)
                         for w in extras]
     if rank == 0 and line is not None:
         print(json.dumps(line), flush=True)

@@ -253,6 +253,10 @@ __device__ __forceinline__ void tmem_wait_st() {
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
 
+// EXCL: the NEXT-3 "exclude stale self-duplicates" variant, a separate instantiation so the
+// default softmax loop is compiled exactly as without it (measured: a runtime flag there cost
+// 10 % at c3)
+template <bool EXCL>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
     dcp_pc_kernel(const __grid_constant__ CUtensorMap tm3p, const __grid_constant__ CUtensorMap tm3q,
                   const PCParams p) {
@@ -438,7 +442,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                 const int row = rg * PC_R + r;
                 const float2 ab = p.row_ab[row];
                 const int tg = p.row_tgt[row];
-                const int hent = p.excl ? p.row_hent[row] : -1;
+                const int hent = EXCL ? p.row_hent[row] : -1;
                 // x_hat (this thread's row, d half h) -> TMEM A operand columns
                 mbar_wait(&aux->xfree, (sg & 1) ^ 1);
                 tc_fence_after();
@@ -525,7 +529,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                                     }
                             }
                         }
-                        if (p.excl) {  // NEXT-3: drop this row's stale self-duplicates of tile t
+                        if constexpr (EXCL) {  // NEXT-3: drop this row's stale self-duplicates of tile t
                             const int o1 = p.dup_off[t + 1];
                             for (int o = p.dup_off[t]; o < o1; ++o) {
                                 const int2 v = p.dup_list[o];

@@ -410,7 +410,9 @@ int f2c_dcp_create_k(int64_t C, int32_t K, int32_t d, int32_t dtype, int32_t wor
     }
     if (cudaFuncSetAttribute(dcp_tp64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              TP_SMEM_BYTES) != cudaSuccess ||
-        cudaFuncSetAttribute(dcp_pc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(dcp_pc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             PC_SMEM_BYTES) != cudaSuccess ||
+        cudaFuncSetAttribute(dcp_pc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              PC_SMEM_BYTES) != cudaSuccess) {
         delete h;
         return fail(F2C_ECUDA, "cudaFuncSetAttribute(smem) failed");
@@ -696,7 +698,7 @@ static int phase_compact(f2c_dcp *h, Rank &R, const StepCtx &c, const int *tmax_
         LAUNCH_CHECK();
     }
     const int row_bytes = h->d * 2;
-    k_gather<<<static_cast<unsigned>(c.N + 1), 64, 0, c.st>>>(c.x, R.at<int>(L.pos_row), R.sc(), row_bytes,
+    k_gather<<<static_cast<unsigned>((c.N + 1 + 7) / 8), 256, 0, c.st>>>(c.x, R.at<int>(L.pos_row), R.sc(), row_bytes,
                                                           R.base + L.X_pos, R.base + L.T, R.at<int>(L.row_tgt),
                                                           R.at<float2>(L.row_ab));
     LAUNCH_CHECK();
@@ -754,7 +756,10 @@ static int phase_main(f2c_dcp *h, Rank &R, const StepCtx &c, int64_t occ_loc) {
         q.row_hent = R.at<int>(L.row_hent);
         q.dbg = p.dbg;
         q.dbg_flags = h->dbg_flags;
-        dcp_pc_kernel<<<(h->G / 2) * 2, PC_THREADS, PC_SMEM_BYTES, c.st>>>(R.tm3p, R.tm3q, q);
+        if (q.excl)
+            dcp_pc_kernel<true><<<(h->G / 2) * 2, PC_THREADS, PC_SMEM_BYTES, c.st>>>(R.tm3p, R.tm3q, q);
+        else
+            dcp_pc_kernel<false><<<(h->G / 2) * 2, PC_THREADS, PC_SMEM_BYTES, c.st>>>(R.tm3p, R.tm3q, q);
     }
     LAUNCH_CHECK();
     if (e1) CUDA_TRY(cudaEventRecord(e1, c.st));
@@ -800,6 +805,9 @@ static CombineArgs combine_args(f2c_dcp *h, Rank &R, const StepCtx &c, int64_t o
     a.my_rank = R.rank < 0 ? 0 : R.rank;
     a.seg_arg = R.at<int>(L.seg_arg);
     a.wslot = h->K > 1 ? R.at<float>(L.wslot) : nullptr;
+    a.hkeys = R.at<int64_t>(L.hkeys);
+    a.hvals = R.at<unsigned long long>(L.hvals);
+    a.H = L.H;
     return a;
 }
 
@@ -893,7 +901,6 @@ static int loss_multi(f2c_dcp *h, const uint8_t *x, const int64_t *labels, const
                                                                    R.at<float>(R.L.dx_part));
         LAUNCH_CHECK();
         k_loss<<<1, 1024, 0, st>>>(R.at<double>(R.L.rowloss), R.at<int>(R.L.comp_idx), N, R.sc(), loss,
-                                   R.at<int64_t>(R.L.hkeys), R.at<unsigned long long>(R.L.hvals), R.L.H,
                                    static_cast<double>(h->lam));
         LAUNCH_CHECK();
     }
@@ -951,7 +958,6 @@ extern "C" int f2c_dcp_loss_fwd_bwd(f2c_dcp *h, const void *x, const int64_t *la
     k_combine<__nv_bfloat16><<<static_cast<unsigned>(c.N), 128, 0, st>>>(a);
     LAUNCH_CHECK();
     k_loss<<<1, 1024, 0, st>>>(R.at<double>(L.rowloss), R.at<int>(L.comp_idx), c.N, R.sc(), loss,
-                               R.at<int64_t>(L.hkeys), R.at<unsigned long long>(L.hvals), L.H,
                                static_cast<double>(h->lam));
     LAUNCH_CHECK();
     return F2C_OK;

@@ -297,9 +297,23 @@ __global__ void k_rownorm_insert(const T *__restrict__ x, const int64_t *__restr
     const int lane = threadIdx.x & 31;
     if (i >= N) return;
     float ss = 0.f;
-    for (int k = lane; k < d; k += 32) {
-        float v = to_f<T>(x[i * d + k]);
-        ss += v * v;
+    {  // 16-byte vector loads (d is a multiple of 128, rows 16-byte aligned)
+        const uint4 *row = reinterpret_cast<const uint4 *>(x + i * d);
+        const int nvec = d * static_cast<int>(sizeof(T)) / 16;
+        for (int u = lane; u < nvec; u += 32) {
+            const uint4 v = row[u];
+            const uint32_t q[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                if (sizeof(T) == 2) {
+                    const float lo = __uint_as_float(q[e] << 16), hi = __uint_as_float(q[e] & 0xffff0000u);
+                    ss += lo * lo + hi * hi;
+                } else {
+                    const float f = __uint_as_float(q[e]);
+                    ss += f * f;
+                }
+            }
+        }
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
@@ -576,37 +590,45 @@ struct CompactArgs {
 };
 __global__ void __launch_bounds__(1024) k_compact(CompactArgs a) {
     __shared__ int wsum[32];
+    __shared__ int s_tot;
     const int tid = threadIdx.x, nt = blockDim.x;
-    const int64_t per = (a.N + nt - 1) / nt;
-    const int64_t r0 = tid * per, r1 = r0 + per < a.N ? r0 + per : a.N;
-    int cnt = 0;
-    for (int64_t i = r0; i < r1; ++i) cnt += a.tseq[i] >= 0;
-    // block exclusive scan of cnt
     const int lane = tid & 31, w = tid >> 5;
-    int v = cnt;
+    // n_pos: coalesced count of the in-pool rows
+    int cnt = 0;
+    for (int64_t i = tid; i < a.N; i += nt) cnt += a.tseq[i] >= 0;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        int t = __shfl_up_sync(0xffffffffu, v, o);
-        if (lane >= o) v += t;
-    }
-    if (lane == 31) wsum[w] = v;
+    for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if (lane == 0) wsum[w] = cnt;
     __syncthreads();
-    if (w == 0) {
-        int s2 = wsum[lane];
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            int t = __shfl_up_sync(0xffffffffu, s2, o);
-            if (lane >= o) s2 += t;
-        }
-        wsum[lane] = s2;  // inclusive
+    if (tid == 0) {
+        int t = 0;
+        for (int q = 0; q < (nt >> 5); ++q) t += wsum[q];
+        s_tot = t;
     }
     __syncthreads();
-    int k = (w > 0 ? wsum[w - 1] : 0) + v - cnt;
-    const int n_pos = wsum[31];
+    const int n_pos = s_tot;
     const float tmax = __int_as_float(*a.tmax_bits);
     const float B = a.ref_scale * tmax;
-    for (int64_t i = r0; i < r1; ++i) {
-        const int64_t ts = a.tseq[i];
+    // rows in chunks of nt (one per thread, coalesced); k = in-pool rows before row i, from a
+    // ballot scan of the chunk plus the running base
+    int base = 0;
+    for (int64_t c0 = 0; c0 < a.N; c0 += nt) {
+        const int64_t i = c0 + tid;
+        const int64_t ts = i < a.N ? a.tseq[i] : -1;
+        const bool f = i < a.N && ts >= 0;
+        const unsigned bal = __ballot_sync(0xffffffffu, f);
+        __syncthreads();  // (wsum reuse)
+        if (lane == 0) wsum[w] = __popc(bal);
+        __syncthreads();
+        int wpre = 0, tot = 0;
+        for (int q = 0; q < (nt >> 5); ++q) {
+            const int v = wsum[q];
+            wpre += q < w ? v : 0;
+            tot += v;
+        }
+        const int k = base + wpre + __popc(bal & ((1u << lane) - 1u));
+        base += tot;
+        if (i >= a.N) continue;
         if (a.pairing && a.pairing[i] >= 0) {
             const bool inb = a.pairing[i] < a.M_last;
             // pure Eq. 7: block row j sits at write index E - M_last + j; after a
@@ -633,7 +655,6 @@ __global__ void __launch_bounds__(1024) k_compact(CompactArgs a) {
             const int64_t slot = ts % a.C;
             a.row_tgt[k] = (slot >= a.lo && slot < a.hi) ? static_cast<int>(slot - a.lo) : -1;
             a.ttgt[k] = -INFINITY;
-            ++k;
         } else {
             a.comp_idx[i] = -1;
         }
@@ -665,19 +686,19 @@ __global__ void __launch_bounds__(1024) k_compact(CompactArgs a) {
 // is the unmargined target logit (computed by the shard that owns the target slot; other
 // shards keep bound - 100).  Every exponent is then <= 100 (no overflow of p or O), and
 // the dominant terms stay representable for any |cos| <= 1 at s <= 76.
-__global__ void __launch_bounds__(64) k_gather(const uint8_t *__restrict__ x, const int *__restrict__ pos_row,
-                                               const Scalars *__restrict__ sc, int row_bytes,
-                                               uint8_t *__restrict__ Xp, const uint8_t *__restrict__ T,
-                                               const int *__restrict__ row_tgt, float2 *__restrict__ row_ab) {
-    __shared__ float red[2];
-    const int k = blockIdx.x;
+__global__ void __launch_bounds__(256) k_gather(const uint8_t *__restrict__ x, const int *__restrict__ pos_row,
+                                                const Scalars *__restrict__ sc, int row_bytes,
+                                                uint8_t *__restrict__ Xp, const uint8_t *__restrict__ T,
+                                                const int *__restrict__ row_tgt, float2 *__restrict__ row_ab) {
+    // one warp per compacted row, 8 rows per CTA
+    const int k = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
     if (k >= sc->n_rows || k == sc->n_pos) return;  // (row n_pos is the mu row)
     const int4 *src = reinterpret_cast<const int4 *>(x + static_cast<int64_t>(pos_row[k]) * row_bytes);
     int4 *dst = reinterpret_cast<int4 *>(Xp + static_cast<int64_t>(k) * row_bytes);
     const int ts = row_tgt[k];  // local target slot, -1 (not on this shard), -2 (out-of-pool row)
     const int4 *tr = reinterpret_cast<const int4 *>(T + static_cast<int64_t>(ts < 0 ? 0 : ts) * row_bytes);
     float dot = 0.f;
-    for (int u = threadIdx.x; u < row_bytes / 16; u += blockDim.x) {
+    for (int u = lane; u < row_bytes / 16; u += 32) {
         const int4 v = src[u];
         dst[u] = v;
         if (ts >= 0) {
@@ -694,12 +715,10 @@ __global__ void __launch_bounds__(64) k_gather(const uint8_t *__restrict__ x, co
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = dot;
-    __syncthreads();
-    if (threadIdx.x == 0 && ts != -2) {  // (-2: out-of-pool row of NEXT-3, (a, b) final)
+    if (lane == 0 && ts != -2) {  // (-2: out-of-pool row of NEXT-3, (a, b) final)
         float2 ab = row_ab[k];
         const float floor_b = ab.y - 100.f;  // ab.y holds the global bound on entry
-        const float zt = ab.x * (red[0] + red[1]);
+        const float zt = ab.x * dot;
         ab.y = ts >= 0 ? fmaxf(zt, floor_b) : floor_b;
         row_ab[k] = ab;
     }
@@ -734,7 +753,21 @@ struct CombineArgs {
     float lam;
     const int *seg_arg;         // [S][128] local argmax slot of a segment (neg_mode 2)
     const float *wslot;         // [C_loc] 1/||T_bar_c|| (K >= 2) or null
+    // the batch-label hash, cleared for the next loss call by the final per-row kernel
+    // (k_combine / k_finalize_multi: block i clears its slice)
+    int64_t *hkeys;
+    unsigned long long *hvals;
+    int H;
 };
+
+__device__ __forceinline__ void clear_hash_slice(const CombineArgs &a, int64_t nblk) {
+    const int64_t per = (a.H + nblk - 1) / nblk;
+    const int64_t h0 = static_cast<int64_t>(blockIdx.x) * per;
+    for (int64_t h = h0 + threadIdx.x; h < h0 + per && h < a.H; h += blockDim.x) {
+        a.hkeys[h] = -1;
+        a.hvals[h] = 0ull;
+    }
+}
 
 __device__ __forceinline__ float block_sum_128(float v, float *red) {
 #pragma unroll
@@ -758,18 +791,39 @@ __device__ __forceinline__ void gather_row_partials(const CombineArgs &a, int n_
     for (int j = 0; j < 4; ++j) o[j] = 0.f;
     if (a.n_tiles <= 0) return;
     const int S = tp_choose_S(n_rg, a.G, a.n_tiles);
-    for (int s = 0; s < S; ++s) {
-        const long long t0 = static_cast<long long>(s) * a.n_tiles / S;
-        const long long t1 = static_cast<long long>(s + 1) * a.n_tiles / S;
-        if (t1 <= t0) continue;
-        const long long seg = static_cast<long long>(s) * n_rg + rg;
-        lsum += a.seg_l[seg * RG + r];
-        mx = fmaxf(mx, a.seg_mx[seg * RG + r]);
-        const float *src = a.seg_O + (seg * RG + r) * a.d;
+    // segments in batches of B: all loads of a batch are issued before the (fixed-order)
+    // accumulation, so the L2 latency is paid once per batch, not once per segment
+    constexpr int B = 8;
+    for (int s0 = 0; s0 < S; s0 += B) {
+        float lv[B], mv[B], ov[B][4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int dd = threadIdx.x + 128 * j;
-            if (dd < a.d) o[j] += src[dd];
+        for (int u = 0; u < B; ++u) {
+            const int s = s0 + u;
+            lv[u] = 0.f;
+            mv[u] = -INFINITY;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) ov[u][j] = 0.f;
+            if (s >= S) continue;
+            const long long t0 = static_cast<long long>(s) * a.n_tiles / S;
+            const long long t1 = static_cast<long long>(s + 1) * a.n_tiles / S;
+            if (t1 <= t0) continue;
+            const long long seg = static_cast<long long>(s) * n_rg + rg;
+            lv[u] = a.seg_l[seg * RG + r];
+            mv[u] = a.seg_mx[seg * RG + r];
+            const float *src = a.seg_O + (seg * RG + r) * a.d;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int dd = threadIdx.x + 128 * j;
+                if (dd < a.d) ov[u][j] = src[dd];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < B; ++u) {
+            if (s0 + u >= S) break;
+            lsum += lv[u];
+            mx = fmaxf(mx, mv[u]);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) o[j] += ov[u][j];
         }
     }
 }
@@ -828,6 +882,7 @@ template <typename TX>
 __global__ void __launch_bounds__(128) k_combine(CombineArgs a) {
     __shared__ float red[4];
     const int64_t i = blockIdx.x;
+    clear_hash_slice(a, gridDim.x);
     const int n_pos = a.sc->n_pos, n_neg = a.sc->n_neg;
     const int n_rg = (a.sc->n_rows + a.rows_per_group - 1) / a.rows_per_group;
     const int k = a.comp_idx[i];
@@ -965,6 +1020,7 @@ __global__ void __launch_bounds__(128) k_finalize_multi(CombineArgs a, const flo
                                                         int W, int64_t N, float *__restrict__ dx_part) {
     __shared__ float red[4];
     const int64_t i = blockIdx.x;
+    clear_hash_slice(a, gridDim.x);
     const int n_pos = a.sc->n_pos, n_neg = a.sc->n_neg;
     const int n_rg = (a.sc->n_rows + a.rows_per_group - 1) / a.rows_per_group;
     const int k = a.comp_idx[i];
@@ -1104,8 +1160,7 @@ __global__ void k_unpack_tseq(const int64_t *__restrict__ ext, int64_t N, int64_
 // also clears the label hash table for the next call.
 __global__ void __launch_bounds__(1024) k_loss(const double *__restrict__ rowloss,
                                                const int *__restrict__ comp_idx, int64_t N,
-                                               Scalars *sc, float *loss, int64_t *keys,
-                                               unsigned long long *vals, int H, double lam) {
+                                               Scalars *sc, float *loss, double lam) {
     __shared__ double sa[1024], sb[1024];
     const int tid = threadIdx.x;
     double ce = 0.0, cs = 0.0;
@@ -1133,10 +1188,6 @@ __global__ void __launch_bounds__(1024) k_loss(const double *__restrict__ rowlos
         sc->loss3[2] = Lcos;
         *loss = static_cast<float>(L);
         if (!isfinite(L)) latch(sc, ERR_DEVICE, DET_NONFINITE);
-    }
-    for (int h = tid; h < H; h += 1024) {
-        keys[h] = -1;
-        vals[h] = 0ull;
     }
 }
 

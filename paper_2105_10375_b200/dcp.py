@@ -10,7 +10,8 @@ import torch
 BF16, F32 = 0, 1
 PHI_MEAN, PHI_SUM, PHI_MAX = 0, 1, 2
 _HERE = os.path.dirname(os.path.abspath(__file__))
-lib_path = os.path.join(_HERE, "libf2c_dcp.so")
+# F2C_LIB overrides the library path (A/B timing experiments only; the default is in-tree)
+lib_path = os.environ.get("F2C_LIB") or os.path.join(_HERE, "libf2c_dcp.so")
 
 STATUS = {0: "F2C_OK", 1: "F2C_EINVAL", 2: "F2C_ESHAPE", 3: "F2C_ECAPACITY", 4: "F2C_EPAIRING",
           5: "F2C_ECUDA", 6: "F2C_ENCCL", 7: "F2C_EDEVICE"}
@@ -58,7 +59,8 @@ def load_library():
     L.f2c_dcp_set_lcos.argtypes = [P, i32, i32, ctypes.c_double]
     L.f2c_dcp_set_dup_mode.argtypes = [P, i32]
     L.f2c_dcp_set_enqueue_mode.argtypes = [P, i32]
-    for f in (L.f2c_dcp_create, L.f2c_dcp_create_k, L.f2c_dcp_set_lcos, L.f2c_dcp_set_dup_mode, L.f2c_dcp_set_enqueue_mode, L.f2c_dcp_enqueue, L.f2c_dcp_loss_fwd_bwd, L.f2c_gnet_ema,
+    for f in (L.f2c_dcp_create, L.f2c_dcp_create_k, L.f2c_dcp_set_lcos, L.f2c_dcp_set_dup_mode,
+              L.f2c_dcp_set_enqueue_mode, L.f2c_dcp_enqueue, L.f2c_dcp_loss_fwd_bwd, L.f2c_gnet_ema,
               L.f2c_dcp_get_state, L.f2c_dcp_set_state, L.f2c_dcp_row_stats, L.f2c_dcp_check,
               L.f2c_last_launch_count, L.f2c_dcp_profile, L.f2c_dcp_profile_read):
         f.restype = ctypes.c_int

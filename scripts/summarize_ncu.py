@@ -41,6 +41,8 @@ with open(os.path.join(out, f"{tag}_launches_{w}.csv"), "w") as f:
 print(open(os.path.join(out, f"{tag}_launches_{w}.csv")).read())
 
 # ---- full capture of the fused kernel
+if "--launches-only" in sys.argv:
+    sys.exit(0)
 rep = os.path.join(ROOT, "gpurun_out", f"prof_{w}.ncu-rep")
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rr = list(csv.reader(io.StringIO(raw)))
