@@ -678,7 +678,7 @@ static int phase_compact(f2c_dcp *h, Rank &R, const StepCtx &c, const int *tmax_
     a.hslot = R.at<int>(L.hslot);
     a.row_hent = R.at<int>(L.row_hent);
     a.hgseq = R.at<int64_t>(L.hgseq);
-    k_compact<<<1, 1024, 0, c.st>>>(a);
+    k_compact<<<static_cast<unsigned>((c.N + 1023) / 1024), 1024, 0, c.st>>>(a);
     LAUNCH_CHECK();
     const int64_t occ = occ_local(h, R);
     if (h->excl_dup && occ > 0) {  // NEXT-3: per-tile lists of the shard's stale self-duplicates
@@ -698,7 +698,7 @@ static int phase_compact(f2c_dcp *h, Rank &R, const StepCtx &c, const int *tmax_
         LAUNCH_CHECK();
     }
     const int row_bytes = h->d * 2;
-    k_gather<<<static_cast<unsigned>((c.N + 1 + 7) / 8), 256, 0, c.st>>>(c.x, R.at<int>(L.pos_row), R.sc(), row_bytes,
+    k_gather<<<static_cast<unsigned>(L.R_max / 8), 256, 0, c.st>>>(c.x, R.at<int>(L.pos_row), R.sc(), row_bytes,
                                                           R.base + L.X_pos, R.base + L.T, R.at<int>(L.row_tgt),
                                                           R.at<float2>(L.row_ab));
     LAUNCH_CHECK();
@@ -877,7 +877,7 @@ static int loss_multi(f2c_dcp *h, const uint8_t *x, const int64_t *labels, const
         const int64_t occ = occ_local(h, R);
         if ((rc = phase_main(h, R, ctx[q], occ))) return rc;
         CombineArgs a = combine_args(h, R, ctx[q], occ, nullptr);
-        k_local_rows<<<static_cast<unsigned>(N), 128, 0, st>>>(a, R.at<float4>(R.L.rs_buf));
+        k_local_rows<<<static_cast<unsigned>((N + CB_ROWS - 1) / CB_ROWS), 256, 0, st>>>(a, R.at<float4>(R.L.rs_buf));
         LAUNCH_CHECK();
     }
     // ---- C3: all-gather of the per-row partials
@@ -897,7 +897,7 @@ static int loss_multi(f2c_dcp *h, const uint8_t *x, const int64_t *labels, const
     for (size_t q = 0; q < h->ranks.size(); ++q) {
         Rank &R = h->ranks[q];
         CombineArgs a = combine_args(h, R, ctx[q], occ_local(h, R), nullptr);
-        k_finalize_multi<<<static_cast<unsigned>(N), 128, 0, st>>>(a, R.at<float4>(R.L.rs_all), W, N,
+        k_finalize_multi<<<static_cast<unsigned>((N + CB_ROWS - 1) / CB_ROWS), 256, 0, st>>>(a, R.at<float4>(R.L.rs_all), W, N,
                                                                    R.at<float>(R.L.dx_part));
         LAUNCH_CHECK();
         k_loss<<<1, 1024, 0, st>>>(R.at<double>(R.L.rowloss), R.at<int>(R.L.comp_idx), N, R.sc(), loss,
@@ -955,7 +955,7 @@ extern "C" int f2c_dcp_loss_fwd_bwd(f2c_dcp *h, const void *x, const int64_t *la
     const int64_t occ = occ_local(h, R);
     if ((rc = phase_main(h, R, c, occ))) return rc;
     CombineArgs a = combine_args(h, R, c, occ, static_cast<uint8_t *>(dx));
-    k_combine<__nv_bfloat16><<<static_cast<unsigned>(c.N), 128, 0, st>>>(a);
+    k_combine<<<static_cast<unsigned>((c.N + CB_ROWS - 1) / CB_ROWS), 256, 0, st>>>(a);
     LAUNCH_CHECK();
     k_loss<<<1, 1024, 0, st>>>(R.at<double>(L.rowloss), R.at<int>(L.comp_idx), c.N, R.sc(), loss,
                                static_cast<double>(h->lam));

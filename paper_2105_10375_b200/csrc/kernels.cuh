@@ -589,30 +589,45 @@ struct CompactArgs {
     int64_t *hgseq;           // [H]
 };
 __global__ void __launch_bounds__(1024) k_compact(CompactArgs a) {
-    __shared__ int wsum[32];
-    __shared__ int s_tot;
+    // CTA b compacts rows [b*1024, (b+1)*1024).  Every CTA counts the in-pool rows of the
+    // whole batch (n_pos) and of the rows before its chunk (its base) in one coalesced pass
+    // (N int64 from L2), so the chunks are independent.
+    __shared__ int wsum[32], wpre_s[32];
+    __shared__ int s_tot, s_before;
     const int tid = threadIdx.x, nt = blockDim.x;
     const int lane = tid & 31, w = tid >> 5;
-    // n_pos: coalesced count of the in-pool rows
-    int cnt = 0;
-    for (int64_t i = tid; i < a.N; i += nt) cnt += a.tseq[i] >= 0;
+    const int64_t c0 = static_cast<int64_t>(blockIdx.x) * nt;
+    int cnt = 0, before = 0;
+    for (int64_t i = tid; i < a.N; i += nt) {
+        const int f = a.tseq[i] >= 0;
+        cnt += f;
+        before += (i < c0) ? f : 0;
+    }
 #pragma unroll
-    for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-    if (lane == 0) wsum[w] = cnt;
+    for (int o = 16; o; o >>= 1) {
+        cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+        before += __shfl_xor_sync(0xffffffffu, before, o);
+    }
+    if (lane == 0) {
+        wsum[w] = cnt;
+        wpre_s[w] = before;
+    }
     __syncthreads();
     if (tid == 0) {
-        int t = 0;
-        for (int q = 0; q < (nt >> 5); ++q) t += wsum[q];
+        int t = 0, b = 0;
+        for (int q = 0; q < (nt >> 5); ++q) {
+            t += wsum[q];
+            b += wpre_s[q];
+        }
         s_tot = t;
+        s_before = b;
     }
     __syncthreads();
     const int n_pos = s_tot;
     const float tmax = __int_as_float(*a.tmax_bits);
     const float B = a.ref_scale * tmax;
-    // rows in chunks of nt (one per thread, coalesced); k = in-pool rows before row i, from a
-    // ballot scan of the chunk plus the running base
-    int base = 0;
-    for (int64_t c0 = 0; c0 < a.N; c0 += nt) {
+    // this CTA's chunk, one row per thread; k = in-pool rows before row i (ballot scan)
+    {
         const int64_t i = c0 + tid;
         const int64_t ts = i < a.N ? a.tseq[i] : -1;
         const bool f = i < a.N && ts >= 0;
@@ -620,51 +635,49 @@ __global__ void __launch_bounds__(1024) k_compact(CompactArgs a) {
         __syncthreads();  // (wsum reuse)
         if (lane == 0) wsum[w] = __popc(bal);
         __syncthreads();
-        int wpre = 0, tot = 0;
-        for (int q = 0; q < (nt >> 5); ++q) {
-            const int v = wsum[q];
-            wpre += q < w ? v : 0;
-            tot += v;
-        }
-        const int k = base + wpre + __popc(bal & ((1u << lane) - 1u));
-        base += tot;
-        if (i >= a.N) continue;
-        if (a.pairing && a.pairing[i] >= 0) {
-            const bool inb = a.pairing[i] < a.M_last;
-            // pure Eq. 7: block row j sits at write index E - M_last + j; after a
-            // refresh-in-place enqueue (NEXT-3) at the planned blk_seq[j]
-            const int64_t want = !inb ? -2 : (a.blk_seq ? a.blk_seq[a.pairing[i]] : a.E - a.M_last + a.pairing[i]);
-            if (!inb || ts != want) latch(a.sc, ERR_PAIRING, DET_PAIRING);
-        }
-        if (ts < 0 && a.neg_mode) {
-            const int kn = n_pos + 1 + static_cast<int>(i - k);  // i - k = out-of-pool rows before i
-            a.comp_idx[i] = -2 - kn;
-            a.pos_row[kn] = static_cast<int>(i);
-            a.row_ab[kn] = make_float2(a.inv_n[i], 0.f);  // e = <x, T> / ||x|| = cosine
-            a.row_tgt[kn] = -2;
-            a.ttgt[kn] = -INFINITY;
-        } else if (ts >= 0) {
-            a.comp_idx[i] = k;
-            a.pos_row[k] = static_cast<int>(i);
-            if (a.excl) {
-                const int he = a.hslot[i];
-                a.row_hent[k] = he;
-                if (he >= 0) a.hgseq[he] = ts;  // rows sharing a label share the target
+        int wpre = 0;
+        for (int q = 0; q < w; ++q) wpre += wsum[q];
+        const int k = s_before + wpre + __popc(bal & ((1u << lane) - 1u));
+        if (i < a.N) {
+            if (a.pairing && a.pairing[i] >= 0) {
+                const bool inb = a.pairing[i] < a.M_last;
+                // pure Eq. 7: block row j sits at write index E - M_last + j; after a
+                // refresh-in-place enqueue (NEXT-3) at the planned blk_seq[j]
+                const int64_t want = !inb ? -2 : (a.blk_seq ? a.blk_seq[a.pairing[i]] : a.E - a.M_last + a.pairing[i]);
+                if (!inb || ts != want) latch(a.sc, ERR_PAIRING, DET_PAIRING);
             }
-            a.row_ab[k] = make_float2(a.log2e_s * a.inv_n[i], B);
-            const int64_t slot = ts % a.C;
-            a.row_tgt[k] = (slot >= a.lo && slot < a.hi) ? static_cast<int>(slot - a.lo) : -1;
-            a.ttgt[k] = -INFINITY;
-        } else {
-            a.comp_idx[i] = -1;
+            if (ts < 0 && a.neg_mode) {
+                const int kn = n_pos + 1 + static_cast<int>(i - k);  // i - k = out-of-pool rows before i
+                a.comp_idx[i] = -2 - kn;
+                a.pos_row[kn] = static_cast<int>(i);
+                a.row_ab[kn] = make_float2(a.inv_n[i], 0.f);  // e = <x, T> / ||x|| = cosine
+                a.row_tgt[kn] = -2;
+                a.ttgt[kn] = -INFINITY;
+            } else if (ts >= 0) {
+                a.comp_idx[i] = k;
+                a.pos_row[k] = static_cast<int>(i);
+                if (a.excl) {
+                    const int he = a.hslot[i];
+                    a.row_hent[k] = he;
+                    if (he >= 0) a.hgseq[he] = ts;  // rows sharing a label share the target
+                }
+                a.row_ab[k] = make_float2(a.log2e_s * a.inv_n[i], B);
+                const int64_t slot = ts % a.C;
+                a.row_tgt[k] = (slot >= a.lo && slot < a.hi) ? static_cast<int>(slot - a.lo) : -1;
+                a.ttgt[k] = -INFINITY;
+            } else {
+                a.comp_idx[i] = -1;
+            }
         }
     }
-    // the mu row and the padding rows of the last row group
+    if (blockIdx.x != 0) return;
+    // (CTA 0) the mu row and the padding rows of the last row group
     const int n_rows = a.neg_mode ? static_cast<int>(a.N) + 1 : n_pos + 1;
     if (a.excl)
         for (int r = n_pos + tid; r < a.R_max; r += nt) a.row_hent[r] = -1;  // mu, out-of-pool, padding
+    // padding rows: e = -inf, so p = 0 (zero P operand in GEMM 2); the mu row: p = 1
     for (int r = (a.neg_mode ? n_rows : n_pos) + tid; r < a.R_max; r += nt) {
-        a.row_ab[r] = make_float2(0.f, 0.f);
+        a.row_ab[r] = make_float2(0.f, r == n_pos ? 0.f : INFINITY);
         a.row_tgt[r] = -1;
         a.ttgt[r] = -INFINITY;
     }
@@ -692,7 +705,15 @@ __global__ void __launch_bounds__(256) k_gather(const uint8_t *__restrict__ x, c
                                                 const int *__restrict__ row_tgt, float2 *__restrict__ row_ab) {
     // one warp per compacted row, 8 rows per CTA
     const int k = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-    if (k >= sc->n_rows || k == sc->n_pos) return;  // (row n_pos is the mu row)
+    if (k >= sc->n_rows || k == sc->n_pos) {
+        // the mu row and the padding rows of the last row group: zero operands (their
+        // products are discarded; zeros keep the tensor pipe's switching power down)
+        if (k < ((sc->n_rows + 127) & ~127)) {
+            int4 *dst = reinterpret_cast<int4 *>(Xp + static_cast<int64_t>(k) * row_bytes);
+            for (int u = lane; u < row_bytes / 16; u += 32) dst[u] = make_int4(0, 0, 0, 0);
+        }
+        return;
+    }
     const int4 *src = reinterpret_cast<const int4 *>(x + static_cast<int64_t>(pos_row[k]) * row_bytes);
     int4 *dst = reinterpret_cast<int4 *>(Xp + static_cast<int64_t>(k) * row_bytes);
     const int ts = row_tgt[k];  // local target slot, -1 (not on this shard), -2 (out-of-pool row)
@@ -769,40 +790,64 @@ __device__ __forceinline__ void clear_hash_slice(const CombineArgs &a, int64_t n
     }
 }
 
-__device__ __forceinline__ float block_sum_128(float v, float *red) {
+// The per-row kernels below run one WARP per global row (8 rows per 256-thread CTA, no
+// block-level synchronisation).  Lane l holds the 16 elements dd = 128 j + 4 l + e
+// (j < d/128 <= 4, e < 4) of every d-vector: float4 / 4 x bf16 vector accesses, coalesced.
+constexpr int CB_ROWS = 8;  // rows (warps) per CTA
+struct RowVec {
+    float v[16];
+};
+__device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
     for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    __syncthreads();
-    if (lane == 0) red[w] = v;
-    __syncthreads();
-    return red[0] + red[1] + red[2] + red[3];
+    return v;
+}
+__device__ __forceinline__ void zero16(float (&v)[16]) {
+#pragma unroll
+    for (int q = 0; q < 16; ++q) v[q] = 0.f;
+}
+// bf16 row -> fp32 lane elements (times scale)
+__device__ __forceinline__ void load_bf16_row(const __nv_bfloat16 *row, int d, int lane, float scale,
+                                              float (&v)[16]) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int dd = 128 * j + 4 * lane;
+        if (dd < d) {
+            const uint2 u = *reinterpret_cast<const uint2 *>(row + dd);
+            v[4 * j + 0] = __uint_as_float(u.x << 16) * scale;
+            v[4 * j + 1] = __uint_as_float(u.x & 0xffff0000u) * scale;
+            v[4 * j + 2] = __uint_as_float(u.y << 16) * scale;
+            v[4 * j + 3] = __uint_as_float(u.y & 0xffff0000u) * scale;
+        } else {
+            v[4 * j] = v[4 * j + 1] = v[4 * j + 2] = v[4 * j + 3] = 0.f;
+        }
+    }
 }
 
 // sum the partials of compacted row k over its segments (fixed range order);
-// the schedule (tp_choose_S) is the main kernel's.
-__device__ __forceinline__ void gather_row_partials(const CombineArgs &a, int n_rg, int k, float (&o)[4],
+// the schedule (tp_choose_S) is the main kernel's.  Segments are read in batches of B so
+// that the L2 latency is paid once per batch; the accumulation order is the segment order.
+__device__ __forceinline__ void gather_row_partials(const CombineArgs &a, int n_rg, int k, float (&o)[16],
                                                     float &lsum, float &mx) {
     const int RG = a.rows_per_group;
     const int rg = k / RG, r = k % RG;
+    const int lane = threadIdx.x & 31;
     lsum = 0.f;
     mx = -INFINITY;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) o[j] = 0.f;
+    zero16(o);
     if (a.n_tiles <= 0) return;
     const int S = tp_choose_S(n_rg, a.G, a.n_tiles);
-    // segments in batches of B: all loads of a batch are issued before the (fixed-order)
-    // accumulation, so the L2 latency is paid once per batch, not once per segment
-    constexpr int B = 8;
+    constexpr int B = 4;
     for (int s0 = 0; s0 < S; s0 += B) {
-        float lv[B], mv[B], ov[B][4];
+        float lv[B], mv[B];
+        float4 ov[B][4];
 #pragma unroll
         for (int u = 0; u < B; ++u) {
             const int s = s0 + u;
             lv[u] = 0.f;
             mv[u] = -INFINITY;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) ov[u][j] = 0.f;
+            for (int j = 0; j < 4; ++j) ov[u][j] = make_float4(0.f, 0.f, 0.f, 0.f);
             if (s >= S) continue;
             const long long t0 = static_cast<long long>(s) * a.n_tiles / S;
             const long long t1 = static_cast<long long>(s + 1) * a.n_tiles / S;
@@ -813,8 +858,8 @@ __device__ __forceinline__ void gather_row_partials(const CombineArgs &a, int n_
             const float *src = a.seg_O + (seg * RG + r) * a.d;
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-                const int dd = threadIdx.x + 128 * j;
-                if (dd < a.d) ov[u][j] = src[dd];
+                const int dd = 128 * j + 4 * lane;
+                if (dd < a.d) ov[u][j] = *reinterpret_cast<const float4 *>(src + dd);
             }
         }
 #pragma unroll
@@ -823,7 +868,12 @@ __device__ __forceinline__ void gather_row_partials(const CombineArgs &a, int n_
             lsum += lv[u];
             mx = fmaxf(mx, mv[u]);
 #pragma unroll
-            for (int j = 0; j < 4; ++j) o[j] += ov[u][j];
+            for (int j = 0; j < 4; ++j) {
+                o[4 * j + 0] += ov[u][j].x;
+                o[4 * j + 1] += ov[u][j].y;
+                o[4 * j + 2] += ov[u][j].z;
+                o[4 * j + 3] += ov[u][j].w;
+            }
         }
     }
 }
@@ -853,7 +903,7 @@ __device__ __forceinline__ void gather_row_max(const CombineArgs &a, int n_rg, i
 // dL_cos/dx_hat of an out-of-pool row handled by the main kernel (neg_mode 1 / 2), before
 // the factor lambda / N_neg; phi_raw = the shard's unreduced phi partial (sum of hinged
 // cosines, or the max cosine).
-__device__ __forceinline__ void neg_row_local(const CombineArgs &a, int n_rg, int kn, float (&g)[4],
+__device__ __forceinline__ void neg_row_local(const CombineArgs &a, int n_rg, int kn, float (&g)[16],
                                               float &phi_raw, int &carg) {
     carg = -1;
     if (a.neg_mode == 1) {
@@ -864,39 +914,39 @@ __device__ __forceinline__ void neg_row_local(const CombineArgs &a, int n_rg, in
         float cmax;
         gather_row_max(a, n_rg, kn, cmax, carg);
         phi_raw = cmax;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) g[j] = 0.f;
+        zero16(g);
     }
 }
-__device__ __forceinline__ void add_center(const CombineArgs &a, int carg, float coef, float (&g)[4]) {
+__device__ __forceinline__ void add_center(const CombineArgs &a, int carg, float coef, float (&g)[16]) {
     const float wc = a.wslot ? a.wslot[carg] : 1.f;
     const __nv_bfloat16 *Tc = reinterpret_cast<const __nv_bfloat16 *>(a.T) + static_cast<int64_t>(carg) * a.d;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        const int dd = threadIdx.x + 128 * j;
-        g[j] = dd < a.d ? coef * wc * __bfloat162float(Tc[dd]) : 0.f;
-    }
+    load_bf16_row(Tc, a.d, threadIdx.x & 31, coef * wc, g);
 }
 
-template <typename TX>
-__global__ void __launch_bounds__(128) k_combine(CombineArgs a) {
-    __shared__ float red[4];
-    const int64_t i = blockIdx.x;
+// normalisation Jacobian and output: dst = (g - (g . x_hat) x_hat) / ||x||
+__device__ __forceinline__ void jacobian(const float (&g)[16], const float (&xh)[16], float inv, float (&out)[16]) {
+    float gd = 0.f;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) gd += g[q] * xh[q];
+    gd = warp_sum(gd);
+#pragma unroll
+    for (int q = 0; q < 16; ++q) out[q] = (g[q] - gd * xh[q]) * inv;
+}
+
+__global__ void __launch_bounds__(256, 2) k_combine(CombineArgs a) {
     clear_hash_slice(a, gridDim.x);
+    const int lane = threadIdx.x & 31;
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * CB_ROWS + (threadIdx.x >> 5);
+    if (i >= a.N) return;
     const int n_pos = a.sc->n_pos, n_neg = a.sc->n_neg;
     const int n_rg = (a.sc->n_rows + a.rows_per_group - 1) / a.rows_per_group;
     const int k = a.comp_idx[i];
-    const TX *xr = reinterpret_cast<const TX *>(a.x) + i * a.d;
     const float inv = a.inv_n[i];
-    float xh[4], g[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        const int dd = threadIdx.x + 128 * j;
-        xh[j] = dd < a.d ? to_f<TX>(xr[dd]) * inv : 0.f;
-    }
+    float xh[16], g[16];
+    load_bf16_row(reinterpret_cast<const __nv_bfloat16 *>(a.x) + i * a.d, a.d, lane, inv, xh);
     double row_loss = 0.0;
     if (k >= 0) {
-        float o[4], lsum, mx;
+        float o[16], lsum, mx;
         gather_row_partials(a, n_rg, k, o, lsum, mx);
         const double tt = static_cast<double>(a.ttgt[k]);
         const double lr = static_cast<double>(lsum);
@@ -904,17 +954,16 @@ __global__ void __launch_bounds__(128) k_combine(CombineArgs a) {
         const double l = lr + et;
         const float2 ab = a.row_ab[k];
         const int ts = a.row_tgt[k];
-        const TX *Tt = reinterpret_cast<const TX *>(a.T) + static_cast<int64_t>(ts < 0 ? 0 : ts) * a.d;
         const double w = static_cast<double>(a.s) / static_cast<double>(n_pos);
         const float alpha = static_cast<float>(w / l), beta = static_cast<float>(w * (lr / l));
+        float Tt[16];
+        load_bf16_row(reinterpret_cast<const __nv_bfloat16 *>(a.T) + static_cast<int64_t>(ts < 0 ? 0 : ts) * a.d,
+                      a.d, lane, 1.f, Tt);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int dd = threadIdx.x + 128 * j;
-            g[j] = dd < a.d ? alpha * o[j] - beta * to_f<TX>(Tt[dd]) : 0.f;
-        }
+        for (int q = 0; q < 16; ++q) g[q] = alpha * o[q] - beta * Tt[q];
         const double ell = log1p(lr * exp2(-tt));  // = lse - z_t
         row_loss = ell;
-        if (threadIdx.x == 0) {
+        if (lane == 0) {
             a.st_ell[i] = static_cast<float>(ell);
             a.st_lse[i] = static_cast<float>((static_cast<double>(ab.y) + log2(l)) * 0.6931471805599453);
             a.st_cos[i] = static_cast<float>((tt + a.margin_l2 + ab.y) / (a.s * 1.4426950408889634));
@@ -930,15 +979,15 @@ __global__ void __launch_bounds__(128) k_combine(CombineArgs a) {
         float phi;
         if (k == -1) {
             // mu path: mu = sum over occupied slots of w_c T_bar_c (the mu row, index n_pos)
-            float mu[4], lsum, mx;
+            float mu[16], lsum, mx;
             gather_row_partials(a, n_rg, n_pos, mu, lsum, mx);
             float dot = 0.f;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                g[j] = w * rs * mu[j];
-                dot += xh[j] * mu[j];
+            for (int q = 0; q < 16; ++q) {
+                g[q] = w * rs * mu[q];
+                dot += xh[q] * mu[q];
             }
-            dot = block_sum_128(dot, red);
+            dot = warp_sum(dot);
             phi = a.C_occ > 0 ? dot * rs : 0.f;
         } else {
             float raw;
@@ -947,67 +996,84 @@ __global__ void __launch_bounds__(128) k_combine(CombineArgs a) {
             if (a.neg_mode == 1) {
                 phi = a.C_occ > 0 ? raw * rs : 0.f;
 #pragma unroll
-                for (int j = 0; j < 4; ++j) g[j] *= w * rs;
+                for (int q = 0; q < 16; ++q) g[q] *= w * rs;
             } else {
                 phi = carg < 0 ? 0.f : (a.hinge ? fmaxf(raw, 0.f) : raw);
                 if (carg >= 0 && !(a.hinge && raw <= 0.f)) add_center(a, carg, w, g);
             }
         }
         row_loss = phi;
-        if (threadIdx.x == 0) {
+        if (lane == 0) {
             a.st_phi[i] = phi;
             a.st_ell[i] = 0.f;
             a.st_lse[i] = 0.f;
             a.st_cos[i] = 0.f;
         }
     }
-    // normalisation Jacobian: dx = (g - (g . x_hat) x_hat) / ||x||
-    float gd = 0.f;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) gd += g[j] * xh[j];
-    gd = block_sum_128(gd, red);
-    TX *dxr = reinterpret_cast<TX *>(a.dx) + i * a.d;
+    float out[16];
+    jacobian(g, xh, inv, out);
+    __nv_bfloat16 *dxr = reinterpret_cast<__nv_bfloat16 *>(a.dx) + i * a.d;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-        const int dd = threadIdx.x + 128 * j;
-        if (dd < a.d) dxr[dd] = from_f<TX>((g[j] - gd * xh[j]) * inv);
+        const int dd = 128 * j + 4 * lane;
+        if (dd < a.d) {
+            const __nv_bfloat162 p0 = __floats2bfloat162_rn(out[4 * j], out[4 * j + 1]);
+            const __nv_bfloat162 p1 = __floats2bfloat162_rn(out[4 * j + 2], out[4 * j + 3]);
+            uint2 u;
+            u.x = *reinterpret_cast<const uint32_t *>(&p0);
+            u.y = *reinterpret_cast<const uint32_t *>(&p1);
+            *reinterpret_cast<uint2 *>(dxr + dd) = u;
+        }
     }
-    if (threadIdx.x == 0) a.rowloss[i] = row_loss;
+    if (lane == 0) a.rowloss[i] = row_loss;
 }
 
 // ------------------------------------------------------------------ multi-rank combine
 // Per global row i, this rank's partial of the softmax statistics over its slot shard:
-//   in-pool rows:     (l_rest_r, max_r, ttgt_r, 0)   (ttgt_r = -inf unless rank r owns t_i)
-//   out-of-pool rows: (phi_r, 0, 0, 0)               phi_r = x_hat_i . mu_r / C_occ
+//   in-pool rows:     (l_rest_r, max_r, ttgt_r, b_r)  (ttgt_r = -inf unless rank r owns t_i)
+//   out-of-pool rows: (phi_r, 0, 0, 0)               phi_r = x_hat_i . mu_r (unreduced)
 // These are all-gathered (C3); every rank then finalises identically (k_finalize_multi).
-__global__ void __launch_bounds__(128) k_local_rows(CombineArgs a, float4 *__restrict__ scal) {
-    __shared__ float red[4];
-    const int64_t i = blockIdx.x;
+__global__ void __launch_bounds__(256, 2) k_local_rows(CombineArgs a, float4 *__restrict__ scal) {
+    const int lane = threadIdx.x & 31;
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * CB_ROWS + (threadIdx.x >> 5);
+    if (i >= a.N) return;
     const int n_pos = a.sc->n_pos;
     const int n_rg = (a.sc->n_rows + a.rows_per_group - 1) / a.rows_per_group;
     const int k = a.comp_idx[i];
     if (k >= 0) {
-        float o[4], lsum, mx;
-        gather_row_partials(a, n_rg, k, o, lsum, mx);  // (o unused here)
-        if (threadIdx.x == 0) scal[i] = make_float4(lsum, mx, a.ttgt[k], a.row_ab[k].y);
+        // (only the scalars: l_rest and max over the segments)
+        const int RG = a.rows_per_group;
+        const int rg = k / RG, r = k % RG;
+        float lsum = 0.f, mx = -INFINITY;
+        if (a.n_tiles > 0) {
+            const int S = tp_choose_S(n_rg, a.G, a.n_tiles);
+            for (int s = lane; s < S; s += 32) {  // lanes split the segments, fixed-order tree below
+                const long long t0 = static_cast<long long>(s) * a.n_tiles / S;
+                const long long t1 = static_cast<long long>(s + 1) * a.n_tiles / S;
+                if (t1 <= t0) continue;
+                const long long seg = static_cast<long long>(s) * n_rg + rg;
+                lsum += a.seg_l[seg * RG + r];
+                mx = fmaxf(mx, a.seg_mx[seg * RG + r]);
+            }
+        }
+        lsum = warp_sum(lsum);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        if (lane == 0) scal[i] = make_float4(lsum, mx, a.ttgt[k], a.row_ab[k].y);
     } else if (k <= -2) {
-        float g[4], raw;
+        float g[16], raw;
         int carg;
         neg_row_local(a, n_rg, -2 - k, g, raw, carg);
-        if (threadIdx.x == 0) scal[i] = make_float4(raw, 0.f, 0.f, 0.f);
+        if (lane == 0) scal[i] = make_float4(raw, 0.f, 0.f, 0.f);
     } else {
-        float mu[4], lsum, mx;
+        float mu[16], lsum, mx, xh[16];
         gather_row_partials(a, n_rg, n_pos, mu, lsum, mx);
-        const __nv_bfloat16 *xr = reinterpret_cast<const __nv_bfloat16 *>(a.x) + i * a.d;
-        const float inv = a.inv_n[i];
+        load_bf16_row(reinterpret_cast<const __nv_bfloat16 *>(a.x) + i * a.d, a.d, lane, a.inv_n[i], xh);
         float dot = 0.f;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int dd = threadIdx.x + 128 * j;
-            if (dd < a.d) dot += __bfloat162float(xr[dd]) * inv * mu[j];
-        }
-        dot = block_sum_128(dot, red);
-        if (threadIdx.x == 0) scal[i] = make_float4(dot, 0.f, 0.f, 0.f);  // x_hat . mu_r (unreduced)
+        for (int q = 0; q < 16; ++q) dot += xh[q] * mu[q];
+        dot = warp_sum(dot);
+        if (lane == 0) scal[i] = make_float4(dot, 0.f, 0.f, 0.f);  // x_hat . mu_r (unreduced)
     }
 }
 
@@ -1016,22 +1082,18 @@ __global__ void __launch_bounds__(128) k_local_rows(CombineArgs a, float4 *__res
 // reduce-scatter (C4):
 //   in-pool:     g_r = (s/N_pos) (O_r / l - [r owns t] (l_rest / l) T_t)
 //   out-of-pool: g_r = mu_r / (N_neg C_occ)
-__global__ void __launch_bounds__(128) k_finalize_multi(CombineArgs a, const float4 *__restrict__ scal_all,
+__global__ void __launch_bounds__(256, 2) k_finalize_multi(CombineArgs a, const float4 *__restrict__ scal_all,
                                                         int W, int64_t N, float *__restrict__ dx_part) {
-    __shared__ float red[4];
-    const int64_t i = blockIdx.x;
     clear_hash_slice(a, gridDim.x);
+    const int lane = threadIdx.x & 31;
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * CB_ROWS + (threadIdx.x >> 5);
+    if (i >= N) return;
     const int n_pos = a.sc->n_pos, n_neg = a.sc->n_neg;
     const int n_rg = (a.sc->n_rows + a.rows_per_group - 1) / a.rows_per_group;
     const int k = a.comp_idx[i];
-    const __nv_bfloat16 *xr = reinterpret_cast<const __nv_bfloat16 *>(a.x) + i * a.d;
     const float inv = a.inv_n[i];
-    float xh[4], g[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        const int dd = threadIdx.x + 128 * j;
-        xh[j] = dd < a.d ? __bfloat162float(xr[dd]) * inv : 0.f;
-    }
+    float xh[16], g[16];
+    load_bf16_row(reinterpret_cast<const __nv_bfloat16 *>(a.x) + i * a.d, a.d, lane, inv, xh);
     double row_loss = 0.0;
     if (k >= 0) {
         // every shard used its own reference b_r: rescale to the common B* = max_r b_r
@@ -1045,7 +1107,7 @@ __global__ void __launch_bounds__(128) k_finalize_multi(CombineArgs a, const flo
             mx = fmaxf(mx, v.y + (v.w - Bs));
             tt = fmaxf(tt, v.z + (v.w - Bs));
         }
-        float o[4], lsum, mxl;
+        float o[16], lsum, mxl;
         gather_row_partials(a, n_rg, k, o, lsum, mxl);
         const double l = lr + exp2(static_cast<double>(tt));
         const double w = static_cast<double>(a.s) / static_cast<double>(n_pos);
@@ -1053,15 +1115,14 @@ __global__ void __launch_bounds__(128) k_finalize_multi(CombineArgs a, const flo
         const float my_scale = static_cast<float>(exp2(static_cast<double>(a.row_ab[k].y) - Bs));
         const float alpha = static_cast<float>(w / l) * my_scale;
         const float beta = ts >= 0 ? static_cast<float>(w * (lr / l)) : 0.f;
-        const __nv_bfloat16 *Tt = reinterpret_cast<const __nv_bfloat16 *>(a.T) + static_cast<int64_t>(ts < 0 ? 0 : ts) * a.d;
+        float Tt[16];
+        load_bf16_row(reinterpret_cast<const __nv_bfloat16 *>(a.T) + static_cast<int64_t>(ts < 0 ? 0 : ts) * a.d,
+                      a.d, lane, 1.f, Tt);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int dd = threadIdx.x + 128 * j;
-            g[j] = dd < a.d ? alpha * o[j] - beta * __bfloat162float(Tt[dd]) : 0.f;
-        }
+        for (int q = 0; q < 16; ++q) g[q] = alpha * o[q] - beta * Tt[q];
         const double ell = log1p(lr * exp2(-static_cast<double>(tt)));
         row_loss = ell;
-        if (threadIdx.x == 0) {
+        if (lane == 0) {
             a.st_ell[i] = static_cast<float>(ell);
             a.st_lse[i] = static_cast<float>((static_cast<double>(Bs) + log2(l)) * 0.6931471805599453);
             a.st_cos[i] = static_cast<float>((static_cast<double>(tt) + a.margin_l2 + Bs) / (a.s * 1.4426950408889634));
@@ -1097,29 +1158,27 @@ __global__ void __launch_bounds__(128) k_finalize_multi(CombineArgs a, const flo
                 gather_row_partials(a, n_rg, n_pos, g, lsum, mxl);
             }
 #pragma unroll
-            for (int j = 0; j < 4; ++j) g[j] *= w * rs;
+            for (int q = 0; q < 16; ++q) g[q] *= w * rs;
             for (int r = 0; r < W; ++r) phi += static_cast<double>(scal_all[static_cast<int64_t>(r) * N + i].x);
             phi = a.C_occ > 0 ? phi * rs : 0.0;
         }
         row_loss = phi;
-        if (threadIdx.x == 0) {
+        if (lane == 0) {
             a.st_phi[i] = static_cast<float>(phi);
             a.st_ell[i] = 0.f;
             a.st_lse[i] = 0.f;
             a.st_cos[i] = 0.f;
         }
     }
-    float gd = 0.f;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) gd += g[j] * xh[j];
-    gd = block_sum_128(gd, red);
+    float out[16];
+    jacobian(g, xh, inv, out);
     float *dst = dx_part + i * a.d;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-        const int dd = threadIdx.x + 128 * j;
-        if (dd < a.d) dst[dd] = (g[j] - gd * xh[j]) * inv;
+        const int dd = 128 * j + 4 * lane;
+        if (dd < a.d) *reinterpret_cast<float4 *>(dst + dd) = make_float4(out[4 * j], out[4 * j + 1], out[4 * j + 2], out[4 * j + 3]);
     }
-    if (threadIdx.x == 0) a.rowloss[i] = row_loss;
+    if (lane == 0) a.rowloss[i] = row_loss;
 }
 
 __global__ void k_cast_bf16(const float *__restrict__ src, __nv_bfloat16 *__restrict__ dst, int64_t n) {
