@@ -407,6 +407,8 @@ int f2c_dcp_create_k(int64_t C, int32_t K, int32_t d, int32_t dtype, int32_t wor
     {
         const char *kv = getenv("F2C_KERNEL");
         h->use_tp64 = kv && strcmp(kv, "tp64") == 0 && K == 1;
+        const char *fl = getenv("F2C_DBG_FLAGS");  // timing experiments only (results void)
+        h->dbg_flags = fl ? atoi(fl) : 0;
     }
     if (cudaFuncSetAttribute(dcp_tp64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              TP_SMEM_BYTES) != cudaSuccess ||
@@ -593,12 +595,9 @@ extern "C" int f2c_gnet_ema(const float *p, float *g, int64_t n, double momentum
     if ((p < g + n) && (g < p + n)) return fail(F2C_EINVAL, "p and g overlap");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const int64_t n4 = n / 4;
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (n4 > 0) {
-        int64_t blocks = (n4 + 255) / 256;
-        if (blocks > static_cast<int64_t>(sms) * 8) blocks = static_cast<int64_t>(sms) * 8;
+        const int64_t blocks = (n4 + 256 * EMA_PER_THREAD - 1) / (256 * EMA_PER_THREAD);
+        if (blocks > 0x7fffffffll) return fail(F2C_ESHAPE, "n too large");
         k_ema<<<static_cast<unsigned>(blocks), 256, 0, st>>>(reinterpret_cast<const float4 *>(p),
                                                              reinterpret_cast<float4 *>(g), n4,
                                                              momentum, 1.0 - momentum);

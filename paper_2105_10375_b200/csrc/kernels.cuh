@@ -260,17 +260,33 @@ __device__ __forceinline__ float ema1(float gv, float pv, double m, double om) {
     return __double2float_rn(__dadd_rn(__dmul_rn(m, static_cast<double>(gv)),
                                        __dmul_rn(om, static_cast<double>(pv))));
 }
-__global__ void k_ema(const float4 *__restrict__ p, float4 *__restrict__ g, int64_t n4, double m,
-                      double om) {
-    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n4;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const float4 a = __ldcs(p + i);
-        float4 b = __ldcs(g + i);
-        b.x = ema1(b.x, a.x, m, om);
-        b.y = ema1(b.y, a.y, m, om);
-        b.z = ema1(b.z, a.z, m, om);
-        b.w = ema1(b.w, a.w, m, om);
-        __stcs(g + i, b);
+// One CTA per 1024 float4 (16 KB of g): short-lived CTAs, so a concurrently launched
+// persistent kernel (the fused loss kernel) gets its SMs back within microseconds when the
+// EMA runs on a side stream; four independent 16-B loads per thread in flight.
+constexpr int EMA_PER_THREAD = 4;
+__global__ void __launch_bounds__(256) k_ema(const float4 *__restrict__ p, float4 *__restrict__ g, int64_t n4,
+                                             double m, double om) {
+    const int64_t base = static_cast<int64_t>(blockIdx.x) * (256 * EMA_PER_THREAD) + threadIdx.x;
+    float4 a[EMA_PER_THREAD], b[EMA_PER_THREAD];
+#pragma unroll
+    for (int u = 0; u < EMA_PER_THREAD; ++u) {
+        const int64_t i = base + u * 256;
+        if (i < n4) {
+            a[u] = __ldcs(p + i);
+            b[u] = __ldcs(g + i);
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < EMA_PER_THREAD; ++u) {
+        const int64_t i = base + u * 256;
+        if (i < n4) {
+            float4 v = b[u];
+            v.x = ema1(v.x, a[u].x, m, om);
+            v.y = ema1(v.y, a[u].y, m, om);
+            v.z = ema1(v.z, a[u].z, m, om);
+            v.w = ema1(v.w, a[u].w, m, om);
+            __stcs(g + i, v);
+        }
     }
 }
 __global__ void k_ema_tail(const float *__restrict__ p, float *__restrict__ g, int64_t lo, int64_t n,
