@@ -429,6 +429,10 @@ def _workload(name):
     if name.startswith("c4r_"):  # c4r_<pct>_<global batch>: one rank of a W=8 c4 point
         _, pct, n = name.split("_")
         return c4_rank_config(int(pct) / 100, int(n))
+    if name.startswith("c3r_"):  # c3r_<W>: the compute of one rank of c3 at W ranks (no collectives)
+        W = int(name.split("_")[1])
+        base = synth.CONFIGS["c3"]
+        return synth.scaled(base, name=name, C=base.C // W, M_loc=base.M_loc * W, n_id=base.n_id // W)
     return synth.CONFIGS[name]
 
 
@@ -464,7 +468,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c3",
-                    help="c1 | c2 | c3 | c4r_<pct>_<global batch> (one rank of a W=8 c4 point)")
+                    help="c1 | c2 | c3 | c4r_<pct>_<global batch> (one rank of a W=8 c4 point) | "
+                         "c3r_<W> (one rank of c3 at W GPUs, collectives excluded)")
     ap.add_argument("--ring", type=int, default=8)
     ap.add_argument("--ema-overlap", type=int, default=1,
                     help="1: G-Net EMA on a low-priority side stream (overlaps the head's small kernels)")
