@@ -114,6 +114,7 @@ struct PCParams {
     unsigned long long *dbg;
     int dbg_flags;         // timing experiments only: 1 = skip P smem writes, 128 = skip DSMEM copy,
                            // 4 / 8 = no producer / consumer pool loads, 16 = no softmax arithmetic,
+                           // 16384 = every CTA loads only pool tiles 0-15 (L2-hot; same smem traffic),
                            // 64 = softmax warps idle (barrier protocol only), 256 = no GEMM-2 MMAs
 };
 
@@ -351,7 +352,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                                 continue;
                             }
                             mbar_arrive_expect_tx(&aux->tfull[st], PC_P_STAGE_BYTES);
-                            tma_load_3d(sT + st * PC_P_STAGE_BYTES, &tm3p, &aux->tfull[st], 0, t * PC_TILE, g * cps_p);
+                            const int tl = (p.dbg_flags & 16384) ? (t & 15) : t;  // 16384: hot tiles (experiment)
+                            tma_load_3d(sT + st * PC_P_STAGE_BYTES, &tm3p, &aux->tfull[st], 0, tl * PC_TILE, g * cps_p);
                         }
                 }
             }
@@ -642,7 +644,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                                 continue;
                             }
                             mbar_arrive_expect_tx(&aux->qfull[st], stage_bytes);
-                            tma_load_3d(sT + st * PC_STAGE_BYTES, &tm3q, &aux->qfull[st], 0, t * PC_TILE, g * cps);
+                            const int tl = (p.dbg_flags & 16384) ? (t & 15) : t;
+                            tma_load_3d(sT + st * PC_STAGE_BYTES, &tm3q, &aux->qfull[st], 0, tl * PC_TILE, g * cps);
                         }
                 }
             }
