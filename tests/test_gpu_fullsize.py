@@ -68,3 +68,55 @@ def test_c2_full_size_sampled_rows():
     cfg = synth.CONFIGS["c2"]
     head, loss, gdx, rs, ref, rows = _run(cfg, 16, seed=1)
     _check(cfg, loss, gdx, rs, ref, rows)
+
+
+@pytest.mark.slow
+def test_c3_full_size_sampled_rows():
+    """BJ:10 at W=1 -- the workload bench.py times by default (4,194,304 slots, batch 1024):
+    the pool prefilled through the enqueue kernel from the seeded generator, 8 sampled rows
+    checked one by one against the oracle, properties on all rows."""
+    cfg = synth.CONFIGS["c3"]
+    head, loss, gdx, rs, ref, rows = _run(cfg, 8, seed=2)
+    _check(cfg, loss, gdx, rs, ref, rows)
+
+
+@pytest.mark.slow
+def test_c3_w8_emulated_full_size_sampled_rows():
+    """BJ:10 at W=8 -- the sharded configuration of the scaling run (524,288 slots per rank,
+    global batch 8192, global enqueue block 4096) -- through the multi-rank protocol (C1-C5)
+    in the emulated world (all eight shards on this device, collectives as device copies):
+    sampled rows against the single-pool oracle (D16), properties on all rows."""
+    import paper_2105_10375_b200 as dcp
+    cfg, W = synth.CONFIGS["c3"], 8
+    Mg = cfg.M_glob(W)
+    head = dcp.DCPHead(cfg.C, cfg.d, dcp.BF16, world=W, rank=-1, n_local_max=cfg.N_loc(),
+                       m_local_max=cfg.M_loc)
+    pool = oracle.Pool(cfg.C, cfg.d, oracle.BF16)
+    for b in range(cfg.prefill_blocks(W)):
+        parts = [synth.prefill_block(cfg, b, r, W) for r in range(W)]
+        G = np.concatenate([p[0] for p in parts])
+        y = np.concatenate([p[1] for p in parts])
+        head.enqueue(to_dev(G, synth.BF16), lt(y))
+        pool.enqueue(G, y)
+    sts = [synth.step_inputs(cfg, 0, r, W) for r in range(W)]
+    g = np.concatenate([s.g for s in sts])
+    gy = np.concatenate([s.gy for s in sts])
+    head.enqueue(to_dev(g, synth.BF16), lt(gy))
+    pool.enqueue(g, gy)
+    x = np.concatenate([s.x for s in sts])
+    y = np.concatenate([s.y for s in sts])
+    pr = np.concatenate([s.pairing for s in sts])
+    loss, dx = head.loss_fwd_bwd(to_dev(x, synth.BF16), lt(y), it(pr), cfg.s, cfg.m)
+    torch.cuda.synchronize()
+    head.check()
+    N = len(y)
+    rs = head.row_stats(N)
+    gdx = from_dev(dx)
+    rng = np.random.default_rng(3)
+    M = cfg.M_loc
+    # rows of ranks 0, 3 and 7: instance rows [r*2M, r*2M+M), identity rows [r*2M+M, (r+1)*2M)
+    rows = np.sort(np.concatenate([r * 2 * M + rng.choice(M, 1, replace=False) for r in (0, 3, 7)] +
+                                  [r * 2 * M + M + rng.choice(M, 1, replace=False) for r in (0, 3, 7)]))
+    ref = pool.loss_rows(x, y, pr, cfg.s, cfg.m, rows)
+    _check(cfg, loss, gdx, rs, ref, rows)
+    assert Mg == 4096 and rs["N_pos"] >= Mg
