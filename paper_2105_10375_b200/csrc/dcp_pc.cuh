@@ -42,7 +42,11 @@ constexpr int PCQ_OFF_P = 0;                              // 2 x 32 KB P slots
 constexpr int PCQ_OFF_T = PCQ_OFF_P + 2 * PC_PBYTES;      // 2 x 64 KB pool stages
 constexpr int PCQ_OFF_AUX = PCQ_OFF_T + PC_Q_NSTAGE * PC_STAGE_BYTES;
 constexpr int PC_OFF_AUX = PCP_OFF_AUX > PCQ_OFF_AUX ? PCP_OFF_AUX : PCQ_OFF_AUX;
-constexpr int PC_SMEM_BYTES = PC_OFF_AUX + 4096 + 1024;
+// consumer: O-drain staging, one [32 rows x 16 fp32] TMA-store box per drain warp
+constexpr int PC_OFF_OSTG = PC_OFF_AUX + 4096;
+constexpr int PC_OSTG_BYTES = 8 * 2048;
+constexpr int PC_SMEM_BYTES = PC_OFF_OSTG + PC_OSTG_BYTES + 1024;   // with the drain staging
+constexpr int PC_SMEM_BYTES_NOSTG = PC_OFF_OSTG + 1024;            // without it
 
 // the same struct (same offsets) in both CTAs, so multicast commits can target a
 // barrier of the peer by its local offset
@@ -111,6 +115,8 @@ struct PCParams {
     const int *dup_off;
     const int2 *dup_list;
     const int *row_hent;
+    int drain_tma;         // O drain through smem staging + TMA stores (short units); else direct
+                           // stores (launched without the staging smem)
     unsigned long long *dbg;
     int dbg_flags;         // timing experiments only: 1 = skip P smem writes, 128 = skip DSMEM copy,
                            // 4 / 8 = no producer / consumer pool loads, 16 = no softmax arithmetic,
@@ -250,6 +256,25 @@ __device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *m, uin
         "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(z)
         : "memory");
 }
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+// TMA store of one 2D box from shared memory (bulk async-group)
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap *m, uint32_t src, int x, int y) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                     reinterpret_cast<uint64_t>(m)),
+                 "r"(src), "r"(x), "r"(y)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
 __device__ __forceinline__ void tmem_wait_st() {
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
@@ -260,7 +285,7 @@ __device__ __forceinline__ void tmem_wait_st() {
 template <bool EXCL>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
     dcp_pc_kernel(const __grid_constant__ CUtensorMap tm3p, const __grid_constant__ CUtensorMap tm3q,
-                  const PCParams p) {
+                  const __grid_constant__ CUtensorMap tmO, const PCParams p) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                 ~static_cast<uintptr_t>(1023));
@@ -306,7 +331,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
             mbar_init(&aux->qempty[i], 1);
         }
         mbar_init(&aux->ofull, 1);
-        mbar_init(&aux->oempty, 4);
+        mbar_init(&aux->oempty, 8);
         if (crank == 1 && !(p.dbg_flags & 128)) {  // arm both P slots before the producer can copy into them
             mbar_arrive_expect_tx(&aux->pfull[0], PC_PBYTES);
             mbar_arrive_expect_tx(&aux->pfull[1], PC_PBYTES);
@@ -321,6 +346,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
     if (warp == 9) {
         tma_prefetch_desc(&tm3p);
         tma_prefetch_desc(&tm3q);
+        tma_prefetch_desc(&tmO);
         tmem_alloc(&aux->tmem_base, 512);
         tmem_relinquish();
     }
@@ -685,26 +711,56 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                     ++sg;
                 }
             }
-        } else if (warp < 4) {
-            // -------- O drain at segment end: warp w -> rows 32w..32w+31 (TMEM lanes)
-            const uint32_t lane_base = static_cast<uint32_t>(warp * 32) << 16;
-            const int r = warp * 32 + lane;
+        } else if (warp < 8) {
+            // -------- O drain at segment end: warp w -> rows 32(w%4).. (its TMEM lane quadrant),
+            // columns [w/4 * d/2, (w/4 + 1) * d/2): eight warps, so the next unit's GEMM 2 waits less
+            const int q = warp & 3, hcol = warp >> 2;
+            const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
+            const int r = q * 32 + lane;
             uint32_t sg = 0;
+            // staged through shared memory and written by TMA stores: each store is one
+            // [32 rows x 16 fp32] box of seg_O (row-per-lane global stores scatter one row per
+            // lane and took ~45K cycles per unit)
+            const uint32_t stg = smem_u32(smem + PC_OFF_OSTG + warp * 2048);
             while (sch.next(rg, t0, t1, seg)) {
                 mbar_wait(&aux->ofull, sg & 1);
                 tc_fence_after();
-                float4 *dst = reinterpret_cast<float4 *>(p.seg_O + (static_cast<size_t>(seg) * PC_R + r) * d);
-                for (int c0 = 0; c0 < d; c0 += 32) {
-                    float o[32];
-                    tmem_ld32(tmem + lane_base + c0, o);
-                    tmem_wait_ld();
+                if (!p.drain_tma) {  // long units: the drain is off the critical path
+                    float4 *dst = reinterpret_cast<float4 *>(p.seg_O + (static_cast<size_t>(seg) * PC_R + r) * d);
+                    for (int c0 = hcol * (d / 2); c0 < (hcol + 1) * (d / 2); c0 += 32) {
+                        float o[32];
+                        tmem_ld32(tmem + lane_base + c0, o);
+                        tmem_wait_ld();
 #pragma unroll
-                    for (int u = 0; u < 8; ++u)
-                        dst[c0 / 4 + u] = make_float4(o[4 * u], o[4 * u + 1], o[4 * u + 2], o[4 * u + 3]);
+                        for (int u = 0; u < 8; ++u)
+                            dst[c0 / 4 + u] = make_float4(o[4 * u], o[4 * u + 1], o[4 * u + 2], o[4 * u + 3]);
+                    }
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&aux->oempty);
+                    ++sg;
+                    continue;
+                }
+                const int row0 = seg * PC_R + q * 32;
+                for (int c0 = hcol * (d / 2); c0 < (hcol + 1) * (d / 2); c0 += 16) {
+                    float o[16];
+                    tmem_ld16(tmem + lane_base + c0, o);
+                    tmem_wait_ld();
+                    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                    __syncwarp();
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+                        st_shared_v4(stg + lane * 64 + u * 16, __float_as_uint(o[4 * u]), __float_as_uint(o[4 * u + 1]),
+                                     __float_as_uint(o[4 * u + 2]), __float_as_uint(o[4 * u + 3]));
+                    fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) tma_store_2d(&tmO, stg, c0, row0);
                 }
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&aux->oempty);
+                if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+                __syncwarp();
                 ++sg;
             }
         }

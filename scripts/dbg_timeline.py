@@ -6,7 +6,8 @@ import paper_2105_10375_b200 as dcp
 from paper_2105_10375_b200.dcp import load_library
 wl = sys.argv[1] if len(sys.argv) > 1 else "c2"
 import synth
-cfg = synth.CONFIGS[wl]
+from bench import _workload
+cfg = _workload(wl)
 L = load_library()
 head = dcp.DCPHead(cfg.C, cfg.d, 0, 1, 0, n_local_max=cfg.N_loc(), m_local_max=cfg.M_loc)
 gen = torch.Generator(device="cuda"); gen.manual_seed(1)
