@@ -276,3 +276,16 @@ def test_degenerate_all_negative_cosines(dcp, world):
     gdx = from_dev(dx)
     assert_dx_close(gdx, ref.dx)
     assert_dx_rows_close(gdx, ref.dx, np.where(ref.tslot >= 0)[0], what="dx in-pool")
+
+
+@pytest.mark.parametrize("d", [128, 512])
+def test_tp64_comparison_kernel_parity(dcp, d, monkeypatch):
+    """The first single-CTA design (dcp_tp64_kernel, F2C_KERNEL=tp64) is
+    kept as a comparison point: it must meet the same bar."""
+    monkeypatch.setenv("F2C_KERNEL", "tp64")
+    C, M, n_id = 1500, 100, 2000
+    blocks = _random_pool_blocks(C, d, M, 17, n_id, 21)
+    X = synth.unit_rows(22, synth.S_INST, 0, 0, 150, d)
+    y = synth.uniform_labels(22, synth.S_INST_LAB, 0, 0, 150, n_id)
+    y[::2] = blocks[-1][1][: len(y[::2])]        # half the rows in-pool (70+ rows: two 64-row groups)
+    _run_case(dcp, C, d, blocks, X, y, None, 64.0, 0.35)
