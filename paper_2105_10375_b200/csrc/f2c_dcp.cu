@@ -637,7 +637,7 @@ struct StepCtx {
 
 
 // a2 + a3: norms, label hash, local target resolve (tseq = newest local seq or -1)
-static int phase_resolve(f2c_dcp *h, Rank &R, const StepCtx &c) {
+static int phase_resolve(f2c_dcp *h, Rank &R, const StepCtx &c, bool materialize_tseq = true) {
     const Layout &L = R.L;
     const unsigned rows_blocks = static_cast<unsigned>((c.N * 32 + 255) / 256);
     if (h->dtype == F2C_BF16)
@@ -661,17 +661,21 @@ static int phase_resolve(f2c_dcp *h, Rank &R, const StepCtx &c) {
             R.at<unsigned long long>(L.hvals), L.H);
         LAUNCH_CHECK();
     }
-    k_resolve<<<static_cast<unsigned>((c.N + 255) / 256), 256, 0, c.st>>>(
-        R.at<int>(L.hslot), R.at<unsigned long long>(L.hvals), c.N, R.at<int64_t>(L.tseq));
-    LAUNCH_CHECK();
+    if (materialize_tseq) {  // (W = 1: k_compact resolves from the hash itself)
+        k_resolve<<<static_cast<unsigned>((c.N + 255) / 256), 256, 0, c.st>>>(
+            R.at<int>(L.hslot), R.at<unsigned long long>(L.hvals), c.N, R.at<int64_t>(L.tseq));
+        LAUNCH_CHECK();
+    }
     return F2C_OK;
 }
 
 // a3 split + compaction + gather
-static int phase_compact(f2c_dcp *h, Rank &R, const StepCtx &c, const int *tmax_bits) {
+static int phase_compact(f2c_dcp *h, Rank &R, const StepCtx &c, const int *tmax_bits, bool resolve_here = false) {
     const Layout &L = R.L;
     CompactArgs a;
     a.tseq = R.at<int64_t>(L.tseq);
+    a.rs_hslot = resolve_here ? R.at<int>(L.hslot) : nullptr;
+    a.rs_hvals = resolve_here ? R.at<unsigned long long>(L.hvals) : nullptr;
     a.inv_n = R.at<float>(L.inv_n);
     a.pairing = c.pair;
     a.N = c.N; a.C = h->C; a.lo = R.lo; a.hi = R.hi; a.E = h->E; a.M_last = h->M_last;
@@ -916,11 +920,8 @@ static int loss_multi(f2c_dcp *h, const uint8_t *x, const int64_t *labels, const
     for (size_t q = 0; q < h->ranks.size(); ++q) {
         Rank &R = h->ranks[q];
         CombineArgs a = combine_args(h, R, ctx[q], occ_local(h, R), nullptr);
-        k_finalize_multi<<<static_cast<unsigned>((N + CB_ROWS - 1) / CB_ROWS), 256, 0, st>>>(a, R.at<float4>(R.L.rs_all), W, N,
-                                                                   R.at<float>(R.L.dx_part));
-        LAUNCH_CHECK();
-        k_loss<<<1, 1024, 0, st>>>(R.at<double>(R.L.rowloss), R.at<int>(R.L.comp_idx), N, R.sc(), loss,
-                                   static_cast<double>(h->lam));
+        k_finalize_multi<<<static_cast<unsigned>((N + CB_ROWS - 1) / CB_ROWS), 256, 0, st>>>(
+            a, R.at<float4>(R.L.rs_all), W, N, R.at<float>(R.L.dx_part), loss);
         LAUNCH_CHECK();
     }
     if (h->emulated) {
@@ -969,15 +970,12 @@ extern "C" int f2c_dcp_loss_fwd_bwd(f2c_dcp *h, const void *x, const int64_t *la
     const Layout &L = R.L;
     StepCtx c{n_local, s, m, static_cast<const uint8_t *>(x), labels, pairing, st};
     h->last_N = c.N;
-    if ((rc = phase_resolve(h, R, c))) return rc;
-    if ((rc = phase_compact(h, R, c, &R.sc()->tmax_bits))) return rc;
+    if ((rc = phase_resolve(h, R, c, false))) return rc;
+    if ((rc = phase_compact(h, R, c, &R.sc()->tmax_bits, true))) return rc;
     const int64_t occ = occ_local(h, R);
     if ((rc = phase_main(h, R, c, occ))) return rc;
     CombineArgs a = combine_args(h, R, c, occ, static_cast<uint8_t *>(dx));
-    k_combine<<<static_cast<unsigned>((c.N + CB_ROWS - 1) / CB_ROWS), 256, 0, st>>>(a);
-    LAUNCH_CHECK();
-    k_loss<<<1, 1024, 0, st>>>(R.at<double>(L.rowloss), R.at<int>(L.comp_idx), c.N, R.sc(), loss,
-                               static_cast<double>(h->lam));
+    k_combine<<<static_cast<unsigned>((c.N + CB_ROWS - 1) / CB_ROWS), 256, 0, st>>>(a, loss);
     LAUNCH_CHECK();
     return F2C_OK;
 }

@@ -29,6 +29,7 @@ struct Scalars {          // lives at the start of the per-rank scratch
     double loss3[3];      // L, L_ce, L_cos (fp64) of the last loss call
     unsigned long long n_pos_sum;  // sum of n_pos over loss calls (bench accounting)
     long long n_app;      // rows appended by the last refresh-in-place enqueue (NEXT-3)
+    unsigned loss_done;   // CTAs of the final per-row kernel done (the last one sums the loss)
 };
 
 __device__ __forceinline__ void latch(Scalars *s, int code, int detail) {
@@ -579,7 +580,10 @@ __global__ void k_dup_fill(const int64_t *__restrict__ lab, int64_t n_occ_loc, i
 // the pairing check (D13), and the mu row (index N_pos) with coefficients (0, 0) so
 // that the main kernel's p = 2^0 = 1 gives sum_c T_c.
 struct CompactArgs {
-    const int64_t *tseq;      // [N] global write index of the target or -1
+    int64_t *tseq;            // [N] global write index of the target or -1 (written here when
+                              // hslot/hvals are given: W = 1 resolves inside this kernel)
+    const int *rs_hslot;      // [N] or null
+    const unsigned long long *rs_hvals;  // [H] or null
     const float *inv_n;       // [N]
     const int32_t *pairing;   // [N] or null
     int64_t N, C, lo, hi, E, M_last;
@@ -613,9 +617,16 @@ __global__ void __launch_bounds__(1024) k_compact(CompactArgs a) {
     const int tid = threadIdx.x, nt = blockDim.x;
     const int lane = tid & 31, w = tid >> 5;
     const int64_t c0 = static_cast<int64_t>(blockIdx.x) * nt;
+    // target write index of row i: resolved here from the label hash (W = 1), or given (W > 1,
+    // after the MAX all-reduce)
+    auto tseq_of = [&](int64_t i) -> int64_t {
+        if (!a.rs_hslot) return a.tseq[i];
+        const int h = a.rs_hslot[i];
+        return h < 0 ? -1 : static_cast<int64_t>(a.rs_hvals[h]) - 1;
+    };
     int cnt = 0, before = 0;
     for (int64_t i = tid; i < a.N; i += nt) {
-        const int f = a.tseq[i] >= 0;
+        const int f = tseq_of(i) >= 0;
         cnt += f;
         before += (i < c0) ? f : 0;
     }
@@ -645,7 +656,8 @@ __global__ void __launch_bounds__(1024) k_compact(CompactArgs a) {
     // this CTA's chunk, one row per thread; k = in-pool rows before row i (ballot scan)
     {
         const int64_t i = c0 + tid;
-        const int64_t ts = i < a.N ? a.tseq[i] : -1;
+        const int64_t ts = i < a.N ? tseq_of(i) : -1;
+        if (a.rs_hslot && i < a.N) a.tseq[i] = ts;  // (row_stats reads it)
         const bool f = i < a.N && ts >= 0;
         const unsigned bal = __ballot_sync(0xffffffffu, f);
         __syncthreads();  // (wsum reuse)
@@ -949,11 +961,55 @@ __device__ __forceinline__ void jacobian(const float (&g)[16], const float (&xh)
     for (int q = 0; q < 16; ++q) out[q] = (g[q] - gd * xh[q]) * inv;
 }
 
-__global__ void __launch_bounds__(256, 2) k_combine(CombineArgs a) {
-    clear_hash_slice(a, gridDim.x);
+// a6: the loss from the per-row terms, by the LAST CTA of the final per-row kernel to finish
+// (fixed-order fp64 sums, so deterministic): L_ce = (1/N_pos) sum ell_i, L_cos =
+// (1/N_neg) sum phi_i, L = L_ce + lambda L_cos (D11; lambda S:408).
+// Replaces a separate one-CTA launch.
+__device__ __forceinline__ void loss_tail(const CombineArgs &a, float *loss) {
+    __shared__ double sa[256], sb[256];
+    __shared__ bool last;
+    __syncthreads();  // every row of this CTA has its rowloss written
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(&a.sc_w->loss_done, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    const int tid = threadIdx.x;
+    double ce = 0.0, cs = 0.0;
+    for (int64_t i = tid; i < a.N; i += blockDim.x) {
+        const double v = __ldcg(a.rowloss + i);
+        if (a.comp_idx[i] >= 0) ce += v;
+        else cs += v;
+    }
+    sa[tid] = ce;
+    sb[tid] = cs;
+    __syncthreads();
+    for (int s2 = blockDim.x / 2; s2; s2 >>= 1) {
+        if (tid < s2) {
+            sa[tid] += sa[tid + s2];
+            sb[tid] += sb[tid + s2];
+        }
+        __syncthreads();
+    }
+    if (tid == 0) {
+        Scalars *sc = a.sc_w;
+        const int np = sc->n_pos, nn = sc->n_neg;
+        const double Lce = np > 0 ? sa[0] / np : 0.0;
+        const double Lcos = nn > 0 ? sb[0] / nn : 0.0;
+        const double L = Lce + static_cast<double>(a.lam) * Lcos;
+        sc->loss3[0] = L;
+        sc->loss3[1] = Lce;
+        sc->loss3[2] = Lcos;
+        *loss = static_cast<float>(L);
+        if (!isfinite(L)) latch(sc, ERR_DEVICE, DET_NONFINITE);
+        sc->loss_done = 0u;  // for the next call
+    }
+}
+
+__device__ __forceinline__ void combine_row(const CombineArgs &a, int64_t i) {
     const int lane = threadIdx.x & 31;
-    const int64_t i = static_cast<int64_t>(blockIdx.x) * CB_ROWS + (threadIdx.x >> 5);
-    if (i >= a.N) return;
     const int n_pos = a.sc->n_pos, n_neg = a.sc->n_neg;
     const int n_rg = (a.sc->n_rows + a.rows_per_group - 1) / a.rows_per_group;
     const int k = a.comp_idx[i];
@@ -1044,6 +1100,13 @@ __global__ void __launch_bounds__(256, 2) k_combine(CombineArgs a) {
     if (lane == 0) a.rowloss[i] = row_loss;
 }
 
+__global__ void __launch_bounds__(256, 2) k_combine(CombineArgs a, float *loss) {
+    clear_hash_slice(a, gridDim.x);
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * CB_ROWS + (threadIdx.x >> 5);
+    if (i < a.N) combine_row(a, i);
+    loss_tail(a, loss);
+}
+
 // ------------------------------------------------------------------ multi-rank combine
 // Per global row i, this rank's partial of the softmax statistics over its slot shard:
 //   in-pool rows:     (l_rest_r, max_r, ttgt_r, b_r)  (ttgt_r = -inf unless rank r owns t_i)
@@ -1098,12 +1161,9 @@ __global__ void __launch_bounds__(256, 2) k_local_rows(CombineArgs a, float4 *__
 // reduce-scatter (C4):
 //   in-pool:     g_r = (s/N_pos) (O_r / l - [r owns t] (l_rest / l) T_t)
 //   out-of-pool: g_r = mu_r / (N_neg C_occ)
-__global__ void __launch_bounds__(256, 2) k_finalize_multi(CombineArgs a, const float4 *__restrict__ scal_all,
-                                                        int W, int64_t N, float *__restrict__ dx_part) {
-    clear_hash_slice(a, gridDim.x);
+__device__ __forceinline__ void finalize_row(const CombineArgs &a, const float4 *__restrict__ scal_all, int W,
+                                             int64_t N, float *__restrict__ dx_part, int64_t i) {
     const int lane = threadIdx.x & 31;
-    const int64_t i = static_cast<int64_t>(blockIdx.x) * CB_ROWS + (threadIdx.x >> 5);
-    if (i >= N) return;
     const int n_pos = a.sc->n_pos, n_neg = a.sc->n_neg;
     const int n_rg = (a.sc->n_rows + a.rows_per_group - 1) / a.rows_per_group;
     const int k = a.comp_idx[i];
@@ -1197,6 +1257,14 @@ __global__ void __launch_bounds__(256, 2) k_finalize_multi(CombineArgs a, const 
     if (lane == 0) a.rowloss[i] = row_loss;
 }
 
+__global__ void __launch_bounds__(256, 2) k_finalize_multi(CombineArgs a, const float4 *__restrict__ scal_all,
+                                                        int W, int64_t N, float *__restrict__ dx_part, float *loss) {
+    clear_hash_slice(a, gridDim.x);
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * CB_ROWS + (threadIdx.x >> 5);
+    if (i < N) finalize_row(a, scal_all, W, N, dx_part, i);
+    loss_tail(a, loss);
+}
+
 __global__ void k_cast_bf16(const float *__restrict__ src, __nv_bfloat16 *__restrict__ dst, int64_t n) {
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x)
@@ -1230,40 +1298,5 @@ __global__ void k_unpack_tseq(const int64_t *__restrict__ ext, int64_t N, int64_
     }
 }
 
-// ------------------------------------------------------------------ a6: loss reduction
-// L = (1/N_pos) sum ell + lambda (1/N_neg) sum phi in fp64, fixed order (deterministic);
-// also clears the label hash table for the next call.
-__global__ void __launch_bounds__(1024) k_loss(const double *__restrict__ rowloss,
-                                               const int *__restrict__ comp_idx, int64_t N,
-                                               Scalars *sc, float *loss, double lam) {
-    __shared__ double sa[1024], sb[1024];
-    const int tid = threadIdx.x;
-    double ce = 0.0, cs = 0.0;
-    for (int64_t i = tid; i < N; i += 1024) {
-        if (comp_idx[i] >= 0) ce += rowloss[i];
-        else cs += rowloss[i];
-    }
-    sa[tid] = ce;
-    sb[tid] = cs;
-    __syncthreads();
-    for (int s = 512; s; s >>= 1) {
-        if (tid < s) {
-            sa[tid] += sa[tid + s];
-            sb[tid] += sb[tid + s];
-        }
-        __syncthreads();
-    }
-    if (tid == 0) {
-        const int np = sc->n_pos, nn = sc->n_neg;
-        const double Lce = np > 0 ? sa[0] / np : 0.0;
-        const double Lcos = nn > 0 ? sb[0] / nn : 0.0;
-        const double L = Lce + lam * Lcos;  // lambda = 1: P:170; NEXT-3 weight
-        sc->loss3[0] = L;
-        sc->loss3[1] = Lce;
-        sc->loss3[2] = Lcos;
-        *loss = static_cast<float>(L);
-        if (!isfinite(L)) latch(sc, ERR_DEVICE, DET_NONFINITE);
-    }
-}
 
 }  // namespace f2c
