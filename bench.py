@@ -125,11 +125,11 @@ def run_reference(args, cfg, world):
     print(json.dumps(line), flush=True)
 
 
-def _config(cfg, world, ema_overlap=True):
+def _config(cfg, world, ema_overlap=True, K=1):
     return {"workload": cfg.name, "model": "DCP head (F2C)", "C": cfg.C, "C_per_gpu": cfg.C // world,
             "d": cfg.d, "global_batch": cfg.N_loc() * world, "M_glob": cfg.M_glob(world),
             "n_id": cfg.n_id, "s": cfg.s, "m": cfg.m, "pair_noise_sigma": cfg.sigma,
-            "ema_params": EMA_PARAMS, "parallelism": f"slot-range sharded pool x{world}",
+            "ema_params": EMA_PARAMS, "K": K, "parallelism": f"slot-range sharded pool x{world}",
             "l2_hygiene": "inputs larger than L2 (the pool streams through L2 every step)",
             "prefill": "normalised Gaussian rows + uniform labels through the enqueue kernel (D20)",
             "ema_stream": ("low-priority side stream, after the step's loss (overlaps the next step's "
@@ -200,8 +200,9 @@ def run_ours(args, cfg, world, rank, local_rank, device_only=False):
             t = torch.zeros(128, dtype=torch.uint8, device=dev)
         dist.broadcast(t, 0)
         uid = bytes(t.cpu().tolist())
+    K = args.K
     head = dcp.DCPHead(cfg.C, d, dcp.BF16, world, rank if world > 1 else 0, n_local_max=N_loc,
-                       m_local_max=M, nccl_uid=uid, device=dev)
+                       m_local_max=M, nccl_uid=uid, device=dev, K=K)
     # the head runs on a high-priority stream; the G-Net EMA (a10, independent of the head's
     # data) on a low-priority side stream, after the step's loss, so that it overlaps the
     # head's latency-bound kernels of the next step instead of extending the step
@@ -215,8 +216,8 @@ def run_ours(args, cfg, world, rank, local_rank, device_only=False):
     gen.manual_seed(cfg.seed * 1000 + rank)
     nblk = cfg.prefill_blocks(world)
     for b in range(nblk):
-        gb = torch.randn(M, d, device=dev, generator=gen)
-        gb = (gb / gb.norm(dim=1, keepdim=True)).to(torch.bfloat16)
+        gb = torch.randn(M, K, d, device=dev, generator=gen) if K > 1 else torch.randn(M, d, device=dev, generator=gen)
+        gb = (gb / gb.norm(dim=-1, keepdim=True)).to(torch.bfloat16)
         yb = torch.randint(0, cfg.n_id, (M,), device=dev, generator=gen)
         head.enqueue(gb, yb)
     torch.cuda.synchronize()
@@ -227,7 +228,11 @@ def run_ours(args, cfg, world, rank, local_rank, device_only=False):
     for t in range(R):
         s = synth.step_inputs(cfg, t, rank, world)
         hx = torch.from_numpy(s.x.view(np.int16)).view(torch.bfloat16).pin_memory()
-        hg = torch.from_numpy(s.g.view(np.int16)).view(torch.bfloat16).pin_memory()
+        g = s.g
+        if K > 1:  # K features per identity (NEXT-1): the G-Net pair plus K-1 more noisy copies
+            g = np.stack([s.g] + [synth.pair_rows(cfg.seed, 1_000_000 * k + t, rank * M, M, d, cfg.sigma)[1]
+                                  for k in range(1, K)], axis=1)
+        hg = torch.from_numpy(np.ascontiguousarray(g).view(np.int16)).view(torch.bfloat16).pin_memory()
         hy = torch.from_numpy(s.y).pin_memory()
         hp = torch.from_numpy(s.pairing).pin_memory()
         hgy = torch.from_numpy(s.gy).pin_memory()
@@ -314,7 +319,7 @@ def run_ours(args, cfg, world, rank, local_rank, device_only=False):
         return {"workload": cfg.name, "value": value, "unit": UNIT, "ms_per_step": ms / K,
                 "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                              "frac": achieved / peak, "avg_launch_ms": t_launch * 1e3, "N_pos_avg": npos_avg},
-                "clocks": clocks, "config": _config(cfg, world, args.ema_overlap)}
+                "clocks": clocks, "config": _config(cfg, world, args.ema_overlap, args.K)}
 
     # ---- end-to-end through the public API with host buffers (e2e)
     loss_host = torch.zeros((), dtype=torch.float32).pin_memory()
@@ -355,7 +360,7 @@ def run_ours(args, cfg, world, rank, local_rank, device_only=False):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
         "warmup": args.warmup, "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "bf16", "data": "synthetic", "config": _config(cfg, world, args.ema_overlap),
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic", "config": _config(cfg, world, args.ema_overlap, args.K),
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": "dcp_pc_kernel (producer: TMEM-A logits GEMM + softmax -> DSMEM P; consumer: P x pool GEMM, O in TMEM)",
@@ -471,6 +476,7 @@ def main():
                     help="c1 | c2 | c3 | c4r_<pct>_<global batch> (one rank of a W=8 c4 point) | "
                          "c3r_<W> (one rank of c3 at W GPUs, collectives excluded)")
     ap.add_argument("--ring", type=int, default=8)
+    ap.add_argument("--K", type=int, default=1, help="features per pool slot (NEXT-1; the paper's default is 2)")
     ap.add_argument("--ema-overlap", type=int, default=1,
                     help="1: G-Net EMA on a low-priority side stream (overlaps the head's small kernels)")
     ap.add_argument("--no-cpu-baseline", action="store_true")

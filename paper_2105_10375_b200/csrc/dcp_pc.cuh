@@ -42,8 +42,12 @@ constexpr int PCQ_OFF_P = 0;                              // 2 x 32 KB P slots
 constexpr int PCQ_OFF_T = PCQ_OFF_P + 2 * PC_PBYTES;      // 2 x 64 KB pool stages
 constexpr int PCQ_OFF_AUX = PCQ_OFF_T + PC_Q_NSTAGE * PC_STAGE_BYTES;
 constexpr int PC_OFF_AUX = PCP_OFF_AUX > PCQ_OFF_AUX ? PCP_OFF_AUX : PCQ_OFF_AUX;
+// producer: the mu row's weight ring (K >= 2), PC_WRING x 128 bf16; deep enough that the TMA
+// warp (a tile or two ahead of the softmax warps) never waits on it
+constexpr int PC_WRING = 8;
+constexpr int PC_OFF_WRING = PC_OFF_AUX + 4096;
 // consumer: O-drain staging, one [32 rows x 16 fp32] TMA-store box per drain warp
-constexpr int PC_OFF_OSTG = PC_OFF_AUX + 4096;
+constexpr int PC_OFF_OSTG = PC_OFF_WRING + PC_WRING * 256;
 constexpr int PC_OSTG_BYTES = 8 * 2048;
 constexpr int PC_SMEM_BYTES = PC_OFF_OSTG + PC_OSTG_BYTES + 1024;   // with the drain staging
 constexpr int PC_SMEM_BYTES_NOSTG = PC_OFF_OSTG + 1024;            // without it
@@ -78,6 +82,7 @@ struct PCAux {
     uint64_t xready, xfree;
     uint64_t pready[2], pstage_free[2];
     uint64_t pslot_free[2];            // arrived by the consumer's multicast commit
+    uint64_t wfull[PC_WRING], wempty[PC_WRING];  // the mu row's weight ring (K >= 2)
     // consumer
     uint64_t qfull[PC_Q_NSTAGE], qempty[PC_Q_NSTAGE];
     uint64_t pfull[2];                 // complete_tx by the producer's bulk copy
@@ -102,7 +107,8 @@ struct PCParams {
     const float2 *row_ab;  // [R_max] (a_r, b_r)
     const int *row_tgt;    // [R_max] local target slot or -1
     const uint8_t *X_pos;  // [R_max, d] bf16 compacted rows
-    const float *wslot;    // K >= 2: per-slot 1/||T_bar_c|| weights of the mu row (else null)
+    const float *wslot;    // K >= 2: per-slot 1/||T_bar_c|| (NEXT-3 out-of-pool rows; else null)
+    const __nv_bfloat16 *wmu;  // K >= 2: the same weights in bf16, the mu row's P (padded to a tile)
     float margin_l2;       // s * m * log2(e)
     float *ttgt;           // [R_max]
     float *seg_l;          // [S][128]
@@ -332,6 +338,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
         }
         mbar_init(&aux->ofull, 1);
         mbar_init(&aux->oempty, 8);
+        for (int i = 0; i < PC_WRING; ++i) {
+            mbar_init(&aux->wfull[i], 1);
+            mbar_init(&aux->wempty[i], 2);  // the mu row's two threads (slot halves)
+        }
         if (crank == 1 && !(p.dbg_flags & 128)) {  // arm both P slots before the producer can copy into them
             mbar_arrive_expect_tx(&aux->pfull[0], PC_PBYTES);
             mbar_arrive_expect_tx(&aux->pfull[1], PC_PBYTES);
@@ -368,8 +378,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
             // -------- TMA: pool stages [cps chunks x 128 slots x 64 d] (3D box)
             if (lane == 0) {
                 uint32_t pc = 0;
+                uint32_t wc_n = 0;
                 while (sch.next(rg, t0, t1, seg)) {
-                    for (int t = t0; t < t1; ++t)
+                    const bool wmu = p.wmu != nullptr && rg == n_pos / PC_R;
+                    for (int t = t0; t < t1; ++t) {
+                        if (wmu) {  // the mu row's bf16 weights of tile t (256 B) -> weight ring
+                            const uint32_t wb = wc_n % PC_WRING;
+                            mbar_wait(&aux->wempty[wb], ((wc_n / PC_WRING) & 1) ^ 1);
+                            mbar_arrive_expect_tx(&aux->wfull[wb], 256);
+                            asm volatile(
+                                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 256, [%2];" ::"r"(
+                                    smem_u32(smem + PC_OFF_WRING + wb * 256)),
+                                "l"(reinterpret_cast<uint64_t>(p.wmu + static_cast<size_t>(t) * PC_TILE)),
+                                "r"(smem_u32(&aux->wfull[wb]))
+                                : "memory");
+                            ++wc_n;
+                        }
                         for (int g = 0; g < nstg_p; ++g, ++pc) {
                             const uint32_t st = pc % PC_P_NSTAGE, ph = (pc / PC_P_NSTAGE) & 1;
                             mbar_wait(&aux->tempty[st], ph ^ 1);
@@ -381,6 +405,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                             const int tl = (p.dbg_flags & 16384) ? (t & 15) : t;  // 16384: hot tiles (experiment)
                             tma_load_3d(sT + st * PC_P_STAGE_BYTES, &tm3p, &aux->tfull[st], 0, tl * PC_TILE, g * cps_p);
                         }
+                    }
                 }
             }
         } else if (warp == 9) {
@@ -465,7 +490,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
             const int q = warp & 3, h = warp >> 2;
             const int r = q * 32 + lane;
             const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
-            uint32_t jt = 0, sg = 0;
+            uint32_t jt = 0, sg = 0, wc_n = 0;
             while (sch.next(rg, t0, t1, seg)) {
                 const int row = rg * PC_R + r;
                 const float2 ab = p.row_ab[row];
@@ -494,6 +519,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                 if (lane == 0) mbar_arrive(&aux->xready);
                 float lacc = 0.f, mx = -INFINITY;
                 int barg = -1;
+                const bool wmu = p.wmu != nullptr && rg == n_pos / PC_R;  // this unit holds the mu row
                 // NEXT-3: out-of-pool rows compacted after the mu row (a = 1/||x||, b = 0)
                 const bool negrow = p.neg_mode != 0 && row > n_pos && row < n_rows;
                 for (int t = t0; t < t1; ++t, ++jt) {
@@ -569,11 +595,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                                 }
                             }
                         }
-                        if (p.wslot && row == n_pos) {  // mu row with K >= 2: p_c = 1/||T_bar_c||
-#pragma unroll
-                            for (int k = 0; k < 64; ++k)
-                                e[k] = k < nval ? __log2f(fmaxf(p.wslot[base + k], 1e-30f)) : -INFINITY;
-                        }
                         // 2-wide packed sums (FADD2) and 3-input max (FMNMX3), 4 chains each for ILP
                         float la[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
                         float ma[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
@@ -587,6 +608,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                         }
                         lacc += ((la[0] + la[1]) + (la[2] + la[3])) + ((la[4] + la[5]) + (la[6] + la[7]));
                         mx = fmaxf(mx, fmaxf(fmaxf(ma[0], ma[1]), fmaxf(ma[2], ma[3])));
+                        if (wmu && row == n_pos) {
+                            // mu row with K >= 2: p_c = 1/||T_bar_c||, bf16 weights of this tile staged in
+                            // smem by the TMA warp (its l and max are unused)
+                            const uint32_t wb = wc_n % PC_WRING;
+                            mbar_wait(&aux->wfull[wb], (wc_n / PC_WRING) & 1);
+                            const uint4 *src = reinterpret_cast<const uint4 *>(smem + PC_OFF_WRING + wb * 256 + h * 128);
+#pragma unroll
+                            for (int u = 0; u < 8; ++u) {
+                                const uint4 v = src[u];
+                                w[4 * u] = v.x; w[4 * u + 1] = v.y; w[4 * u + 2] = v.z; w[4 * u + 3] = v.w;
+                            }
+                            if (nval < 64)  // slots past the occupied range
+#pragma unroll
+                                for (int k = 0; k < 64; k += 2)
+                                    w[k >> 1] = (k < nval ? (w[k >> 1] & 0xffffu) : 0u) |
+                                                (k + 1 < nval ? (w[k >> 1] & 0xffff0000u) : 0u);
+                            mbar_arrive(&aux->wempty[wb]);
+                            ++wc_n;
+                        }
                     } else {
                         // cosine c = <x_hat, T_bar_c> w_c (w_c = 1 for K = 1; zero centers are
                         // no candidates for the max and contribute 0 to the hinge)

@@ -103,7 +103,7 @@ struct Layout {
     size_t T, lab, sc, x_all, y_all, pair_all, blk_x, blk_y, inv_n, hslot, hkeys, hvals, tseq,
         comp_idx, pos_row, X_pos, row_ab, row_tgt, ttgt, seg_l, seg_mx, seg_O, rowloss, st_lse,
         st_cos, st_phi, st_ell, seg_arg, rs_buf, rs_all, dx_part, tseq_ext, dx32, tmax_glob, mu_buf, Traw, wslot,
-        hgseq, row_hent, dup_cnt, dup_off, dup_list, ekeys, evals, ehslot, rseq, dst_seq, total;
+        hgseq, row_hent, dup_cnt, dup_off, dup_list, ekeys, evals, ehslot, rseq, dst_seq, wmu, total;
     int64_t C_loc, N, Mg, R_max, S_max;
     int H, He;
 };
@@ -171,6 +171,8 @@ static Layout make_layout(int64_t C, int d, int dtype, int W, int rank, int64_t 
     // K >= 2: raw features [C_loc][K][d] (state) and 1/||T_bar_c|| (the T region holds T_bar)
     L.Traw = take(K > 1 ? static_cast<size_t>(L.C_loc) * K * d * es : 0, 1024);
     L.wslot = take(K > 1 ? static_cast<size_t>(L.C_loc) * 4 : 0);
+    // the same weights in bf16 (the mu row's P in the fused kernel), padded by one tile of zeros
+    L.wmu = take(K > 1 ? static_cast<size_t>(L.C_loc + 128) * 2 : 0);
     // NEXT-3 stale self-duplicate lists (f2c_dcp_set_dup_mode): per hash entry the target
     // write index, per compacted row its hash entry, per 128-slot tile a count / offset, and
     // at most one (slot, entry) pair per local slot
@@ -515,7 +517,8 @@ static int enqueue_rank(f2c_dcp *h, Rank &R, const uint8_t *g, const int64_t *y,
         k_enqueue_k<<<static_cast<unsigned>(blocks), 256, 0, st>>>(
             reinterpret_cast<const __nv_bfloat16 *>(g), y, m_glob, h->K, h->d, h->E, h->C, R.lo, R.hi,
             R.at<__nv_bfloat16>(R.L.Traw), R.at<__nv_bfloat16>(R.L.T), R.at<float>(R.L.wslot),
-            R.at<int64_t>(R.L.lab), R.sc(), h->refresh ? R.at<int64_t>(R.L.dst_seq) : nullptr);
+            R.at<__nv_bfloat16>(R.L.wmu), R.at<int64_t>(R.L.lab), R.sc(),
+            h->refresh ? R.at<int64_t>(R.L.dst_seq) : nullptr);
         LAUNCH_CHECK();
         return F2C_OK;
     }
@@ -763,6 +766,7 @@ static int phase_main(f2c_dcp *h, Rank &R, const StepCtx &c, int64_t occ_loc) {
         q.row_tgt = p.row_tgt;
         q.X_pos = R.base + L.X_pos;
         q.wslot = h->K > 1 ? R.at<float>(L.wslot) : nullptr;
+        q.wmu = h->K > 1 ? R.at<__nv_bfloat16>(L.wmu) : nullptr;
         q.margin_l2 = p.margin_l2;
         q.ttgt = p.ttgt;
         q.seg_l = p.seg_l;
@@ -1098,7 +1102,7 @@ extern "C" int f2c_dcp_set_state(f2c_dcp *h, const void *feats_host, const int64
         if (occ > 0 && h->K > 1) {
             k_rebuild_k<<<static_cast<unsigned>((occ * 32 + 255) / 256), 256>>>(
                 R.at<__nv_bfloat16>(R.L.Traw), occ, h->K, h->d, R.at<__nv_bfloat16>(R.L.T),
-                R.at<float>(R.L.wslot), R.sc());
+                R.at<float>(R.L.wslot), R.at<__nv_bfloat16>(R.L.wmu), R.sc());
             CUDA_TRY(cudaGetLastError());
         } else if (occ > 0) {
             k_pool_norm_max<<<static_cast<unsigned>((occ * 32 + 255) / 256), 256>>>(

@@ -138,8 +138,8 @@ __global__ void __launch_bounds__(256) k_enqueue_k(const __nv_bfloat16 *__restri
                                                    int64_t m_glob, int K, int d, int64_t E, int64_t C,
                                                    int64_t lo, int64_t hi, __nv_bfloat16 *__restrict__ Traw,
                                                    __nv_bfloat16 *__restrict__ Tbar, float *__restrict__ wslot,
-                                                   int64_t *__restrict__ lab, Scalars *sc,
-                                                   const int64_t *__restrict__ dst_seq) {
+                                                   __nv_bfloat16 *__restrict__ wmu, int64_t *__restrict__ lab,
+                                                   Scalars *sc, const int64_t *__restrict__ dst_seq) {
     __shared__ float wmax[8];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
@@ -184,7 +184,9 @@ __global__ void __launch_bounds__(256) k_enqueue_k(const __nv_bfloat16 *__restri
         for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
         if (lane == 0) {
             lab[c - lo] = yl;
-            wslot[c - lo] = ss > 0.f ? rsqrtf(ss) : 0.f;
+            const float wv = ss > 0.f ? rsqrtf(ss) : 0.f;
+            wslot[c - lo] = wv;
+            wmu[c - lo] = __float2bfloat16_rn(wv);
         }
         nmax = fmaxf(nmax, ss);
     }
@@ -202,7 +204,7 @@ __global__ void __launch_bounds__(256) k_enqueue_k(const __nv_bfloat16 *__restri
 // set_state with K >= 2: rebuild T_bar, w and the norm bound from the raw features
 __global__ void __launch_bounds__(256) k_rebuild_k(const __nv_bfloat16 *__restrict__ Traw, int64_t rows, int K, int d,
                                                    __nv_bfloat16 *__restrict__ Tbar, float *__restrict__ wslot,
-                                                   Scalars *sc) {
+                                                   __nv_bfloat16 *__restrict__ wmu, Scalars *sc) {
     const int lane = threadIdx.x & 31;
     const int64_t r = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     if (r >= rows) return;
@@ -217,7 +219,9 @@ __global__ void __launch_bounds__(256) k_rebuild_k(const __nv_bfloat16 *__restri
 #pragma unroll
     for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
     if (lane == 0) {
-        wslot[r] = ss > 0.f ? rsqrtf(ss) : 0.f;
+        const float wv = ss > 0.f ? rsqrtf(ss) : 0.f;
+        wslot[r] = wv;
+        wmu[r] = __float2bfloat16_rn(wv);
         float nrm = sqrtf(ss);
         if (nrm > 0.f) atomicMax(&sc->tmax_bits, __float_as_int(nrm));
     }

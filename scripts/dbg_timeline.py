@@ -9,15 +9,18 @@ import synth
 from bench import _workload
 cfg = _workload(wl)
 L = load_library()
-head = dcp.DCPHead(cfg.C, cfg.d, 0, 1, 0, n_local_max=cfg.N_loc(), m_local_max=cfg.M_loc)
+K = int(os.environ.get("F2C_TL_K", "1"))
+head = dcp.DCPHead(cfg.C, cfg.d, 0, 1, 0, n_local_max=cfg.N_loc(), m_local_max=cfg.M_loc, K=K)
 gen = torch.Generator(device="cuda"); gen.manual_seed(1)
 for b in range(cfg.prefill_blocks()):
-    g = torch.randn(cfg.M_loc, cfg.d, device="cuda", generator=gen); g = (g / g.norm(dim=1, keepdim=True)).bfloat16()
+    g = torch.randn(cfg.M_loc, K, cfg.d, device="cuda", generator=gen) if K > 1 else torch.randn(cfg.M_loc, cfg.d, device="cuda", generator=gen)
+    g = (g / g.norm(dim=-1, keepdim=True)).bfloat16()
     head.enqueue(g, torch.randint(0, cfg.n_id, (cfg.M_loc,), device="cuda", generator=gen))
 st = synth.step_inputs(cfg, 0)
 x = torch.from_numpy(st.x.view(np.int16)).view(torch.bfloat16).cuda()
 y = torch.from_numpy(st.y).cuda(); pr = torch.from_numpy(st.pairing).cuda()
-head.enqueue(torch.from_numpy(st.g.view(np.int16)).view(torch.bfloat16).cuda(), torch.from_numpy(st.gy).cuda())
+gk = np.stack([st.g] * K, axis=1) if K > 1 else st.g
+head.enqueue(torch.from_numpy(np.ascontiguousarray(gk).view(np.int16)).view(torch.bfloat16).cuda(), torch.from_numpy(st.gy).cuda())
 buf = torch.zeros(64 * 16 + 64, dtype=torch.int64, device="cuda")
 L.f2c_dcp_debug_timestamps.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
 for it in range(3):
