@@ -125,11 +125,22 @@ def run_reference(args, cfg, world):
     print(json.dumps(line), flush=True)
 
 
-def _config(cfg, world, ema_overlap=True, K=1):
+def _variant(args):
+    v = []
+    if args.lcos:
+        v.append(f"lcos={args.lcos}")
+    if args.excl_dup:
+        v.append("exclude-stale-duplicates")
+    if args.refresh:
+        v.append("refresh-in-place enqueue")
+    return ", ".join(v) if v else "default (D8, D10, pure Eq. 7)"
+
+
+def _config(cfg, world, ema_overlap=True, K=1, variant="default (D8, D10, pure Eq. 7)"):
     return {"workload": cfg.name, "model": "DCP head (F2C)", "C": cfg.C, "C_per_gpu": cfg.C // world,
             "d": cfg.d, "global_batch": cfg.N_loc() * world, "M_glob": cfg.M_glob(world),
             "n_id": cfg.n_id, "s": cfg.s, "m": cfg.m, "pair_noise_sigma": cfg.sigma,
-            "ema_params": EMA_PARAMS, "K": K, "parallelism": f"slot-range sharded pool x{world}",
+            "ema_params": EMA_PARAMS, "K": K, "variant": variant, "parallelism": f"slot-range sharded pool x{world}",
             "l2_hygiene": "inputs larger than L2 (the pool streams through L2 every step)",
             "prefill": "normalised Gaussian rows + uniform labels through the enqueue kernel (D20)",
             "ema_stream": ("low-priority side stream, after the step's loss (overlaps the next step's "
@@ -203,6 +214,11 @@ def run_ours(args, cfg, world, rank, local_rank, device_only=False):
     K = args.K
     head = dcp.DCPHead(cfg.C, d, dcp.BF16, world, rank if world > 1 else 0, n_local_max=N_loc,
                        m_local_max=M, nccl_uid=uid, device=dev, K=K)
+    if args.lcos:  # NEXT-3 variants (timing of the variant paths)
+        mode, hinge, lam = args.lcos.split(",")
+        head.set_lcos(int(mode), bool(int(hinge)), float(lam))
+    if args.excl_dup:
+        head.set_dup_mode(True)
     # the head runs on a high-priority stream; the G-Net EMA (a10, independent of the head's
     # data) on a low-priority side stream, after the step's loss, so that it overlaps the
     # head's latency-bound kernels of the next step instead of extending the step
@@ -221,6 +237,8 @@ def run_ours(args, cfg, world, rank, local_rank, device_only=False):
         yb = torch.randint(0, cfg.n_id, (M,), device=dev, generator=gen)
         head.enqueue(gb, yb)
     torch.cuda.synchronize()
+    if args.refresh:  # NEXT-3: refresh-in-place enqueue for the timed steps
+        head.set_enqueue_mode(True)
 
     # ---- per-step inputs: a ring of R seeded steps (synth), pinned host + device copies
     R = args.ring
@@ -319,7 +337,7 @@ def run_ours(args, cfg, world, rank, local_rank, device_only=False):
         return {"workload": cfg.name, "value": value, "unit": UNIT, "ms_per_step": ms / K,
                 "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                              "frac": achieved / peak, "avg_launch_ms": t_launch * 1e3, "N_pos_avg": npos_avg},
-                "clocks": clocks, "config": _config(cfg, world, args.ema_overlap, args.K)}
+                "clocks": clocks, "config": _config(cfg, world, args.ema_overlap, args.K, _variant(args))}
 
     # ---- end-to-end through the public API with host buffers (e2e)
     loss_host = torch.zeros((), dtype=torch.float32).pin_memory()
@@ -360,7 +378,7 @@ def run_ours(args, cfg, world, rank, local_rank, device_only=False):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
         "warmup": args.warmup, "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "bf16", "data": "synthetic", "config": _config(cfg, world, args.ema_overlap, args.K),
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic", "config": _config(cfg, world, args.ema_overlap, args.K, _variant(args)),
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": "dcp_pc_kernel (producer: TMEM-A logits GEMM + softmax -> DSMEM P; consumer: P x pool GEMM, O in TMEM)",
@@ -477,6 +495,9 @@ def main():
                          "c3r_<W> (one rank of c3 at W GPUs, collectives excluded)")
     ap.add_argument("--ring", type=int, default=8)
     ap.add_argument("--K", type=int, default=1, help="features per pool slot (NEXT-1; the paper's default is 2)")
+    ap.add_argument("--lcos", default="", help="NEXT-3 L_cos variant 'phi_mode,hinge,lambda' (e.g. 2,0,1 = max)")
+    ap.add_argument("--excl-dup", action="store_true", help="NEXT-3: exclude stale self-duplicates")
+    ap.add_argument("--refresh", action="store_true", help="NEXT-3: refresh-in-place enqueue")
     ap.add_argument("--ema-overlap", type=int, default=1,
                     help="1: G-Net EMA on a low-priority side stream (overlaps the head's small kernels)")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -101,7 +101,8 @@ struct PCParams {
     int d;                 // feature dim (multiple of 128, <= 512)
     int n_slots;           // occupied slots of this shard
     const int *n_pos;      // device: in-pool rows; the mu row is row *n_pos
-    const int *n_rows;     // device: rows to process (n_pos + 1, or N + 1 with NEXT-3 neg rows)
+    const int *n_rows;     // device: rows to process (n_pos + 1, or neg0 + N_neg with NEXT-3 neg rows)
+    const int *neg0;       // device: first out-of-pool row (NEXT-3 hinge / max)
     int neg_mode;          // 0; 1 = hinge (p = [cos > 0] w_c, l = sum relu(cos)); 2 = max cos
     int *seg_arg;          // [S][128] local argmax slot (neg_mode 2)
     const float2 *row_ab;  // [R_max] (a_r, b_r)
@@ -124,6 +125,7 @@ struct PCParams {
     int drain_tma;         // O drain through smem staging + TMA stores (short units); else direct
                            // stores (launched without the staging smem)
     unsigned long long *dbg;
+    int dbg_cluster;       // the cluster whose per-tile clocks the debug hook records
     int dbg_flags;         // timing experiments only: 1 = skip P smem writes, 128 = skip DSMEM copy,
                            // 4 / 8 = no producer / consumer pool loads, 16 = no softmax arithmetic,
                            // 16384 = every CTA loads only pool tiles 0-15 (L2-hot; same smem traffic),
@@ -308,13 +310,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
     const uint32_t stage_bytes = static_cast<uint32_t>(cps) * 16384;
     const int n_pos = *p.n_pos;
     const int n_rows = *p.n_rows;
+    const int neg0 = *p.neg0;
     const int n_rg = (n_rows + PC_R - 1) / PC_R;
     const int n_tiles = (p.n_slots + PC_TILE - 1) / PC_TILE;
-    if (p.dbg && threadIdx.x == 0 && blockIdx.x < 2) {  // kernel-span clocks (debug hook)
+    if (p.dbg && threadIdx.x == 0 && (blockIdx.x >> 1) == static_cast<unsigned>(p.dbg_cluster)) {  // kernel-span clocks (debug hook)
         unsigned long long gt;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
-        p.dbg[1024 + blockIdx.x * 4] = clock64();
-        p.dbg[1025 + blockIdx.x * 4] = gt;
+        p.dbg[1024 + (blockIdx.x & 1) * 4] = clock64();
+        p.dbg[1025 + (blockIdx.x & 1) * 4] = gt;
     }
 
     if (threadIdx.x == 0) {
@@ -340,7 +343,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
         mbar_init(&aux->oempty, 8);
         for (int i = 0; i < PC_WRING; ++i) {
             mbar_init(&aux->wfull[i], 1);
-            mbar_init(&aux->wempty[i], 2);  // the mu row's two threads (slot halves)
+            mbar_init(&aux->wempty[i], 8);  // every softmax warp of a weight unit
         }
         if (crank == 1 && !(p.dbg_flags & 128)) {  // arm both P slots before the producer can copy into them
             mbar_arrive_expect_tx(&aux->pfull[0], PC_PBYTES);
@@ -380,7 +383,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                 uint32_t pc = 0;
                 uint32_t wc_n = 0;
                 while (sch.next(rg, t0, t1, seg)) {
-                    const bool wmu = p.wmu != nullptr && rg == n_pos / PC_R;
+                    const bool wmu = p.wmu != nullptr &&
+                                     (rg == n_pos / PC_R || (p.neg_mode != 0 && rg * PC_R + PC_R - 1 >= neg0));
                     for (int t = t0; t < t1; ++t) {
                         if (wmu) {  // the mu row's bf16 weights of tile t (256 B) -> weight ring
                             const uint32_t wb = wc_n % PC_WRING;
@@ -419,7 +423,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                     mbar_wait(&aux->xready, sg & 1);
                     tc_fence_after();
                     for (int t = t0; t < t1; ++t, ++jt) {
-                        unsigned long long *dbg = (p.dbg && blockIdx.x == 0 && jt < 64 && lane == 0) ? p.dbg + jt * 16 : nullptr;
+                        unsigned long long *dbg = (p.dbg && blockIdx.x == 2u * p.dbg_cluster && jt < 64 && lane == 0) ? p.dbg + jt * 16 : nullptr;
                         const uint32_t sb = jt & 1, sph = (jt >> 1) & 1;
                         const uint32_t dcol = tmem + S_COL + sb * PC_TILE;
                         if (nstg_p == 4) {  // d = 512: the whole tile in one elected issue
@@ -456,7 +460,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                         const uint32_t b = jt & 1, ph = (jt >> 1) & 1;
                         mbar_wait(&aux->pready[b], ph);
                         mbar_wait(&aux->pslot_free[b], ph ^ 1);
-                        unsigned long long *dbg = (p.dbg && blockIdx.x == 0 && jt < 64) ? p.dbg + jt * 16 : nullptr;
+                        unsigned long long *dbg = (p.dbg && blockIdx.x == 2u * p.dbg_cluster && jt < 64) ? p.dbg + jt * 16 : nullptr;
                         if (dbg) dbg[4] = clock64();
                         const uint32_t dst = mapa_shared(smem_u32(smem + PCQ_OFF_P + b * PC_PBYTES), 1);
                         const uint32_t rbar = mapa_shared(smem_u32(&aux->pfull[b]), 1);
@@ -519,18 +523,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                 if (lane == 0) mbar_arrive(&aux->xready);
                 float lacc = 0.f, mx = -INFINITY;
                 int barg = -1;
-                const bool wmu = p.wmu != nullptr && rg == n_pos / PC_R;  // this unit holds the mu row
+                // K >= 2: this unit's tiles bring their weights through the smem ring (it holds
+                // the mu row, or out-of-pool rows of NEXT-3 hinge / max)
+                const bool wmu = p.wmu != nullptr &&
+                                 (rg == n_pos / PC_R || (p.neg_mode != 0 && rg * PC_R + PC_R - 1 >= neg0));
                 // NEXT-3: out-of-pool rows compacted after the mu row (a = 1/||x||, b = 0)
-                const bool negrow = p.neg_mode != 0 && row > n_pos && row < n_rows;
+                // (the padding rows after n_rows take this path too: zero operands, discarded
+                // results, and no divergence with the last out-of-pool rows of their warp)
+                const bool negrow = p.neg_mode != 0 && row >= neg0;
                 for (int t = t0; t < t1; ++t, ++jt) {
                     const uint32_t sb = jt & 1, sph = (jt >> 1) & 1;
                     mbar_wait(&aux->sfull[sb], sph);
                     tc_fence_after();
-                    unsigned long long *dbg = (p.dbg && blockIdx.x == 0 && jt < 64 && threadIdx.x == 0) ? p.dbg + jt * 16 : nullptr;
+                    unsigned long long *dbg = (p.dbg && blockIdx.x == 2u * p.dbg_cluster && jt < 64 && threadIdx.x == 0) ? p.dbg + jt * 16 : nullptr;
                     if (dbg) dbg[2] = clock64();
                     if (p.dbg_flags & 64) {  // timing experiment: softmax warps only keep the protocol
                         __syncwarp();
                         if (lane == 0) mbar_arrive(&aux->sempty[sb]);
+                        if (wmu) {
+                            mbar_wait(&aux->wfull[wc_n % PC_WRING], (wc_n / PC_WRING) & 1);
+                            __syncwarp();
+                            if (lane == 0) mbar_arrive(&aux->wempty[wc_n % PC_WRING]);
+                            ++wc_n;
+                        }
                         const uint32_t b = jt & 1, ph = (jt >> 1) & 1;
                         if (!(p.dbg_flags & 4096)) {
                             mbar_wait(&aux->pstage_free[b], ph ^ 1);
@@ -556,6 +571,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&aux->sempty[sb]);
+                    if (wmu) mbar_wait(&aux->wfull[wc_n % PC_WRING], (wc_n / PC_WRING) & 1);  // weight ring
                     if (dbg) dbg[8] = clock64();
                     const int base = t * PC_TILE + h * 64;
                     const int nval = p.n_slots - base;  // valid slots in my 64-wide half
@@ -612,7 +628,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                             // mu row with K >= 2: p_c = 1/||T_bar_c||, bf16 weights of this tile staged in
                             // smem by the TMA warp (its l and max are unused)
                             const uint32_t wb = wc_n % PC_WRING;
-                            mbar_wait(&aux->wfull[wb], (wc_n / PC_WRING) & 1);
                             const uint4 *src = reinterpret_cast<const uint4 *>(smem + PC_OFF_WRING + wb * 256 + h * 128);
 #pragma unroll
                             for (int u = 0; u < 8; ++u) {
@@ -624,36 +639,97 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                                 for (int k = 0; k < 64; k += 2)
                                     w[k >> 1] = (k < nval ? (w[k >> 1] & 0xffffu) : 0u) |
                                                 (k + 1 < nval ? (w[k >> 1] & 0xffff0000u) : 0u);
-                            mbar_arrive(&aux->wempty[wb]);
-                            ++wc_n;
                         }
                     } else {
                         // cosine c = <x_hat, T_bar_c> w_c (w_c = 1 for K = 1; zero centers are
-                        // no candidates for the max and contribute 0 to the hinge)
+                        // no candidates for the max and contribute 0 to the hinge).
+                        // Branch-free, four independent max chains (a per-element data-dependent
+                        // branch here made these rows 5.8x slower than the softmax rows).
                         float pv[64];
+                        if (!p.wslot) {
+                            // K = 1: a_r = 1/||x|| > 0 scales every cosine of the row alike, so the
+                            // hinge and the argmax work on the raw products e
 #pragma unroll
-                        for (int k = 0; k < 64; ++k) {
-                            float c = e[k] * ab.x, wc = 1.f;
-                            bool ok = k < nval;
-                            if (p.wslot && ok) {
-                                wc = p.wslot[base + k];
-                                ok = wc > 0.f;
-                                c *= wc;
-                            }
+                            for (int k = 0; k < 64; ++k) e[k] = k < nval ? e[k] : -INFINITY;
                             if (p.neg_mode == 1) {
-                                const bool pos = ok && c > 0.f;
-                                lacc += pos ? c : 0.f;
-                                pv[k] = pos ? wc : 0.f;
-                            } else {
-                                if (ok && c > mx) {
-                                    mx = c;
-                                    barg = base + k;
+                                float s4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+                                for (int k = 0; k < 64; ++k) {
+                                    s4[k & 3] += fmaxf(e[k], 0.f);
+                                    pv[k] = e[k] > 0.f ? 1.f : 0.f;
                                 }
-                                pv[k] = 0.f;
+                                lacc += ((s4[0] + s4[1]) + (s4[2] + s4[3])) * ab.x;
+                            } else {
+                                float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+                                for (int k = 0; k < 64; k += 2) fmax3_acc(m4[(k >> 1) & 3], e[k], e[k + 1]);
+                                const float m = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
+                                int ka = -1;
+#pragma unroll
+                                for (int k = 63; k >= 0; --k) ka = e[k] == m ? k : ka;  // lowest slot on ties
+                                const float c = m * ab.x;
+                                if (ka >= 0 && c > mx) {  // strict: earlier tiles win ties
+                                    mx = c;
+                                    barg = base + ka;
+                                }
+#pragma unroll
+                                for (int k = 0; k < 64; ++k) pv[k] = 0.f;
                             }
+                        } else {
+                        // K >= 2: the tile's weights from the smem ring (bf16 w_c: the hinge decision
+                        // c > 0 does not depend on w_c > 0, and P = w_c is bf16 anyway)
+                        float wv[64];
+                        {
+                            const uint4 *src = reinterpret_cast<const uint4 *>(smem + PC_OFF_WRING +
+                                                                               (wc_n % PC_WRING) * 256 + h * 128);
+#pragma unroll
+                            for (int u = 0; u < 8; ++u) {
+                                const uint4 v = src[u];
+                                const uint32_t q4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                                for (int j = 0; j < 4; ++j) {
+                                    const int k = 8 * u + 2 * j;
+                                    wv[k] = k < nval ? __uint_as_float(q4[j] << 16) : 0.f;
+                                    wv[k + 1] = k + 1 < nval ? __uint_as_float(q4[j] & 0xffff0000u) : 0.f;
+                                }
+                            }
+                        }
+                        // c_k / a_r = e_k w_k (a_r > 0 factored out as in the K = 1 path); zero
+                        // centers (w = 0) are no candidates
+#pragma unroll
+                        for (int k = 0; k < 64; ++k) e[k] = wv[k] > 0.f ? e[k] * wv[k] : -INFINITY;
+                        if (p.neg_mode == 1) {
+                            float s4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+                            for (int k = 0; k < 64; ++k) {
+                                s4[k & 3] += fmaxf(e[k], 0.f);
+                                pv[k] = e[k] > 0.f ? wv[k] : 0.f;
+                            }
+                            lacc += ((s4[0] + s4[1]) + (s4[2] + s4[3])) * ab.x;
+                        } else {
+                            float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+                            for (int k = 0; k < 64; k += 2) fmax3_acc(m4[(k >> 1) & 3], e[k], e[k + 1]);
+                            const float m = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
+                            int ka = -1;
+#pragma unroll
+                            for (int k = 63; k >= 0; --k) ka = e[k] == m ? k : ka;  // lowest slot on ties
+                            const float c = m * ab.x;
+                            if (ka >= 0 && c > mx) {  // strict: earlier tiles win ties
+                                mx = c;
+                                barg = base + ka;
+                            }
+#pragma unroll
+                            for (int k = 0; k < 64; ++k) pv[k] = 0.f;
+                        }
                         }
 #pragma unroll
                         for (int k = 0; k < 64; k += 2) w[k >> 1] = pack_bf16x2(pv[k], pv[k + 1]);
+                    }
+                    if (wmu) {  // this warp is done with the tile's weights
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&aux->wempty[wc_n % PC_WRING]);
+                        ++wc_n;
                     }
                     // P -> staging buffer in the consumer's K-major SW128 A layout:
                     // chunk h = slots [64h, 64h+64), row r: 128 B, 16-B unit u at u ^ (r & 7)
@@ -726,7 +802,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                         const bool first = (t == t0);
                         const uint32_t b = jt & 1, ph = (jt >> 1) & 1;
                         mbar_wait(&aux->pfull[b], ph);
-                        unsigned long long *dbg = (p.dbg && blockIdx.x == 1 && jt < 64 && lane == 0) ? p.dbg + jt * 16 : nullptr;
+                        unsigned long long *dbg = (p.dbg && blockIdx.x == 2u * p.dbg_cluster + 1 && jt < 64 && lane == 0) ? p.dbg + jt * 16 : nullptr;
                         if (dbg) dbg[6] = clock64();
                         if (lane == 0 && !(p.dbg_flags & 128)) mbar_arrive_expect_tx(&aux->pfull[b], PC_PBYTES);  // arm the next use
                         __syncwarp();
@@ -807,11 +883,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
     }
     tc_fence_before();
     __syncthreads();
-    if (p.dbg && threadIdx.x == 0 && blockIdx.x < 2) {
+    if (p.dbg && threadIdx.x == 0 && (blockIdx.x >> 1) == static_cast<unsigned>(p.dbg_cluster)) {
         unsigned long long gt;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
-        p.dbg[1026 + blockIdx.x * 4] = clock64();
-        p.dbg[1027 + blockIdx.x * 4] = gt;
+        p.dbg[1026 + (blockIdx.x & 1) * 4] = clock64();
+        p.dbg[1027 + (blockIdx.x & 1) * 4] = gt;
     }
     cluster_sync_all();
     if (warp == 9) {

@@ -118,7 +118,8 @@ static Layout make_layout(int64_t C, int d, int dtype, int W, int rank, int64_t 
     if (rank < 0) L.C_loc = (C + W - 1) / W;
     L.N = n_loc * W;
     L.Mg = m_loc * W;
-    L.R_max = (L.N + 1 + 127) / 128 * 128;   // row groups of 64 (TP64) or 128 (PC)
+    // row groups of 64 (TP64) or 128 (PC); + 31 for the warp alignment of the NEXT-3 out-of-pool rows
+    L.R_max = (L.N + 32 + 127) / 128 * 128;
     L.S_max = L.R_max / 64 + 2 * G_MAX + 1;  // units R*S <= 2G + R (tp_choose_S)
     int H = 64;
     while (H < 2 * L.N) H <<= 1;
@@ -236,7 +237,8 @@ struct f2c_dcp {
     unsigned long long npos_base = 0;
     unsigned long long *dbg = nullptr;  // debug timestamps (f2c_dcp_debug_timestamps)
     bool use_tp64 = false;
-    int dbg_flags = 0;              // F2C_KERNEL=tp64 selects the single-CTA kernel
+    int dbg_flags = 0;              // timing experiments (F2C_DBG_FLAGS)
+    int dbg_cluster = 0;            // debug timestamps of this cluster (F2C_DBG_CLUSTER)
     ~f2c_dcp() {
         for (cudaEvent_t e : ev) cudaEventDestroy(e);
         if (n_app_host) cudaFreeHost(n_app_host);
@@ -760,6 +762,7 @@ static int phase_main(f2c_dcp *h, Rank &R, const StepCtx &c, int64_t occ_loc) {
         q.n_slots = p.n_slots;
         q.n_pos = p.n_pos;
         q.n_rows = &R.sc()->n_rows;
+        q.neg0 = &R.sc()->neg0;
         q.neg_mode = h->neg_mode();
         q.seg_arg = R.at<int>(L.seg_arg);
         q.row_ab = p.row_ab;
@@ -782,6 +785,7 @@ static int phase_main(f2c_dcp *h, Rank &R, const StepCtx &c, int64_t occ_loc) {
         q.dup_list = R.at<int2>(L.dup_list);
         q.row_hent = R.at<int>(L.row_hent);
         q.dbg = p.dbg;
+        q.dbg_cluster = h->dbg_cluster;
         q.dbg_flags = h->dbg_flags;
         if (q.excl)
             dcp_pc_kernel<true><<<(h->G / 2) * 2, PC_THREADS, smem, c.st>>>(R.tm3p, R.tm3q, R.tmO, q);
@@ -1155,6 +1159,8 @@ extern "C" int f2c_dcp_debug_timestamps(f2c_dcp *h, unsigned long long *dev_buf)
     h->dbg = dev_buf;
     const char *fl = getenv("F2C_DBG_FLAGS");
     h->dbg_flags = fl ? atoi(fl) : 0;
+    const char *cl = getenv("F2C_DBG_CLUSTER");
+    h->dbg_cluster = cl ? atoi(cl) : 0;
     return F2C_OK;
 }
 

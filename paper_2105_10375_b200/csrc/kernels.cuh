@@ -24,6 +24,8 @@ struct Scalars {          // lives at the start of the per-rank scratch
     int tmax_bits;        // max ||T_c|| over rows ever written (float bits, >= 0)
     int n_pos;            // in-pool rows of the last loss call
     int n_neg;
+    int neg0;             // first compacted out-of-pool row (NEXT-3 hinge / max): n_pos + 1 rounded
+                          // up to a warp (32 rows), so no warp mixes softmax rows and cosine rows
     int n_rows;           // compacted rows the main kernel processes (n_pos + 1, or N + 1
                           // when the out-of-pool rows go through it: NEXT-3 hinge / max)
     double loss3[3];      // L, L_ce, L_cos (fp64) of the last loss call
@@ -594,7 +596,7 @@ struct CompactArgs {
     float s, log2e_s;         // s, s*log2(e)
     int R_max;
     int neg_mode;             // 0: mu path; 1 (hinge) / 2 (max): out-of-pool rows are compacted
-                              // after the mu row (index n_pos + 1 + j) and run through the kernel
+                              // after the mu row (index neg0 + j, neg0 = n_pos + 1 rounded up to 32) and run through the kernel
     int *comp_idx;            // [N]: k >= 0 in-pool row k; -1 out-of-pool (mu path); -2 - k
                               // out-of-pool row compacted at k (neg_mode != 0)
     int *pos_row;             // [R_max]
@@ -655,6 +657,7 @@ __global__ void __launch_bounds__(1024) k_compact(CompactArgs a) {
     }
     __syncthreads();
     const int n_pos = s_tot;
+    const int neg0 = a.neg_mode ? (n_pos + 1 + 31) & ~31 : n_pos + 1;
     const float tmax = __int_as_float(*a.tmax_bits);
     const float B = a.ref_scale * tmax;
     // this CTA's chunk, one row per thread; k = in-pool rows before row i (ballot scan)
@@ -679,7 +682,7 @@ __global__ void __launch_bounds__(1024) k_compact(CompactArgs a) {
                 if (!inb || ts != want) latch(a.sc, ERR_PAIRING, DET_PAIRING);
             }
             if (ts < 0 && a.neg_mode) {
-                const int kn = n_pos + 1 + static_cast<int>(i - k);  // i - k = out-of-pool rows before i
+                const int kn = neg0 + static_cast<int>(i - k);  // i - k = out-of-pool rows before i
                 a.comp_idx[i] = -2 - kn;
                 a.pos_row[kn] = static_cast<int>(i);
                 a.row_ab[kn] = make_float2(a.inv_n[i], 0.f);  // e = <x, T> / ||x|| = cosine
@@ -704,21 +707,19 @@ __global__ void __launch_bounds__(1024) k_compact(CompactArgs a) {
     }
     if (blockIdx.x != 0) return;
     // (CTA 0) the mu row and the padding rows of the last row group
-    const int n_rows = a.neg_mode ? static_cast<int>(a.N) + 1 : n_pos + 1;
+    const int n_rows = a.neg_mode ? neg0 + static_cast<int>(a.N) - n_pos : n_pos + 1;
     if (a.excl)
         for (int r = n_pos + tid; r < a.R_max; r += nt) a.row_hent[r] = -1;  // mu, out-of-pool, padding
-    // padding rows: e = -inf, so p = 0 (zero P operand in GEMM 2); the mu row: p = 1
-    for (int r = (a.neg_mode ? n_rows : n_pos) + tid; r < a.R_max; r += nt) {
+    // padding rows (after the mu row up to neg0, and after n_rows): e = -inf, so p = 0 (zero P
+    // operand in GEMM 2); the mu row: p = 1
+    for (int r = n_pos + tid; r < a.R_max; r += nt) {
+        if (r >= neg0 && r < n_rows) continue;  // (out-of-pool rows, written above)
         a.row_ab[r] = make_float2(0.f, r == n_pos ? 0.f : INFINITY);
         a.row_tgt[r] = -1;
         a.ttgt[r] = -INFINITY;
     }
-    if (a.neg_mode && tid == 0) {
-        a.row_ab[n_pos] = make_float2(0.f, 0.f);
-        a.row_tgt[n_pos] = -1;
-        a.ttgt[n_pos] = -INFINITY;
-    }
     if (tid == 0) {
+        a.sc->neg0 = neg0;
         a.sc->n_rows = n_rows;
         a.sc->n_pos = n_pos;
         a.sc->n_neg = static_cast<int>(a.N) - n_pos;
@@ -737,7 +738,7 @@ __global__ void __launch_bounds__(256) k_gather(const uint8_t *__restrict__ x, c
                                                 const int *__restrict__ row_tgt, float2 *__restrict__ row_ab) {
     // one warp per compacted row, 8 rows per CTA
     const int k = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-    if (k >= sc->n_rows || k == sc->n_pos) {
+    if (k >= sc->n_rows || k == sc->n_pos || (k > sc->n_pos && k < sc->neg0)) {
         // the mu row and the padding rows of the last row group: zero operands (their
         // products are discarded; zeros keep the tensor pipe's switching power down)
         if (k < ((sc->n_rows + 127) & ~127)) {

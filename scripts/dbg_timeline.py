@@ -11,6 +11,9 @@ cfg = _workload(wl)
 L = load_library()
 K = int(os.environ.get("F2C_TL_K", "1"))
 head = dcp.DCPHead(cfg.C, cfg.d, 0, 1, 0, n_local_max=cfg.N_loc(), m_local_max=cfg.M_loc, K=K)
+if os.environ.get("F2C_TL_LCOS"):  # e.g. "2,0,1" (NEXT-3 max)
+    m_, h_, l_ = os.environ["F2C_TL_LCOS"].split(",")
+    head.set_lcos(int(m_), bool(int(h_)), float(l_))
 gen = torch.Generator(device="cuda"); gen.manual_seed(1)
 for b in range(cfg.prefill_blocks()):
     g = torch.randn(cfg.M_loc, K, cfg.d, device="cuda", generator=gen) if K > 1 else torch.randn(cfg.M_loc, cfg.d, device="cuda", generator=gen)
