@@ -109,3 +109,48 @@ def test_nccl_transport_single_rank(dcp, monkeypatch):
     assert_dx_close(from_dev(dx), ref.dx)
     feats, labs, E = head.get_state()
     np.testing.assert_array_equal(labs, pool.lab)
+
+
+@pytest.mark.parametrize("K,variant", [(1, "refresh"), (1, "excl"), (2, "max_hinge"), (2, "refresh")])
+def test_nccl_transport_single_rank_variants(dcp, monkeypatch, K, variant):
+    """The NEXT-1 / NEXT-3 variants through the real NCCL transport (1-rank communicator):
+    the refresh-in-place enqueue's residency MAX all-reduce, the stale-duplicate lists built
+    after C2, the hinge / max partials in C3 -- all against the single-pool oracle."""
+    monkeypatch.setenv("F2C_FORCE_MULTI", "1")
+    C, d, m_loc, n = 650, 128, 40, 48
+    head = dcp.DCPHead(C, d, dcp.BF16, world=1, rank=0, n_local_max=n, m_local_max=m_loc, K=K)
+    monkeypatch.delenv("F2C_FORCE_MULTI")
+    pool = oracle.Pool(C, d, oracle.BF16, K=K)
+    if variant == "refresh":
+        head.set_enqueue_mode(True)
+    if variant == "excl":
+        head.set_dup_mode(True)
+    if variant == "max_hinge":
+        head.set_lcos(oracle.PHI_MAX, True, 1.0)
+    rng = np.random.default_rng(40 + K)
+    for b in range(24):
+        G = synth.unit_rows(41, synth.S_PRE, b, 0, m_loc * K, d)
+        if K > 1:
+            # on a 2^-9 grid so the K-mean is exact in bf16 (as in tests/test_gpu_variants.py)
+            G = np.clip(np.rint(oracle.bf16_to_f64(G) * 512), -127, 127) / 512
+            G = oracle.f64_to_bf16(G).reshape(m_loc, K, d)
+        y = rng.choice(200, size=m_loc, replace=False).astype(np.int64)
+        head.enqueue(to_dev(G, synth.BF16), lt(y))
+        pool.enqueue(G, y, refresh=(variant == "refresh"))
+    X = synth.unit_rows(42, synth.S_INST, 0, 0, n, d)
+    y = rng.integers(0, 260, n).astype(np.int64)
+    loss, dx = head.loss_fwd_bwd(to_dev(X, synth.BF16), lt(y), None, 64.0, 0.35)
+    torch.cuda.synchronize()
+    head.check()
+    kw = {}
+    if variant == "excl":
+        kw = dict(excl_dup=True)
+    if variant == "max_hinge":
+        kw = dict(phi_mode=oracle.PHI_MAX, hinge=True)
+    ref = pool.loss(X, y, None, 64.0, 0.35, **kw)
+    assert ref.N_pos > 0 and ref.N_neg > 0
+    assert_loss_close(float(loss.item()), ref.L)
+    assert_dx_close(from_dev(dx), ref.dx)
+    feats, labs, E = head.get_state()
+    assert E == int(pool.E[0])
+    np.testing.assert_array_equal(labs, pool.lab)
