@@ -120,3 +120,14 @@ def test_c3_w8_emulated_full_size_sampled_rows():
     ref = pool.loss_rows(x, y, pr, cfg.s, cfg.m, rows)
     _check(cfg, loss, gdx, rs, ref, rows)
     assert Mg == 4096 and rs["N_pos"] >= Mg
+
+
+@pytest.mark.slow
+def test_c4_largest_batch_rank_shape_sampled_rows():
+    """BJ:11's largest batch at the 10 % pool, as one rank of W=8 computes it: all 16,384 global
+    rows against a 125,000-slot shard (multi-CTA compaction, 129 row groups, one segment per
+    unit); 8 sampled rows against the oracle, properties on all rows."""
+    base = synth.c4_point(0.10, 16384, world=8)
+    cfg = synth.scaled(base, name="c4r_10_16384", C=base.C // 8, M_loc=16384 // 2, n_id=base.n_id // 8)
+    head, loss, gdx, rs, ref, rows = _run(cfg, 8, seed=4)
+    _check(cfg, loss, gdx, rs, ref, rows)

@@ -118,7 +118,7 @@ def _random_pool_blocks(C, d, M, nblk, n_id, seed):
     return out
 
 
-@pytest.mark.parametrize("d", [128, 256, 512])
+@pytest.mark.parametrize("d", [128, 256, 384, 512])
 def test_loss_small_ragged(dcp, d):
     """C not a multiple of the 128-slot tile, N_pos not a multiple of 64, wrap."""
     C, M, n_id = 333, 50, 400
