@@ -43,7 +43,7 @@ if os.environ.get("F2C_KERNEL") == "tp64":
 else:
     P = a[:, :6] - a[0, 0]; Q = a[:, 6:] - a[0, 6]
     print("producer cols: g1_start g1_issued sfull_seen pready copy_issue copy_done | consumer: pfull_seen g2_issued")
-    for j in range(24):
+    for j in range(int(os.environ.get("F2C_TL_ROWS", "24"))):
         print(j, P[j].tolist(), Q[j].tolist())
     n = 40
     for j in range(8):
