@@ -14,6 +14,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges cost nothing without a tool attached
+
 #include "../../include/f2c_dcp.h"
 #include "dcp_main.cuh"
 #include "kernels.cuh"
@@ -21,6 +23,13 @@
 using namespace f2c;
 
 // ============================================================================ errors
+// NVTX range per phase of the hot path (enqueue, resolve, compaction, fused kernel, combine,
+// each collective), visible in Nsight Systems / ncu --nvtx
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+
 static thread_local std::string g_err;
 static thread_local int g_launches = 0;
 
@@ -60,6 +69,7 @@ struct NcclApi {
     int (*GroupStart)() = nullptr;
     int (*GroupEnd)() = nullptr;
     const char *(*GetErrorString)(int) = nullptr;
+    int (*CommGetAsyncError)(nccl_comm_t, int *) = nullptr;
     bool ok = false;
 };
 static NcclApi &nccl() {
@@ -79,6 +89,7 @@ static NcclApi &nccl() {
             api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(h, "ncclGetUniqueId");
             api.GroupEnd = (decltype(api.GroupEnd))dlsym(h, "ncclGroupEnd");
             api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
+            api.CommGetAsyncError = (decltype(api.CommGetAsyncError))dlsym(h, "ncclCommGetAsyncError");
             api.ok = api.CommInitRank && api.AllGather && api.AllReduce && api.ReduceScatter &&
                      api.GroupStart && api.GroupEnd;
         }
@@ -536,6 +547,7 @@ static int enqueue_rank(f2c_dcp *h, Rank &R, const uint8_t *g, const int64_t *y,
 
 extern "C" int f2c_dcp_enqueue(f2c_dcp *h, const void *g_feats, const int64_t *labels,
                                int64_t m_local, void *stream) {
+    NvtxRange nv("f2c_dcp_enqueue (a1)");
     g_launches = 0;
     if (!h) return fail(F2C_EINVAL, "NULL handle");
     if (!g_feats || !labels) return fail(F2C_EINVAL, "NULL g_feats/labels");
@@ -605,6 +617,7 @@ extern "C" int f2c_dcp_enqueue(f2c_dcp *h, const void *g_feats, const int64_t *l
 
 // ============================================================================ EMA
 extern "C" int f2c_gnet_ema(const float *p, float *g, int64_t n, double momentum, void *stream) {
+    NvtxRange nv("f2c_gnet_ema (a10)");
     g_launches = 0;
     if (n < 0) return fail(F2C_ESHAPE, "n < 0");
     if (!(momentum >= 0.0 && momentum <= 1.0)) return fail(F2C_EINVAL, "momentum must be in [0, 1]");
@@ -643,6 +656,7 @@ struct StepCtx {
 
 // a2 + a3: norms, label hash, local target resolve (tseq = newest local seq or -1)
 static int phase_resolve(f2c_dcp *h, Rank &R, const StepCtx &c, bool materialize_tseq = true) {
+    NvtxRange nv("f2c: a2+a3 norms, label hash, target resolve");
     const Layout &L = R.L;
     const unsigned rows_blocks = static_cast<unsigned>((c.N * 32 + 255) / 256);
     if (h->dtype == F2C_BF16)
@@ -676,6 +690,7 @@ static int phase_resolve(f2c_dcp *h, Rank &R, const StepCtx &c, bool materialize
 
 // a3 split + compaction + gather
 static int phase_compact(f2c_dcp *h, Rank &R, const StepCtx &c, const int *tmax_bits, bool resolve_here = false) {
+    NvtxRange nv("f2c: a3 split + compaction + gather");
     const Layout &L = R.L;
     CompactArgs a;
     a.tseq = R.at<int64_t>(L.tseq);
@@ -729,6 +744,7 @@ static int phase_compact(f2c_dcp *h, Rank &R, const StepCtx &c, const int *tmax_
 }
 
 static int phase_main(f2c_dcp *h, Rank &R, const StepCtx &c, int64_t occ_loc) {
+    NvtxRange nv("f2c: a4-a9 fused loss kernel");
     const Layout &L = R.L;
     TPParams p;
     p.d = h->d;
@@ -867,6 +883,7 @@ static int loss_multi(f2c_dcp *h, const uint8_t *x, const int64_t *labels, const
     } else {
         Rank &R = h->ranks[0];
         NcclApi &api = nccl();
+        NvtxRange nvc("f2c: C1 all-gather x, labels, pairing");
         api.GroupStart();
         api.AllGather(x, R.base + R.L.x_all, n_local * rb, NCCL_INT8, h->comm, st);
         api.AllGather(labels, R.base + R.L.y_all, n_local, NCCL_INT64, h->comm, st);
@@ -894,6 +911,7 @@ static int loss_multi(f2c_dcp *h, const uint8_t *x, const int64_t *labels, const
                                      (N + 1) * 8, cudaMemcpyDeviceToDevice, st));
     } else {
         Rank &R = h->ranks[0];
+        NvtxRange nvc("f2c: C2 MAX all-reduce");
         if ((rc = nccl_check(nccl().AllReduce(R.at<int64_t>(R.L.tseq_ext), R.at<int64_t>(R.L.tseq_ext), N + 1,
                                               NCCL_INT64, NCCL_MAX, h->comm, st), "C2 all-reduce")))
             return rc;
@@ -920,6 +938,7 @@ static int loss_multi(f2c_dcp *h, const uint8_t *x, const int64_t *labels, const
                                          cudaMemcpyDeviceToDevice, st));
     } else {
         Rank &R = h->ranks[0];
+        NvtxRange nvc("f2c: C3 all-gather row partials");
         if ((rc = nccl_check(nccl().AllGather(R.at<float4>(R.L.rs_buf), R.at<float4>(R.L.rs_all), N * 4, NCCL_FLOAT32,
                                               h->comm, st), "C3 all-gather")))
             return rc;
@@ -944,6 +963,7 @@ static int loss_multi(f2c_dcp *h, const uint8_t *x, const int64_t *labels, const
         LAUNCH_CHECK();
     } else {
         Rank &R = h->ranks[0];
+        NvtxRange nvc("f2c: C4 reduce-scatter dx");
         if ((rc = nccl_check(nccl().ReduceScatter(R.at<float>(R.L.dx_part), R.at<float>(R.L.dx32), n_local * h->d,
                                                   NCCL_FLOAT32, NCCL_SUM, h->comm, st), "C4 reduce-scatter")))
             return rc;
@@ -957,6 +977,7 @@ static int loss_multi(f2c_dcp *h, const uint8_t *x, const int64_t *labels, const
 extern "C" int f2c_dcp_loss_fwd_bwd(f2c_dcp *h, const void *x, const int64_t *labels,
                                     const int32_t *pairing, int64_t n_local, float s, float m,
                                     float *loss, void *dx, void *stream) {
+    NvtxRange nv("f2c_dcp_loss_fwd_bwd (a2-a9)");
     g_launches = 0;
     if (!h) return fail(F2C_EINVAL, "NULL handle");
     if (!x || !labels || !loss || !dx) return fail(F2C_EINVAL, "NULL x/labels/loss/dx");
@@ -1045,6 +1066,12 @@ extern "C" int f2c_dcp_check(f2c_dcp *h) {
     if (!h) return fail(F2C_EINVAL, "NULL handle");
     if (h->last_stream) CUDA_TRY(cudaStreamSynchronize(h->last_stream));
     CUDA_TRY(cudaDeviceSynchronize());
+    if (h->comm && nccl().CommGetAsyncError) {  // failure detection of the collectives
+        int async_err = 0;
+        if (nccl().CommGetAsyncError(h->comm, &async_err) == 0 && async_err != 0)
+            return fail(F2C_ENCCL, "NCCL asynchronous error: %s",
+                        nccl().GetErrorString ? nccl().GetErrorString(async_err) : "?");
+    }
     return latched(h, true);
 }
 

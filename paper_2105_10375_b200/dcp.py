@@ -174,6 +174,25 @@ class DCPHead:
         _check(load_library().f2c_dcp_set_state(self._h, feats.ctypes.data_as(ctypes.c_void_p),
                                                 labels.ctypes.data_as(ctypes.c_void_p), int(E)))
 
+    # -- checkpoint / resume: this rank's shard of the pool, as a file --------
+    def save(self, path: str):
+        """Write this handle's pool state (features as stored, labels, E) and its geometry to an
+        .npz file; one file per rank (a world > 1 job saves every rank's shard)."""
+        import numpy as np
+        feats, labs, E = self.get_state()
+        np.savez(path, feats=feats, labels=labs, E=np.int64(E),
+                 geometry=np.array([self.C, self.d, self.dtype, self.K, self.world, self.rank], dtype=np.int64))
+
+    def load(self, path: str):
+        """Restore a pool written by save() into a handle of the same geometry (C, d, dtype, K,
+        world, rank); raises DCPError(F2C_ESHAPE) on a mismatch."""
+        import numpy as np
+        z = np.load(path)
+        geo = [self.C, self.d, self.dtype, self.K, self.world, self.rank]
+        if z["geometry"].tolist() != geo:
+            raise DCPError(2, f"checkpoint geometry {z['geometry'].tolist()} != handle {geo}")
+        self.set_state(z["feats"], z["labels"], int(z["E"]))
+
     def row_stats(self, n_global: int):
         import numpy as np
         lse, cos, phi, ell = (np.empty(n_global, np.float32) for _ in range(4))

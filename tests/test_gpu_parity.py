@@ -289,3 +289,34 @@ def test_tp64_comparison_kernel_parity(dcp, d, monkeypatch):
     y = synth.uniform_labels(22, synth.S_INST_LAB, 0, 0, 150, n_id)
     y[::2] = blocks[-1][1][: len(y[::2])]        # half the rows in-pool (70+ rows: two 64-row groups)
     _run_case(dcp, C, d, blocks, X, y, None, 64.0, 0.35)
+
+
+def test_checkpoint_save_load_resume(dcp, tmp_path):
+    """Checkpoint / resume: save() after some steps, load() into a fresh handle, continue --
+    enqueue state and loss identical to the uninterrupted handle, bit for bit."""
+    C, d, M = 900, 128, 60
+    a = _head(dcp, C, d, 120, M)
+    blocks = _random_pool_blocks(C, d, M, 20, 700, 61)
+    for G, y in blocks[:12]:
+        a.enqueue(to_dev(G, synth.BF16), lt(y))
+    path = str(tmp_path / "pool.npz")
+    a.save(path)
+    b = _head(dcp, C, d, 120, M)
+    b.load(path)
+    for G, y in blocks[12:]:
+        a.enqueue(to_dev(G, synth.BF16), lt(y))
+        b.enqueue(to_dev(G, synth.BF16), lt(y))
+    X = synth.unit_rows(62, synth.S_INST, 0, 0, 100, d)
+    y = synth.uniform_labels(62, synth.S_INST_LAB, 0, 0, 100, 700)
+    y[::3] = blocks[-1][1][: len(y[::3])]
+    la, dxa = a.loss_fwd_bwd(to_dev(X, synth.BF16), lt(y), None, 64.0, 0.35)
+    la, dxa = float(la.item()), dxa.clone()
+    lb, dxb = b.loss_fwd_bwd(to_dev(X, synth.BF16), lt(y), None, 64.0, 0.35)
+    torch.cuda.synchronize()
+    assert float(lb.item()) == la and torch.equal(dxa, dxb)
+    fa, ya, Ea = a.get_state()
+    fb, yb, Eb = b.get_state()
+    assert Ea == Eb and np.array_equal(ya, yb) and np.array_equal(fa, fb)
+    c = _head(dcp, C + 1, d, 120, M)
+    with pytest.raises(dcp.DCPError):
+        c.load(path)
