@@ -397,7 +397,7 @@ int f2c_dcp_create_k(int64_t C, int32_t K, int32_t d, int32_t dtype, int32_t wor
         if (n >= 1 && 2 * n <= h->G) h->G = 2 * n;
     }
     {   // the fused kernel keeps each cluster's unit list in smem (PC_MAX_UNITS)
-        const int64_t R_groups = (n_local_max * world + 1 + 127) / 128;
+        const int64_t R_groups = (n_local_max * world + 32 + 127) / 128;  // (as L.R_max)
         if (2 + (R_groups + h->G / 2 - 1) / (h->G / 2) > PC_MAX_UNITS) {
             delete h;
             return fail(F2C_ECAPACITY, "world*n_local_max = %lld rows exceeds the fused kernel's schedule",
