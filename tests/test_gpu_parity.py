@@ -320,3 +320,29 @@ def test_checkpoint_save_load_resume(dcp, tmp_path):
     c = _head(dcp, C + 1, d, 120, M)
     with pytest.raises(dcp.DCPError):
         c.load(path)
+
+
+@pytest.mark.parametrize("W,C", [(1, 50), (4, 200), (3, 7)])
+def test_tiny_pools_and_shards(dcp, W, C):
+    """Pools (and shards) smaller than one 128-slot tile, down to 2-3 slots per shard: the TMA
+    boxes run past the end of the tensor (zero fill), every shard has a single partial tile."""
+    d, m_loc = 128, 1
+    while (m_loc + 1) * W <= min(C, 16):
+        m_loc += 1
+    head = dcp.DCPHead(C, d, dcp.BF16, world=W, rank=0 if W == 1 else -1, n_local_max=24, m_local_max=m_loc)
+    pool = oracle.Pool(C, d, oracle.BF16)
+    for b in range(2 * C // (m_loc * W) + 2):
+        G = synth.unit_rows(71, synth.S_PRE, b, 0, m_loc * W, d)
+        y = synth.uniform_labels(71, synth.S_PRE_LAB, b, 0, m_loc * W, 3 * C)
+        head.enqueue(to_dev(G, synth.BF16), lt(y))
+        pool.enqueue(G, y)
+    N = 24 * W
+    X = synth.unit_rows(72, synth.S_INST, 0, 0, N, d)
+    y = synth.uniform_labels(72, synth.S_INST_LAB, 0, 0, N, 3 * C)
+    y[::2] = pool.lab[np.arange(N // 2) % pool.C_occ]
+    loss, dx = head.loss_fwd_bwd(to_dev(X, synth.BF16), lt(y), None, 30.0, 0.2)
+    torch.cuda.synchronize()
+    head.check()
+    ref = pool.loss(X, y, None, 30.0, 0.2)
+    assert_loss_close(float(loss.item()), ref.L)
+    assert_dx_close(from_dev(dx), ref.dx)
