@@ -83,16 +83,19 @@ __host__ __device__ inline int tp_choose_S(int R, int G, int n_tiles) {
     if (s_hi > n_tiles) s_hi = n_tiles;
     if (s_lo > s_hi) s_lo = s_hi;
     int best = s_lo;
-    double best_eff = -1.0;
+    // (single precision: this runs in every CTA's prologue and in every combine row, and fp64
+    // divisions there cost thousands of cycles)
+    float best_eff = -1.f;
+    const float work = static_cast<float>(n_tiles) * static_cast<float>(R) / static_cast<float>(G);
     for (int S = s_lo; S <= s_hi; ++S) {
         const long long U = static_cast<long long>(R) * S;
         const long long waves = (U + G - 1) / G;
         // time ~ waves * ceil(n_tiles / S); work ~ n_tiles * R / G per CTA
-        const double t = static_cast<double>(waves) * ((n_tiles + S - 1) / S);
+        const float t = static_cast<float>(waves) * static_cast<float>((n_tiles + S - 1) / S);
         // a second wave re-streams ranges whose row groups no longer run together (L2 reuse
         // is lost across waves): single-wave schedules get a 6 % credit
-        const double eff = (static_cast<double>(n_tiles) * R / G) / t * (waves == 1 ? 1.06 : 1.0);
-        if (eff > best_eff + 0.01) {
+        const float eff = work / t * (waves == 1 ? 1.06f : 1.f);
+        if (eff > best_eff + 0.01f) {
             best_eff = eff;
             best = S;
         }

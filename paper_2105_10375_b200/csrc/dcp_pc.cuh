@@ -320,6 +320,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
         p.dbg[1025 + (blockIdx.x & 1) * 4] = gt;
     }
 
+    // debug hook: prologue stamps [1040 + 8 * cta + k] of the recorded cluster
+    const bool dbgc = p.dbg && (blockIdx.x >> 1) == static_cast<unsigned>(p.dbg_cluster);
+#define PC_STAMP(k) do { if (dbgc) p.dbg[1040 + (blockIdx.x & 1) * 8 + (k)] = clock64(); } while (0)
+    if (threadIdx.x == 0) PC_STAMP(0);
     if (threadIdx.x == 0) {
         for (int i = 0; i < PC_P_NSTAGE; ++i) {
             mbar_init(&aux->tfull[i], 1);
@@ -355,6 +359,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
         int n = 0, a, b, c, s;
         while (n < PC_MAX_UNITS && ts.next(a, b, c, s)) aux->units[n++] = make_int4(a, b, c, s);
         aux->n_units = n;
+        PC_STAMP(1);
     }
     if (warp == 9) {
         tma_prefetch_desc(&tm3p);
@@ -367,6 +372,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
     __syncthreads();
     cluster_sync_all();
     tc_fence_after();
+    if (threadIdx.x == 0) PC_STAMP(2);
     const uint32_t tmem = aux->tmem_base;
 
     PCUnitIt sch{aux->units, aux->n_units, 0};
@@ -421,6 +427,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                 uint32_t pc = 0, jt = 0, sg = 0;
                 while (sch.next(rg, t0, t1, seg)) {
                     mbar_wait(&aux->xready, sg & 1);
+                    if (lane == 0 && sg == 0) PC_STAMP(4);
                     tc_fence_after();
                     for (int t = t0; t < t1; ++t, ++jt) {
                         unsigned long long *dbg = (p.dbg && blockIdx.x == 2u * p.dbg_cluster && jt < 64 && lane == 0) ? p.dbg + jt * 16 : nullptr;
@@ -521,6 +528,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&aux->xready);
+                if (threadIdx.x == 0 && sg == 0) PC_STAMP(3);
                 float lacc = 0.f, mx = -INFINITY;
                 int barg = -1;
                 // K >= 2: this unit's tiles bring their weights through the smem ring (it holds

@@ -50,6 +50,13 @@ else:
         r = st[j] - a[16 + j, 0]
         print("tile", 16 + j, "stage (wait_start, wait_done) rel g1_start:", r.tolist(), " g1_issued", a[16 + j, 1] - a[16 + j, 0])
     sp = bb[1024:1032]
+    ntl = int((a16[:, 0] > 0).sum())
+    pro = bb[1040:1056].reshape(2, 8)
+    print("prologue stamps CTA0 rel start: units done %d, cluster sync %d, x_hat in TMEM %d, MMA saw xready %d"
+          % tuple(pro[0, 1:5] - pro[0, 0]))
+    print("prologue (CTA 0 start -> tile 0 GEMM-1 issue): %d cycles; tiles recorded %d" % (a[0, 0] - sp[0], ntl))
+    print("epilogue (last recorded tile GEMM-1 issue -> CTA 0 end): %d cycles; consumer end - its last GEMM-2 issue: %d"
+          % (sp[2] - a[ntl - 1, 0], sp[6] - a16[ntl - 1, 7]))
     for c in range(2):
         cyc, ns = sp[4 * c + 2] - sp[4 * c], sp[4 * c + 3] - sp[4 * c + 1]
         print("CTA", c, "span: %d cycles, %.3f ms, eff clock %.0f MHz" % (cyc, ns / 1e6, cyc / max(ns, 1) * 1e3))
