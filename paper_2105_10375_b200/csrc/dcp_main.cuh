@@ -88,8 +88,8 @@ __host__ __device__ inline int tp_choose_S(int R, int G, int n_tiles) {
     float best_eff = -1.f;
     const float work = static_cast<float>(n_tiles) * static_cast<float>(R) / static_cast<float>(G);
     for (int S = s_lo; S <= s_hi; ++S) {
-        const long long U = static_cast<long long>(R) * S;
-        const long long waves = (U + G - 1) / G;
+        const int U = R * S;                 // (32-bit: R*S <= 2G + R)
+        const int waves = (U + G - 1) / G;
         // time ~ waves * ceil(n_tiles / S); work ~ n_tiles * R / G per CTA
         const float t = static_cast<float>(waves) * static_cast<float>((n_tiles + S - 1) / S);
         // a second wave re-streams ranges whose row groups no longer run together (L2 reuse
@@ -103,24 +103,32 @@ __host__ __device__ inline int tp_choose_S(int R, int G, int n_tiles) {
     return best;
 }
 
+// First tile of range s when n_tiles tiles are cut into S ranges: q or q + 1 tiles each (the
+// first n_tiles % S ranges get one more).  32-bit arithmetic only: 64-bit divisions cost ~100
+// instructions each, and this runs in every CTA's prologue and in every combine row.
+__host__ __device__ inline int tp_range_begin(int s, int n_tiles, int S) {
+    const int q = n_tiles / S, rem = n_tiles - q * S;
+    return s * q + (s < rem ? s : rem);
+}
+
 struct TPSched {
     int R, S, n_tiles, G;
-    long long u, U;
+    int u, U;
     __device__ void init(int b, int G_, int R_, int nt) {
         R = R_;
         G = G_;
         n_tiles = nt;
         S = tp_choose_S(R, G, nt);
-        U = nt > 0 ? static_cast<long long>(R) * S : 0;
+        U = nt > 0 ? R * S : 0;
         u = b;
     }
     __device__ bool next(int &rg, int &t0, int &t1, int &seg) {
         while (u < U) {
-            const int s = static_cast<int>(u / R);
-            rg = static_cast<int>(u % R);
-            seg = static_cast<int>(u);
-            t0 = static_cast<int>(static_cast<long long>(s) * n_tiles / S);
-            t1 = static_cast<int>(static_cast<long long>(s + 1) * n_tiles / S);
+            const int s = u / R;
+            rg = u - s * R;
+            seg = u;
+            t0 = tp_range_begin(s, n_tiles, S);
+            t1 = tp_range_begin(s + 1, n_tiles, S);
             u += G;
             if (t1 > t0) return true;
         }

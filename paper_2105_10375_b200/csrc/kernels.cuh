@@ -882,8 +882,8 @@ __device__ __forceinline__ void gather_row_partials(const CombineArgs &a, int n_
 #pragma unroll
             for (int j = 0; j < 4; ++j) ov[u][j] = make_float4(0.f, 0.f, 0.f, 0.f);
             if (s >= S) continue;
-            const long long t0 = static_cast<long long>(s) * a.n_tiles / S;
-            const long long t1 = static_cast<long long>(s + 1) * a.n_tiles / S;
+            const int t0 = tp_range_begin(s, a.n_tiles, S);
+            const int t1 = tp_range_begin(s + 1, a.n_tiles, S);
             if (t1 <= t0) continue;
             const long long seg = static_cast<long long>(s) * n_rg + rg;
             lv[u] = a.seg_l[seg * RG + r];
@@ -921,8 +921,8 @@ __device__ __forceinline__ void gather_row_max(const CombineArgs &a, int n_rg, i
     if (a.n_tiles <= 0) return;
     const int S = tp_choose_S(n_rg, a.G, a.n_tiles);
     for (int s = 0; s < S; ++s) {
-        const long long t0 = static_cast<long long>(s) * a.n_tiles / S;
-        const long long t1 = static_cast<long long>(s + 1) * a.n_tiles / S;
+        const int t0 = tp_range_begin(s, a.n_tiles, S);
+        const int t1 = tp_range_begin(s + 1, a.n_tiles, S);
         if (t1 <= t0) continue;
         const long long seg = static_cast<long long>(s) * n_rg + rg;
         const float v = a.seg_mx[seg * RG + r];
@@ -1132,8 +1132,8 @@ __global__ void __launch_bounds__(256, 2) k_local_rows(CombineArgs a, float4 *__
         if (a.n_tiles > 0) {
             const int S = tp_choose_S(n_rg, a.G, a.n_tiles);
             for (int s = lane; s < S; s += 32) {  // lanes split the segments, fixed-order tree below
-                const long long t0 = static_cast<long long>(s) * a.n_tiles / S;
-                const long long t1 = static_cast<long long>(s + 1) * a.n_tiles / S;
+                const int t0 = tp_range_begin(s, a.n_tiles, S);
+                const int t1 = tp_range_begin(s + 1, a.n_tiles, S);
                 if (t1 <= t0) continue;
                 const long long seg = static_cast<long long>(s) * n_rg + rg;
                 lsum += a.seg_l[seg * RG + r];
