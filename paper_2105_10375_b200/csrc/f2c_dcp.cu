@@ -629,9 +629,9 @@ extern "C" int f2c_gnet_ema(const float *p, float *g, int64_t n, double momentum
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const int64_t n4 = n / 4;
     if (n4 > 0) {
-        const int64_t blocks = (n4 + 256 * EMA_PER_THREAD - 1) / (256 * EMA_PER_THREAD);
+        const int64_t blocks = (n4 + EMA_THREADS * EMA_PER_THREAD - 1) / (EMA_THREADS * EMA_PER_THREAD);
         if (blocks > 0x7fffffffll) return fail(F2C_ESHAPE, "n too large");
-        k_ema<<<static_cast<unsigned>(blocks), 256, 0, st>>>(reinterpret_cast<const float4 *>(p),
+        k_ema<<<static_cast<unsigned>(blocks), EMA_THREADS, 0, st>>>(reinterpret_cast<const float4 *>(p),
                                                              reinterpret_cast<float4 *>(g), n4,
                                                              momentum, 1.0 - momentum);
         LAUNCH_CHECK();

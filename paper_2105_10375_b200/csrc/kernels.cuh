@@ -270,14 +270,18 @@ __device__ __forceinline__ float ema1(float gv, float pv, double m, double om) {
 // One CTA per 1024 float4 (16 KB of g): short-lived CTAs, so a concurrently launched
 // persistent kernel (the fused loss kernel) gets its SMs back within microseconds when the
 // EMA runs on a side stream; four independent 16-B loads per thread in flight.
-constexpr int EMA_PER_THREAD = 4;
-__global__ void __launch_bounds__(256) k_ema(const float4 *__restrict__ p, float4 *__restrict__ g, int64_t n4,
-                                             double m, double om) {
-    const int64_t base = static_cast<int64_t>(blockIdx.x) * (256 * EMA_PER_THREAD) + threadIdx.x;
+// Small CTAs (128 threads, <= 40 registers, no smem) fit next to the fused loss kernel on an
+// SM (its CTA leaves ~6K registers and ~24 KB of smem free), so an EMA on a side stream can run
+// concurrently with it instead of waiting for its SMs.
+constexpr int EMA_PER_THREAD = 2;
+constexpr int EMA_THREADS = 128;
+__global__ void __launch_bounds__(EMA_THREADS, 12) k_ema(const float4 *__restrict__ p, float4 *__restrict__ g, int64_t n4,
+                                                        double m, double om) {
+    const int64_t base = static_cast<int64_t>(blockIdx.x) * (EMA_THREADS * EMA_PER_THREAD) + threadIdx.x;
     float4 a[EMA_PER_THREAD], b[EMA_PER_THREAD];
 #pragma unroll
     for (int u = 0; u < EMA_PER_THREAD; ++u) {
-        const int64_t i = base + u * 256;
+        const int64_t i = base + u * EMA_THREADS;
         if (i < n4) {
             a[u] = __ldcs(p + i);
             b[u] = __ldcs(g + i);
@@ -285,7 +289,7 @@ __global__ void __launch_bounds__(256) k_ema(const float4 *__restrict__ p, float
     }
 #pragma unroll
     for (int u = 0; u < EMA_PER_THREAD; ++u) {
-        const int64_t i = base + u * 256;
+        const int64_t i = base + u * EMA_THREADS;
         if (i < n4) {
             float4 v = b[u];
             v.x = ema1(v.x, a[u].x, m, om);
