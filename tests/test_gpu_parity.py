@@ -346,3 +346,21 @@ def test_tiny_pools_and_shards(dcp, W, C):
     ref = pool.loss(X, y, None, 30.0, 0.2)
     assert_loss_close(float(loss.item()), ref.L)
     assert_dx_close(from_dev(dx), ref.dx)
+
+
+@pytest.mark.parametrize("W", [1, 2])
+def test_empty_pool(dcp, W):
+    """Before the first enqueue (D9: slots start empty): no row is in-pool, C_occ = 0, so
+    L_ce = L_cos = 0 (D10/D11) and dx = 0 -- on the single-rank and the sharded path."""
+    C, d = 256, 128
+    head = dcp.DCPHead(C, d, dcp.BF16, world=W, rank=0 if W == 1 else -1, n_local_max=16, m_local_max=8)
+    pool = oracle.Pool(C, d, oracle.BF16)
+    X = synth.unit_rows(81, synth.S_INST, 0, 0, 16 * W, d)
+    y = synth.uniform_labels(81, synth.S_INST_LAB, 0, 0, 16 * W, 100)
+    loss, dx = head.loss_fwd_bwd(to_dev(X, synth.BF16), lt(y), None, 64.0, 0.35)
+    torch.cuda.synchronize()
+    head.check()
+    ref = pool.loss(X, y, None, 64.0, 0.35)
+    assert ref.L == 0.0 and ref.N_pos == 0 and ref.C_occ == 0
+    assert float(loss.item()) == 0.0
+    assert np.all(from_dev(dx) == 0.0)
