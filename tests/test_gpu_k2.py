@@ -40,7 +40,7 @@ def _batch(pool, C, n, d, n_id, seed):
     return X, y
 
 
-@pytest.mark.parametrize("K,C,d,m", [(2, 1000, 128, 64), (2, 777, 256, 100), (3, 513, 512, 50)])
+@pytest.mark.parametrize("K,C,d,m", [(2, 1000, 128, 64), (2, 777, 256, 100), (3, 513, 512, 50), (8, 400, 512, 40)])
 def test_k_enqueue_state_bit_exact(dcp, K, C, d, m):
     head = dcp.DCPHead(C, d, dcp.BF16, 1, 0, n_local_max=64, m_local_max=m, K=K)
     pool = oracle.Pool(C, d, oracle.BF16, K=K)
@@ -53,7 +53,7 @@ def test_k_enqueue_state_bit_exact(dcp, K, C, d, m):
 
 
 @pytest.mark.parametrize("W", [1, 2])
-@pytest.mark.parametrize("K,C,d", [(2, 1000, 128), (2, 1301, 256), (3, 900, 512)])
+@pytest.mark.parametrize("K,C,d", [(2, 1000, 128), (2, 1301, 256), (3, 900, 512), (8, 700, 512)])
 def test_k_loss_parity(dcp, W, K, C, d):
     n_loc, m_loc, n_id = 200, 60, 1500
     head = dcp.DCPHead(C, d, dcp.BF16, world=W, rank=0 if W == 1 else -1, n_local_max=n_loc,
