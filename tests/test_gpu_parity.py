@@ -364,3 +364,31 @@ def test_empty_pool(dcp, W):
     assert ref.L == 0.0 and ref.N_pos == 0 and ref.C_occ == 0
     assert float(loss.item()) == 0.0
     assert np.all(from_dev(dx) == 0.0)
+
+
+def test_large_batch_multi_unit_schedule(dcp):
+    """40,000 rows against a 3,000-slot pool: ~160 row groups, so every cluster runs several
+    units in sequence (x_hat reloads, O drains and segment partials per unit), the compaction
+    runs on 40 CTAs and the label hash has 131,072 entries."""
+    C, d, M, n_id = 3000, 128, 500, 20000
+    head = _head(dcp, C, d, 40000, M)
+    pool = oracle.Pool(C, d, oracle.BF16)
+    for G, yy in _random_pool_blocks(C, d, M, 8, n_id, 91):
+        _enqueue_both(head, pool, G, yy)
+    N = 40000
+    X = synth.unit_rows(92, synth.S_INST, 0, 0, N, d)
+    y = synth.uniform_labels(92, synth.S_INST_LAB, 0, 0, N, n_id)
+    y[::3] = pool.lab[np.arange(len(y[::3])) % pool.C_occ]
+    loss, dx = head.loss_fwd_bwd(to_dev(X, synth.BF16), lt(y), None, 64.0, 0.35)
+    torch.cuda.synchronize()
+    head.check()
+    rows = np.arange(0, N, 397)
+    ref = pool.loss_rows(X, y, None, 64.0, 0.35, rows)
+    st = head.row_stats(N)
+    assert st["N_pos"] == ref["N_pos"] and st["N_neg"] == ref["N_neg"]
+    pos = ref["tslot"] >= 0
+    np.testing.assert_allclose(st["lse"][rows][pos], ref["lse"][pos], rtol=1e-3, atol=2e-3)
+    gdx = from_dev(dx)
+    for sel in (pos, ~pos):
+        err = np.abs(gdx[rows][sel] - ref["dx"][sel]).max()
+        assert err <= 1e-2 * np.abs(ref["dx"][sel]).max() + 1e-12
