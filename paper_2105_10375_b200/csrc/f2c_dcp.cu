@@ -1144,7 +1144,8 @@ extern "C" int f2c_dcp_set_state(f2c_dcp *h, const void *feats_host, const int64
     }
     CUDA_TRY(cudaDeviceSynchronize());
     h->E = enq_count;
-    h->M_last = 0;
+    h->M_last = 0;            // (no block since the restore: pairing checks fail until the next enqueue)
+    h->last_refresh = false;
     return F2C_OK;
 }
 
