@@ -164,10 +164,10 @@ int f2c_dcp_enqueue(f2c_dcp *h, const void *g_feats, const int64_t *labels, int6
  *   target is row j of the most recent global enqueue block (checked on the
  *   device, F2C_EPAIRING); -1 marks an instance row (D13);
  * s > 0 (logit scale), m finite (cosine margin).  The softmax runs against a per-row reference
- *   2^b_r, b_r = max(target logit, bound - 100) in log2 units (R1): exact for any s
- *   up to ~76 with unit-norm features.  A row whose every logit lies more than 2^-100 below the
- *   reference while that could matter (possible for larger s) latches F2C_EDEVICE ("softmax
- *   underflow") instead of returning a wrong loss;
+ *   2^b_r, b_r = max(target logit, bound - 100) in log2 units (R1), exact up to s ~ 69
+ *   with unit-norm features; for s > 68 a refinement pass lowers the reference of any row whose
+ *   terms fell far below it to that row's exact maximum and re-runs the fused kernel (its CTAs
+ *   exit at once when no row needs it).  A row still underflowing latches F2C_EDEVICE;
  * loss: device fp32 scalar (global-batch loss, identical on every rank);
  * dx: [n_local, d] dtype, must not alias x.  For world > 1, dx is the gradient of
  *   the GLOBAL loss w.r.t. this rank's rows: backbone gradients must be summed,

@@ -126,6 +126,7 @@ struct PCParams {
                            // stores (launched without the staging smem)
     unsigned long long *dbg;
     int dbg_cluster;       // the cluster whose per-tile clocks the debug hook records
+    const int *run_flag;   // refinement pass (R1 fallback): run only if *run_flag != 0
     int dbg_flags;         // timing experiments only: 1 = skip P smem writes, 128 = skip DSMEM copy,
                            // 4 / 8 = no producer / consumer pool loads, 16 = no softmax arithmetic,
                            // 16384 = every CTA loads only pool tiles 0-15 (L2-hot; same smem traffic),
@@ -294,6 +295,9 @@ template <bool EXCL>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
     dcp_pc_kernel(const __grid_constant__ CUtensorMap tm3p, const __grid_constant__ CUtensorMap tm3q,
                   const __grid_constant__ CUtensorMap tmO, const PCParams p) {
+    // the refinement pass exits before any barrier or TMEM allocation unless a row needs it
+    // (every CTA reads the same flag, so whole clusters exit together)
+    if (p.run_flag != nullptr && *p.run_flag == 0) return;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                 ~static_cast<uintptr_t>(1023));

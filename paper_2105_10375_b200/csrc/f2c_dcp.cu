@@ -743,7 +743,7 @@ static int phase_compact(f2c_dcp *h, Rank &R, const StepCtx &c, const int *tmax_
     return F2C_OK;
 }
 
-static int phase_main(f2c_dcp *h, Rank &R, const StepCtx &c, int64_t occ_loc) {
+static int phase_main(f2c_dcp *h, Rank &R, const StepCtx &c, int64_t occ_loc, const int *run_flag = nullptr) {
     NvtxRange nv("f2c: a4-a9 fused loss kernel");
     const Layout &L = R.L;
     TPParams p;
@@ -803,6 +803,7 @@ static int phase_main(f2c_dcp *h, Rank &R, const StepCtx &c, int64_t occ_loc) {
         q.dbg = p.dbg;
         q.dbg_cluster = h->dbg_cluster;
         q.dbg_flags = h->dbg_flags;
+        q.run_flag = run_flag;
         if (q.excl)
             dcp_pc_kernel<true><<<(h->G / 2) * 2, PC_THREADS, smem, c.st>>>(R.tm3p, R.tm3q, R.tmO, q);
         else
@@ -856,6 +857,19 @@ static CombineArgs combine_args(f2c_dcp *h, Rank &R, const StepCtx &c, int64_t o
     a.hvals = R.at<unsigned long long>(L.hvals);
     a.H = L.H;
     return a;
+}
+
+// R1 fallback for large s (R1): rows whose largest non-target exponent fell far
+// below their reference get it lowered to that maximum, and the fused kernel runs once more
+// (its CTAs exit at once unless some row was refined).  Below s = 68 no row with |cos| <= 1 can
+// get there, so the pass is not even launched.
+static int phase_refine(f2c_dcp *h, Rank &R, const StepCtx &c, int64_t occ) {
+    if (!(c.s > 68.f) || (h->use_tp64 && h->neg_mode() == 0 && !h->excl_dup)) return F2C_OK;
+    NvtxRange nv("f2c: R1 refinement pass");
+    CombineArgs a = combine_args(h, R, c, occ, nullptr);
+    k_refine_ref<<<static_cast<unsigned>((c.N + 255) / 256), 256, 0, c.st>>>(a, R.at<float2>(R.L.row_ab));
+    LAUNCH_CHECK();
+    return phase_main(h, R, c, occ, &R.sc()->refine);
 }
 
 static unsigned grid_for(int64_t n) {
@@ -925,6 +939,7 @@ static int loss_multi(f2c_dcp *h, const uint8_t *x, const int64_t *labels, const
         if ((rc = phase_compact(h, R, ctx[q], R.at<int>(R.L.tmax_glob)))) return rc;
         const int64_t occ = occ_local(h, R);
         if ((rc = phase_main(h, R, ctx[q], occ))) return rc;
+        if ((rc = phase_refine(h, R, ctx[q], occ))) return rc;
         CombineArgs a = combine_args(h, R, ctx[q], occ, nullptr);
         k_local_rows<<<static_cast<unsigned>((N + CB_ROWS - 1) / CB_ROWS), 256, 0, st>>>(a, R.at<float4>(R.L.rs_buf));
         LAUNCH_CHECK();
@@ -1003,6 +1018,7 @@ extern "C" int f2c_dcp_loss_fwd_bwd(f2c_dcp *h, const void *x, const int64_t *la
     if ((rc = phase_compact(h, R, c, &R.sc()->tmax_bits, true))) return rc;
     const int64_t occ = occ_local(h, R);
     if ((rc = phase_main(h, R, c, occ))) return rc;
+    if ((rc = phase_refine(h, R, c, occ))) return rc;
     CombineArgs a = combine_args(h, R, c, occ, static_cast<uint8_t *>(dx));
     k_combine<<<static_cast<unsigned>((c.N + CB_ROWS - 1) / CB_ROWS), 256, 0, st>>>(a, loss);
     LAUNCH_CHECK();

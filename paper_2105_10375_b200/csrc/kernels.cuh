@@ -32,6 +32,7 @@ struct Scalars {          // lives at the start of the per-rank scratch
     unsigned long long n_pos_sum;  // sum of n_pos over loss calls (bench accounting)
     long long n_app;      // rows appended by the last refresh-in-place enqueue (NEXT-3)
     unsigned loss_done;   // CTAs of the final per-row kernel done (the last one sums the loss)
+    int refine;           // R1 fallback: some row's reference was lowered, re-run the fused kernel
 };
 
 __device__ __forceinline__ void latch(Scalars *s, int code, int detail) {
@@ -723,6 +724,7 @@ __global__ void __launch_bounds__(1024) k_compact(CompactArgs a) {
         a.ttgt[r] = -INFINITY;
     }
     if (tid == 0) {
+        a.sc->refine = 0;
         a.sc->neg0 = neg0;
         a.sc->n_rows = n_rows;
         a.sc->n_pos = n_pos;
@@ -940,6 +942,25 @@ __device__ __forceinline__ void gather_row_max(const CombineArgs &a, int n_rg, i
 // dL_cos/dx_hat of an out-of-pool row handled by the main kernel (neg_mode 1 / 2), before
 // the factor lambda / N_neg; phi_raw = the shard's unreduced phi partial (sum of hinged
 // cosines, or the max cosine).
+// R1 fallback (large s): after the fused kernel, an in-pool row whose largest non-target
+// exponent fell below REFINE_BELOW (relative to its reference b_r) gets b_r lowered to that
+// maximum, and the fused kernel runs again for the batch (R1).  With the exact row
+// maximum as the reference no term of the row can underflow or overflow.
+constexpr float REFINE_BELOW = -50.f;
+__global__ void k_refine_ref(CombineArgs a, float2 *__restrict__ row_ab) {
+    const int n_pos = a.sc->n_pos;
+    const int n_rg = (a.sc->n_rows + a.rows_per_group - 1) / a.rows_per_group;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n_pos; k += gridDim.x * blockDim.x) {
+        float cmax;
+        int carg;
+        gather_row_max(a, n_rg, k, cmax, carg);
+        if (cmax < REFINE_BELOW && cmax > -INFINITY) {
+            row_ab[k].y += cmax;
+            a.sc_w->refine = 1;
+        }
+    }
+}
+
 __device__ __forceinline__ void neg_row_local(const CombineArgs &a, int n_rg, int kn, float (&g)[16],
                                               float &phi_raw, int &carg) {
     carg = -1;

@@ -245,10 +245,12 @@ def test_determinism(dcp):
 
 
 @pytest.mark.parametrize("world", [1, 2])
-def test_degenerate_all_negative_cosines(dcp, world):
-    """Every slot points away from every row (cos ~ -0.99 at s = 64): with a single global
-    reference all softmax terms would underflow; the per-row reference (R1) keeps the
-    result exact within the parity bar (single pool and emulated 2-rank world)."""
+@pytest.mark.parametrize("s", [64.0, 128.0])
+def test_degenerate_all_negative_cosines(dcp, world, s):
+    """Every slot points away from every row (cos ~ -0.99): with a single global reference all
+    softmax terms would underflow.  The per-row reference (R1) keeps the result exact at
+    s = 64; at s = 128 the rows fall below it and the refinement pass (the R1 fallback, run
+    for s > 68) re-runs them against their exact maximum (single pool and emulated 2-rank world)."""
     d, C, n = 128, 300, 24
     rng = np.random.default_rng(17)
     u = rng.standard_normal(d)
@@ -268,10 +270,10 @@ def test_degenerate_all_negative_cosines(dcp, world):
     step = C // world * world if world > 1 else C
     head.enqueue(to_dev(G[:step], synth.BF16), lt(labs[:step]))
     pool.enqueue(G[:step], labs[:step])
-    loss, dx = head.loss_fwd_bwd(to_dev(X, synth.BF16), lt(y), None, 64.0, 0.35)
+    loss, dx = head.loss_fwd_bwd(to_dev(X, synth.BF16), lt(y), None, s, 0.35)
     torch.cuda.synchronize()
     head.check()
-    ref = pool.loss(X, y, None, 64.0, 0.35)
+    ref = pool.loss(X, y, None, s, 0.35)
     assert_loss_close(float(loss.item()), ref.L)
     gdx = from_dev(dx)
     assert_dx_close(gdx, ref.dx)
@@ -392,3 +394,24 @@ def test_large_batch_multi_unit_schedule(dcp):
     for sel in (pos, ~pos):
         err = np.abs(gdx[rows][sel] - ref["dx"][sel]).max()
         assert err <= 1e-2 * np.abs(ref["dx"][sel]).max() + 1e-12
+
+
+@pytest.mark.parametrize("W", [1, 2])
+def test_large_scale_refinement_pass(dcp, W):
+    """s = 100 on ordinary inputs (mixed in-pool / out-of-pool rows, duplicates, partial pool):
+    the refinement pass runs, touches only rows that need it, and the result meets the bar."""
+    C, d, M, n_id = 700, 256, 50, 900
+    head = dcp.DCPHead(C, d, dcp.BF16, world=W, rank=0 if W == 1 else -1, n_local_max=60, m_local_max=M)
+    pool = oracle.Pool(C, d, oracle.BF16)
+    for G, yy in _random_pool_blocks(C, d, M * W, 9, n_id, 95):
+        head.enqueue(to_dev(G, synth.BF16), lt(yy))
+        pool.enqueue(G, yy)
+    X = synth.unit_rows(96, synth.S_INST, 0, 0, 60 * W, d)
+    y = synth.uniform_labels(96, synth.S_INST_LAB, 0, 0, 60 * W, n_id)
+    y[::2] = pool.lab[np.arange(len(y[::2])) % pool.C_occ]
+    loss, dx = head.loss_fwd_bwd(to_dev(X, synth.BF16), lt(y), None, 100.0, 0.35)
+    torch.cuda.synchronize()
+    head.check()
+    ref = pool.loss(X, y, None, 100.0, 0.35)
+    assert_loss_close(float(loss.item()), ref.L)
+    assert_dx_close(from_dev(dx), ref.dx)
