@@ -31,7 +31,7 @@ def _case(i):
     m_loc = int(rng.integers(1, max(2, min(96, C // W) + 1)))
     n_loc = int(rng.integers(1, 200))
     fill = float(rng.choice([0.3, 1.0, 2.5]))            # partial pool, just full, wrapped
-    s = float(rng.choice([1.0, 30.0, 64.0]))
+    s = float(rng.choice([1.0, 30.0, 64.0, 100.0]))
     m = float(rng.choice([0.0, 0.2, 0.35]))
     phi_mode = int(rng.choice([oracle.PHI_MEAN, oracle.PHI_MEAN, oracle.PHI_SUM, oracle.PHI_MAX]))
     hinge = bool(rng.random() < 0.25)
