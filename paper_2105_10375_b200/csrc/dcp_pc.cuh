@@ -14,10 +14,14 @@
 //     consumer's mbarrier).
 //   consumer (cluster rank 1): O[128 rows x d] fp32 occupies all 512 TMEM columns;
 //     GEMM 2  O[r, :] += sum_c P[r, c] T[c, :]   M = 128, N = 256 (d block), K = slots
-//     (A = P from smem, B = pool chunk MN-major from smem).
+//     (A = P from smem, B = pool chunk MN-major from smem).  At a unit's end eight warps
+//     drain O to the segment partial (through smem + TMA stores for short units).
 // The N x C logit matrix only exists as one 128x128 tile at a time (TMEM, then smem).
-// The softmax reference b_r is an upper bound of every logit, identical across
-// slots, so partials of different clusters / tiles / ranks add without rescaling.
+// The softmax reference b_r (R1) is fixed per row before the pass, identical across
+// slots, so partials of different clusters / tiles / ranks add without rescaling; rows that
+// fall far below it (large s) are re-run by the refinement pass (run_flag).
+// Variants: EXCL (stale self-duplicates masked per tile, NEXT-3), the K >= 2 mu-row weights
+// through an smem ring (NEXT-1), out-of-pool cosine rows for hinge / max (NEXT-3).
 #pragma once
 #include "dcp_main.cuh"
 #include "sm100.cuh"
