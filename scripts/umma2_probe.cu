@@ -48,7 +48,7 @@ __global__ void __cluster_dims__(2, 1, 1) probe(int mode, const __nv_bfloat16 *A
     const uint32_t cr = ctarank();
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     // operand rows held by this CTA
-    const int arows = mode == 3 ? 64 : 128;
+    const int arows = mode >= 3 ? 64 : 128;
     const int a0 = (mode == 1) ? 0 : cr * arows;       // global A row offset
     const int brows = mode == 1 ? 128 : 64;
     const int b0 = (mode == 1) ? 0 : cr * 64;          // global B (N) row offset
@@ -67,10 +67,10 @@ __global__ void __cluster_dims__(2, 1, 1) probe(int mode, const __nv_bfloat16 *A
     }
     if (warp == 0) {
         if (mode == 1) {
-            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(smem_u32(&tbase)) : "memory");
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(&tbase)) : "memory");
             asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
         } else {
-            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(smem_u32(&tbase)) : "memory");
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(&tbase)) : "memory");
             asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
         }
     }
@@ -101,12 +101,49 @@ __global__ void __cluster_dims__(2, 1, 1) probe(int mode, const __nv_bfloat16 *A
     const int M = mode == 2 ? 256 : 128;
     const uint32_t idesc = umma_idesc_bf16(M, 128, 0, 0);
     const bool issuer = (mode == 1) || cr == 0;
+    // modes 4/5: A (this CTA's 64 rows x 64 K, bf16 pairs per 32-bit column) into TMEM columns
+    // [128, 160): mode 4 = rows on lanes 0-63 (lanes 64-127 zero); mode 5 = rows on lanes 0-63
+    // for K 0-31 and on lanes 64-127 for K 32-63 (columns [128, 144))
+    const uint32_t ACOL = 128;
+    if (mode >= 4 && warp < 4) {
+        uint32_t w[32];
+        const int lr = warp * 32 + lane;  // TMEM lane
+        for (int j = 0; j < 32; ++j) {
+            int row = -1, k0 = 0;
+            if (mode == 4 && lr < 64) { row = lr; k0 = 2 * j; }
+            if (mode == 5 && j < 16) { row = lr & 63; k0 = (lr < 64 ? 0 : 32) + 2 * j; }
+            uint32_t v = 0;
+            if (row >= 0) {
+                const __nv_bfloat16 lo = A[(a0 + row) * 64 + k0], hi = A[(a0 + row) * 64 + k0 + 1];
+                v = static_cast<uint32_t>(__bfloat16_as_ushort(lo)) | (static_cast<uint32_t>(__bfloat16_as_ushort(hi)) << 16);
+            }
+            w[j] = v;
+        }
+        asm volatile(
+            "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+            "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(tmem + (static_cast<uint32_t>(warp * 32) << 16) + ACOL),
+            "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7]), "r"(w[8]), "r"(w[9]),
+            "r"(w[10]), "r"(w[11]), "r"(w[12]), "r"(w[13]), "r"(w[14]), "r"(w[15]), "r"(w[16]), "r"(w[17]), "r"(w[18]),
+            "r"(w[19]), "r"(w[20]), "r"(w[21]), "r"(w[22]), "r"(w[23]), "r"(w[24]), "r"(w[25]), "r"(w[26]), "r"(w[27]),
+            "r"(w[28]), "r"(w[29]), "r"(w[30]), "r"(w[31])
+            : "memory");
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    cl_sync();
+    tc_fence_after();
     if (warp == 1 && issuer && lane == 0) {
         for (int ks = 0; ks < 4; ++ks) {
             const uint64_t ad = umma_desc_sw128(smem_u32(sA) + ks * 32, 16, 1024);
             const uint64_t bd = umma_desc_sw128(smem_u32(sB) + ks * 32, 16, 1024);
             const uint32_t acc = ks > 0;
-            if (mode == 1)
+            if (mode >= 4) {
+                // A from TMEM: K step ks = 16 bf16 = 8 columns (mode 4) or 4 columns (mode 5)
+                const uint32_t acol = tmem + ACOL + ks * (mode == 4 ? 8 : 4);
+                asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n}\n"
+                             ::"r"(tmem), "r"(acol), "l"(bd), "r"(idesc), "r"(acc) : "memory");
+            } else if (mode == 1)
                 asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n"
                              ::"r"(tmem), "l"(ad), "l"(bd), "r"(idesc), "r"(acc) : "memory");
             else
@@ -135,9 +172,9 @@ __global__ void __cluster_dims__(2, 1, 1) probe(int mode, const __nv_bfloat16 *A
     cl_sync();
     if (warp == 0) {
         if (mode == 1)
-            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem) : "memory");
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem) : "memory");
         else
-            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 128;" ::"r"(tmem) : "memory");
+            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 256;" ::"r"(tmem) : "memory");
     }
 }
 
@@ -174,7 +211,7 @@ int main() {
     cudaMemcpy(dA, Ah.data(), MR * K * 2, cudaMemcpyHostToDevice);
     cudaMemcpy(dB, Bh.data(), NR * K * 2, cudaMemcpyHostToDevice);
     cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 40000);
-    for (int mode = 1; mode <= 3; ++mode) {
+    for (int mode = 1; mode <= 5; ++mode) {
         cudaMemset(dump, 0xff, 2 * 128 * 128 * 4);
         cudaMemset(derr, 0, 4);
         probe<<<2, 128, 40000>>>(mode, dA, dB, dump, derr);
@@ -203,7 +240,7 @@ int main() {
             (void)col_half_match;
         }
         printf("  rows found: %d of %d\n", found, M);
-        if (mode == 3) {  // partial matches: 64-column halves of D rows anywhere in the dumps
+        if (mode >= 3) {  // partial matches: 64-column halves of D rows anywhere in the dumps
             int shown = 0;
             for (int cta = 0; cta < 2; ++cta)
                 for (int ln = 0; ln < 128; ++ln)
