@@ -48,7 +48,7 @@ __global__ void __cluster_dims__(2, 1, 1) probe(int mode, const __nv_bfloat16 *A
     const uint32_t cr = ctarank();
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     // operand rows held by this CTA
-    const int arows = mode >= 3 ? 64 : 128;
+    const int arows = (mode >= 3 && mode != 6) ? 64 : 128;
     const int a0 = (mode == 1) ? 0 : cr * arows;       // global A row offset
     const int brows = mode == 1 ? 128 : 64;
     const int b0 = (mode == 1) ? 0 : cr * 64;          // global B (N) row offset
@@ -98,19 +98,20 @@ __global__ void __cluster_dims__(2, 1, 1) probe(int mode, const __nv_bfloat16 *A
     __syncthreads();
     cl_sync();
     tc_fence_after();
-    const int M = mode == 2 ? 256 : 128;
+    const int M = (mode == 2 || mode == 6) ? 256 : 128;
     const uint32_t idesc = umma_idesc_bf16(M, 128, 0, 0);
     const bool issuer = (mode == 1) || cr == 0;
     // modes 4/5: A (this CTA's 64 rows x 64 K, bf16 pairs per 32-bit column) into TMEM columns
     // [128, 160): mode 4 = rows on lanes 0-63 (lanes 64-127 zero); mode 5 = rows on lanes 0-63
     // for K 0-31 and on lanes 64-127 for K 32-63 (columns [128, 144))
     const uint32_t ACOL = 128;
-    if (mode >= 4 && warp < 4) {
+    if (mode >= 4 && warp < 4) {  // (mode 6: M = 256, rows 0-127 of this CTA on lanes 0-127)
         uint32_t w[32];
         const int lr = warp * 32 + lane;  // TMEM lane
         for (int j = 0; j < 32; ++j) {
             int row = -1, k0 = 0;
             if (mode == 4 && lr < 64) { row = lr; k0 = 2 * j; }
+            if (mode == 6) { row = lr; k0 = 2 * j; }
             if (mode == 5 && j < 16) { row = lr & 63; k0 = (lr < 64 ? 0 : 32) + 2 * j; }
             uint32_t v = 0;
             if (row >= 0) {
@@ -139,8 +140,8 @@ __global__ void __cluster_dims__(2, 1, 1) probe(int mode, const __nv_bfloat16 *A
             const uint64_t bd = umma_desc_sw128(smem_u32(sB) + ks * 32, 16, 1024);
             const uint32_t acc = ks > 0;
             if (mode >= 4) {
-                // A from TMEM: K step ks = 16 bf16 = 8 columns (mode 4) or 4 columns (mode 5)
-                const uint32_t acol = tmem + ACOL + ks * (mode == 4 ? 8 : 4);
+                // A from TMEM: K step ks = 16 bf16 = 8 columns (modes 4, 6) or 4 columns (mode 5)
+                const uint32_t acol = tmem + ACOL + ks * (mode == 5 ? 4 : 8);
                 asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n}\n"
                              ::"r"(tmem), "r"(acol), "l"(bd), "r"(idesc), "r"(acc) : "memory");
             } else if (mode == 1)
@@ -211,7 +212,7 @@ int main() {
     cudaMemcpy(dA, Ah.data(), MR * K * 2, cudaMemcpyHostToDevice);
     cudaMemcpy(dB, Bh.data(), NR * K * 2, cudaMemcpyHostToDevice);
     cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 40000);
-    for (int mode = 1; mode <= 5; ++mode) {
+    for (int mode = 1; mode <= 6; ++mode) {
         cudaMemset(dump, 0xff, 2 * 128 * 128 * 4);
         cudaMemset(derr, 0, 4);
         probe<<<2, 128, 40000>>>(mode, dA, dB, dump, derr);
@@ -223,7 +224,7 @@ int main() {
         printf("mode %d: launch/sync %s, timeout flag %d\n", mode, cudaGetErrorString(e), herr);
         if (e != cudaSuccess) return 1;
         // for every expected D row (M rows of this mode), find (cta, lane) whose 128 columns match it
-        const int M = mode == 2 ? 256 : 128;
+        const int M = (mode == 2 || mode == 6) ? 256 : 128;
         int found = 0, col_half_match = 0;
         for (int r = 0; r < M; ++r) {
             int where = -1;
@@ -240,7 +241,7 @@ int main() {
             (void)col_half_match;
         }
         printf("  rows found: %d of %d\n", found, M);
-        if (mode >= 3) {  // partial matches: 64-column halves of D rows anywhere in the dumps
+        if (mode >= 3 && mode != 6) {  // partial matches: 64-column halves of D rows anywhere in the dumps
             int shown = 0;
             for (int cta = 0; cta < 2; ++cta)
                 for (int ln = 0; ln < 128; ++ln)
