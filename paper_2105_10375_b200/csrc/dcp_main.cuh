@@ -46,7 +46,7 @@ constexpr int TP_SMEM_BYTES = TP_OFF_AUX + 4096 + 1024;      // + alignment slac
 struct TPParams {
     int d;                 // feature dim (multiple of 128, <= 512)
     int n_slots;           // occupied slots of this shard: tiles cover [0, n_slots)
-    const int *n_pos;      // device: number of in-pool rows; the mu row is row *n_pos
+    const int *n_pos;      // device: number of in-pool rows
     const float2 *row_ab;  // [R_max] (a_r, b_r) per compacted row (0,0 for padding)
     const int *row_tgt;    // [R_max] local slot of the row's target, -1 if not in this shard
     float margin_l2;       // s * m * log2(e)
@@ -170,7 +170,7 @@ __global__ void __launch_bounds__(TP_THREADS, 1)
     const int d = p.d;
     const int npair = d >> 7;
     const int n_pos = *p.n_pos;
-    const int n_rg = (n_pos + 1 + TP_R - 1) / TP_R;  // +1: the mu row
+    const int n_rg = (n_pos + TP_R - 1) / TP_R;
     const int n_tiles = (p.n_slots + TP_TILE - 1) / TP_TILE;
 
     if (warp == 8 && lane == 0) {
@@ -304,7 +304,6 @@ __global__ void __launch_bounds__(TP_THREADS, 1)
                 aux->tgt[tid] = p.row_tgt[rg * TP_R + tid];
             }
             named_bar_sync(1, TP_EPI_THREADS);
-            const int mu_k = n_pos - rg * TP_R - hw * 32;  // mu row column within my half
             const int tg = aux->tgt[hw * 32 + lane];
             float lacc[32], mxacc[32];
 #pragma unroll
@@ -342,11 +341,6 @@ __global__ void __launch_bounds__(TP_THREADS, 1)
                                 e[k] = -INFINITY;
                             }
                     }
-                }
-                if (mu_k >= 0 && mu_k < 32) {  // the mu row: weight 1 on every valid slot
-#pragma unroll
-                    for (int k = 0; k < 32; ++k)
-                        if (k == mu_k) e[k] = valid ? 0.f : -INFINITY;
                 }
                 uint32_t pk[16];
 #pragma unroll

@@ -20,8 +20,8 @@
 // The softmax reference b_r (R1) is fixed per row before the pass, identical across
 // slots, so partials of different clusters / tiles / ranks add without rescaling; rows that
 // fall far below it (large s) are re-run by the refinement pass (run_flag).
-// Variants: EXCL (stale self-duplicates masked per tile, NEXT-3), the K >= 2 mu-row weights
-// through an smem ring (NEXT-1), out-of-pool cosine rows for hinge / max (NEXT-3).
+// Variants: EXCL (stale self-duplicates masked per tile, NEXT-3), out-of-pool cosine rows for
+// hinge / max (NEXT-3), with K >= 2 (NEXT-1) their weights w_c through an smem ring.
 #pragma once
 #include "dcp_main.cuh"
 #include "sm100.cuh"
@@ -46,7 +46,7 @@ constexpr int PCQ_OFF_P = 0;                              // 2 x 32 KB P slots
 constexpr int PCQ_OFF_T = PCQ_OFF_P + 2 * PC_PBYTES;      // 2 x 64 KB pool stages
 constexpr int PCQ_OFF_AUX = PCQ_OFF_T + PC_Q_NSTAGE * PC_STAGE_BYTES;
 constexpr int PC_OFF_AUX = PCP_OFF_AUX > PCQ_OFF_AUX ? PCP_OFF_AUX : PCQ_OFF_AUX;
-// producer: the mu row's weight ring (K >= 2), PC_WRING x 128 bf16; deep enough that the TMA
+// producer: the out-of-pool rows' weight ring (K >= 2), PC_WRING x 128 bf16; deep enough that the TMA
 // warp (a tile or two ahead of the softmax warps) never waits on it
 constexpr int PC_WRING = 8;
 constexpr int PC_OFF_WRING = PC_OFF_AUX + 4096;
@@ -86,7 +86,7 @@ struct PCAux {
     uint64_t xready, xfree;
     uint64_t pready[2], pstage_free[2];
     uint64_t pslot_free[2];            // arrived by the consumer's multicast commit
-    uint64_t wfull[PC_WRING], wempty[PC_WRING];  // the mu row's weight ring (K >= 2)
+    uint64_t wfull[PC_WRING], wempty[PC_WRING];  // the out-of-pool rows' weight ring (K >= 2)
     // consumer
     uint64_t qfull[PC_Q_NSTAGE], qempty[PC_Q_NSTAGE];
     uint64_t pfull[2];                 // complete_tx by the producer's bulk copy
@@ -104,8 +104,8 @@ static_assert(sizeof(PCAux) <= 4096, "PCAux must fit the aux region");
 struct PCParams {
     int d;                 // feature dim (multiple of 128, <= 512)
     int n_slots;           // occupied slots of this shard
-    const int *n_pos;      // device: in-pool rows; the mu row is row *n_pos
-    const int *n_rows;     // device: rows to process (n_pos + 1, or neg0 + N_neg with NEXT-3 neg rows)
+    const int *n_pos;      // device: in-pool rows
+    const int *n_rows;     // device: rows to process (n_pos, or neg0 + N_neg with NEXT-3 neg rows)
     const int *neg0;       // device: first out-of-pool row (NEXT-3 hinge / max)
     int neg_mode;          // 0; 1 = hinge (p = [cos > 0] w_c, l = sum relu(cos)); 2 = max cos
     int *seg_arg;          // [S][128] local argmax slot (neg_mode 2)
@@ -113,7 +113,7 @@ struct PCParams {
     const int *row_tgt;    // [R_max] local target slot or -1
     const uint8_t *X_pos;  // [R_max, d] bf16 compacted rows
     const float *wslot;    // K >= 2: per-slot 1/||T_bar_c|| (NEXT-3 out-of-pool rows; else null)
-    const __nv_bfloat16 *wmu;  // K >= 2: the same weights in bf16, the mu row's P (padded to a tile)
+    const __nv_bfloat16 *wmu;  // K >= 2: the same weights in bf16 for the weight ring (padded to a tile)
     float margin_l2;       // s * m * log2(e)
     float *ttgt;           // [R_max]
     float *seg_l;          // [S][128]
@@ -316,7 +316,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
     const int cps = (d % 256 == 0) ? 4 : 2;
     const int nstg = nchunk / cps;
     const uint32_t stage_bytes = static_cast<uint32_t>(cps) * 16384;
-    const int n_pos = *p.n_pos;
     const int n_rows = *p.n_rows;
     const int neg0 = *p.neg0;
     const int n_rg = (n_rows + PC_R - 1) / PC_R;
@@ -397,10 +396,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                 uint32_t pc = 0;
                 uint32_t wc_n = 0;
                 while (sch.next(rg, t0, t1, seg)) {
-                    const bool wmu = p.wmu != nullptr &&
-                                     (rg == n_pos / PC_R || (p.neg_mode != 0 && rg * PC_R + PC_R - 1 >= neg0));
+                    const bool wmu = p.wmu != nullptr && p.neg_mode != 0 && rg * PC_R + PC_R - 1 >= neg0;
                     for (int t = t0; t < t1; ++t) {
-                        if (wmu) {  // the mu row's bf16 weights of tile t (256 B) -> weight ring
+                        if (wmu) {  // the tile's bf16 weights w_c (256 B) -> weight ring
                             const uint32_t wb = wc_n % PC_WRING;
                             mbar_wait(&aux->wempty[wb], ((wc_n / PC_WRING) & 1) ^ 1);
                             mbar_arrive_expect_tx(&aux->wfull[wb], 256);
@@ -540,10 +538,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                 float lacc = 0.f, mx = -INFINITY;
                 int barg = -1;
                 // K >= 2: this unit's tiles bring their weights through the smem ring (it holds
-                // the mu row, or out-of-pool rows of NEXT-3 hinge / max)
-                const bool wmu = p.wmu != nullptr &&
-                                 (rg == n_pos / PC_R || (p.neg_mode != 0 && rg * PC_R + PC_R - 1 >= neg0));
-                // NEXT-3: out-of-pool rows compacted after the mu row (a = 1/||x||, b = 0)
+                // out-of-pool rows of NEXT-3 hinge / max)
+                const bool wmu = p.wmu != nullptr && p.neg_mode != 0 && rg * PC_R + PC_R - 1 >= neg0;
+                // NEXT-3: out-of-pool rows compacted after the in-pool rows (a = 1/||x||, b = 0)
                 // (the padding rows after n_rows take this path too: zero operands, discarded
                 // results, and no divergence with the last out-of-pool rows of their warp)
                 const bool negrow = p.neg_mode != 0 && row >= neg0;
@@ -640,22 +637,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                         }
                         lacc += ((la[0] + la[1]) + (la[2] + la[3])) + ((la[4] + la[5]) + (la[6] + la[7]));
                         mx = fmaxf(mx, fmaxf(fmaxf(ma[0], ma[1]), fmaxf(ma[2], ma[3])));
-                        if (wmu && row == n_pos) {
-                            // mu row with K >= 2: p_c = 1/||T_bar_c||, bf16 weights of this tile staged in
-                            // smem by the TMA warp (its l and max are unused)
-                            const uint32_t wb = wc_n % PC_WRING;
-                            const uint4 *src = reinterpret_cast<const uint4 *>(smem + PC_OFF_WRING + wb * 256 + h * 128);
-#pragma unroll
-                            for (int u = 0; u < 8; ++u) {
-                                const uint4 v = src[u];
-                                w[4 * u] = v.x; w[4 * u + 1] = v.y; w[4 * u + 2] = v.z; w[4 * u + 3] = v.w;
-                            }
-                            if (nval < 64)  // slots past the occupied range
-#pragma unroll
-                                for (int k = 0; k < 64; k += 2)
-                                    w[k >> 1] = (k < nval ? (w[k >> 1] & 0xffffu) : 0u) |
-                                                (k + 1 < nval ? (w[k >> 1] & 0xffff0000u) : 0u);
-                        }
                     } else {
                         // cosine c = <x_hat, T_bar_c> w_c (w_c = 1 for K = 1; zero centers are
                         // no candidates for the max and contribute 0 to the hinge).

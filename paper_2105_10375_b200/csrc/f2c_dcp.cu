@@ -113,7 +113,7 @@ static bool force_multi() {
 struct Layout {
     size_t T, lab, sc, x_all, y_all, pair_all, blk_x, blk_y, inv_n, hslot, hkeys, hvals, tseq,
         comp_idx, pos_row, X_pos, row_ab, row_tgt, ttgt, seg_l, seg_mx, seg_O, rowloss, st_lse,
-        st_cos, st_phi, st_ell, seg_arg, rs_buf, rs_all, dx_part, tseq_ext, dx32, tmax_glob, mu_buf, Traw, wslot,
+        st_cos, st_phi, st_ell, seg_arg, rs_buf, rs_all, dx_part, tseq_ext, dx32, tmax_glob, mu_fx, Traw, wslot,
         hgseq, row_hent, dup_cnt, dup_off, dup_list, ekeys, evals, ehslot, rseq, dst_seq, wmu, total;
     int64_t C_loc, N, Mg, R_max, S_max;
     int H, He;
@@ -179,11 +179,12 @@ static Layout make_layout(int64_t C, int d, int dtype, int W, int rank, int64_t 
     L.tseq_ext = take(multi ? static_cast<size_t>(L.N + 1) * 8 : 0);
     L.dx32 = take(multi ? static_cast<size_t>(n_loc) * d * 4 : 0);
     L.tmax_glob = take(64);
-    L.mu_buf = take(static_cast<size_t>(d) * 4);
+    L.mu_fx = take(static_cast<size_t>(d) * 8);  // this shard's pool sum mu, fixed point (k_mu_sum)
     // K >= 2: raw features [C_loc][K][d] (state) and 1/||T_bar_c|| (the T region holds T_bar)
     L.Traw = take(K > 1 ? static_cast<size_t>(L.C_loc) * K * d * es : 0, 1024);
     L.wslot = take(K > 1 ? static_cast<size_t>(L.C_loc) * 4 : 0);
-    // the same weights in bf16 (the mu row's P in the fused kernel), padded by one tile of zeros
+    // the same weights in bf16 (the out-of-pool rows' weight ring in the fused kernel), padded by
+    // one tile of zeros
     L.wmu = take(K > 1 ? static_cast<size_t>(L.C_loc + 128) * 2 : 0);
     // NEXT-3 stale self-duplicate lists (f2c_dcp_set_dup_mode): per hash entry the target
     // write index, per compacted row its hash entry, per 128-slot tile a count / offset, and
@@ -522,7 +523,31 @@ static int refresh_plan(f2c_dcp *h, Rank &R, int64_t m_glob, cudaStream_t st) {
     return F2C_OK;
 }
 
+static int enqueue_copy(f2c_dcp *h, Rank &R, const uint8_t *g, const int64_t *y, int64_t m_glob,
+                        cudaStream_t st);
+// this shard's mu over the slots the enqueue writes: sign -1 before the copy, +1 after
+static int mu_update(f2c_dcp *h, Rank &R, int64_t m_glob, int sign, cudaStream_t st) {
+    int64_t blocks = m_glob < 4 * static_cast<int64_t>(h->G) ? m_glob : 4 * static_cast<int64_t>(h->G);
+    if (blocks < 1) return F2C_OK;
+    const bool kk = h->K > 1;
+    k_mu_sum<<<static_cast<unsigned>(blocks), 256, 0, st>>>(
+        R.base + R.L.T, kk ? 0 : (h->dtype == F2C_BF16 ? 0 : 1), kk ? R.at<float>(R.L.wslot) : nullptr, h->d, m_glob,
+        h->E, h->C, R.lo, R.hi, h->refresh ? R.at<int64_t>(R.L.dst_seq) : nullptr, sign,
+        R.at<unsigned long long>(R.L.mu_fx));
+    LAUNCH_CHECK();
+    return F2C_OK;
+}
+
 static int enqueue_rank(f2c_dcp *h, Rank &R, const uint8_t *g, const int64_t *y, int64_t m_glob,
+                        cudaStream_t st) {
+    int rc = mu_update(h, R, m_glob, -1, st);
+    if (rc) return rc;
+    rc = enqueue_copy(h, R, g, y, m_glob, st);
+    if (rc) return rc;
+    return mu_update(h, R, m_glob, +1, st);
+}
+
+static int enqueue_copy(f2c_dcp *h, Rank &R, const uint8_t *g, const int64_t *y, int64_t m_glob,
                         cudaStream_t st) {
     if (h->K > 1) {
         int64_t blocks = (m_glob + 7) / 8;
@@ -828,6 +853,7 @@ static CombineArgs combine_args(f2c_dcp *h, Rank &R, const StepCtx &c, int64_t o
     a.seg_mx = R.at<float>(L.seg_mx);
     a.seg_O = R.at<float>(L.seg_O);
     a.T = R.base + L.T;
+    a.mu_fx = R.at<long long>(L.mu_fx);
     a.sc = R.sc();
     a.sc_w = R.sc();
     a.N = c.N;
@@ -1154,6 +1180,16 @@ extern "C" int f2c_dcp_set_state(f2c_dcp *h, const void *feats_host, const int64
         } else if (occ > 0) {
             k_pool_norm_max<<<static_cast<unsigned>((occ * 32 + 255) / 256), 256>>>(
                 R.base + R.L.T, occ, static_cast<int>(rb), h->dtype, R.sc());
+            CUDA_TRY(cudaGetLastError());
+        }
+        // mu over the restored slots lo .. lo + occ - 1
+        CUDA_TRY(cudaMemset(R.base + R.L.mu_fx, 0, static_cast<size_t>(h->d) * 8));
+        if (occ > 0) {
+            const int64_t blocks = occ < 4 * static_cast<int64_t>(h->G) ? occ : 4 * static_cast<int64_t>(h->G);
+            k_mu_sum<<<static_cast<unsigned>(blocks), 256>>>(
+                R.base + R.L.T, h->K > 1 ? 0 : (h->dtype == F2C_BF16 ? 0 : 1),
+                h->K > 1 ? R.at<float>(R.L.wslot) : nullptr, h->d, occ, R.lo, h->C, R.lo, R.hi, nullptr, +1,
+                R.at<unsigned long long>(R.L.mu_fx));
             CUDA_TRY(cudaGetLastError());
         }
         row0 += n;

@@ -24,9 +24,9 @@ struct Scalars {          // lives at the start of the per-rank scratch
     int tmax_bits;        // max ||T_c|| over rows ever written (float bits, >= 0)
     int n_pos;            // in-pool rows of the last loss call
     int n_neg;
-    int neg0;             // first compacted out-of-pool row (NEXT-3 hinge / max): n_pos + 1 rounded
+    int neg0;             // first compacted out-of-pool row (NEXT-3 hinge / max): n_pos rounded
                           // up to a warp (32 rows), so no warp mixes softmax rows and cosine rows
-    int n_rows;           // compacted rows the main kernel processes (n_pos + 1, or N + 1
+    int n_rows;           // compacted rows the main kernel processes (n_pos, or neg0 + N_neg
                           // when the out-of-pool rows go through it: NEXT-3 hinge / max)
     double loss3[3];      // L, L_ce, L_cos (fp64) of the last loss call
     unsigned long long n_pos_sum;  // sum of n_pos over loss calls (bench accounting)
@@ -227,6 +227,52 @@ __global__ void __launch_bounds__(256) k_rebuild_k(const __nv_bfloat16 *__restri
         wmu[r] = __float2bfloat16_rn(wv);
         float nrm = sqrtf(ss);
         if (nrm > 0.f) atomicMax(&sc->tmax_bits, __float_as_int(nrm));
+    }
+}
+
+// ------------------------------------------------------------------ the pool sum mu (L_cos)
+// mu = sum over occupied slots of w_c T_bar_c (w_c = 1 for K = 1; reading R3) is kept per
+// shard in 64-bit fixed point (quantum 2^-36): every slot's contribution is rounded once, the
+// same way whenever it is added or removed, and integer addition is exact and associative,
+// so the running sum equals the sum over the current pool exactly (any order, any number of
+// steps).  The enqueue subtracts the contributions of the slots it is about to overwrite
+// (sign -1, before the copy) and adds the new ones (sign +1, after); set_state rebuilds it.
+// Rows m of the call -> slot (dst_seq ? dst_seq[m] : E + m) mod C, skipped outside [lo, hi).
+// Thread t owns columns 2t, 2t+1; each CTA adds its column sums with one atomic each.
+constexpr float MU_FX_SCALE = 68719476736.0f;  // 2^36
+constexpr double MU_FX_INV = 1.0 / 68719476736.0;
+__device__ __forceinline__ long long mu_fx_of(float v) { return __float2ll_rn(v * MU_FX_SCALE); }
+__global__ void __launch_bounds__(256) k_mu_sum(const uint8_t *__restrict__ T, int dtype, const float *__restrict__ wslot,
+                                                int d, int64_t m, int64_t E, int64_t C, int64_t lo, int64_t hi,
+                                                const int64_t *__restrict__ dst_seq, int sign,
+                                                unsigned long long *__restrict__ mu_fx) {
+    const int c0 = 2 * threadIdx.x;
+    long long acc0 = 0, acc1 = 0;
+    for (int64_t j = blockIdx.x; j < m; j += gridDim.x) {
+        const int64_t c = (dst_seq ? dst_seq[j] : E + j) % C;
+        if (c < lo || c >= hi || c0 >= d) continue;
+        const int64_t sl = c - lo;
+        float v0, v1;
+        if (dtype == 0) {  // bf16 (T_bar for K >= 2)
+            const uint32_t u = *reinterpret_cast<const uint32_t *>(T + (sl * d + c0) * 2);
+            v0 = __uint_as_float(u << 16);
+            v1 = __uint_as_float(u & 0xffff0000u);
+        } else {
+            const float2 f = *reinterpret_cast<const float2 *>(T + (sl * d + c0) * 4);
+            v0 = f.x;
+            v1 = f.y;
+        }
+        if (wslot) {
+            const float w = wslot[sl];
+            v0 = __fmul_rn(w, v0);
+            v1 = __fmul_rn(w, v1);
+        }
+        acc0 += mu_fx_of(v0);
+        acc1 += mu_fx_of(v1);
+    }
+    if (c0 < d && (acc0 | acc1)) {
+        atomicAdd(mu_fx + c0, static_cast<unsigned long long>(sign * acc0));
+        atomicAdd(mu_fx + c0 + 1, static_cast<unsigned long long>(sign * acc1));
     }
 }
 
@@ -588,8 +634,7 @@ __global__ void k_dup_fill(const int64_t *__restrict__ lab, int64_t n_occ_loc, i
 // ------------------------------------------------------------------ a3: split + compaction
 // Single CTA (1024 threads): Eq. 6's split into in-pool (F_p^DCP) and out-of-pool
 // rows, compaction of the in-pool rows in batch order, per-row softmax coefficients,
-// the pairing check (D13), and the mu row (index N_pos) with coefficients (0, 0) so
-// that the main kernel's p = 2^0 = 1 gives sum_c T_c.
+// the pairing check (D13), and coefficients (0, +inf) -- p = 0 -- for the padding rows.
 struct CompactArgs {
     int64_t *tseq;            // [N] global write index of the target or -1 (written here when
                               // hslot/hvals are given: W = 1 resolves inside this kernel)
@@ -601,7 +646,7 @@ struct CompactArgs {
     float s, log2e_s;         // s, s*log2(e)
     int R_max;
     int neg_mode;             // 0: mu path; 1 (hinge) / 2 (max): out-of-pool rows are compacted
-                              // after the mu row (index neg0 + j, neg0 = n_pos + 1 rounded up to 32) and run through the kernel
+                              // after the in-pool rows (index neg0 + j, neg0 = n_pos rounded up to 32) and run through the kernel
     int *comp_idx;            // [N]: k >= 0 in-pool row k; -1 out-of-pool (mu path); -2 - k
                               // out-of-pool row compacted at k (neg_mode != 0)
     int *pos_row;             // [R_max]
@@ -662,7 +707,7 @@ __global__ void __launch_bounds__(1024) k_compact(CompactArgs a) {
     }
     __syncthreads();
     const int n_pos = s_tot;
-    const int neg0 = a.neg_mode ? (n_pos + 1 + 31) & ~31 : n_pos + 1;
+    const int neg0 = a.neg_mode ? (n_pos + 31) & ~31 : n_pos;
     const float tmax = __int_as_float(*a.tmax_bits);
     const float B = a.ref_scale * tmax;
     // this CTA's chunk, one row per thread; k = in-pool rows before row i (ballot scan)
@@ -711,15 +756,15 @@ __global__ void __launch_bounds__(1024) k_compact(CompactArgs a) {
         }
     }
     if (blockIdx.x != 0) return;
-    // (CTA 0) the mu row and the padding rows of the last row group
-    const int n_rows = a.neg_mode ? neg0 + static_cast<int>(a.N) - n_pos : n_pos + 1;
+    // (CTA 0) the padding rows of the last row group (the mu vector of the L_cos gradient is
+    // not a kernel row: it is kept incrementally by the enqueue, k_mu_sum)
+    const int n_rows = a.neg_mode ? neg0 + static_cast<int>(a.N) - n_pos : n_pos;
     if (a.excl)
-        for (int r = n_pos + tid; r < a.R_max; r += nt) a.row_hent[r] = -1;  // mu, out-of-pool, padding
-    // padding rows (after the mu row up to neg0, and after n_rows): e = -inf, so p = 0 (zero P
-    // operand in GEMM 2); the mu row: p = 1
+        for (int r = n_pos + tid; r < a.R_max; r += nt) a.row_hent[r] = -1;  // out-of-pool, padding
+    // padding rows (up to neg0, and after n_rows): e = -inf, so p = 0 (zero P operand in GEMM 2)
     for (int r = n_pos + tid; r < a.R_max; r += nt) {
         if (r >= neg0 && r < n_rows) continue;  // (out-of-pool rows, written above)
-        a.row_ab[r] = make_float2(0.f, r == n_pos ? 0.f : INFINITY);
+        a.row_ab[r] = make_float2(0.f, INFINITY);
         a.row_tgt[r] = -1;
         a.ttgt[r] = -INFINITY;
     }
@@ -744,8 +789,8 @@ __global__ void __launch_bounds__(256) k_gather(const uint8_t *__restrict__ x, c
                                                 const int *__restrict__ row_tgt, float2 *__restrict__ row_ab) {
     // one warp per compacted row, 8 rows per CTA
     const int k = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-    if (k >= sc->n_rows || k == sc->n_pos || (k > sc->n_pos && k < sc->neg0)) {
-        // the mu row and the padding rows of the last row group: zero operands (their
+    if (k >= sc->n_rows || (k >= sc->n_pos && k < sc->neg0)) {
+        // the padding rows of the last row group: zero operands (their
         // products are discarded; zeros keep the tensor pipe's switching power down)
         if (k < ((sc->n_rows + 127) & ~127)) {
             int4 *dst = reinterpret_cast<int4 *>(Xp + static_cast<int64_t>(k) * row_bytes);
@@ -813,12 +858,24 @@ struct CombineArgs {
     float lam;
     const int *seg_arg;         // [S][128] local argmax slot of a segment (neg_mode 2)
     const float *wslot;         // [C_loc] 1/||T_bar_c|| (K >= 2) or null
+    const long long *mu_fx;     // [d] this shard's sum_c w_c T_bar_c, fixed point (k_mu_sum)
     // the batch-label hash, cleared for the next loss call by the final per-row kernel
     // (k_combine / k_finalize_multi: block i clears its slice)
     int64_t *hkeys;
     unsigned long long *hvals;
     int H;
 };
+
+// this shard's mu (fixed point -> fp32), the lane's 16 columns in the load_bf16_row layout
+__device__ __forceinline__ void load_mu(const CombineArgs &a, int lane, float (&mu)[16]) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int dd = 128 * j + 4 * lane + u;
+            mu[4 * j + u] = dd < a.d ? static_cast<float>(static_cast<double>(__ldg(a.mu_fx + dd)) * MU_FX_INV) : 0.f;
+        }
+}
 
 __device__ __forceinline__ void clear_hash_slice(const CombineArgs &a, int64_t nblk) {
     const int64_t per = (a.H + nblk - 1) / nblk;
@@ -1080,9 +1137,9 @@ __device__ __forceinline__ void combine_row(const CombineArgs &a, int64_t i) {
         const float w = n_neg > 0 ? a.lam / static_cast<float>(n_neg) : 0.f;
         float phi;
         if (k == -1) {
-            // mu path: mu = sum over occupied slots of w_c T_bar_c (the mu row, index n_pos)
-            float mu[16], lsum, mx;
-            gather_row_partials(a, n_rg, n_pos, mu, lsum, mx);
+            // mu path: mu = sum over occupied slots of w_c T_bar_c (kept by the enqueue)
+            float mu[16];
+            load_mu(a, lane, mu);
             float dot = 0.f;
 #pragma unroll
             for (int q = 0; q < 16; ++q) {
@@ -1175,8 +1232,8 @@ __global__ void __launch_bounds__(256, 2) k_local_rows(CombineArgs a, float4 *__
         neg_row_local(a, n_rg, -2 - k, g, raw, carg);
         if (lane == 0) scal[i] = make_float4(raw, 0.f, 0.f, 0.f);
     } else {
-        float mu[16], lsum, mx, xh[16];
-        gather_row_partials(a, n_rg, n_pos, mu, lsum, mx);
+        float mu[16], xh[16];
+        load_mu(a, lane, mu);
         load_bf16_row(reinterpret_cast<const __nv_bfloat16 *>(a.x) + i * a.d, a.d, lane, a.inv_n[i], xh);
         float dot = 0.f;
 #pragma unroll
@@ -1260,8 +1317,7 @@ __device__ __forceinline__ void finalize_row(const CombineArgs &a, const float4 
                 int carg;
                 neg_row_local(a, n_rg, -2 - k, g, raw, carg);
             } else {
-                float lsum, mxl;
-                gather_row_partials(a, n_rg, n_pos, g, lsum, mxl);
+                load_mu(a, lane, g);
             }
 #pragma unroll
             for (int q = 0; q < 16; ++q) g[q] *= w * rs;
