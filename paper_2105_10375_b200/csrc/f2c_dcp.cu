@@ -523,31 +523,7 @@ static int refresh_plan(f2c_dcp *h, Rank &R, int64_t m_glob, cudaStream_t st) {
     return F2C_OK;
 }
 
-static int enqueue_copy(f2c_dcp *h, Rank &R, const uint8_t *g, const int64_t *y, int64_t m_glob,
-                        cudaStream_t st);
-// this shard's mu over the slots the enqueue writes: sign -1 before the copy, +1 after
-static int mu_update(f2c_dcp *h, Rank &R, int64_t m_glob, int sign, cudaStream_t st) {
-    int64_t blocks = m_glob < 4 * static_cast<int64_t>(h->G) ? m_glob : 4 * static_cast<int64_t>(h->G);
-    if (blocks < 1) return F2C_OK;
-    const bool kk = h->K > 1;
-    k_mu_sum<<<static_cast<unsigned>(blocks), 256, 0, st>>>(
-        R.base + R.L.T, kk ? 0 : (h->dtype == F2C_BF16 ? 0 : 1), kk ? R.at<float>(R.L.wslot) : nullptr, h->d, m_glob,
-        h->E, h->C, R.lo, R.hi, h->refresh ? R.at<int64_t>(R.L.dst_seq) : nullptr, sign,
-        R.at<unsigned long long>(R.L.mu_fx));
-    LAUNCH_CHECK();
-    return F2C_OK;
-}
-
 static int enqueue_rank(f2c_dcp *h, Rank &R, const uint8_t *g, const int64_t *y, int64_t m_glob,
-                        cudaStream_t st) {
-    int rc = mu_update(h, R, m_glob, -1, st);
-    if (rc) return rc;
-    rc = enqueue_copy(h, R, g, y, m_glob, st);
-    if (rc) return rc;
-    return mu_update(h, R, m_glob, +1, st);
-}
-
-static int enqueue_copy(f2c_dcp *h, Rank &R, const uint8_t *g, const int64_t *y, int64_t m_glob,
                         cudaStream_t st) {
     if (h->K > 1) {
         int64_t blocks = (m_glob + 7) / 8;
@@ -556,7 +532,7 @@ static int enqueue_copy(f2c_dcp *h, Rank &R, const uint8_t *g, const int64_t *y,
             reinterpret_cast<const __nv_bfloat16 *>(g), y, m_glob, h->K, h->d, h->E, h->C, R.lo, R.hi,
             R.at<__nv_bfloat16>(R.L.Traw), R.at<__nv_bfloat16>(R.L.T), R.at<float>(R.L.wslot),
             R.at<__nv_bfloat16>(R.L.wmu), R.at<int64_t>(R.L.lab), R.sc(),
-            h->refresh ? R.at<int64_t>(R.L.dst_seq) : nullptr);
+            h->refresh ? R.at<int64_t>(R.L.dst_seq) : nullptr, R.at<unsigned long long>(R.L.mu_fx));
         LAUNCH_CHECK();
         return F2C_OK;
     }
@@ -565,7 +541,8 @@ static int enqueue_copy(f2c_dcp *h, Rank &R, const uint8_t *g, const int64_t *y,
     if (blocks > static_cast<int64_t>(h->G) * 8) blocks = static_cast<int64_t>(h->G) * 8;
     k_enqueue<<<static_cast<unsigned>(blocks), 256, 0, st>>>(
         g, y, m_glob, h->E, h->C, R.lo, R.hi, row_bytes, h->dtype, R.base + R.L.T,
-        R.at<int64_t>(R.L.lab), R.sc(), h->refresh ? R.at<int64_t>(R.L.dst_seq) : nullptr);
+        R.at<int64_t>(R.L.lab), R.sc(), h->refresh ? R.at<int64_t>(R.L.dst_seq) : nullptr,
+        R.at<unsigned long long>(R.L.mu_fx));
     LAUNCH_CHECK();
     return F2C_OK;
 }

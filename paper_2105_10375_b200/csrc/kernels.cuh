@@ -63,6 +63,31 @@ template <>
 __device__ __forceinline__ float from_f<float>(float v) { return v; }
 
 // ------------------------------------------------------------------ a1: enqueue
+// The pool sum mu = sum over occupied slots of w_c T_bar_c (w_c = 1 for K = 1; reading R3) of
+// the L_cos gradient is kept per shard in 64-bit fixed point (quantum 2^-36): every slot's
+// contribution is rounded once, the same way whenever it is added or removed, and integer
+// addition is exact and associative, so the running sum equals the sum over the current pool
+// exactly (any order, any number of steps).  The enqueue kernels read each overwritten row
+// before storing the new one and add (new - old) contributions to a per-warp sum in shared
+// memory (lanes own distinct columns: plain adds), then one global atomic per column per
+// block; set_state rebuilds it (k_mu_sum).
+constexpr float MU_FX_SCALE = 68719476736.0f;  // 2^36
+constexpr double MU_FX_INV = 1.0 / 68719476736.0;
+__device__ __forceinline__ long long mu_fx_of(float v) { return __float2ll_rn(v * MU_FX_SCALE); }
+constexpr int MU_WARPS = 8;  // (256-thread enqueue blocks)
+__device__ __forceinline__ void mu_block_init(long long (*smu)[512], int d) {
+    for (int i = threadIdx.x; i < MU_WARPS * 512; i += blockDim.x) smu[i / 512][i % 512] = 0;
+    __syncthreads();
+}
+__device__ __forceinline__ void mu_block_flush(const long long (*smu)[512], int d, unsigned long long *mu_fx) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < d; i += blockDim.x) {
+        long long v = 0;
+#pragma unroll
+        for (int w = 0; w < MU_WARPS; ++w) v += smu[w][i];
+        if (v) atomicAdd(mu_fx + i, static_cast<unsigned long long>(v));
+    }
+}
 // Eq. 7 / Algorithm 1: global block row j -> slot (E+j) mod C.
 // One warp per block row; the rows owned by this shard [lo, hi) are copied with
 // 16-byte vector loads/stores (bit-exact), labels written by lane 0, and the running
@@ -71,10 +96,14 @@ __global__ void __launch_bounds__(256) k_enqueue(const uint8_t *__restrict__ g, 
                                                  int64_t m_glob, int64_t E, int64_t C, int64_t lo, int64_t hi,
                                                  int row_bytes, int dtype, uint8_t *__restrict__ T,
                                                  int64_t *__restrict__ lab, Scalars *sc,
-                                                 const int64_t *__restrict__ dst_seq) {
+                                                 const int64_t *__restrict__ dst_seq,
+                                                 unsigned long long *__restrict__ mu_fx) {
     __shared__ float wmax[8];
+    __shared__ long long smu[MU_WARPS][512];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+    const int epv = dtype == 0 ? 8 : 4;  // elements per 16-byte vector
+    mu_block_init(smu, (row_bytes / 16) * epv);  // d columns
     float nmax = 0.f;
     for (int64_t j = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + wib; j < m_glob; j += nwarps) {
         // pure Eq. 7: row j -> slot (E + j) mod C; refresh-in-place (NEXT-3): the planned slot
@@ -90,11 +119,14 @@ __global__ void __launch_bounds__(256) k_enqueue(const uint8_t *__restrict__ g, 
         const int nvec = row_bytes / 16;
         float ss = 0.f;
         for (int u0 = 0; u0 < nvec; u0 += 64) {  // 2 independent 16-B loads in flight per lane
-            int4 v[2];
+            int4 v[2], ov[2];
 #pragma unroll
             for (int q = 0; q < 2; ++q) {
                 const int u = u0 + q * 32 + lane;
-                if (u < nvec) v[q] = __ldcs(src + u);
+                if (u < nvec) {
+                    v[q] = __ldcs(src + u);
+                    ov[q] = dst[u];  // the overwritten row (its mu contribution leaves)
+                }
             }
 #pragma unroll
             for (int q = 0; q < 2; ++q) {
@@ -103,14 +135,21 @@ __global__ void __launch_bounds__(256) k_enqueue(const uint8_t *__restrict__ g, 
                 __stcs(dst + u, v[q]);
                 const uint32_t w[4] = {static_cast<uint32_t>(v[q].x), static_cast<uint32_t>(v[q].y),
                                        static_cast<uint32_t>(v[q].z), static_cast<uint32_t>(v[q].w)};
+                const uint32_t o[4] = {static_cast<uint32_t>(ov[q].x), static_cast<uint32_t>(ov[q].y),
+                                       static_cast<uint32_t>(ov[q].z), static_cast<uint32_t>(ov[q].w)};
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
                     if (dtype == 0) {
                         const float a = __uint_as_float(w[i] << 16), b = __uint_as_float(w[i] & 0xffff0000u);
                         ss += a * a + b * b;
+                        const float oa = __uint_as_float(o[i] << 16), ob = __uint_as_float(o[i] & 0xffff0000u);
+                        const int col = u * 8 + 2 * i;
+                        smu[wib][col] += mu_fx_of(a) - mu_fx_of(oa);
+                        smu[wib][col + 1] += mu_fx_of(b) - mu_fx_of(ob);
                     } else {
                         const float a = __uint_as_float(w[i]);
                         ss += a * a;
+                        smu[wib][u * 4 + i] += mu_fx_of(a) - mu_fx_of(__uint_as_float(o[i]));
                     }
                 }
             }
@@ -120,6 +159,7 @@ __global__ void __launch_bounds__(256) k_enqueue(const uint8_t *__restrict__ g, 
         if (lane == 0) lab[c - lo] = yl;
         nmax = fmaxf(nmax, ss);
     }
+    mu_block_flush(smu, (row_bytes / 16) * epv, mu_fx);
     // one atomic per block for the running norm bound (the softmax reference, R1)
     if (lane == 0) wmax[wib] = nmax;
     __syncthreads();
@@ -142,10 +182,13 @@ __global__ void __launch_bounds__(256) k_enqueue_k(const __nv_bfloat16 *__restri
                                                    int64_t lo, int64_t hi, __nv_bfloat16 *__restrict__ Traw,
                                                    __nv_bfloat16 *__restrict__ Tbar, float *__restrict__ wslot,
                                                    __nv_bfloat16 *__restrict__ wmu, int64_t *__restrict__ lab,
-                                                   Scalars *sc, const int64_t *__restrict__ dst_seq) {
+                                                   Scalars *sc, const int64_t *__restrict__ dst_seq,
+                                                   unsigned long long *__restrict__ mu_fx) {
     __shared__ float wmax[8];
+    __shared__ long long smu[MU_WARPS][512];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+    mu_block_init(smu, d);
     float nmax = 0.f;
     for (int64_t j = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + wib; j < m_glob; j += nwarps) {
         const int64_t c = (dst_seq ? dst_seq[j] : E + j) % C;
@@ -173,26 +216,39 @@ __global__ void __launch_bounds__(256) k_enqueue_k(const __nv_bfloat16 *__restri
         }
         float ss = 0.f;
         const float invK = 1.0f / static_cast<float>(K);
+        const float wold = wslot[c - lo];  // the overwritten slot's mu contribution leaves
+        float mfv[16];
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
             const int col = e * 32 + lane;
+            mfv[e] = 0.f;
             if (col < d) {
                 const __nv_bfloat16 m = __float2bfloat16_rn(acc[e] * invK);
+                const float ob = __bfloat162float(Tbar[(c - lo) * d + col]);
+                smu[wib][col] -= mu_fx_of(__fmul_rn(wold, ob));
                 Tbar[(c - lo) * d + col] = m;
                 const float mf = __bfloat162float(m);
+                mfv[e] = mf;
                 ss += mf * mf;
             }
         }
 #pragma unroll
         for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+        const float wv = ss > 0.f ? rsqrtf(ss) : 0.f;  // (every lane holds the full ss)
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+            const int col = e * 32 + lane;
+            if (col < d) smu[wib][col] += mu_fx_of(__fmul_rn(wv, mfv[e]));
+        }
+        __syncwarp();  // (every lane has read wold)
         if (lane == 0) {
             lab[c - lo] = yl;
-            const float wv = ss > 0.f ? rsqrtf(ss) : 0.f;
             wslot[c - lo] = wv;
             wmu[c - lo] = __float2bfloat16_rn(wv);
         }
         nmax = fmaxf(nmax, ss);
     }
+    mu_block_flush(smu, d, mu_fx);
     if (lane == 0) wmax[wib] = nmax;
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -231,17 +287,10 @@ __global__ void __launch_bounds__(256) k_rebuild_k(const __nv_bfloat16 *__restri
 }
 
 // ------------------------------------------------------------------ the pool sum mu (L_cos)
-// mu = sum over occupied slots of w_c T_bar_c (w_c = 1 for K = 1; reading R3) is kept per
-// shard in 64-bit fixed point (quantum 2^-36): every slot's contribution is rounded once, the
-// same way whenever it is added or removed, and integer addition is exact and associative,
-// so the running sum equals the sum over the current pool exactly (any order, any number of
-// steps).  The enqueue subtracts the contributions of the slots it is about to overwrite
-// (sign -1, before the copy) and adds the new ones (sign +1, after); set_state rebuilds it.
-// Rows m of the call -> slot (dst_seq ? dst_seq[m] : E + m) mod C, skipped outside [lo, hi).
-// Thread t owns columns 2t, 2t+1; each CTA adds its column sums with one atomic each.
-constexpr float MU_FX_SCALE = 68719476736.0f;  // 2^36
-constexpr double MU_FX_INV = 1.0 / 68719476736.0;
-__device__ __forceinline__ long long mu_fx_of(float v) { return __float2ll_rn(v * MU_FX_SCALE); }
+// set_state: mu over the restored slots from scratch (the same per-slot contributions as the
+// enqueue kernels' running sum).  Rows m of the call -> slot (dst_seq ? dst_seq[m] : E + m)
+// mod C, skipped outside [lo, hi); sign -1 subtracts.  Thread t owns columns 2t, 2t+1; each
+// CTA adds its column sums with one atomic each.
 __global__ void __launch_bounds__(256) k_mu_sum(const uint8_t *__restrict__ T, int dtype, const float *__restrict__ wslot,
                                                 int d, int64_t m, int64_t E, int64_t C, int64_t lo, int64_t hi,
                                                 const int64_t *__restrict__ dst_seq, int sign,
