@@ -19,6 +19,7 @@
 #include "../../include/f2c_dcp.h"
 #include "dcp_main.cuh"
 #include "kernels.cuh"
+#include "dcp_pc4.cuh"
 
 using namespace f2c;
 
@@ -129,8 +130,9 @@ static Layout make_layout(int64_t C, int d, int dtype, int W, int rank, int64_t 
     if (rank < 0) L.C_loc = (C + W - 1) / W;
     L.N = n_loc * W;
     L.Mg = m_loc * W;
-    // row groups of 64 (TP64) or 128 (PC); + 31 for the warp alignment of the NEXT-3 out-of-pool rows
-    L.R_max = (L.N + 32 + 127) / 128 * 128;
+    // row groups of 64 (TP64), 128 (PC) or 256 (PC4); + 31 for the warp alignment of the NEXT-3
+    // out-of-pool rows
+    L.R_max = (L.N + 32 + 255) / 256 * 256;
     L.S_max = L.R_max / 64 + 2 * G_MAX + 1;  // units R*S <= 2G + R (tp_choose_S)
     int H = 64;
     while (H < 2 * L.N) H <<= 1;
@@ -215,7 +217,7 @@ struct Rank {
     int64_t lo, hi;
     Layout L;
     uint8_t *base;
-    CUtensorMap tmT, tmX, tm3p, tm3q, tmO;
+    CUtensorMap tmT, tmX, tm3p, tm3q, tmO, tm4p;
     template <typename P>
     P *at(size_t off) const { return reinterpret_cast<P *>(base + off); }
     Scalars *sc() const { return at<Scalars>(L.sc); }
@@ -249,6 +251,8 @@ struct f2c_dcp {
     unsigned long long npos_base = 0;
     unsigned long long *dbg = nullptr;  // debug timestamps (f2c_dcp_debug_timestamps)
     bool use_tp64 = false;
+    int pc4_mode = 0;               // 1: the 2-SM pair kernel where it applies (F2C_KERNEL=pc4)
+    int G4 = 0;                     // co-resident 4-CTA clusters of dcp_pc4_kernel (its persistent grid / 4)
     int dbg_flags = 0;              // timing experiments (F2C_DBG_FLAGS)
     int dbg_cluster = 0;            // debug timestamps of this cluster (F2C_DBG_CLUSTER)
     ~f2c_dcp() {
@@ -256,6 +260,18 @@ struct f2c_dcp {
         if (n_app_host) cudaFreeHost(n_app_host);
     }
 };
+
+// Which fused kernel a loss call runs (the combine must read the partials with the same row
+// grouping): 1 = dcp_tp64_kernel (F2C_KERNEL=tp64), 2 = dcp_pc4_kernel (F2C_KERNEL=pc4: 2-SM
+// pairs, 256-row groups; default variant, d % 256 == 0), 0 = dcp_pc_kernel (the default: it
+// measured faster on every bench shape but one).
+static int kernel_kind(const f2c_dcp *h, int64_t N) {
+    (void)N;
+    const bool dflt = h->neg_mode() == 0 && !h->excl_dup;
+    if (h->use_tp64 && dflt) return 1;
+    if (dflt && h->K == 1 && h->d % 256 == 0 && h->G4 > 0 && h->pc4_mode > 0) return 2;
+    return 0;
+}
 
 static int64_t occ_local(const f2c_dcp *h, const Rank &R) {
     const int64_t C_occ = h->E < h->C ? h->E : h->C;
@@ -293,12 +309,13 @@ static int make_tmap_bf16(CUtensorMap *m, void *ptr, int64_t rows, int d, int bo
 
 // The pool viewed as [d/64 chunks][rows][64] so that one box [64, 128, cps] lands in
 // shared memory chunk-major: cps SW128 blocks of [128 slots x 64 d] (16 KB each).
-static int make_tmap_pool3d(CUtensorMap *m, void *ptr, int64_t rows, int d, cuuint32_t cps) {
+static int make_tmap_pool3d(CUtensorMap *m, void *ptr, int64_t rows, int d, cuuint32_t cps,
+                            cuuint32_t box_rows = 128) {
     auto fn = encode_fn();
     if (!fn) return fail(F2C_ECUDA, "cuTensorMapEncodeTiled unavailable");
     cuuint64_t dims[3] = {64, static_cast<cuuint64_t>(rows < 1 ? 1 : rows), static_cast<cuuint64_t>(d / 64)};
     cuuint64_t strides[2] = {static_cast<cuuint64_t>(d) * 2, 128};
-    cuuint32_t box[3] = {64, 128, cps};
+    cuuint32_t box[3] = {64, box_rows, cps};
     cuuint32_t es[3] = {1, 1, 1};
     CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, ptr, dims, strides, box, es,
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -423,6 +440,7 @@ int f2c_dcp_create_k(int64_t C, int32_t K, int32_t d, int32_t dtype, int32_t wor
             if ((rc = make_tmap_bf16(&R.tmT, R.base + R.L.T, R.hi - R.lo, d, TP_TILE)) ||
                 (rc = make_tmap_pool3d(&R.tm3p, R.base + R.L.T, R.hi - R.lo, d, 2)) ||
                 (rc = make_tmap_pool3d(&R.tm3q, R.base + R.L.T, R.hi - R.lo, d, (d % 256 == 0) ? 4 : 2)) ||
+                (rc = make_tmap_pool3d(&R.tm4p, R.base + R.L.T, R.hi - R.lo, d, 2, 64)) ||
                 (rc = make_tmap_bf16(&R.tmX, R.base + R.L.X_pos, R.L.R_max, d, TP_R)) ||
                 (rc = make_tmap_segO(&R.tmO, R.base + R.L.seg_O, R.L.S_max * 128, d))) {
                 delete h;
@@ -438,6 +456,7 @@ int f2c_dcp_create_k(int64_t C, int32_t K, int32_t d, int32_t dtype, int32_t wor
     {
         const char *kv = getenv("F2C_KERNEL");
         h->use_tp64 = kv && strcmp(kv, "tp64") == 0 && K == 1;
+        h->pc4_mode = !kv ? 0 : strcmp(kv, "pc4") == 0 ? 1 : strcmp(kv, "pc") == 0 ? -1 : 0;
         const char *fl = getenv("F2C_DBG_FLAGS");  // timing experiments only (results void)
         h->dbg_flags = fl ? atoi(fl) : 0;
     }
@@ -446,9 +465,33 @@ int f2c_dcp_create_k(int64_t C, int32_t K, int32_t d, int32_t dtype, int32_t wor
         cudaFuncSetAttribute(dcp_pc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              PC_SMEM_BYTES) != cudaSuccess ||
         cudaFuncSetAttribute(dcp_pc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             PC_SMEM_BYTES) != cudaSuccess) {
+                             PC_SMEM_BYTES) != cudaSuccess ||
+        cudaFuncSetAttribute(dcp_pc4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             P4_SMEM_BYTES) != cudaSuccess) {
         delete h;
         return fail(F2C_ECUDA, "cudaFuncSetAttribute(smem) failed");
+    }
+    {   // 4-CTA clusters do not tile every GPC: the persistent grid is what fits at once
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 4;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.gridDim = dim3(static_cast<unsigned>((h->G / 4) * 4));
+        cfg.blockDim = dim3(P4_THREADS);
+        cfg.dynamicSmemBytes = P4_SMEM_BYTES;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        int ncl = 0;
+        if (cudaOccupancyMaxActiveClusters(&ncl, dcp_pc4_kernel, &cfg) != cudaSuccess) {
+            cudaGetLastError();
+            ncl = 0;
+        }
+        h->G4 = ncl < h->G / 4 ? ncl : h->G / 4;
+        const int64_t R4 = (n_local_max * world + 32 + 255) / 256;  // 256-row groups (as L.R_max)
+        if (h->G4 > 0 && 2 + (R4 + h->G4 - 1) / h->G4 > PC_MAX_UNITS) h->G4 = 0;  // (unit list in smem)
+        if (getenv("F2C_VERBOSE")) fprintf(stderr, "f2c: dcp_pc4_kernel clusters %d (of %d SMs)\n", h->G4, h->G);
     }
     h->multi = world > 1 || (rank == 0 && force_multi());
     if (h->multi && !h->emulated) {
@@ -772,7 +815,8 @@ static int phase_main(f2c_dcp *h, Rank &R, const StepCtx &c, int64_t occ_loc, co
         h->ev_used += 2;
         CUDA_TRY(cudaEventRecord(e0, c.st));
     }
-    if (h->use_tp64 && h->neg_mode() == 0 && !h->excl_dup) {
+    const int kind = kernel_kind(h, c.N);
+    if (kind == 1) {
         dcp_tp64_kernel<<<h->G, TP_THREADS, TP_SMEM_BYTES, c.st>>>(R.tmT, R.tmX, p);
     } else {
         PCParams q;
@@ -806,7 +850,9 @@ static int phase_main(f2c_dcp *h, Rank &R, const StepCtx &c, int64_t occ_loc, co
         q.dbg_cluster = h->dbg_cluster;
         q.dbg_flags = h->dbg_flags;
         q.run_flag = run_flag;
-        if (q.excl)
+        if (kind == 2)
+            dcp_pc4_kernel<<<h->G4 * 4, P4_THREADS, P4_SMEM_BYTES, c.st>>>(R.tm4p, R.tm3p, q);
+        else if (q.excl)
             dcp_pc_kernel<true><<<(h->G / 2) * 2, PC_THREADS, smem, c.st>>>(R.tm3p, R.tm3q, R.tmO, q);
         else
             dcp_pc_kernel<false><<<(h->G / 2) * 2, PC_THREADS, smem, c.st>>>(R.tm3p, R.tm3q, R.tmO, q);
@@ -837,9 +883,9 @@ static CombineArgs combine_args(f2c_dcp *h, Rank &R, const StepCtx &c, int64_t o
     a.C_occ = h->E < h->C ? h->E : h->C;
     a.d = h->d;
     a.dtype = h->dtype;
-    const bool tp64 = h->use_tp64 && h->neg_mode() == 0 && !h->excl_dup;
-    a.G = tp64 ? h->G : h->G / 2;
-    a.rows_per_group = tp64 ? TP_R : PC_R;
+    const int kind = kernel_kind(h, c.N);
+    a.G = kind == 1 ? h->G : kind == 2 ? h->G4 : h->G / 2;
+    a.rows_per_group = kind == 1 ? TP_R : kind == 2 ? P4_RG : PC_R;
     a.n_tiles = static_cast<int>((occ + TP_TILE - 1) / TP_TILE);
     a.s = c.s;
     a.margin_l2 = c.s * c.m * 1.4426950408889634f;
@@ -867,7 +913,7 @@ static CombineArgs combine_args(f2c_dcp *h, Rank &R, const StepCtx &c, int64_t o
 // (its CTAs exit at once unless some row was refined).  Below s = 68 no row with |cos| <= 1 can
 // get there, so the pass is not even launched.
 static int phase_refine(f2c_dcp *h, Rank &R, const StepCtx &c, int64_t occ) {
-    if (!(c.s > 68.f) || (h->use_tp64 && h->neg_mode() == 0 && !h->excl_dup)) return F2C_OK;
+    if (!(c.s > 68.f) || kernel_kind(h, c.N) == 1) return F2C_OK;
     NvtxRange nv("f2c: R1 refinement pass");
     CombineArgs a = combine_args(h, R, c, occ, nullptr);
     k_refine_ref<<<static_cast<unsigned>((c.N + 255) / 256), 256, 0, c.st>>>(a, R.at<float2>(R.L.row_ab));

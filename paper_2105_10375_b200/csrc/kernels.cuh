@@ -841,7 +841,7 @@ __global__ void __launch_bounds__(256) k_gather(const uint8_t *__restrict__ x, c
     if (k >= sc->n_rows || (k >= sc->n_pos && k < sc->neg0)) {
         // the padding rows of the last row group: zero operands (their
         // products are discarded; zeros keep the tensor pipe's switching power down)
-        if (k < ((sc->n_rows + 127) & ~127)) {
+        if (k < ((sc->n_rows + 255) & ~255)) {  // (256-row groups of dcp_pc4_kernel)
             int4 *dst = reinterpret_cast<int4 *>(Xp + static_cast<int64_t>(k) * row_bytes);
             for (int u = lane; u < row_bytes / 16; u += 32) dst[u] = make_int4(0, 0, 0, 0);
         }
