@@ -48,10 +48,11 @@ __global__ void __cluster_dims__(2, 1, 1) probe(int mode, const __nv_bfloat16 *A
     const uint32_t cr = ctarank();
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     // operand rows held by this CTA
+    const bool g1 = mode == 1 || mode >= 7;            // cta_group::1 modes (each CTA on its own)
     const int arows = (mode >= 3 && mode != 6) ? 64 : 128;
-    const int a0 = (mode == 1) ? 0 : cr * arows;       // global A row offset
-    const int brows = mode == 1 ? 128 : 64;
-    const int b0 = (mode == 1) ? 0 : cr * 64;          // global B (N) row offset
+    const int a0 = g1 ? 0 : cr * arows;                // global A row offset
+    const int brows = g1 ? 128 : 64;
+    const int b0 = g1 ? 0 : cr * 64;                   // global B (N) row offset
     for (int i = tid; i < arows * 64; i += blockDim.x) {
         const int r = i / 64, k = i % 64;
         *reinterpret_cast<__nv_bfloat16 *>(sA + sw128_off(r, k)) = A[(a0 + r) * 64 + k];
@@ -66,7 +67,7 @@ __global__ void __cluster_dims__(2, 1, 1) probe(int mode, const __nv_bfloat16 *A
         fence_mbar_init();
     }
     if (warp == 0) {
-        if (mode == 1) {
+        if (g1) {
             asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(&tbase)) : "memory");
             asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
         } else {
@@ -98,20 +99,22 @@ __global__ void __cluster_dims__(2, 1, 1) probe(int mode, const __nv_bfloat16 *A
     __syncthreads();
     cl_sync();
     tc_fence_after();
-    const int M = (mode == 2 || mode == 6) ? 256 : 128;
+    const int M = (mode == 2 || mode == 6) ? 256 : mode >= 7 ? 64 : 128;
     const uint32_t idesc = umma_idesc_bf16(M, 128, 0, 0);
-    const bool issuer = (mode == 1) || cr == 0;
+    const bool issuer = g1 || cr == 0;
     // modes 4/5: A (this CTA's 64 rows x 64 K, bf16 pairs per 32-bit column) into TMEM columns
     // [128, 160): mode 4 = rows on lanes 0-63 (lanes 64-127 zero); mode 5 = rows on lanes 0-63
     // for K 0-31 and on lanes 64-127 for K 32-63 (columns [128, 144))
     const uint32_t ACOL = 128;
-    if (mode >= 4 && warp < 4) {  // (mode 6: M = 256, rows 0-127 of this CTA on lanes 0-127)
+    if (mode >= 4 && mode != 7 && warp < 4) {  // (mode 6: M = 256, rows 0-127 of this CTA on lanes 0-127)
         uint32_t w[32];
         const int lr = warp * 32 + lane;  // TMEM lane
         for (int j = 0; j < 32; ++j) {
             int row = -1, k0 = 0;
             if (mode == 4 && lr < 64) { row = lr; k0 = 2 * j; }
             if (mode == 6) { row = lr; k0 = 2 * j; }
+            if (mode == 8 && lr < 64) { row = lr; k0 = 2 * j; }                              // M = 64: rows on lanes 0-63
+            if (mode == 9 && (lr & 31) < 16) { row = (lr >> 5) * 16 + (lr & 15); k0 = 2 * j; }  // lanes 0-15 of each quadrant
             if (mode == 5 && j < 16) { row = lr & 63; k0 = (lr < 64 ? 0 : 32) + 2 * j; }
             uint32_t v = 0;
             if (row >= 0) {
@@ -139,7 +142,14 @@ __global__ void __cluster_dims__(2, 1, 1) probe(int mode, const __nv_bfloat16 *A
             const uint64_t ad = umma_desc_sw128(smem_u32(sA) + ks * 32, 16, 1024);
             const uint64_t bd = umma_desc_sw128(smem_u32(sB) + ks * 32, 16, 1024);
             const uint32_t acc = ks > 0;
-            if (mode >= 4) {
+            if (mode == 7) {
+                asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n"
+                             ::"r"(tmem), "l"(ad), "l"(bd), "r"(idesc), "r"(acc) : "memory");
+            } else if (mode >= 8) {
+                const uint32_t acol = tmem + ACOL + ks * 8;
+                asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n"
+                             ::"r"(tmem), "r"(acol), "l"(bd), "r"(idesc), "r"(acc) : "memory");
+            } else if (mode >= 4) {
                 // A from TMEM: K step ks = 16 bf16 = 8 columns (modes 4, 6) or 4 columns (mode 5)
                 const uint32_t acol = tmem + ACOL + ks * (mode == 5 ? 4 : 8);
                 asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n}\n"
@@ -151,7 +161,7 @@ __global__ void __cluster_dims__(2, 1, 1) probe(int mode, const __nv_bfloat16 *A
                 asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n"
                              ::"r"(tmem), "l"(ad), "l"(bd), "r"(idesc), "r"(acc) : "memory");
         }
-        if (mode == 1)
+        if (g1)
             asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&bar)) : "memory");
         else
             asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
@@ -172,7 +182,7 @@ __global__ void __cluster_dims__(2, 1, 1) probe(int mode, const __nv_bfloat16 *A
     __syncthreads();
     cl_sync();
     if (warp == 0) {
-        if (mode == 1)
+        if (g1)
             asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem) : "memory");
         else
             asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 256;" ::"r"(tmem) : "memory");
@@ -212,7 +222,7 @@ int main() {
     cudaMemcpy(dA, Ah.data(), MR * K * 2, cudaMemcpyHostToDevice);
     cudaMemcpy(dB, Bh.data(), NR * K * 2, cudaMemcpyHostToDevice);
     cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 40000);
-    for (int mode = 1; mode <= 6; ++mode) {
+    for (int mode = 1; mode <= 9; ++mode) {
         cudaMemset(dump, 0xff, 2 * 128 * 128 * 4);
         cudaMemset(derr, 0, 4);
         probe<<<2, 128, 40000>>>(mode, dA, dB, dump, derr);
@@ -224,7 +234,7 @@ int main() {
         printf("mode %d: launch/sync %s, timeout flag %d\n", mode, cudaGetErrorString(e), herr);
         if (e != cudaSuccess) return 1;
         // for every expected D row (M rows of this mode), find (cta, lane) whose 128 columns match it
-        const int M = (mode == 2 || mode == 6) ? 256 : 128;
+        const int M = (mode == 2 || mode == 6) ? 256 : mode >= 7 ? 64 : 128;
         int found = 0, col_half_match = 0;
         for (int r = 0; r < M; ++r) {
             int where = -1;
@@ -235,13 +245,13 @@ int main() {
                     if (ok) where = cta * 128 + ln;
                 }
             if (where >= 0) ++found;
-            if (r < 4 || r == M / 2 || r == M / 2 + 1 || r == M - 1 || (mode == 3 && r % 16 == 0))
+            if (r < 4 || r == M / 2 || r == M / 2 + 1 || r == M - 1 || ((mode == 3 || mode >= 7) && r % 8 == 0))
                 printf("  D row %3d -> %s cta %d lane %d\n", r, where >= 0 ? "found at" : "NOT FOUND", where >= 0 ? where / 128 : -1,
                        where >= 0 ? where % 128 : -1);
             (void)col_half_match;
         }
         printf("  rows found: %d of %d\n", found, M);
-        if (mode >= 3 && mode != 6) {  // partial matches: 64-column halves of D rows anywhere in the dumps
+        if (mode >= 3 && mode != 6 && mode < 7) {  // partial matches: 64-column halves of D rows anywhere in the dumps
             int shown = 0;
             for (int cta = 0; cta < 2; ++cta)
                 for (int ln = 0; ln < 128; ++ln)
