@@ -225,6 +225,12 @@ int f2c_last_launch_count(void);
 int f2c_dcp_profile(f2c_dcp *h, int enable);
 int f2c_dcp_profile_read(f2c_dcp *h, double *main_ms, int64_t *launches, int64_t *n_pos_sum);
 
+/* Which fused loss kernel a loss call with n_global global rows runs on this handle (the
+ * choice depends on the variant, K, d and F2C_KERNEL): *kind = 0
+ * dcp_pc_kernel (CTA pairs, 128-row groups), 1 dcp_tp64_kernel, 2 dcp_pc4_kernel
+ * (cta_group::2 SM pairs, 256-row groups); *ctas = its persistent grid (CTAs).  Host only. */
+int f2c_dcp_fused_kernel(f2c_dcp *h, int64_t n_global, int32_t *kind, int32_t *ctas);
+
 /* Release host resources and the NCCL communicator.  The caller frees state_buf. */
 void f2c_dcp_destroy(f2c_dcp *h);
 

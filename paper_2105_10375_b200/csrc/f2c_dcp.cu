@@ -1224,6 +1224,14 @@ extern "C" int f2c_dcp_set_state(f2c_dcp *h, const void *feats_host, const int64
     return F2C_OK;
 }
 
+extern "C" int f2c_dcp_fused_kernel(f2c_dcp *h, int64_t n_global, int32_t *kind, int32_t *ctas) {
+    if (!h || !kind || !ctas) return fail(F2C_EINVAL, "NULL argument");
+    const int k = kernel_kind(h, n_global);
+    *kind = k;
+    *ctas = k == 1 ? h->G : k == 2 ? h->G4 * 4 : (h->G / 2) * 2;
+    return F2C_OK;
+}
+
 extern "C" int f2c_dcp_profile(f2c_dcp *h, int enable) {
     if (!h) return fail(F2C_EINVAL, "NULL handle");
     if (enable) {

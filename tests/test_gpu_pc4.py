@@ -44,6 +44,8 @@ def _run(dcp, c):
     head = dcp.DCPHead(C, d, dcp.BF16, world=W, rank=0 if W == 1 else -1, n_local_max=c["n_loc"],
                        m_local_max=m_loc)
     head.set_lcos(c["phi_mode"], False, 1.0)
+    kind, ctas = head.fused_kernel(c["n_loc"] * W)
+    assert kind == 2 and ctas > 0 and ctas % 4 == 0, (kind, ctas)  # the cta_group::2 kernel runs
     pool = oracle.Pool(C, d, oracle.BF16)
     rng = np.random.default_rng(c["seed"])
     Mg = m_loc * W
