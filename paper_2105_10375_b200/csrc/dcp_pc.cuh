@@ -813,9 +813,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                             mbar_wait(&aux->qfull[st], qph);
                             tc_fence_after();
                             // 8 K steps of 16 slots: A = P (K-major, two 64-slot chunks), B = pool MN-major
-                            umma_ss_stage8(tmem + g * cps * 64, umma_desc_sw128(sPa + b * PC_PBYTES, 16, 1024),
-                                           umma_desc_sw128(sTa + st * PC_STAGE_BYTES, 16384, 1024), idesc,
-                                           !first, &aux->qempty[st]);
+                            if (p.dbg_flags & 256)  // timing / power experiment: no GEMM-2 MMAs
+                                umma_commit_e(&aux->qempty[st]);
+                            else
+                                umma_ss_stage8(tmem + g * cps * 64, umma_desc_sw128(sPa + b * PC_PBYTES, 16, 1024),
+                                               umma_desc_sw128(sTa + st * PC_STAGE_BYTES, 16384, 1024), idesc,
+                                               !first, &aux->qempty[st]);
                         }
                         umma_commit_mc_e(&aux->pslot_free[b], 0x1);  // tell the producer slot b is free
                         if (dbg) dbg[7] = clock64();
