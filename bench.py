@@ -380,7 +380,10 @@ def run_ours(args, cfg, world, rank, local_rank, device_only=False):
     t_launch = main_ms / max(1, main_n) / 1e3
     achieved = flops_alg / t_launch / 1e12
     peak = pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
-    rows_exec = math.ceil((npos_avg + 1) / 128) * 128   # 128-row groups (TMEM lanes)
+    # MMA rows: 128-row groups (TMEM lanes); a last group of <= 64 rows runs with M = 64
+    # (dcp_pc_kernel's tail unit; evaluated at the average N_pos)
+    tail = npos_avg - math.floor(npos_avg / 128) * 128
+    rows_exec = math.floor(npos_avg / 128) * 128 + (0 if tail == 0 else 64 if tail <= 64 else 128)
     flops_exec = 4.0 * rows_exec * C_loc * d
     traffic = None
     prof_file = os.path.join(ROOT, "profiles", f"ncu_main_{cfg.name}.json")

@@ -320,6 +320,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
     const int neg0 = *p.neg0;
     const int n_rg = (n_rows + PC_R - 1) / PC_R;
     const int n_tiles = (p.n_slots + PC_TILE - 1) / PC_TILE;
+    // 64-row tail unit: the last row group with at most 64 rows runs both GEMMs with M = 64
+    // (cta_group::1 M = 64 keeps MMA row r on TMEM lane 32 (r / 16) + r % 16: lanes 0-15 of each
+    // quadrant; profiles/r01c_umma2_probe.txt) -- half the MMA work and energy of a padded
+    // 128-row unit.  Default variant only (the out-of-pool rows of hinge / max keep 128).
+    // (dbg_flags 32768: off, for A/B runs)
+    auto tail64 = [&](int g) {
+        return p.neg_mode == 0 && g == n_rg - 1 && n_rows - g * PC_R <= 64 && !(p.dbg_flags & 32768);
+    };
     if (p.dbg && threadIdx.x == 0 && (blockIdx.x >> 1) == static_cast<unsigned>(p.dbg_cluster)) {  // kernel-span clocks (debug hook)
         unsigned long long gt;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
@@ -427,11 +435,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
         } else if (warp == 9) {
             // -------- UMMA issuer: GEMM 1 (A = x_hat from TMEM, B = pool chunk K-major)
             {  // whole warp; one elected lane issues
-                constexpr uint32_t idesc = umma_idesc_bf16(128, PC_TILE, 0, 0);
                 // descriptors advance by immediates: the start-address field holds addr >> 4
                 const uint64_t bdesc0 = umma_desc_sw128(smem_u32(sT), 16, 1024);
                 uint32_t pc = 0, jt = 0, sg = 0;
                 while (sch.next(rg, t0, t1, seg)) {
+                    const uint32_t idesc = umma_idesc_bf16(tail64(rg) ? 64 : 128, PC_TILE, 0, 0);
                     mbar_wait(&aux->xready, sg & 1);
                     if (lane == 0 && sg == 0) PC_STAMP(4);
                     tc_fence_after();
@@ -503,16 +511,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                 asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
             }
         } else {
-            // -------- softmax warps 0-7: warp w -> rows 32*(w%4)+lane, slot half w/4
+            // -------- softmax warps 0-7: warp w -> rows 32*(w%4)+lane, slot half w/4 (a 64-row
+            // tail unit: rows 16*(w%4)+lane on lanes 0-15; lanes 16-31 idle)
             const int q = warp & 3, h = warp >> 2;
-            const int r = q * 32 + lane;
             const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
+            {   // zero both S buffers once: TMEM lanes an M = 64 GEMM never writes must hold finite values
+                uint32_t z[32];
+#pragma unroll
+                for (int k = 0; k < 32; ++k) z[k] = 0u;
+                for (int c0 = 0; c0 < 2 * PC_TILE; c0 += 64) {
+                    tmem_st32(tmem + lane_base + S_COL + c0 + h * 32, z);
+                }
+                tmem_wait_st();
+            }
             uint32_t jt = 0, sg = 0, wc_n = 0;
             while (sch.next(rg, t0, t1, seg)) {
-                const int row = rg * PC_R + r;
-                const float2 ab = p.row_ab[row];
-                const int tg = p.row_tgt[row];
-                const int hent = EXCL ? p.row_hent[row] : -1;
+                const bool m64 = tail64(rg);
+                const int r = m64 ? (lane < 16 ? q * 16 + lane : -1) : q * 32 + lane;
+                const bool rv = r >= 0;
+                const int row = rg * PC_R + (rv ? r : 0);
+                const float2 ab = rv ? p.row_ab[row] : make_float2(0.f, INFINITY);
+                const int tg = rv ? p.row_tgt[row] : -1;
+                const int hent = EXCL && rv ? p.row_hent[row] : -1;
                 // x_hat (this thread's row, d half h) -> TMEM A operand columns
                 mbar_wait(&aux->xfree, (sg & 1) ^ 1);
                 tc_fence_after();
@@ -524,7 +544,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                         uint32_t w[32];
 #pragma unroll
                         for (int u = 0; u < 8; ++u) {
-                            const uint4 v = src[c0 / 4 + u];
+                            const uint4 v = rv ? src[c0 / 4 + u] : make_uint4(0u, 0u, 0u, 0u);
                             w[4 * u] = v.x; w[4 * u + 1] = v.y; w[4 * u + 2] = v.z; w[4 * u + 3] = v.w;
                         }
                         tmem_st32(tmem + lane_base + X_COL + h * ncol + c0, w);
@@ -735,7 +755,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                     mbar_wait(&aux->pstage_free[b], ph ^ 1);
                     if (dbg) dbg[10] = clock64();
                     const uint32_t rowa = smem_u32(sPS + b * PC_PBYTES + h * 16384 + (r >> 3) * 1024 + (r & 7) * 128);
-                    if (!(p.dbg_flags & 1))
+                    if (rv && !(p.dbg_flags & 1))
 #pragma unroll
                     for (int u = 0; u < 8; ++u)
                         st_shared_v4(rowa + ((u ^ (r & 7)) << 4), w[4 * u], w[4 * u + 1], w[4 * u + 2],
@@ -746,11 +766,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                     if (dbg) dbg[3] = clock64();
                 }
                 // segment end: l and max over both slot halves
-                aux->red_l[h][r] = lacc;
-                aux->red_mx[h][r] = mx;
-                aux->red_arg[h][r] = barg;
+                if (rv) {
+                    aux->red_l[h][r] = lacc;
+                    aux->red_mx[h][r] = mx;
+                    aux->red_arg[h][r] = barg;
+                }
                 named_bar_sync(1, 256);
-                if (h == 0) {
+                if (h == 0 && rv) {
                     p.seg_l[static_cast<size_t>(seg) * PC_R + r] = aux->red_l[0][r] + aux->red_l[1][r];
                     const float m0 = aux->red_mx[0][r], m1 = aux->red_mx[1][r];
                     p.seg_mx[static_cast<size_t>(seg) * PC_R + r] = fmaxf(m0, m1);
@@ -792,9 +814,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
             // -------- UMMA issuer: GEMM 2 (A = P K-major, B = pool MN-major, N = 256 d)
             {  // whole warp; one elected lane issues
                 const uint32_t sPa = smem_u32(sP), sTa = smem_u32(sT);
-                const uint32_t idesc = cps == 4 ? umma_idesc_bf16(128, 256, 0, 1) : umma_idesc_bf16(128, 128, 0, 1);
                 uint32_t qc = 0, jt = 0, sg = 0;
                 while (sch.next(rg, t0, t1, seg)) {
+                    const int mm = tail64(rg) ? 64 : 128;  // (M = 64 reads P rows 0-63 of each chunk)
+                    const uint32_t idesc = cps == 4 ? umma_idesc_bf16(mm, 256, 0, 1) : umma_idesc_bf16(mm, 128, 0, 1);
                     for (int t = t0; t < t1; ++t, ++jt) {
                         const bool first = (t == t0);
                         const uint32_t b = jt & 1, ph = (jt >> 1) & 1;
@@ -841,15 +864,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
             while (sch.next(rg, t0, t1, seg)) {
                 mbar_wait(&aux->ofull, sg & 1);
                 tc_fence_after();
-                if (!p.drain_tma) {  // long units: the drain is off the critical path
-                    float4 *dst = reinterpret_cast<float4 *>(p.seg_O + (static_cast<size_t>(seg) * PC_R + r) * d);
+                const bool m64 = tail64(rg);
+                if (!p.drain_tma || m64) {  // long units: the drain is off the critical path
+                    // (a 64-row tail unit: rows 16 q + lane on lanes 0-15 of quadrant q)
+                    const int ro = m64 ? q * 16 + lane : r;
+                    const bool st = !m64 || lane < 16;
+                    float4 *dst = reinterpret_cast<float4 *>(p.seg_O + (static_cast<size_t>(seg) * PC_R + ro) * d);
                     for (int c0 = hcol * (d / 2); c0 < (hcol + 1) * (d / 2); c0 += 32) {
                         float o[32];
                         tmem_ld32(tmem + lane_base + c0, o);
                         tmem_wait_ld();
+                        if (st)
 #pragma unroll
-                        for (int u = 0; u < 8; ++u)
-                            dst[c0 / 4 + u] = make_float4(o[4 * u], o[4 * u + 1], o[4 * u + 2], o[4 * u + 3]);
+                            for (int u = 0; u < 8; ++u)
+                                dst[c0 / 4 + u] = make_float4(o[4 * u], o[4 * u + 1], o[4 * u + 2], o[4 * u + 3]);
                     }
                     tc_fence_before();
                     __syncwarp();
