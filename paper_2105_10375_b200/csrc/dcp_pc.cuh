@@ -754,9 +754,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                     if (dbg) dbg[9] = clock64();
                     mbar_wait(&aux->pstage_free[b], ph ^ 1);
                     if (dbg) dbg[10] = clock64();
-                    if (p.dbg_flags & 65536)  // power experiment: an all-zero P operand
-#pragma unroll
-                        for (int k = 0; k < 32; ++k) w[k] = 0u;
                     const uint32_t rowa = smem_u32(sPS + b * PC_PBYTES + h * 16384 + (r >> 3) * 1024 + (r & 7) * 128);
                     if (rv && !(p.dbg_flags & 1))
 #pragma unroll
