@@ -48,6 +48,8 @@ def test_schedule_cluster_counts(dcp, case, clusters, monkeypatch):
     monkeypatch.setenv("F2C_CLUSTERS", str(clusters))
     head = dcp.DCPHead(case["C"], case["d"], dcp.BF16, world=1, rank=0, n_local_max=case["N"],
                        m_local_max=case["M"])
+    kind, ctas = head.fused_kernel(case["N"])
+    assert kind == 0 and ctas == 2 * clusters, (kind, ctas)  # dcp_pc_kernel, one CTA pair per cluster
     for G, y in case["blocks"]:
         head.enqueue(to_dev(G, synth.BF16), lt(y))
     loss, dx = head.loss_fwd_bwd(to_dev(case["X"], synth.BF16), lt(case["y"]), None, 64.0, 0.35)
