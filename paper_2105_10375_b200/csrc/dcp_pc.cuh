@@ -59,6 +59,9 @@ constexpr int PC_SMEM_BYTES_NOSTG = PC_OFF_OSTG + 1024;            // without it
 // the same struct (same offsets) in both CTAs, so multicast commits can target a
 // barrier of the peer by its local offset
 constexpr int PC_MAX_UNITS = 32;
+constexpr int PC_PACE_LAG = 24;      // tiles a unit may run ahead of its range's slowest row group
+constexpr int PC_PACE_EVERY = 8;     // progress published / checked every 8 tiles
+constexpr int PC_PACE_SPINS = 8192;  // polls per unit before pacing is dropped
 constexpr int PC_P_CHUNKS = 4;     // P transfer pieces (see the mover)
 // (Measured and rejected: the softmax warps storing P straight into the consumer's smem with
 // st.shared::cluster + fence.proxy.async.shared::cluster instead of staging + one bulk copy
@@ -98,6 +101,7 @@ struct PCAux {
     int red_arg[2][PC_R];
     int4 units[PC_MAX_UNITS];          // this cluster's (row group, t0, t1, segment) list
     int n_units;
+    int single_wave;                   // every cluster runs at most one unit (range pacing)
 };
 static_assert(sizeof(PCAux) <= 4096, "PCAux must fit the aux region");
 
@@ -131,6 +135,13 @@ struct PCParams {
     unsigned long long *dbg;
     int dbg_cluster;       // the cluster whose per-tile clocks the debug hook records
     const int *run_flag;   // refinement pass (R1 fallback): run only if *run_flag != 0
+    // Range pacing (single-wave schedules): every unit's producer publishes its progress through
+    // its tile range, (epoch << 32) | tiles issued, with relaxed stores, and stays at most
+    // PC_PACE_LAG tiles ahead of the slowest row group of the same range, so the range's row
+    // groups keep sharing each pool tile through L2 (a free-running 64-row tail unit, or box
+    // clock behaviour, let them drift apart and re-read part of the pool from DRAM)
+    unsigned long long *prog;  // [U] per unit (seg = range * n_rg + row group)
+    unsigned int epoch;        // this launch's tag (never 0)
     int dbg_flags;         // timing experiments only: 1 = skip P smem writes, 128 = skip DSMEM copy,
                            // 4 / 8 = no producer / consumer pool loads, 16 = no softmax arithmetic,
                            // 16384 = every CTA loads only pool tiles 0-15 (L2-hot; same smem traffic),
@@ -374,6 +385,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
         int n = 0, a, b, c, s;
         while (n < PC_MAX_UNITS && ts.next(a, b, c, s)) aux->units[n++] = make_int4(a, b, c, s);
         aux->n_units = n;
+        aux->single_wave = ts.U <= ts.G;
         PC_STAMP(1);
     }
     if (warp == 9) {
@@ -403,9 +415,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
             if (lane == 0) {
                 uint32_t pc = 0;
                 uint32_t wc_n = 0;
+                const bool pace = p.prog != nullptr && aux->single_wave && n_rg >= 2;
+                int spins = 0;
                 while (sch.next(rg, t0, t1, seg)) {
                     const bool wmu = p.wmu != nullptr && p.neg_mode != 0 && rg * PC_R + PC_R - 1 >= neg0;
+                    unsigned long long *pg0 = pace ? p.prog + (seg - rg) : nullptr;  // this range's row groups
                     for (int t = t0; t < t1; ++t) {
+                        if (pace && ((t - t0) % PC_PACE_EVERY) == 0) {
+                            const unsigned long long mine = (static_cast<unsigned long long>(p.epoch) << 32) |
+                                                            static_cast<unsigned long long>(t - t0);
+                            asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(pg0 + rg), "l"(mine) : "memory");
+                            while (spins < PC_PACE_SPINS) {  // wait while > LAG tiles ahead of the slowest
+                                long long slow = 1ll << 40;
+                                for (int g = 0; g < n_rg; ++g) {
+                                    unsigned long long v;
+                                    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(pg0 + g) : "memory");
+                                    const long long dn = (v >> 32) == p.epoch ? static_cast<long long>(v & 0xffffffffull) : 0;
+                                    slow = dn < slow ? dn : slow;
+                                }
+                                if (slow + PC_PACE_LAG >= t - t0) break;
+                                ++spins;
+                                __nanosleep(256);
+                            }
+                        }
                         if (wmu) {  // the tile's bf16 weights w_c (256 B) -> weight ring
                             const uint32_t wb = wc_n % PC_WRING;
                             mbar_wait(&aux->wempty[wb], ((wc_n / PC_WRING) & 1) ^ 1);
@@ -429,6 +461,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                             const int tl = (p.dbg_flags & 16384) ? (t & 15) : t;  // 16384: hot tiles (experiment)
                             tma_load_3d(sT + st * PC_P_STAGE_BYTES, &tm3p, &aux->tfull[st], 0, tl * PC_TILE, g * cps_p);
                         }
+                    }
+                    if (pace) {  // range done: never hold the others back
+                        const unsigned long long fin = (static_cast<unsigned long long>(p.epoch) << 32) | 0xfffffffull;
+                        asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(pg0 + rg), "l"(fin) : "memory");
                     }
                 }
             }

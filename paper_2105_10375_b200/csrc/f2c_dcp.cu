@@ -115,7 +115,7 @@ struct Layout {
     size_t T, lab, sc, x_all, y_all, pair_all, blk_x, blk_y, inv_n, hslot, hkeys, hvals, tseq,
         comp_idx, pos_row, X_pos, row_ab, row_tgt, ttgt, seg_l, seg_mx, seg_O, rowloss, st_lse,
         st_cos, st_phi, st_ell, seg_arg, rs_buf, rs_all, dx_part, tseq_ext, dx32, tmax_glob, mu_fx, Traw, wslot,
-        hgseq, row_hent, dup_cnt, dup_off, dup_list, ekeys, evals, ehslot, rseq, dst_seq, wmu, total;
+        hgseq, row_hent, dup_cnt, dup_off, dup_list, ekeys, evals, ehslot, rseq, dst_seq, wmu, prog, total;
     int64_t C_loc, N, Mg, R_max, S_max;
     int H, He;
 };
@@ -207,6 +207,7 @@ static Layout make_layout(int64_t C, int d, int dtype, int W, int rank, int64_t 
     L.ehslot = take(static_cast<size_t>(L.Mg) * 4);
     L.rseq = take(static_cast<size_t>(L.Mg) * 8);
     L.dst_seq = take(static_cast<size_t>(L.Mg) * 8);
+    L.prog = take(static_cast<size_t>(L.S_max) * 8);  // fused kernel: per unit progress (range pacing)
     L.total = align_up(o, 1024);
     return L;
 }
@@ -253,6 +254,7 @@ struct f2c_dcp {
     bool use_tp64 = false;
     int pc4_mode = 0;               // 1: the 2-SM pair kernel where it applies (F2C_KERNEL=pc4)
     int G4 = 0;                     // co-resident 4-CTA clusters of dcp_pc4_kernel (its persistent grid / 4)
+    unsigned int epoch = 0;         // fused-kernel launch tag (range pacing)
     int dbg_flags = 0;              // timing experiments (F2C_DBG_FLAGS)
     int dbg_cluster = 0;            // debug timestamps of this cluster (F2C_DBG_CLUSTER)
     ~f2c_dcp() {
@@ -850,6 +852,9 @@ static int phase_main(f2c_dcp *h, Rank &R, const StepCtx &c, int64_t occ_loc, co
         q.dbg_cluster = h->dbg_cluster;
         q.dbg_flags = h->dbg_flags;
         q.run_flag = run_flag;
+        if (++h->epoch == 0) h->epoch = 1;
+        q.epoch = h->epoch;
+        q.prog = (h->dbg_flags & 262144) ? nullptr : R.at<unsigned long long>(L.prog);  // (262144: no pacing, A/B)
         if (kind == 2)
             dcp_pc4_kernel<<<h->G4 * 4, P4_THREADS, P4_SMEM_BYTES, c.st>>>(R.tm4p, R.tm3p, q);
         else if (q.excl)
