@@ -102,6 +102,7 @@ struct PCAux {
     int4 units[PC_MAX_UNITS];          // this cluster's (row group, t0, t1, segment) list
     int n_units;
     int single_wave;                   // every cluster runs at most one unit (range pacing)
+    int range_len;                     // tiles per range (n_tiles / S, the same in every cluster)
 };
 static_assert(sizeof(PCAux) <= 4096, "PCAux must fit the aux region");
 
@@ -135,11 +136,12 @@ struct PCParams {
     unsigned long long *dbg;
     int dbg_cluster;       // the cluster whose per-tile clocks the debug hook records
     const int *run_flag;   // refinement pass (R1 fallback): run only if *run_flag != 0
-    // Range pacing (single-wave schedules): every unit's producer publishes its progress through
-    // its tile range, (epoch << 32) | tiles issued, with relaxed stores, and stays at most
-    // PC_PACE_LAG tiles ahead of the slowest row group of the same range, so the range's row
-    // groups keep sharing each pool tile through L2 (a free-running 64-row tail unit, or box
-    // clock behaviour, let them drift apart and re-read part of the pool from DRAM)
+    // Range pacing (single-wave schedules with a 64-row tail unit, <= 8 row groups, ranges of
+    // >= 512 tiles): every unit's producer publishes its progress through its tile range,
+    // (epoch << 32) | tiles issued, with relaxed stores, and stays at most PC_PACE_LAG tiles ahead
+    // of the slowest row group of the same range, so the range's row groups keep sharing each
+    // pool tile through L2 (the faster tail unit drifted ahead and re-read part of the pool from
+    // DRAM)
     unsigned long long *prog;  // [U] per unit (seg = range * n_rg + row group)
     unsigned int epoch;        // this launch's tag (never 0)
     int dbg_flags;         // timing experiments only: 1 = skip P smem writes, 128 = skip DSMEM copy,
@@ -386,6 +388,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
         while (n < PC_MAX_UNITS && ts.next(a, b, c, s)) aux->units[n++] = make_int4(a, b, c, s);
         aux->n_units = n;
         aux->single_wave = ts.U <= ts.G;
+        aux->range_len = n_tiles / ts.S;
         PC_STAMP(1);
     }
     if (warp == 9) {
@@ -415,7 +418,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
             if (lane == 0) {
                 uint32_t pc = 0;
                 uint32_t wc_n = 0;
-                const bool pace = p.prog != nullptr && aux->single_wave && n_rg >= 2;
+                // (only where it pays: a 64-row tail unit -- the row group that drifts ahead --, few row
+                // groups and long ranges; measured 1.5-8.5 % slower at c2 / c1 / c3r_8 otherwise)
+                const bool pace = p.prog != nullptr && aux->single_wave && n_rg >= 2 && n_rg <= 8 &&
+                                  tail64(n_rg - 1) && aux->range_len >= 512;
                 int spins = 0;
                 while (sch.next(rg, t0, t1, seg)) {
                     const bool wmu = p.wmu != nullptr && p.neg_mode != 0 && rg * PC_R + PC_R - 1 >= neg0;
