@@ -22,6 +22,10 @@
 // fall far below it (large s) are re-run by the refinement pass (run_flag).
 // Variants: EXCL (stale self-duplicates masked per tile, NEXT-3), out-of-pool cosine rows for
 // hinge / max (NEXT-3), with K >= 2 (NEXT-1) their weights w_c through an smem ring.
+// A last row group of <= 64 rows runs as a 64-row tail unit (M = 64 MMAs: half the MMA work
+// and energy of a padded group), and on long single-wave schedules the row groups of a tile
+// range keep within PC_PACE_LAG tiles of each other (relaxed progress counters in global
+// memory) so they share each pool tile through L2.
 #pragma once
 #include "dcp_main.cuh"
 #include "sm100.cuh"
