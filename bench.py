@@ -2,14 +2,18 @@
 """Benchmark of the F2C DCP head on B200 (contract: DESIGN.md section 8).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c3|c2|c1]
-  torchrun --nproc-per-node N bench.py --gpus N ...      (one process per GPU, NCCL)
+      --gpus N > 1 without WORLD_SIZE in the environment re-launches this script under
+      torch.distributed.run with N ranks (one process per GPU, NCCL); under torchrun
+      WORLD_SIZE must equal N.
   python bench.py --impl reference ...                   (the CPU oracle arm)
 
 One step = one pass of the whole hot path: enqueue of the
 step's G-Net identity block, the fused loss forward+backward over the mixed P-Net
 batch, and the G-Net EMA over a 65M-parameter fp32 vector.  Rank 0 prints ONE JSON
-line.  Inputs: synthetic and seeded (synth/), pool prefilled through the enqueue
-kernel (D20).
+line.  Before anything is timed, every rank runs a small W-rank step whose loss, dx and
+pool state are checked against the fp64 oracle on the rank-ordered concatenation (D16,
+pin P9): `w_parity` in the line; a failing check prints no value and exits 1.
+Inputs: synthetic and seeded (synth/), pool prefilled through the enqueue kernel (D20).
 """
 from __future__ import annotations
 
@@ -17,6 +21,7 @@ import argparse
 import json
 import math
 import os
+import platform
 import statistics
 import subprocess
 import sys
@@ -33,14 +38,41 @@ import synth  # noqa: E402
 METRIC = "DCP head fwd+bwd+enqueue samples/s"
 UNIT = "samples/s"
 EMA_PARAMS = 65_000_000
+LOSS_RTOL, DX_FRAC = 2e-3, 1e-2   # BJ:5 parity bars (also tests/helpers.py)
 
 
 def _peaks():
     try:
-        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        pk = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        pk["_source"] = "MEASURED_PEAKS.json (driver-measured on this pool's B200s)"
+        return pk
     except Exception:
+        # /opt/skills/guides/B200_PROFILING.md fallback figures
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
-                "_fallback": True}
+                "sm_max_mhz": 1965.0, "_source": "B200_PROFILING.md fallback (MEASURED_PEAKS.json absent)"}
+
+
+def host_cpu():
+    """The host the CPU legs run on: lscpu model, nproc, governor."""
+    model = platform.processor() or "?"
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.lower().startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    gov = None
+    try:
+        gov = open("/sys/devices/system/cpu/cpu0/cpufreq/scaling_governor").read().strip()
+    except Exception:
+        gov = "n/a (no cpufreq in this guest)"
+    try:
+        affinity = len(os.sched_getaffinity(0))
+    except Exception:
+        affinity = os.cpu_count()
+    return {"lscpu_model": model, "nproc": os.cpu_count(), "affinity_cpus": affinity, "governor": gov}
 
 
 # --------------------------------------------------------------------------- CPU oracle timing
@@ -87,12 +119,15 @@ def cpu_baseline(cfg, world, budget_s=20.0):
     if r["wall"] < budget_s / 3 and C_s < cfg.C:  # grow the sample toward ~budget
         k = int(min(128, k * max(1.0, budget_s / max(r["wall"], 1e-3) / 2)))
         r = oracle_sample_time(cfg, world, C_s, k)
+    extrap = cfg.C / C_s
     return dict(value=r["N"] / r["t_step"], unit=UNIT, cores=1, kind="oracle",
                 sample=(f"fp64 C oracle (1 thread) on {r['rows']} sampled rows (half identity, half "
                         f"instance) of step 0 against a {C_s}-slot sub-pool, plus the full "
                         f"target-resolve/mu pass over that sub-pool; step time extrapolated x"
-                        f"{cfg.C / C_s:.1f} to C={cfg.C} and to all {r['N']} rows"),
-                sample_wall_s=round(r["wall"], 2))
+                        f"{extrap:.1f} to C={cfg.C} and to all {r['N']} rows"
+                        + (" (an estimate, not a timing of the full step)" if extrap > 1 or r["rows"] < r["N"] else "")),
+                sample_wall_s=round(r["wall"], 2), extrapolated=bool(extrap > 1 or r["rows"] < r["N"]),
+                host=host_cpu())
 
 
 def run_reference(args, cfg, world):
@@ -105,22 +140,26 @@ def run_reference(args, cfg, world):
     per_row = max(probe["t_rows"] / 2, 1e-6)
     C_s = int(min(cfg.C, max(4096, C_s * budget / max(probe["wall"], 1e-3) / 2)))
     C_s = max(4096, min(C_s, cfg.C, 262144))
-    times = []
+    times, walls = [], []
     for i in range(W + K):
         r = oracle_sample_time(cfg, world, C_s, 2, step=i % 4)
         if i >= W:
             times.append(r["t_step"])
+            walls.append(r["wall"])
     N = probe["N"]
     tot = sum(times)
     val = K * N / tot
-    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": world,
             "steps": K, "warmup": W, "ms_per_step": 1e3 * tot / K, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": _config(cfg, world),
             "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle",
                              "sample": f"per step: 2 sampled rows against a {C_s}-slot sub-pool + "
                                        f"the resolve/mu pass, extrapolated x{cfg.C / C_s:.1f} to "
-                                       f"C={cfg.C} and to {N} rows; per-row cost {per_row:.3f}s"},
+                                       f"C={cfg.C} and to {N} rows (an estimate, not a timing of the "
+                                       f"full step); per-row cost {per_row:.3f}s",
+                             "sample_wall_s_per_step": round(sum(walls) / max(1, len(walls)), 3),
+                             "extrapolated": True, "host": host_cpu()},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -157,7 +196,7 @@ class Clocks:
         self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
         try:
             self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}",
-                                       "--format=csv,noheader,nounits", "-lms", "200", "-i",
+                                       "--format=csv,noheader,nounits", "-lms", "100", "-i",
                                        str(gpu_index)], stdout=self.f, stderr=subprocess.DEVNULL)
         except Exception:
             self.p = None
@@ -174,12 +213,13 @@ class Clocks:
         self.f.flush()
         rows = [ln.strip().split(",") for ln in open(self.f.name) if ln.strip()]
         os.unlink(self.f.name)
-        sm, mx, reasons = [], 0.0, set()
+        sm, mx, pw, reasons = [], 0.0, [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for r in rows:
             try:
                 sm.append(float(r[1]))
                 mx = max(mx, float(r[2]))
+                pw.append(float(r[3]))
                 for nm, v in zip(names, r[5:9]):
                     if "Active" in v and "Not" not in v:
                         reasons.add(nm)
@@ -188,11 +228,171 @@ class Clocks:
         if not sm:
             return None
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "sm_mhz_min": min(sm), "power_w_max": max(pw) if pw else None}
+
+
+# --------------------------------------------------------------------------- multi-rank plumbing
+def _nccl_uid(world, rank, dev):
+    """The library's NCCL communicator is bootstrapped from a unique id made by rank 0 and
+    broadcast over the torch process group (torch only for plumbing)."""
+    import torch
+    import torch.distributed as dist
+    if world == 1:
+        return None
+    if rank == 0:
+        raw = bytes(torch.cuda.nccl.unique_id())
+        t = torch.tensor(list(raw), dtype=torch.uint8, device=dev)
+    else:
+        t = torch.zeros(128, dtype=torch.uint8, device=dev)
+    dist.broadcast(t, 0)
+    return bytes(t.cpu().tolist())
+
+
+def w_parity(world, rank, local_rank, dev, emulate=0):
+    """Self-check before timing: one W-rank step (prefill, enqueue of the
+    step's identity block, loss) of a small seeded workload with ragged shards and a wrapped
+    ring, through the same NCCL protocol as the timed run; loss, dx and the pool state are
+    gathered to rank 0 and compared with the fp64 oracle on the rank-ordered concatenation
+    (D16, pin P9).  emulate > 1 (W = 1 only): the same check through the emulated world of
+    `emulate` ranks on one device.  Returns the result dict on every rank (ok broadcast)."""
+    import torch
+    import torch.distributed as dist
+    import paper_2105_10375_b200 as dcp
+    Wl = world if world > 1 else max(1, emulate)
+    cfg = synth.scaled(synth.CONFIGS["c1"], name="w_parity", C=1000 * Wl + 37, M_loc=32,
+                       n_id=3000 * Wl, prefill=0, seed=synth.SEED_BASE + 77)
+    M, N_loc, d = cfg.M_loc, cfg.N_loc(), cfg.d
+    uid = _nccl_uid(world, rank, dev)
+    if world > 1:
+        head = dcp.DCPHead(cfg.C, d, dcp.BF16, world, rank, n_local_max=N_loc, m_local_max=M, nccl_uid=uid,
+                           device=dev)
+    else:
+        head = dcp.DCPHead(cfg.C, d, dcp.BF16, Wl, -1 if Wl > 1 else 0, n_local_max=N_loc, m_local_max=M,
+                           device=dev)
+    my_ranks = [rank] if world > 1 else list(range(Wl))
+
+    def block(parts):
+        return np.concatenate(parts) if len(parts) > 1 else parts[0]
+
+    nblk = cfg.prefill_blocks(Wl) + 3          # the ring wraps
+    for b in range(nblk):
+        parts = [synth.prefill_block(cfg, b, r, Wl) for r in my_ranks]
+        g = block([p[0] for p in parts])
+        y = block([p[1] for p in parts])
+        head.enqueue(torch.from_numpy(g.view(np.int16)).view(torch.bfloat16).to(dev), torch.from_numpy(y).to(dev))
+    st = [synth.step_inputs(cfg, 0, r, Wl) for r in my_ranks]
+    head.enqueue(torch.from_numpy(block([s.g for s in st]).view(np.int16)).view(torch.bfloat16).to(dev),
+                 torch.from_numpy(block([s.gy for s in st])).to(dev))
+    x = torch.from_numpy(block([s.x for s in st]).view(np.int16)).view(torch.bfloat16).to(dev)
+    loss, dx = head.loss_fwd_bwd(x, torch.from_numpy(block([s.y for s in st])).to(dev),
+                                 torch.from_numpy(block([s.pairing for s in st])).to(dev), cfg.s, cfg.m)
+    torch.cuda.synchronize()
+    err = None
+    try:
+        head.check()
+    except Exception as e:  # a latched device error fails the check below
+        err = str(e)
+    feats, labs, E = head.get_state()
+    L = float(loss.item())
+    dx_u16 = dx.view(torch.int16).cpu().numpy().view(np.uint16)
+    head.close()
+    if world > 1:
+        gathered = [None] * world
+        dist.all_gather_object(gathered, (L, dx_u16, feats, labs, E, err))
+    else:
+        gathered = [(L, dx_u16, feats, labs, E, err)]
+    res = None
+    ok = 1
+    if rank == 0:
+        import oracle
+        pool = oracle.Pool(cfg.C, d, oracle.BF16)
+        for b in range(nblk):
+            parts = [synth.prefill_block(cfg, b, r, Wl) for r in range(Wl)]
+            pool.enqueue(np.concatenate([p[0] for p in parts]), np.concatenate([p[1] for p in parts]))
+        sa = [synth.step_inputs(cfg, 0, r, Wl) for r in range(Wl)]
+        pool.enqueue(np.concatenate([s.g for s in sa]), np.concatenate([s.gy for s in sa]))
+        ref = pool.loss(np.concatenate([s.x for s in sa]), np.concatenate([s.y for s in sa]),
+                        np.concatenate([s.pairing for s in sa]), cfg.s, cfg.m)
+        dxg = oracle.bf16_to_f64(np.concatenate([g[1] for g in gathered]))
+        losses = [g[0] for g in gathered]
+        feats_all = np.concatenate([g[2] for g in gathered])
+        labs_all = np.concatenate([g[3] for g in gathered])
+        loss_rel = abs(losses[0] - ref.L) / abs(ref.L)
+        dx_frac = float(np.abs(dxg - ref.dx).max() / np.abs(ref.dx).max())
+        pos = ref.tslot >= 0
+        dx_frac_out = (float(np.abs(dxg[~pos] - ref.dx[~pos]).max() / np.abs(ref.dx[~pos]).max())
+                       if (~pos).any() else 0.0)
+        state_ok = (all(g[4] == int(pool.E[0]) for g in gathered) and np.array_equal(labs_all, pool.lab)
+                    and np.array_equal(feats_all[: pool.C_occ], pool.T[: pool.C_occ]))
+        same_loss = all(v == losses[0] for v in losses)
+        errs = [g[5] for g in gathered if g[5]]
+        ok = int(loss_rel <= LOSS_RTOL and dx_frac <= DX_FRAC and dx_frac_out <= DX_FRAC and state_ok
+                 and same_loss and not errs)
+        res = {"ok": bool(ok), "world": Wl, "transport": ("nccl" if world > 1 else
+                                                          ("emulated" if Wl > 1 else "single")),
+               "loss_rel": loss_rel, "dx_frac": dx_frac, "dx_frac_out_of_pool": dx_frac_out,
+               "state_bitexact": bool(state_ok), "loss_identical_on_ranks": bool(same_loss),
+               "device_errors": errs, "N_pos": ref.N_pos, "N_neg": ref.N_neg,
+               "config": {"C": cfg.C, "d": d, "global_batch": N_loc * Wl, "M_glob": M * Wl,
+                          "prefill_blocks": nblk, "s": cfg.s, "m": cfg.m},
+               "bars": {"loss_rel": LOSS_RTOL, "dx_frac": DX_FRAC}}
+    if world > 1:
+        t = torch.tensor([ok], dtype=torch.int32, device=dev)
+        dist.broadcast(t, 0)
+        ok = int(t.item())
+    return res if rank == 0 else {"ok": bool(ok)}
+
+
+# --------------------------------------------------------------------------- roofline
+def roofline_block(cfg, world, d, npos_avg, t_launch, ms_step, clocks, pk, share):
+    """Roofline of the dominant kernel (dcp_pc_kernel) and of the whole step.
+    Peak: burst when the median SM clock under load is within 5 % of its maximum, else the
+    sustained (power-capped) figure; both fractions are reported."""
+    C_loc = cfg.C // world
+    burst = pk["bf16_tflops"]
+    sus = pk.get("bf16_tflops_sustained", burst)
+    near_max = (clocks is None or clocks.get("sm_max_mhz", 0) <= 0 or
+                clocks["sm_mhz"] >= 0.95 * clocks["sm_max_mhz"])
+    peak = burst if near_max else sus
+    flops_alg = 4.0 * npos_avg * C_loc * d          # GEMM 1 + GEMM 2 on the in-pool rows
+    achieved = flops_alg / t_launch / 1e12
+    # MMA rows: 128-row groups (TMEM lanes); a last group of <= 64 rows runs with M = 64
+    # (dcp_pc_kernel's tail unit; evaluated at the average N_pos)
+    full = math.floor(npos_avg / 128) * 128
+    tail = npos_avg - full
+    rows_exec = full + (0 if tail == 0 else 64 if tail <= 64 else 128)
+    flops_exec = 4.0 * rows_exec * C_loc * d
+    N = cfg.N_loc() * world
+    # algorithmic bytes of one step per GPU: the pool read once, x in / dx out, the enqueue
+    # (block read + slot write), the EMA (p, g read, g write); NVLink: C1 + C3 + C4 + C5
+    hbm_bytes = C_loc * d * 2 + N * d * 2 * 2 + cfg.M_glob(world) * d * 2 * 2 + EMA_PARAMS * 12
+    nvl_bytes = 0.0 if world == 1 else (N * d * 2 + N * 16 * world + N * d * 4 + cfg.M_glob(world) * d * 2) * (world - 1) / world
+    t_roof = max(flops_alg / (burst * 1e12), hbm_bytes / (pk["hbm_gbs"] * 1e9), nvl_bytes / 900e9)
+    traffic = None
+    prof_file = os.path.join(ROOT, "profiles", f"ncu_main_{cfg.name}.json")
+    if os.path.exists(prof_file):
+        try:
+            traffic = json.load(open(prof_file)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    return {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+            "frac": achieved / peak, "traffic": traffic,
+            "kernel": "dcp_pc_kernel (producer: TMEM-A logits GEMM + softmax -> DSMEM P; consumer: P x pool GEMM, O in TMEM)",
+            "peak_kind": ("burst bf16 (median SM clock within 5 % of max)" if near_max else
+                          "sustained bf16 (SM clock > 5 % below max: power-capped run)"),
+            "peak_source": pk.get("_source"),
+            "frac_vs_burst": achieved / burst, "frac_vs_sustained": achieved / sus,
+            "algorithmic_flops_per_launch": flops_alg, "executed_mma_flops_per_launch": flops_exec,
+            "tensor_pipe_frac": flops_exec / t_launch / 1e12 / peak,
+            "avg_launch_ms": t_launch * 1e3, "N_pos_avg": npos_avg, "main_kernel_share_of_step": share,
+            "step": {"t_roof_ms": t_roof * 1e3, "t_step_ms": ms_step, "frac": t_roof * 1e3 / ms_step,
+                     "hbm_bytes": hbm_bytes, "nvlink_bytes": nvl_bytes,
+                     "definition": "T_roof = max(F_alg / burst bf16, HBM bytes / measured copy BW, "
+                                   "NVLink bytes / 900 GB/s); frac = T_roof / T_step (SURVEY 8(d))"}}
 
 
 # --------------------------------------------------------------------------- GPU arm
-def run_ours(args, cfg, world, rank, local_rank, device_only=False):
+def run_ours(args, cfg, world, rank, local_rank, device_only=False, cpu=True):
     import torch
     import torch.distributed as dist
     import paper_2105_10375_b200 as dcp
@@ -200,17 +400,7 @@ def run_ours(args, cfg, world, rank, local_rank, device_only=False):
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     M, N_loc, d = cfg.M_loc, cfg.N_loc(), cfg.d
-    uid = None
-    if world > 1:
-        # the library's NCCL communicator is bootstrapped from a unique id made by rank 0
-        # and broadcast over the torch process group (torch only for plumbing)
-        if rank == 0:
-            raw = bytes(torch.cuda.nccl.unique_id())
-            t = torch.tensor(list(raw), dtype=torch.uint8, device=dev)
-        else:
-            t = torch.zeros(128, dtype=torch.uint8, device=dev)
-        dist.broadcast(t, 0)
-        uid = bytes(t.cpu().tolist())
+    uid = _nccl_uid(world, rank, dev)
     K = args.K
     head = dcp.DCPHead(cfg.C, d, dcp.BF16, world, rank if world > 1 else 0, n_local_max=N_loc,
                        m_local_max=M, nccl_uid=uid, device=dev, K=K)
@@ -300,44 +490,47 @@ def run_ours(args, cfg, world, rank, local_rank, device_only=False):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    # ---- device-resident timed run (value)
-    K = args.steps
+    # ---- device-resident timed run (value): `trials` timed regions of exactly K steps each
+    Ks, T = args.steps, max(1, args.trials)
     barrier()
     clk = Clocks(local_rank) if rank == 0 else None
     head.profile(True)
     launches[0] = 0
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    torch.cuda.nvtx.range_push("timed_steps")  # ncu --nvtx-include timed_steps/ selects these launches
-    for i in range(K):
-        step(devin[i % R])
-    join()
-    torch.cuda.nvtx.range_pop()
-    e1.record(stream)
-    barrier()
+    trial_ms = []
+    for _ in range(T):
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        torch.cuda.nvtx.range_push("timed_steps")  # ncu --nvtx-include timed_steps/ selects these launches
+        for i in range(Ks):
+            step(devin[i % R])
+        join()
+        torch.cuda.nvtx.range_pop()
+        e1.record(stream)
+        barrier()
+        trial_ms.append(maxrank(e0.elapsed_time(e1)))
     clocks = clk.stop() if clk else None
-    ms = maxrank(e0.elapsed_time(e1))
-    n_launch = launches[0]
+    n_launch = launches[0] // T
     main_ms, main_n, npos_sum = head.profile_read()
     head.profile(False)
     if not timing_experiment:
         head.check()
-    value = K * N_loc * world / (ms / 1e3)
+    ms = statistics.median(trial_ms)
+    value = Ks * N_loc * world / (ms / 1e3)
+    best = Ks * N_loc * world / (min(trial_ms) / 1e3)
+    npos_avg = npos_sum / max(1, main_n)
+    t_launch = main_ms / max(1, main_n) / 1e3
+    share = (main_ms / T) / ms
+    pk = _peaks()
+    roof = roofline_block(cfg, world, d, npos_avg, t_launch, ms / Ks, clocks, pk, share)
+    trials = {"n": T, "ms_per_step": [t / Ks for t in trial_ms], "median_value": value, "best_value": best}
 
     if device_only:
+        head.close()
         if rank != 0:
             return None
-        pk = _peaks()
-        C_loc = cfg.C // world
-        npos_avg = npos_sum / max(1, main_n)
-        t_launch = main_ms / max(1, main_n) / 1e3
-        achieved = 4.0 * npos_avg * C_loc * d / t_launch / 1e12
-        peak = pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
-        head.close()
-        return {"workload": cfg.name, "value": value, "unit": UNIT, "ms_per_step": ms / K,
-                "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                             "frac": achieved / peak, "avg_launch_ms": t_launch * 1e3, "N_pos_avg": npos_avg},
-                "clocks": clocks, "config": _config(cfg, world, args.ema_overlap, args.K, _variant(args))}
+        return {"workload": cfg.name, "value": value, "unit": UNIT, "ms_per_step": ms / Ks, "trials": trials,
+                "roofline": roof, "clocks": clocks, "config": _config(cfg, world, args.ema_overlap, args.K, _variant(args))}
 
     # ---- end-to-end through the public API with host buffers (e2e): every step copies its
     # inputs from pinned host memory and reads the loss back.  The copies run on a copy
@@ -347,70 +540,52 @@ def run_ours(args, cfg, world, rank, local_rank, device_only=False):
     copy_st = torch.cuda.Stream(device=dev)
     copied = [torch.cuda.Event() for _ in range(2)]
     freed = [torch.cuda.Event() for _ in range(2)]
-    barrier()
-    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e2.record(stream)
-    copy_st.wait_event(e2)                       # no upload before the timed region starts
-    for i in range(K):
-        b = i % 2
-        if i >= 2:
-            copy_st.wait_event(freed[b])         # step i-2 is done with buffer b
-        with torch.cuda.stream(copy_st):
-            for dst, src in zip(bufs[b], host[i % R]):
-                dst.copy_(src, non_blocking=True)
-        copied[b].record(copy_st)
-        stream.wait_event(copied[b])
-        step(bufs[b])
-        freed[b].record(stream)
-        loss_host.copy_(loss, non_blocking=True)
-    join()
-    stream.wait_stream(copy_st)
-    e3.record(stream)
-    barrier()
-    ms_e2e = maxrank(e2.elapsed_time(e3))
-    value_e2e = K * N_loc * world / (ms_e2e / 1e3)
-
+    e2e_ms = []
+    for _ in range(T):
+        barrier()
+        e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e2.record(stream)
+        copy_st.wait_event(e2)                       # no upload before the timed region starts
+        for i in range(Ks):
+            b = i % 2
+            if i >= 2:
+                copy_st.wait_event(freed[b])         # step i-2 is done with buffer b
+            with torch.cuda.stream(copy_st):
+                for dst, src in zip(bufs[b], host[i % R]):
+                    dst.copy_(src, non_blocking=True)
+            copied[b].record(copy_st)
+            stream.wait_event(copied[b])
+            step(bufs[b])
+            freed[b].record(stream)
+            loss_host.copy_(loss, non_blocking=True)
+        join()
+        stream.wait_stream(copy_st)
+        e3.record(stream)
+        barrier()
+        e2e_ms.append(maxrank(e2.elapsed_time(e3)))
+    if not timing_experiment:
+        head.check()
+    ms_e2e = statistics.median(e2e_ms)
+    value_e2e = Ks * N_loc * world / (ms_e2e / 1e3)
+    head.close()
     if rank != 0:
-        head.close()
         return None
-    pk = _peaks()
-    C_loc = cfg.C // world
-    npos_avg = npos_sum / max(1, main_n)
-    flops_alg = 4.0 * npos_avg * C_loc * d          # GEMM 1 + GEMM 2 on the in-pool rows
-    t_launch = main_ms / max(1, main_n) / 1e3
-    achieved = flops_alg / t_launch / 1e12
-    peak = pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
-    # MMA rows: 128-row groups (TMEM lanes); a last group of <= 64 rows runs with M = 64
-    # (dcp_pc_kernel's tail unit; evaluated at the average N_pos)
-    tail = npos_avg - math.floor(npos_avg / 128) * 128
-    rows_exec = math.floor(npos_avg / 128) * 128 + (0 if tail == 0 else 64 if tail <= 64 else 128)
-    flops_exec = 4.0 * rows_exec * C_loc * d
-    traffic = None
-    prof_file = os.path.join(ROOT, "profiles", f"ncu_main_{cfg.name}.json")
-    if os.path.exists(prof_file):
-        try:
-            traffic = json.load(open(prof_file)).get("dram_bytes_per_launch")
-        except Exception:
-            traffic = None
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
-        "warmup": args.warmup, "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "bf16", "data": "synthetic", "config": _config(cfg, world, args.ema_overlap, args.K, _variant(args)),
-        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": achieved / peak, "traffic": traffic,
-                     "kernel": "dcp_pc_kernel (producer: TMEM-A logits GEMM + softmax -> DSMEM P; consumer: P x pool GEMM, O in TMEM)",
-                     "algorithmic_flops_per_launch": flops_alg,
-                     "executed_mma_flops_per_launch": flops_exec,
-                     "tensor_pipe_frac": flops_exec / t_launch / 1e12 / peak,
-                     "avg_launch_ms": t_launch * 1e3, "N_pos_avg": npos_avg,
-                     "peak_kind": "measured sustained bf16 (MEASURED_PEAKS.json), kernel timed inside a long step",
-                     "main_kernel_share_of_step": main_ms / ms},
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": Ks,
+        "warmup": args.warmup, "ms_per_step": ms / Ks, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": _config(cfg, world, args.ema_overlap, args.K, _variant(args)),
+        "trials": trials,
+        "roofline": roof,
         "e2e": {"value": value_e2e, "unit": UNIT, "h2d_bytes_per_step": h2d_bytes,
-                "d2h_bytes_per_step": 4, "ms_per_step": ms_e2e / K},
+                "d2h_bytes_per_step": 4, "ms_per_step": ms_e2e / Ks,
+                "trials_ms_per_step": [t / Ks for t in e2e_ms],
+                "readback": "the fp32 loss scalar each step; dx (the backbone's input gradient) stays "
+                            "on the device where the training step consumes it"},
         "gpu_launches": n_launch,
         "clocks": clocks,
     }
-    if world == 1 and not args.no_cpu_baseline:
+    if world == 1 and cpu and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(cfg, world)
     return line
 
@@ -440,6 +615,7 @@ def kernel_bench(args):
     byt = M * d * 2 * 2 + M * 8 * 2
     out["enqueue"] = {"rows": M, "bytes": byt, "best_ms": min(ts), "GBps": byt / (min(ts) * 1e-3) / 1e9,
                       "frac_of_measured_copy": byt / (min(ts) * 1e-3) / 1e9 / pk["hbm_gbs"]}
+    head.close()
     del head
     p = torch.randn(EMA_PARAMS, device=dev) * 0.05
     gq = torch.randn(EMA_PARAMS, device=dev) * 0.05
@@ -501,11 +677,57 @@ def sweep_c4(args):
                       "steps": args.steps, "warmup": args.warmup, "points": pts}), flush=True)
 
 
-def main():
+def _free_port():
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def spawn_ranks(n, argv):
+    """--gpus N > 1 outside torchrun: re-launch this script as N ranks (one process per GPU)
+    with the driver's own launcher form; rank 0 prints the line, and the exit code is the
+    launcher's."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+           os.path.abspath(__file__), *argv]
+    env = dict(os.environ)
+    env.setdefault("OMP_NUM_THREADS", "1")
+    return subprocess.call(cmd, env=env)
+
+
+def dry_run(world, rank, local_rank):
+    """--dry-run: the launch path only (process group, rank / world agreement); no kernels."""
+    import torch
+    import torch.distributed as dist
+    if world > 1:
+        use_nccl = torch.cuda.is_available() and torch.cuda.device_count() >= world
+        if use_nccl:
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group("gloo")
+        got = [None] * world
+        dist.all_gather_object(got, (rank, local_rank, os.getpid()))
+        backend = dist.get_backend()
+        dist.destroy_process_group()
+    else:
+        got, backend = [(0, 0, os.getpid())], None
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "backend": backend,
+                          "ranks": [g[0] for g in got], "local_ranks": [g[1] for g in got],
+                          "distinct_processes": len({g[2] for g in got})}), flush=True)
+
+
+def main(argv=None):
+    argv = sys.argv[1:] if argv is None else argv
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--trials", type=int, default=3, help="timed regions of --steps steps each (median, best)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c3",
                     help="c1 | c2 | c3 | c4r_<pct>_<global batch> (one rank of a W=8 c4 point) | "
@@ -518,44 +740,83 @@ def main():
     ap.add_argument("--ema-overlap", type=int, default=1,
                     help="1: G-Net EMA on a low-priority side stream (overlaps the head's small kernels)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-w-parity", action="store_true", help="skip the pre-timing self-check (debug only)")
+    ap.add_argument("--dry-run", action="store_true", help="launch path only: ranks, world, backend")
     ap.add_argument("--kernel-bench", action="store_true", help="HBM-bound kernels alone (enqueue, EMA)")
     ap.add_argument("--sweep-c4", action="store_true", help="BJ:11 sweep, one rank of W=8 per point (evidence)")
-    ap.add_argument("--also", default="c2", help="extra single-GPU workloads measured device-resident "
+    ap.add_argument("--also", default="c2", help="extra single-GPU workloads measured in the same run "
                     "(the north-star 1M-slot config c2 by default); 'none' to skip")
-    args = ap.parse_args()
+    args = ap.parse_args(argv)
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
+    in_launcher = "WORLD_SIZE" in os.environ
+    if args.impl == "reference":
+        # the CPU arm: rank 0 alone works (under torchrun the other ranks exit without work);
+        # its config is the GPU arm's at N = --gpus ranks
+        world = int(os.environ.get("WORLD_SIZE", args.gpus))
+        if in_launcher and world != args.gpus:
+            sys.exit(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}")
+        if int(os.environ.get("RANK", "0")) == 0:
+            run_reference(args, _workload(args.workload), world)
+        return 0
+    if args.gpus > 1 and not in_launcher:
+        return spawn_ranks(args.gpus, argv)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        sys.exit(f"bench.py: {world} ranks launched but --gpus {args.gpus}: refusing to report a "
+                 f"{world}-rank number as {args.gpus} GPUs")
+    if args.dry_run:
+        dry_run(world, rank, local_rank)
+        return 0
     cfg = _workload(args.workload)
     if args.kernel_bench:
         kernel_bench(args)
-        return
+        return 0
     if args.sweep_c4:
         sweep_c4(args)
-        return
-    if args.impl == "reference":
-        if rank == 0:
-            run_reference(args, cfg, world)
-        return
+        return 0
+    import torch
     if world > 1:
-        import torch
         import torch.distributed as dist
+        if torch.cuda.device_count() < world:
+            sys.exit(f"bench.py: --gpus {world} but only {torch.cuda.device_count()} visible GPU(s)")
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    wp = None
+    if not args.no_w_parity:
+        wp = w_parity(world, rank, local_rank, dev, emulate=0 if world > 1 else 2)
+        if not wp["ok"]:
+            if rank == 0:
+                print(json.dumps({"metric": METRIC, "value": None, "unit": UNIT, "n_gpus": world,
+                                  "error": "w_parity self-check failed: no value reported", "w_parity": wp}),
+                      flush=True)
+            if world > 1:
+                torch.distributed.destroy_process_group()
+            return 1
     line = run_ours(args, cfg, world, rank, local_rank)
     extras = [w.strip("'\"") for w in args.also.split(",")]
     extras = [w for w in extras if w and w != "none" and w != args.workload] if world == 1 else []
     if extras:
-        import torch
         torch.cuda.empty_cache()
-        line["also"] = [run_ours(args, _workload(w), world, rank, local_rank, device_only=True)
-                        for w in extras]
+        line["also"] = []
+        for w in extras:
+            r = run_ours(args, _workload(w), world, rank, local_rank)
+            torch.cuda.empty_cache()
+            r = {k: v for k, v in r.items() if k not in ("metric", "higher_is_better", "scaling", "vs_baseline",
+                                                        "data", "dtype", "n_gpus", "steps", "warmup")}
+            line["also"].append({"workload": w, **r})
     if rank == 0 and line is not None:
+        if wp is not None:
+            line["w_parity"] = wp
         print(json.dumps(line), flush=True)
     if world > 1:
-        import torch.distributed as dist
-        dist.destroy_process_group()
+        torch.distributed.destroy_process_group()
+    return 0
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main())

@@ -17,8 +17,15 @@
  *     thread-local message for the last failure on the calling thread.
  *   - Errors that only the device can see (negative labels in device buffers,
  *     pairing mismatches, zero-norm rows, non-finite loss, softmax underflow that
- *     the kernels could not absorb) are latched in a device error word and
- *     reported by f2c_dcp_check() and by the next host call on the handle.
+ *     the kernels could not absorb) are latched in a device error word.  The
+ *     kernel that latches one also writes it to a mapped pinned host word of the
+ *     handle, and every later f2c_dcp_enqueue / f2c_dcp_loss_fwd_bwd call reads
+ *     that word before launching anything (no synchronisation, no copy): the first
+ *     such call made after the error became visible to the host returns it
+ *     (F2C_EPAIRING / F2C_EDEVICE, message via f2c_last_error) and launches
+ *     nothing, and so does every later call until f2c_dcp_check() clears the
+ *     latch.  Calls issued while the latching kernel is still queued or running
+ *     cannot see it yet; f2c_dcp_check() synchronises and always reports it.
  *   - dtype: F2C_BF16 (pool and features bf16, fp32 accumulation) or F2C_F32
  *     (fp32 storage; the loss path of this build requires F2C_BF16, see
  *     DESIGN.md section 9, D21).  Feature dimension d: multiple of 128, <= 512.
@@ -207,7 +214,8 @@ int f2c_dcp_row_stats(f2c_dcp *h, float *lse, int64_t *target_seq, float *cos_t,
                       float *ell, int64_t *counts);
 
 /* Synchronise the last stream used with the handle and return the latched device
- * error (F2C_OK, F2C_EPAIRING or F2C_EDEVICE); clears the latch. */
+ * error (F2C_OK, F2C_EPAIRING or F2C_EDEVICE, or F2C_ENCCL for an asynchronous
+ * NCCL error); clears the latch (device word and host mirror). */
 int f2c_dcp_check(f2c_dcp *h);
 
 /* Thread-local message for the last non-OK return on this thread. */

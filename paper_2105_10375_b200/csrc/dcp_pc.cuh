@@ -65,7 +65,7 @@ constexpr int PC_SMEM_BYTES_NOSTG = PC_OFF_OSTG + 1024;            // without it
 constexpr int PC_MAX_UNITS = 32;
 constexpr int PC_PACE_LAG = 24;      // tiles a unit may run ahead of its range's slowest row group
 constexpr int PC_PACE_EVERY = 8;     // progress published / checked every 8 tiles
-constexpr int PC_PACE_SPINS = 8192;  // polls per unit before pacing is dropped
+constexpr int PC_PACE_SPINS = 8192;  // polls per unit (>= 256 ns each) before pacing is dropped for it
 constexpr int PC_P_CHUNKS = 4;     // P transfer pieces (see the mover)
 // (Measured and rejected: the softmax warps storing P straight into the consumer's smem with
 // st.shared::cluster + fence.proxy.async.shared::cluster instead of staging + one bulk copy
@@ -426,8 +426,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                 // groups and long ranges; measured 1.5-8.5 % slower at c2 / c1 / c3r_8 otherwise)
                 const bool pace = p.prog != nullptr && aux->single_wave && n_rg >= 2 && n_rg <= 8 &&
                                   tail64(n_rg - 1) && aux->range_len >= 512;
-                int spins = 0;
                 while (sch.next(rg, t0, t1, seg)) {
+                    int spins = 0;  // (per unit: a stalled peer costs at most PC_PACE_SPINS polls per unit)
                     const bool wmu = p.wmu != nullptr && p.neg_mode != 0 && rg * PC_R + PC_R - 1 >= neg0;
                     unsigned long long *pg0 = pace ? p.prog + (seg - rg) : nullptr;  // this range's row groups
                     for (int t = t0; t < t1; ++t) {

@@ -235,6 +235,7 @@ struct f2c_dcp {
     int refresh = 0;   // NEXT-3: refresh-in-place enqueue (f2c_dcp_set_enqueue_mode)
     bool last_refresh = false;  // the last enqueue was a refresh (pairing checks use blk_seq)
     long long *n_app_host = nullptr;  // pinned: rows appended by the last refresh enqueue
+    int *err_host = nullptr;          // mapped pinned {err, detail} per shard (Scalars::err_mirror)
     int neg_mode() const { return phi_mode == 2 ? 2 : (hinge ? 1 : 0); }
     bool emulated;
     int64_t n_local_max, m_local_max;
@@ -260,6 +261,7 @@ struct f2c_dcp {
     ~f2c_dcp() {
         for (cudaEvent_t e : ev) cudaEventDestroy(e);
         if (n_app_host) cudaFreeHost(n_app_host);
+        if (err_host) cudaFreeHost(err_host);
     }
 };
 
@@ -425,6 +427,15 @@ int f2c_dcp_create_k(int64_t C, int32_t K, int32_t d, int32_t dtype, int32_t wor
         }
     }
     const int nr = h->emulated ? world : 1;
+    {   // latched device errors reach the host through mapped pinned words (no per-call copy)
+        void *p = nullptr;
+        if (cudaHostAlloc(&p, static_cast<size_t>(2 * nr) * sizeof(int), cudaHostAllocMapped) != cudaSuccess) {
+            delete h;
+            return fail(F2C_ECUDA, "cudaHostAlloc(error mirror) failed");
+        }
+        h->err_host = static_cast<int *>(p);
+        memset(h->err_host, 0, static_cast<size_t>(2 * nr) * sizeof(int));
+    }
     for (int i = 0; i < nr; ++i) {
         Rank R;
         R.rank = h->emulated ? i : rank;
@@ -435,6 +446,14 @@ int f2c_dcp_create_k(int64_t C, int32_t K, int32_t d, int32_t dtype, int32_t wor
         if (cudaMemset(R.base, 0, R.L.total) != cudaSuccess) {
             delete h;
             return fail(F2C_ECUDA, "cudaMemset(state) failed");
+        }
+        {
+            int *mirror = nullptr;
+            if (cudaHostGetDevicePointer(reinterpret_cast<void **>(&mirror), h->err_host + 2 * i, 0) != cudaSuccess ||
+                cudaMemcpy(&R.sc()->err_mirror, &mirror, sizeof mirror, cudaMemcpyHostToDevice) != cudaSuccess) {
+                delete h;
+                return fail(F2C_ECUDA, "error mirror setup failed");
+            }
         }
         k_hash_clear<<<64, 256>>>(R.at<int64_t>(R.L.hkeys), R.at<unsigned long long>(R.L.hvals), R.L.H);
         k_hash_clear<<<64, 256>>>(R.at<int64_t>(R.L.ekeys), R.at<unsigned long long>(R.L.evals), R.L.He);
@@ -472,6 +491,34 @@ int f2c_dcp_create_k(int64_t C, int32_t K, int32_t d, int32_t dtype, int32_t wor
                              P4_SMEM_BYTES) != cudaSuccess) {
         delete h;
         return fail(F2C_ECUDA, "cudaFuncSetAttribute(smem) failed");
+    }
+    {   // dcp_pc_kernel's range pacing assumes every 2-CTA cluster of its persistent grid is
+        // resident at once: size the grid by what the device can co-schedule (GPC floorsweeping,
+        // MPS / green contexts can leave fewer than SMs / 2)
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 2;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.gridDim = dim3(static_cast<unsigned>((h->G / 2) * 2));
+        cfg.blockDim = dim3(PC_THREADS);
+        cfg.dynamicSmemBytes = PC_SMEM_BYTES;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        int ncl = 0;
+        if (cudaOccupancyMaxActiveClusters(&ncl, dcp_pc_kernel<false>, &cfg) != cudaSuccess) {
+            cudaGetLastError();
+            ncl = 0;
+        }
+        if (ncl >= 1 && 2 * ncl < h->G) h->G = 2 * ncl;
+        const int64_t R_groups = (n_local_max * world + 32 + 127) / 128;
+        if (2 + (R_groups + h->G / 2 - 1) / (h->G / 2) > PC_MAX_UNITS) {
+            delete h;
+            return fail(F2C_ECAPACITY, "world*n_local_max = %lld rows exceeds the fused kernel's schedule on "
+                        "%d co-resident clusters", (long long)(n_local_max * world), h->G / 2);
+        }
+        if (getenv("F2C_VERBOSE")) fprintf(stderr, "f2c: dcp_pc_kernel clusters %d (max active %d)\n", h->G / 2, ncl);
     }
     {   // 4-CTA clusters do not tile every GPC: the persistent grid is what fits at once
         cudaLaunchConfig_t cfg = {};
@@ -1110,23 +1157,47 @@ extern "C" int f2c_dcp_set_dup_mode(f2c_dcp *h, int32_t exclude_stale) {
 }
 
 // ============================================================================ support
+static const char *err_detail_text(int dd) {
+    static const char *det[] = {"", "negative label", "zero-norm (or non-finite) feature row",
+                                "pairing[i] does not name row i's target",
+                                "non-finite loss", "softmax underflow (row max < 2^-100 of the reference)",
+                                "duplicate label within a refresh-in-place enqueue block (S:277)"};
+    return det[(dd >= 0 && dd <= 6) ? dd : 0];
+}
+
+// sync = false (every enqueue / loss call): read the mapped host mirror of each shard's error
+// word (written by the kernel that latched it; no synchronisation, no copy), so a device error
+// is reported by the first host call made after it became visible.  The error stays latched
+// (every later call reports it) until f2c_dcp_check() clears it.
+// sync = true (f2c_dcp_check, after a device synchronisation): read the device word itself,
+// report it and clear it (device word and mirror).
 static int latched(f2c_dcp *h, bool sync) {
-    if (!sync) return F2C_OK;  // only the debug calls synchronise
+    if (!sync) {
+        if (!h->err_host) return F2C_OK;
+        for (size_t i = 0; i < h->ranks.size(); ++i) {
+            const volatile int *m = h->err_host + 2 * i;
+            const int code = m[0];
+            if (code != 0)
+                return fail(code, "device error latched by an earlier call (rank %d): %s; "
+                            "f2c_dcp_check() reports and clears it", h->ranks[i].rank, err_detail_text(m[1]));
+        }
+        return F2C_OK;
+    }
     int worst = F2C_OK;
-    for (Rank &R : h->ranks) {
+    for (size_t i = 0; i < h->ranks.size(); ++i) {
+        Rank &R = h->ranks[i];
         Scalars s;
         if (cudaMemcpy(&s, R.sc(), sizeof s, cudaMemcpyDeviceToHost) != cudaSuccess)
             return fail(F2C_ECUDA, "reading the device error word failed");
         if (s.err) {
-            static const char *det[] = {"", "negative label", "zero-norm (or non-finite) feature row",
-                                        "pairing[i] does not name row i's target",
-                                        "non-finite loss", "softmax underflow (row max < 2^-100 of the reference)",
-                                        "duplicate label within a refresh-in-place enqueue block (S:277)"};
-            const int dd = (s.err_detail >= 0 && s.err_detail <= 6) ? s.err_detail : 0;
-            fail(s.err, "device error (rank %d): %s", R.rank, det[dd]);
+            fail(s.err, "device error (rank %d): %s", R.rank, err_detail_text(s.err_detail));
             worst = s.err;
             int zero[2] = {0, 0};
             cudaMemcpy(R.sc(), zero, sizeof zero, cudaMemcpyHostToDevice);
+        }
+        if (h->err_host) {
+            h->err_host[2 * i] = 0;
+            h->err_host[2 * i + 1] = 0;
         }
     }
     return worst;

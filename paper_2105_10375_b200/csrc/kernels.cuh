@@ -33,10 +33,21 @@ struct Scalars {          // lives at the start of the per-rank scratch
     long long n_app;      // rows appended by the last refresh-in-place enqueue (NEXT-3)
     unsigned loss_done;   // CTAs of the final per-row kernel done (the last one sums the loss)
     int refine;           // R1 fallback: some row's reference was lowered, re-run the fused kernel
+    int *err_mirror;      // mapped pinned host words {err, detail} of this shard: the host reads
+                          // them at the next call on the handle without synchronising
 };
 
 __device__ __forceinline__ void latch(Scalars *s, int code, int detail) {
-    if (atomicCAS(&s->err, 0, code) == 0) s->err_detail = detail;
+    if (atomicCAS(&s->err, 0, code) == 0) {
+        s->err_detail = detail;
+        if (s->err_mirror) {  // (rare: one system-scope store pair per latched error)
+            volatile int *m = s->err_mirror;
+            m[1] = detail;
+            __threadfence_system();
+            m[0] = code;
+            __threadfence_system();
+        }
+    }
 }
 
 __device__ __forceinline__ uint64_t hash64(uint64_t z) {

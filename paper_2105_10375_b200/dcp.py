@@ -110,25 +110,55 @@ class DCPHead:
         uid = None if nccl_uid is None else ctypes.create_string_buffer(bytes(nccl_uid), 128)
         _check(L.f2c_dcp_create_k(C, K, d, dtype, world, rank, uid, _ptr(self.state), nbytes,
                                   n_local_max, m_local_max, ctypes.byref(self._h)))
-        self.loss_buf = torch.zeros((), dtype=torch.float32, device=self.device)
+
+    # -- argument checks (marshalling only: shapes, dtypes, layout, device) ------------------
+    def _rows_per_rank(self):
+        return self.world if self.rank < 0 else 1
+
+    def _check_tensor(self, t, name, dtype, shape=None):
+        if not isinstance(t, torch.Tensor):
+            raise TypeError(f"{name} must be a torch.Tensor")
+        if t.dtype != dtype:
+            raise DCPError(1, f"{name}: dtype {t.dtype}, expected {dtype}")
+        if t.device.type != "cuda" or (self.device.index is not None and t.device.index != self.device.index):
+            raise DCPError(1, f"{name}: on {t.device}, the handle is on {self.device}")
+        if not t.is_contiguous():
+            raise DCPError(1, f"{name} must be contiguous")
+        if shape is not None and tuple(t.shape) != tuple(shape):
+            raise DCPError(2, f"{name}: shape {tuple(t.shape)}, expected {tuple(shape)}")
 
     # -- the hot path -----------------------------------------------------------------
     def enqueue(self, g_feats: torch.Tensor, labels: torch.Tensor, stream=None):
-        assert g_feats.is_contiguous() and labels.is_contiguous() and labels.dtype == torch.int64
-        _check(load_library().f2c_dcp_enqueue(self._h, _ptr(g_feats), _ptr(labels),
-                                              labels.shape[0] // (self.world if self.rank < 0 else 1),
+        """Eq. 7 / Algorithm 1: g_feats [m, d] (K = 1) or [m, K, d] in the handle's dtype, labels
+        int64 [m] (an emulated world passes the rank-ordered global block, m = world * m_local)."""
+        m = labels.shape[0] if labels.dim() == 1 else -1
+        self._check_tensor(labels, "labels", torch.int64, (m,))
+        want = (m, self.d) if self.K == 1 else (m, self.K, self.d)
+        self._check_tensor(g_feats, "g_feats", _tdtype(self.dtype), want)
+        if m % self._rows_per_rank():
+            raise DCPError(2, f"emulated world: {m} block rows not divisible by world {self.world}")
+        _check(load_library().f2c_dcp_enqueue(self._h, _ptr(g_feats), _ptr(labels), m // self._rows_per_rank(),
                                               _stream(stream)))
 
     def loss_fwd_bwd(self, x: torch.Tensor, labels: torch.Tensor, pairing: torch.Tensor | None,
                      s: float, m: float, dx: torch.Tensor | None = None, loss: torch.Tensor | None = None,
                      stream=None):
-        """Returns (loss [fp32 device scalar], dx [same shape/dtype as x])."""
-        assert x.is_contiguous() and labels.dtype == torch.int64
+        """Returns (loss [fp32 device scalar], dx [same shape/dtype as x]).  Without `loss` a fresh
+        device scalar is returned per call (it is written asynchronously on the stream)."""
+        n = x.shape[0] if x.dim() == 2 else -1
+        self._check_tensor(x, "x", _tdtype(self.dtype), (n, self.d))
+        self._check_tensor(labels, "labels", torch.int64, (n,))
         if pairing is not None:
-            assert pairing.dtype == torch.int32 and pairing.is_contiguous()
+            self._check_tensor(pairing, "pairing", torch.int32, (n,))
+        if n % self._rows_per_rank():
+            raise DCPError(2, f"emulated world: {n} batch rows not divisible by world {self.world}")
         dx = torch.empty_like(x) if dx is None else dx
-        loss = self.loss_buf if loss is None else loss
-        n_local = x.shape[0] // (self.world if self.rank < 0 else 1)
+        self._check_tensor(dx, "dx", x.dtype, tuple(x.shape))
+        loss = torch.empty((), dtype=torch.float32, device=x.device) if loss is None else loss
+        self._check_tensor(loss, "loss", torch.float32)
+        if loss.numel() != 1:
+            raise DCPError(2, "loss must hold one fp32 element")
+        n_local = n // self._rows_per_rank()
         _check(load_library().f2c_dcp_loss_fwd_bwd(self._h, _ptr(x), _ptr(labels), _ptr(pairing),
                                                    n_local, float(s), float(m), _ptr(loss), _ptr(dx),
                                                    _stream(stream)))
@@ -168,10 +198,24 @@ class DCPHead:
                                                 labs.ctypes.data_as(ctypes.c_void_p), ctypes.byref(E)))
         return feats, labs, E.value
 
+    def _shard_rows(self):
+        if self.rank < 0 or self.world == 1:
+            return self.C
+        return self.C * (self.rank + 1) // self.world - self.C * self.rank // self.world
+
     def set_state(self, feats, labels, E: int):
+        """Restore this handle's slots (host arrays as get_state returns them: feats uint16 bf16
+        bits or float32, [rows, d] or [rows, K, d]; labels int64 [rows], -1 = empty)."""
         import numpy as np
         feats = np.ascontiguousarray(feats)
-        labels = np.ascontiguousarray(labels, dtype=np.int64)
+        labels = np.ascontiguousarray(labels)
+        rows = self._shard_rows()
+        want = (rows, self.d) if self.K == 1 else (rows, self.K, self.d)
+        want_dt = np.uint16 if self.dtype == BF16 else np.float32
+        if feats.dtype != want_dt or feats.shape != want:
+            raise DCPError(2, f"set_state feats: {feats.dtype}{feats.shape}, expected {np.dtype(want_dt)}{want}")
+        if labels.dtype != np.int64 or labels.shape != (rows,):
+            raise DCPError(2, f"set_state labels: {labels.dtype}{labels.shape}, expected int64({rows},)")
         _check(load_library().f2c_dcp_set_state(self._h, feats.ctypes.data_as(ctypes.c_void_p),
                                                 labels.ctypes.data_as(ctypes.c_void_p), int(E)))
 
@@ -239,5 +283,9 @@ class DCPHead:
 
 def gnet_ema(p: torch.Tensor, g: torch.Tensor, momentum: float, stream=None):
     """In-place g <- m g + (1-m) p (fp32, fp64 arithmetic, bit-exact)."""
-    assert p.dtype == torch.float32 and g.dtype == torch.float32 and p.numel() == g.numel()
+    for name, t in (("p", p), ("g", g)):
+        if t.dtype != torch.float32 or t.device.type != "cuda" or not t.is_contiguous():
+            raise DCPError(1, f"gnet_ema {name}: contiguous fp32 CUDA tensor required")
+    if p.numel() != g.numel() or p.device != g.device:
+        raise DCPError(2, "gnet_ema: p and g must have the same size and device")
     _check(load_library().f2c_gnet_ema(_ptr(p), _ptr(g), g.numel(), float(momentum), _stream(stream)))

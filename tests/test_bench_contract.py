@@ -38,6 +38,36 @@ def test_reference_arm_json_line():
 
 
 def test_reference_arm_nonzero_rank_is_silent():
-    lines = _run(["--impl", "reference", "--steps", "1", "--warmup", "0", "--workload", "c1"],
+    lines = _run(["--impl", "reference", "--gpus", "2", "--steps", "1", "--warmup", "0", "--workload", "c1"],
                  {"RANK": "1", "WORLD_SIZE": "2", "LOCAL_RANK": "1"})
     assert lines == []
+
+
+def test_reference_arm_reports_n_gpus_and_its_config():
+    """--gpus N without a launcher: the CPU arm reports n_gpus = N on the N-rank config (global
+    batch N_loc * N), the same config the GPU arm reports at N ranks."""
+    lines = _run(["--impl", "reference", "--gpus", "2", "--steps", "1", "--warmup", "0", "--workload", "c1"])
+    d = json.loads(lines[0])
+    import bench
+    import synth
+    assert d["n_gpus"] == 2 and d["config"] == bench._config(synth.CONFIGS["c1"], 2)
+    assert d["config"]["global_batch"] == 2 * synth.CONFIGS["c1"].N_loc()
+    host = d["cpu_baseline"]["host"]
+    assert host["nproc"] >= 1 and host["lscpu_model"] and "governor" in host
+
+
+def test_gpus_flag_launches_that_many_ranks():
+    """`bench.py --gpus 2` outside torchrun re-launches itself as 2 ranks (torch.distributed.run,
+    127.0.0.1); rank 0 alone prints.  --dry-run stops after the process group is up (gloo here,
+    NCCL on a GPU box), so the launch path is checked without a GPU."""
+    lines = _run(["--gpus", "2", "--dry-run"])
+    assert len(lines) == 1, lines
+    d = json.loads(lines[0])
+    assert d["dry_run"] and d["n_gpus"] == 2 and d["ranks"] == [0, 1] and d["distinct_processes"] == 2
+
+
+def test_world_size_must_match_gpus():
+    env = dict(os.environ, RANK="0", WORLD_SIZE="2", LOCAL_RANK="0")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "4", "--dry-run"],
+                       capture_output=True, text=True, env=env, cwd=ROOT, timeout=120)
+    assert r.returncode != 0 and "refusing" in r.stderr

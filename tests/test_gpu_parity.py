@@ -66,6 +66,70 @@ def test_enqueue_rejects_bad_args(dcp):
     assert e.value.code == 7
 
 
+def test_latched_error_reported_by_next_call(dcp):
+    """include/f2c_dcp.h: a device-latched error reaches the host through the handle's mapped
+    error word; every later enqueue / loss call returns it without launching anything (no
+    synchronisation inside the call) until f2c_dcp_check() reports and clears it."""
+    d = 128
+    head = _head(dcp, 100, d, 8, 8)
+    G = to_dev(synth.unit_rows(1, 1, 0, 0, 4, d), synth.BF16)
+    head.enqueue(G, lt([1, 2, -5, 3]))           # negative label: latched on the device
+    torch.cuda.synchronize()                      # (the latching kernel has finished)
+    with pytest.raises(dcp.DCPError) as e:
+        head.enqueue(G, lt([1, 2, 4, 3]))
+    assert e.value.code == 7 and "negative label" in str(e.value)
+    X = to_dev(synth.unit_rows(1, 2, 0, 0, 4, d), synth.BF16)
+    with pytest.raises(dcp.DCPError) as e:        # sticky until check()
+        head.loss_fwd_bwd(X, lt([1, 2, 4, 3]), None, 64.0, 0.35)
+    assert e.value.code == 7
+    with pytest.raises(dcp.DCPError) as e:
+        head.check()
+    assert e.value.code == 7
+    head.enqueue(G, lt([1, 2, 4, 3]))             # cleared: calls work again
+    head.loss_fwd_bwd(X, lt([1, 2, 4, 3]), None, 64.0, 0.35)
+    head.check()
+    # a zero-norm batch row (latched by the loss kernels) is reported the same way
+    Z = torch.zeros(4, d, dtype=torch.bfloat16, device="cuda")
+    head.loss_fwd_bwd(Z, lt([1, 2, 4, 3]), None, 64.0, 0.35)
+    torch.cuda.synchronize()
+    with pytest.raises(dcp.DCPError) as e:
+        head.loss_fwd_bwd(X, lt([1, 2, 4, 3]), None, 64.0, 0.35)
+    assert e.value.code == 7 and "zero-norm" in str(e.value)
+    with pytest.raises(dcp.DCPError):
+        head.check()
+    head.check()
+
+
+def test_binding_validates_arguments(dcp):
+    """dcp.py checks dtype, shape, contiguity and device against the handle before any call."""
+    d = 128
+    head = _head(dcp, 100, d, 8, 8)
+    G = to_dev(synth.unit_rows(1, 1, 0, 0, 4, d), synth.BF16)
+    with pytest.raises(dcp.DCPError):
+        head.enqueue(G.float(), lt([1, 2, 3, 4]))               # fp32 features to a bf16 handle
+    with pytest.raises(dcp.DCPError):
+        head.enqueue(G, lt([1, 2, 3]))                          # label count
+    with pytest.raises(dcp.DCPError):
+        head.enqueue(G[:, :64].contiguous(), lt([1, 2, 3, 4]))  # feature width != d
+    head.enqueue(G, lt([1, 2, 3, 4]))
+    X = to_dev(synth.unit_rows(1, 2, 0, 0, 4, d), synth.BF16)
+    with pytest.raises(dcp.DCPError):
+        head.loss_fwd_bwd(X, lt([1, 2, 3]), None, 64.0, 0.35)
+    with pytest.raises(dcp.DCPError):
+        head.loss_fwd_bwd(X, lt([1, 2, 3, 4]).int(), None, 64.0, 0.35)
+    with pytest.raises(dcp.DCPError):
+        head.loss_fwd_bwd(X.t().contiguous().t(), lt([1, 2, 3, 4]), None, 64.0, 0.35)
+    with pytest.raises(dcp.DCPError):
+        head.loss_fwd_bwd(X, lt([1, 2, 3, 4]), None, 64.0, 0.35, dx=torch.empty(4, d, device="cuda"))
+    with pytest.raises(dcp.DCPError):
+        head.set_state(np.zeros((100, d), np.float32), np.full(100, -1, np.int64), 0)
+    l1, _ = head.loss_fwd_bwd(X, lt([1, 2, 3, 4]), None, 64.0, 0.35)
+    l2, _ = head.loss_fwd_bwd(X, lt([1, 2, 3, 9]), None, 64.0, 0.35)
+    torch.cuda.synchronize()
+    assert l1.data_ptr() != l2.data_ptr()                       # a fresh loss scalar per call
+    head.check()
+
+
 # ----------------------------------------------------------------------------- a10 EMA
 @pytest.mark.parametrize("n", [1, 7, 4096 + 3, 1_000_003])
 @pytest.mark.parametrize("m", [0.0, 0.999, 1.0, 0.37])
