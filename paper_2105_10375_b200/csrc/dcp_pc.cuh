@@ -50,12 +50,13 @@ constexpr int PCQ_OFF_P = 0;                              // 2 x 32 KB P slots
 constexpr int PCQ_OFF_T = PCQ_OFF_P + 2 * PC_PBYTES;      // 2 x 64 KB pool stages
 constexpr int PCQ_OFF_AUX = PCQ_OFF_T + PC_Q_NSTAGE * PC_STAGE_BYTES;
 constexpr int PC_OFF_AUX = PCP_OFF_AUX > PCQ_OFF_AUX ? PCP_OFF_AUX : PCQ_OFF_AUX;
-// producer: the out-of-pool rows' weight ring (K >= 2), PC_WRING x 128 bf16; deep enough that the TMA
-// warp (a tile or two ahead of the softmax warps) never waits on it
+// producer: the out-of-pool rows' weight ring (K >= 2), PC_WRING x 128 fp32 w_c; deep enough that the
+// TMA warp (a tile or two ahead of the softmax warps) never waits on it
 constexpr int PC_WRING = 8;
+constexpr int PC_WBYTES = PC_TILE * 4;
 constexpr int PC_OFF_WRING = PC_OFF_AUX + 4096;
 // consumer: O-drain staging, one [32 rows x 16 fp32] TMA-store box per drain warp
-constexpr int PC_OFF_OSTG = PC_OFF_WRING + PC_WRING * 256;
+constexpr int PC_OFF_OSTG = PC_OFF_WRING + PC_WRING * PC_WBYTES;
 constexpr int PC_OSTG_BYTES = 8 * 2048;
 constexpr int PC_SMEM_BYTES = PC_OFF_OSTG + PC_OSTG_BYTES + 1024;   // with the drain staging
 constexpr int PC_SMEM_BYTES_NOSTG = PC_OFF_OSTG + 1024;            // without it
@@ -74,15 +75,23 @@ constexpr int PC_P_CHUNKS = 4;     // P transfer pieces (see the mover)
 // the cluster's unit list, computed once per CTA (TPSched) and read by every role
 struct PCUnitIt {
     const int4 *u;
+    const int *um;
     int n, i;
-    __device__ bool next(int &rg, int &t0, int &t1, int &seg) {
+    // a unit: row group rg, tiles [t0, t1) split at mid into its ranges (pc_unit_tile), segment seg
+    __device__ bool next(int &rg, int &t0, int &t1, int &seg, int &mid) {
         if (i >= n) return false;
-        const int4 v = u[i++];
+        const int4 v = u[i];
+        mid = um ? um[i] : v.z;
+        ++i;
         rg = v.x;
         t0 = v.y;
         t1 = v.z;
         seg = v.w;
         return true;
+    }
+    __device__ bool next(int &rg, int &t0, int &t1, int &seg) {  // (one range per unit: dcp_pc4_kernel)
+        int mid;
+        return next(rg, t0, t1, seg, mid);
     }
 };
 
@@ -104,6 +113,7 @@ struct PCAux {
     float red_mx[2][PC_R];
     int red_arg[2][PC_R];
     int4 units[PC_MAX_UNITS];          // this cluster's (row group, t0, t1, segment) list
+    int umid[PC_MAX_UNITS];            // and where each unit's second range starts (t1: one range)
     int n_units;
     int single_wave;                   // every cluster runs at most one unit (range pacing)
     int range_len;                     // tiles per range (n_tiles / S, the same in every cluster)
@@ -121,8 +131,10 @@ struct PCParams {
     const float2 *row_ab;  // [R_max] (a_r, b_r)
     const int *row_tgt;    // [R_max] local target slot or -1
     const uint8_t *X_pos;  // [R_max, d] bf16 compacted rows
-    const float *wslot;    // K >= 2: per-slot 1/||T_bar_c|| (NEXT-3 out-of-pool rows; else null)
-    const __nv_bfloat16 *wmu;  // K >= 2: the same weights in bf16 for the weight ring (padded to a tile)
+    const float *wslot;    // K >= 2: per-slot 1/||T_bar_c|| (fp32, padded by one tile; the NEXT-3
+                           // out-of-pool rows' weight ring reads it); null for K = 1
+    int kf;                // features per slot K: GEMM 1 contracts x_hat with the K raw rows of a slot
+                           // (K d columns; 1/K is folded into a_r, so the logits use the exact mean)
     float margin_l2;       // s * m * log2(e)
     float *ttgt;           // [R_max]
     float *seg_l;          // [S][128]
@@ -328,8 +340,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
     const uint32_t crank = cluster_ctarank();
     const int d = p.d;
     const int nchunk = d >> 6;                  // 64-wide d chunks
-    // producer stages: 2 chunks (32 KB); consumer stages: one GEMM-2 d block (2 or 4 chunks)
-    const int cps_p = 2, nstg_p = nchunk / 2;
+    // producer stages: 2 chunks (32 KB) of the K d-wide raw rows of a tile (NEXT-1: GEMM 1 contracts
+    // over K d, stage g pairs with x_hat stage g mod (d / 128)); consumer stages: one GEMM-2 d block
+    // (2 or 4 chunks) of T_bar
+    const int cps_p = 2, xstg = nchunk / 2, nstg_p = xstg * p.kf;
     const int cps = (d % 256 == 0) ? 4 : 2;
     const int nstg = nchunk / cps;
     const uint32_t stage_bytes = static_cast<uint32_t>(cps) * 16384;
@@ -386,13 +400,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
             mbar_arrive_expect_tx(&aux->pfull[1], PC_PBYTES);
         }
         fence_mbar_init();
-        TPSched ts;
-        ts.init(blockIdx.x >> 1, gridDim.x >> 1, n_rg, n_tiles);
-        int n = 0, a, b, c, s;
-        while (n < PC_MAX_UNITS && ts.next(a, b, c, s)) aux->units[n++] = make_int4(a, b, c, s);
+        // the cluster's units (pc_unit: a 64-row tail group takes two interleaved ranges)
+        const int Gc = static_cast<int>(gridDim.x >> 1);
+        const int tail = tail64(n_rg - 1) ? 1 : 0;
+        const int S = pc_choose_S(n_rg, Gc, n_tiles, tail);
+        const int U = n_tiles > 0 ? pc_units(n_rg, S, tail) : 0;
+        int n = 0;
+        for (int u = static_cast<int>(blockIdx.x >> 1); u < U && n < PC_MAX_UNITS; u += Gc) {
+            int ug, us, um;
+            pc_unit(u, n_rg, S, tail, ug, us, um);
+            const int a0 = tp_range_begin(us, n_tiles, S), a1 = tp_range_begin(us + 1, n_tiles, S);
+            const int b1 = tp_range_begin(us + um < S ? us + um : S, n_tiles, S);
+            if (b1 <= a0) continue;
+            aux->units[n] = make_int4(ug, a0, b1, us * n_rg + ug);
+            aux->umid[n] = a1;
+            ++n;
+        }
         aux->n_units = n;
-        aux->single_wave = ts.U <= ts.G;
-        aux->range_len = n_tiles / ts.S;
+        aux->single_wave = U <= Gc;
+        aux->range_len = n_tiles / S;
         PC_STAMP(1);
     }
     if (warp == 9) {
@@ -409,8 +435,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
     if (threadIdx.x == 0) PC_STAMP(2);
     const uint32_t tmem = aux->tmem_base;
 
-    PCUnitIt sch{aux->units, aux->n_units, 0};
-    int rg, t0, t1, seg;
+    PCUnitIt sch{aux->units, aux->umid, aux->n_units, 0};
+    int rg, t0, t1, seg, mid;
 
     if (crank == 0) {
         // ================================================================= PRODUCER
@@ -426,36 +452,38 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                 // groups and long ranges; measured 1.5-8.5 % slower at c2 / c1 / c3r_8 otherwise)
                 const bool pace = p.prog != nullptr && aux->single_wave && n_rg >= 2 && n_rg <= 8 &&
                                   tail64(n_rg - 1) && aux->range_len >= 512;
-                while (sch.next(rg, t0, t1, seg)) {
+                while (sch.next(rg, t0, t1, seg, mid)) {
                     int spins = 0;  // (per unit: a stalled peer costs at most PC_PACE_SPINS polls per unit)
-                    const bool wmu = p.wmu != nullptr && p.neg_mode != 0 && rg * PC_R + PC_R - 1 >= neg0;
+                    const bool wmu = p.wslot != nullptr && p.neg_mode != 0 && rg * PC_R + PC_R - 1 >= neg0;
                     unsigned long long *pg0 = pace ? p.prog + (seg - rg) : nullptr;  // this range's row groups
-                    for (int t = t0; t < t1; ++t) {
-                        if (pace && ((t - t0) % PC_PACE_EVERY) == 0) {
+                    const bool upace = pace && !tail64(rg);  // (the tail group keeps pace by construction)
+                    for (int i = 0; i < t1 - t0; ++i) {
+                        const int t = pc_unit_tile(i, t0, mid, t1);
+                        if (upace && (i % PC_PACE_EVERY) == 0) {
                             const unsigned long long mine = (static_cast<unsigned long long>(p.epoch) << 32) |
-                                                            static_cast<unsigned long long>(t - t0);
+                                                            static_cast<unsigned long long>(i);
                             asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(pg0 + rg), "l"(mine) : "memory");
                             while (spins < PC_PACE_SPINS) {  // wait while > LAG tiles ahead of the slowest
                                 long long slow = 1ll << 40;
-                                for (int g = 0; g < n_rg; ++g) {
+                                for (int g = 0; g < n_rg - 1; ++g) {  // (full groups; the tail group never waits)
                                     unsigned long long v;
                                     asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(pg0 + g) : "memory");
                                     const long long dn = (v >> 32) == p.epoch ? static_cast<long long>(v & 0xffffffffull) : 0;
                                     slow = dn < slow ? dn : slow;
                                 }
-                                if (slow + PC_PACE_LAG >= t - t0) break;
+                                if (slow + PC_PACE_LAG >= i) break;
                                 ++spins;
                                 __nanosleep(256);
                             }
                         }
-                        if (wmu) {  // the tile's bf16 weights w_c (256 B) -> weight ring
+                        if (wmu) {  // the tile's fp32 weights w_c (512 B) -> weight ring
                             const uint32_t wb = wc_n % PC_WRING;
                             mbar_wait(&aux->wempty[wb], ((wc_n / PC_WRING) & 1) ^ 1);
-                            mbar_arrive_expect_tx(&aux->wfull[wb], 256);
+                            mbar_arrive_expect_tx(&aux->wfull[wb], PC_WBYTES);
                             asm volatile(
-                                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 256, [%2];" ::"r"(
-                                    smem_u32(smem + PC_OFF_WRING + wb * 256)),
-                                "l"(reinterpret_cast<uint64_t>(p.wmu + static_cast<size_t>(t) * PC_TILE)),
+                                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 512, [%2];" ::"r"(
+                                    smem_u32(smem + PC_OFF_WRING + wb * PC_WBYTES)),
+                                "l"(reinterpret_cast<uint64_t>(p.wslot + static_cast<size_t>(t) * PC_TILE)),
                                 "r"(smem_u32(&aux->wfull[wb]))
                                 : "memory");
                             ++wc_n;
@@ -472,7 +500,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                             tma_load_3d(sT + st * PC_P_STAGE_BYTES, &tm3p, &aux->tfull[st], 0, tl * PC_TILE, g * cps_p);
                         }
                     }
-                    if (pace) {  // range done: never hold the others back
+                    if (upace) {  // range done: never hold the others back
                         const unsigned long long fin = (static_cast<unsigned long long>(p.epoch) << 32) | 0xfffffffull;
                         asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(pg0 + rg), "l"(fin) : "memory");
                     }
@@ -484,16 +512,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                 // descriptors advance by immediates: the start-address field holds addr >> 4
                 const uint64_t bdesc0 = umma_desc_sw128(smem_u32(sT), 16, 1024);
                 uint32_t pc = 0, jt = 0, sg = 0;
-                while (sch.next(rg, t0, t1, seg)) {
+                while (sch.next(rg, t0, t1, seg, mid)) {
                     const uint32_t idesc = umma_idesc_bf16(tail64(rg) ? 64 : 128, PC_TILE, 0, 0);
                     mbar_wait(&aux->xready, sg & 1);
                     if (lane == 0 && sg == 0) PC_STAMP(4);
                     tc_fence_after();
-                    for (int t = t0; t < t1; ++t, ++jt) {
+                    for (int i = 0; i < t1 - t0; ++i, ++jt) {
                         unsigned long long *dbg = (p.dbg && blockIdx.x == 2u * p.dbg_cluster && jt < 64 && lane == 0) ? p.dbg + jt * 16 : nullptr;
                         const uint32_t sb = jt & 1, sph = (jt >> 1) & 1;
                         const uint32_t dcol = tmem + S_COL + sb * PC_TILE;
-                        if (nstg_p == 4) {  // d = 512: the whole tile in one elected issue
+                        if (nstg_p == 4 && p.kf == 1) {  // d = 512, K = 1: the whole tile in one elected issue
                             if (dbg) dbg[0] = clock64();
                             gemm1_tile_issue(dcol, tmem + X_COL, bdesc0, idesc, smem_u32(&aux->sempty[sb]), sph ^ 1,
                                              smem_u32(&aux->tfull[0]), smem_u32(&aux->tempty[0]), jt & 1,
@@ -508,12 +536,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                             mbar_wait(&aux->tfull[st], ph);
                             tc_fence_after();
                             const uint64_t bst = bdesc0 + static_cast<uint64_t>(st * (PC_P_STAGE_BYTES >> 4));
-                            umma_ts_stage8(dcol, tmem + X_COL + g * 64, bst, idesc, g != 0, &aux->tempty[st]);
+                            umma_ts_stage8(dcol, tmem + X_COL + (g % xstg) * 64, bst, idesc, g != 0, &aux->tempty[st]);
                         }
                         umma_commit_e(&aux->sfull[sb]);
                         }
                         if (dbg) dbg[1] = clock64();
-                        if (t == t1 - 1) umma_commit_e(&aux->xfree);
+                        if (i == t1 - t0 - 1) umma_commit_e(&aux->xfree);
                     }
                     ++sg;
                 }
@@ -522,8 +550,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
             // -------- P mover: staging buffer -> consumer's P slot (DSMEM bulk copy)
             if (lane == 0 && !(p.dbg_flags & 4096)) {
                 uint32_t jt = 0;
-                while (sch.next(rg, t0, t1, seg)) {
-                    for (int t = t0; t < t1; ++t, ++jt) {
+                while (sch.next(rg, t0, t1, seg, mid)) {
+                    for (int i = 0; i < t1 - t0; ++i, ++jt) {
                         const uint32_t b = jt & 1, ph = (jt >> 1) & 1;
                         mbar_wait(&aux->pready[b], ph);
                         mbar_wait(&aux->pslot_free[b], ph ^ 1);
@@ -571,7 +599,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                 tmem_wait_st();
             }
             uint32_t jt = 0, sg = 0, wc_n = 0;
-            while (sch.next(rg, t0, t1, seg)) {
+            while (sch.next(rg, t0, t1, seg, mid)) {
                 const bool m64 = tail64(rg);
                 const int r = m64 ? (lane < 16 ? q * 16 + lane : -1) : q * 32 + lane;
                 const bool rv = r >= 0;
@@ -605,12 +633,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                 int barg = -1;
                 // K >= 2: this unit's tiles bring their weights through the smem ring (it holds
                 // out-of-pool rows of NEXT-3 hinge / max)
-                const bool wmu = p.wmu != nullptr && p.neg_mode != 0 && rg * PC_R + PC_R - 1 >= neg0;
+                const bool wmu = p.wslot != nullptr && p.neg_mode != 0 && rg * PC_R + PC_R - 1 >= neg0;
                 // NEXT-3: out-of-pool rows compacted after the in-pool rows (a = 1/||x||, b = 0)
                 // (the padding rows after n_rows take this path too: zero operands, discarded
                 // results, and no divergence with the last out-of-pool rows of their warp)
                 const bool negrow = p.neg_mode != 0 && row >= neg0;
-                for (int t = t0; t < t1; ++t, ++jt) {
+                for (int i = 0; i < t1 - t0; ++i, ++jt) {
+                    const int t = pc_unit_tile(i, t0, mid, t1);
                     const uint32_t sb = jt & 1, sph = (jt >> 1) & 1;
                     mbar_wait(&aux->sfull[sb], sph);
                     tc_fence_after();
@@ -739,22 +768,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                                 for (int k = 0; k < 64; ++k) pv[k] = 0.f;
                             }
                         } else {
-                        // K >= 2: the tile's weights from the smem ring (bf16 w_c: the hinge decision
-                        // c > 0 does not depend on w_c > 0, and P = w_c is bf16 anyway)
+                        // K >= 2: the tile's fp32 weights w_c from the smem ring (the max cosine
+                        // compares e_k w_k across slots, so w_c is not rounded)
                         float wv[64];
                         {
-                            const uint4 *src = reinterpret_cast<const uint4 *>(smem + PC_OFF_WRING +
-                                                                               (wc_n % PC_WRING) * 256 + h * 128);
+                            const float4 *src = reinterpret_cast<const float4 *>(smem + PC_OFF_WRING +
+                                                                                 (wc_n % PC_WRING) * PC_WBYTES + h * 256);
 #pragma unroll
-                            for (int u = 0; u < 8; ++u) {
-                                const uint4 v = src[u];
-                                const uint32_t q4[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-                                for (int j = 0; j < 4; ++j) {
-                                    const int k = 8 * u + 2 * j;
-                                    wv[k] = k < nval ? __uint_as_float(q4[j] << 16) : 0.f;
-                                    wv[k + 1] = k + 1 < nval ? __uint_as_float(q4[j] & 0xffff0000u) : 0.f;
-                                }
+                            for (int u = 0; u < 16; ++u) {
+                                const float4 v = src[u];
+                                const int k = 4 * u;
+                                wv[k] = k < nval ? v.x : 0.f;
+                                wv[k + 1] = k + 1 < nval ? v.y : 0.f;
+                                wv[k + 2] = k + 2 < nval ? v.z : 0.f;
+                                wv[k + 3] = k + 3 < nval ? v.w : 0.f;
                             }
                         }
                         // c_k / a_r = e_k w_k (a_r > 0 factored out as in the K = 1 path); zero
@@ -841,8 +868,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
             // -------- TMA: pool stages [cps chunks x 128 slots x 64 d] (3D box) = one d block
             if (lane == 0) {
                 uint32_t qc = 0;
-                while (sch.next(rg, t0, t1, seg)) {
-                    for (int t = t0; t < t1; ++t)
+                while (sch.next(rg, t0, t1, seg, mid)) {
+                    for (int i = 0; i < t1 - t0; ++i) {
+                        const int t = pc_unit_tile(i, t0, mid, t1);
                         for (int g = 0; g < nstg; ++g, ++qc) {
                             const uint32_t st = qc % PC_Q_NSTAGE, ph = (qc / PC_Q_NSTAGE) & 1;
                             mbar_wait(&aux->qempty[st], ph ^ 1);
@@ -854,6 +882,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                             const int tl = (p.dbg_flags & 16384) ? (t & 15) : t;
                             tma_load_3d(sT + st * PC_STAGE_BYTES, &tm3q, &aux->qfull[st], 0, tl * PC_TILE, g * cps);
                         }
+                    }
                 }
             }
         } else if (warp == 9) {
@@ -861,11 +890,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
             {  // whole warp; one elected lane issues
                 const uint32_t sPa = smem_u32(sP), sTa = smem_u32(sT);
                 uint32_t qc = 0, jt = 0, sg = 0;
-                while (sch.next(rg, t0, t1, seg)) {
+                while (sch.next(rg, t0, t1, seg, mid)) {
                     const int mm = tail64(rg) ? 64 : 128;  // (M = 64 reads P rows 0-63 of each chunk)
                     const uint32_t idesc = cps == 4 ? umma_idesc_bf16(mm, 256, 0, 1) : umma_idesc_bf16(mm, 128, 0, 1);
-                    for (int t = t0; t < t1; ++t, ++jt) {
-                        const bool first = (t == t0);
+                    for (int i = 0; i < t1 - t0; ++i, ++jt) {
+                        const bool first = (i == 0);
                         const uint32_t b = jt & 1, ph = (jt >> 1) & 1;
                         mbar_wait(&aux->pfull[b], ph);
                         unsigned long long *dbg = (p.dbg && blockIdx.x == 2u * p.dbg_cluster + 1 && jt < 64 && lane == 0) ? p.dbg + jt * 16 : nullptr;
@@ -891,7 +920,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                         }
                         umma_commit_mc_e(&aux->pslot_free[b], 0x1);  // tell the producer slot b is free
                         if (dbg) dbg[7] = clock64();
-                        if (t == t1 - 1) umma_commit_e(&aux->ofull);
+                        if (i == t1 - t0 - 1) umma_commit_e(&aux->ofull);
                     }
                     ++sg;
                 }
@@ -907,7 +936,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
             // [32 rows x 16 fp32] box of seg_O (row-per-lane global stores scatter one row per
             // lane and took ~45K cycles per unit)
             const uint32_t stg = smem_u32(smem + PC_OFF_OSTG + warp * 2048);
-            while (sch.next(rg, t0, t1, seg)) {
+            while (sch.next(rg, t0, t1, seg, mid)) {
                 mbar_wait(&aux->ofull, sg & 1);
                 tc_fence_after();
                 const bool m64 = tail64(rg);

@@ -115,7 +115,7 @@ struct Layout {
     size_t T, lab, sc, x_all, y_all, pair_all, blk_x, blk_y, inv_n, hslot, hkeys, hvals, tseq,
         comp_idx, pos_row, X_pos, row_ab, row_tgt, ttgt, seg_l, seg_mx, seg_O, rowloss, st_lse,
         st_cos, st_phi, st_ell, seg_arg, rs_buf, rs_all, dx_part, tseq_ext, dx32, tmax_glob, mu_fx, Traw, wslot,
-        hgseq, row_hent, dup_cnt, dup_off, dup_list, ekeys, evals, ehslot, rseq, dst_seq, wmu, prog, total;
+        hgseq, row_hent, dup_cnt, dup_off, dup_list, ekeys, evals, ehslot, rseq, dst_seq, prog, total;
     int64_t C_loc, N, Mg, R_max, S_max;
     int H, He;
 };
@@ -184,10 +184,8 @@ static Layout make_layout(int64_t C, int d, int dtype, int W, int rank, int64_t 
     L.mu_fx = take(static_cast<size_t>(d) * 8);  // this shard's pool sum mu, fixed point (k_mu_sum)
     // K >= 2: raw features [C_loc][K][d] (state) and 1/||T_bar_c|| (the T region holds T_bar)
     L.Traw = take(K > 1 ? static_cast<size_t>(L.C_loc) * K * d * es : 0, 1024);
-    L.wslot = take(K > 1 ? static_cast<size_t>(L.C_loc) * 4 : 0);
-    // the same weights in bf16 (the out-of-pool rows' weight ring in the fused kernel), padded by
-    // one tile of zeros
-    L.wmu = take(K > 1 ? static_cast<size_t>(L.C_loc + 128) * 2 : 0);
+    // (padded by one tile: the fused kernel's weight ring copies whole 128-slot tiles)
+    L.wslot = take(K > 1 ? static_cast<size_t>(L.C_loc + 128) * 4 : 0);
     // NEXT-3 stale self-duplicate lists (f2c_dcp_set_dup_mode): per hash entry the target
     // write index, per compacted row its hash entry, per 128-slot tile a count / offset, and
     // at most one (slot, entry) pair per local slot
@@ -459,7 +457,8 @@ int f2c_dcp_create_k(int64_t C, int32_t K, int32_t d, int32_t dtype, int32_t wor
         k_hash_clear<<<64, 256>>>(R.at<int64_t>(R.L.ekeys), R.at<unsigned long long>(R.L.evals), R.L.He);
         if (dtype == F2C_BF16) {
             if ((rc = make_tmap_bf16(&R.tmT, R.base + R.L.T, R.hi - R.lo, d, TP_TILE)) ||
-                (rc = make_tmap_pool3d(&R.tm3p, R.base + R.L.T, R.hi - R.lo, d, 2)) ||
+                // producer: the logits GEMM reads the K raw rows of a slot ([C_loc][K d], NEXT-1)
+                (rc = make_tmap_pool3d(&R.tm3p, R.base + (K > 1 ? R.L.Traw : R.L.T), R.hi - R.lo, K * d, 2)) ||
                 (rc = make_tmap_pool3d(&R.tm3q, R.base + R.L.T, R.hi - R.lo, d, (d % 256 == 0) ? 4 : 2)) ||
                 (rc = make_tmap_pool3d(&R.tm4p, R.base + R.L.T, R.hi - R.lo, d, 2, 64)) ||
                 (rc = make_tmap_bf16(&R.tmX, R.base + R.L.X_pos, R.L.R_max, d, TP_R)) ||
@@ -623,8 +622,8 @@ static int enqueue_rank(f2c_dcp *h, Rank &R, const uint8_t *g, const int64_t *y,
         k_enqueue_k<<<static_cast<unsigned>(blocks), 256, 0, st>>>(
             reinterpret_cast<const __nv_bfloat16 *>(g), y, m_glob, h->K, h->d, h->E, h->C, R.lo, R.hi,
             R.at<__nv_bfloat16>(R.L.Traw), R.at<__nv_bfloat16>(R.L.T), R.at<float>(R.L.wslot),
-            R.at<__nv_bfloat16>(R.L.wmu), R.at<int64_t>(R.L.lab), R.sc(),
-            h->refresh ? R.at<int64_t>(R.L.dst_seq) : nullptr, R.at<unsigned long long>(R.L.mu_fx));
+            R.at<int64_t>(R.L.lab), R.sc(), h->refresh ? R.at<int64_t>(R.L.dst_seq) : nullptr,
+            R.at<unsigned long long>(R.L.mu_fx), h->E < h->C ? h->E : h->C);
         LAUNCH_CHECK();
         return F2C_OK;
     }
@@ -795,6 +794,7 @@ static int phase_compact(f2c_dcp *h, Rank &R, const StepCtx &c, const int *tmax_
     a.N = c.N; a.C = h->C; a.lo = R.lo; a.hi = R.hi; a.E = h->E; a.M_last = h->M_last;
     a.s = c.s;
     a.log2e_s = c.s * 1.4426950408889634f;
+    a.a_scale = 1.0f / static_cast<float>(h->K);
     a.ref_scale = a.log2e_s * (1.0f + 1.0f / 1024.0f);
     a.R_max = static_cast<int>(L.R_max);
     a.comp_idx = R.at<int>(L.comp_idx);
@@ -832,7 +832,7 @@ static int phase_compact(f2c_dcp *h, Rank &R, const StepCtx &c, const int *tmax_
     const int row_bytes = h->d * 2;
     k_gather<<<static_cast<unsigned>(L.R_max / 8), 256, 0, c.st>>>(c.x, R.at<int>(L.pos_row), R.sc(), row_bytes,
                                                           R.base + L.X_pos, R.base + L.T, R.at<int>(L.row_tgt),
-                                                          R.at<float2>(L.row_ab));
+                                                          R.at<float2>(L.row_ab), static_cast<float>(h->K));
     LAUNCH_CHECK();
     return F2C_OK;
 }
@@ -880,7 +880,7 @@ static int phase_main(f2c_dcp *h, Rank &R, const StepCtx &c, int64_t occ_loc, co
         q.row_tgt = p.row_tgt;
         q.X_pos = R.base + L.X_pos;
         q.wslot = h->K > 1 ? R.at<float>(L.wslot) : nullptr;
-        q.wmu = h->K > 1 ? R.at<__nv_bfloat16>(L.wmu) : nullptr;
+        q.kf = h->K;
         q.margin_l2 = p.margin_l2;
         q.ttgt = p.ttgt;
         q.seg_l = p.seg_l;
@@ -938,6 +938,7 @@ static CombineArgs combine_args(f2c_dcp *h, Rank &R, const StepCtx &c, int64_t o
     const int kind = kernel_kind(h, c.N);
     a.G = kind == 1 ? h->G : kind == 2 ? h->G4 : h->G / 2;
     a.rows_per_group = kind == 1 ? TP_R : kind == 2 ? P4_RG : PC_R;
+    a.tail_ok = kind == 0 && !(h->dbg_flags & 32768);
     a.n_tiles = static_cast<int>((occ + TP_TILE - 1) / TP_TILE);
     a.s = c.s;
     a.margin_l2 = c.s * c.m * 1.4426950408889634f;
@@ -1272,9 +1273,10 @@ extern "C" int f2c_dcp_set_state(f2c_dcp *h, const void *feats_host, const int64
         int zero = 0;
         CUDA_TRY(cudaMemcpy(&R.sc()->tmax_bits, &zero, 4, cudaMemcpyHostToDevice));
         if (occ > 0 && h->K > 1) {
+            CUDA_TRY(cudaMemset(R.at<float>(R.L.wslot), 0, static_cast<size_t>(n + 128) * 4));
             k_rebuild_k<<<static_cast<unsigned>((occ * 32 + 255) / 256), 256>>>(
                 R.at<__nv_bfloat16>(R.L.Traw), occ, h->K, h->d, R.at<__nv_bfloat16>(R.L.T),
-                R.at<float>(R.L.wslot), R.at<__nv_bfloat16>(R.L.wmu), R.sc());
+                R.at<float>(R.L.wslot), R.sc());
             CUDA_TRY(cudaGetLastError());
         } else if (occ > 0) {
             k_pool_norm_max<<<static_cast<unsigned>((occ * 32 + 255) / 256), 256>>>(
@@ -1283,11 +1285,15 @@ extern "C" int f2c_dcp_set_state(f2c_dcp *h, const void *feats_host, const int64
         }
         // mu over the restored slots lo .. lo + occ - 1
         CUDA_TRY(cudaMemset(R.base + R.L.mu_fx, 0, static_cast<size_t>(h->d) * 8));
-        if (occ > 0) {
+        if (occ > 0 && h->K > 1) {
+            const int64_t blocks = (occ + 7) / 8 < 4 * static_cast<int64_t>(h->G) ? (occ + 7) / 8 : 4 * static_cast<int64_t>(h->G);
+            k_mu_sum_k<<<static_cast<unsigned>(blocks), 256>>>(R.at<__nv_bfloat16>(R.L.Traw), R.at<float>(R.L.wslot),
+                                                                occ, h->K, h->d, R.at<unsigned long long>(R.L.mu_fx));
+            CUDA_TRY(cudaGetLastError());
+        } else if (occ > 0) {
             const int64_t blocks = occ < 4 * static_cast<int64_t>(h->G) ? occ : 4 * static_cast<int64_t>(h->G);
             k_mu_sum<<<static_cast<unsigned>(blocks), 256>>>(
-                R.base + R.L.T, h->K > 1 ? 0 : (h->dtype == F2C_BF16 ? 0 : 1),
-                h->K > 1 ? R.at<float>(R.L.wslot) : nullptr, h->d, occ, R.lo, h->C, R.lo, R.hi, nullptr, +1,
+                R.base + R.L.T, h->dtype == F2C_BF16 ? 0 : 1, nullptr, h->d, occ, R.lo, h->C, R.lo, R.hi, nullptr, +1,
                 R.at<unsigned long long>(R.L.mu_fx));
             CUDA_TRY(cudaGetLastError());
         }

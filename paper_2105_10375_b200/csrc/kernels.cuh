@@ -183,18 +183,42 @@ __global__ void __launch_bounds__(256) k_enqueue(const uint8_t *__restrict__ g, 
     }
 }
 
-// K >= 2 features per slot (NEXT-1): block row j carries K bf16 feature rows.
-// The raw rows are copied bit-exactly (state / checkpoint); the derived operand of every
-// kernel is T_bar = (1/K) sum_k T[c,k] (Eq. 8), fp32 mean rounded to bf16, plus
-// w_c = 1/||T_bar_c|| (0 for a zero center) for the true-cosine L_cos (reading R4).
-// One warp per row, d <= 512 (16 elements per lane).
+// K >= 2 features per slot (NEXT-1).  The center of a slot is the exact mean
+// T_bar_c = (1/K) sum_k T[c,k] (Eq. 8): its fp32 value, computed always in this order (fp32
+// sum over k from 0, then one multiply by 1/K; exact for K = 2 and K = 4 with bf16 features),
+// gives w_c = 1/||T_bar_c|| (reading R4) and the slot's mu contribution w_c T_bar_c (R3).  The
+// logits GEMM contracts x with the K raw rows (1/K folded into a_r), so the logits use the
+// exact mean too; only the P x pool GEMM and the combine read the bf16 rounding of T_bar
+// (R5).  Lane l holds columns 32 e + l (e < 16) of a d <= 512 row.
+__device__ __forceinline__ float slot_mean16(const __nv_bfloat16 *__restrict__ raw, int K, int d, int lane,
+                                             float (&mf)[16]) {
+    const float invK = 1.0f / static_cast<float>(K);
+    float ss = 0.f;
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+        const int col = e * 32 + lane;
+        float acc = 0.f;
+        if (col < d)
+            for (int kk = 0; kk < K; ++kk) acc = __fadd_rn(acc, __bfloat162float(raw[kk * d + col]));
+        mf[e] = __fmul_rn(acc, invK);
+        ss = __fmaf_rn(mf[e], mf[e], ss);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) ss = __fadd_rn(ss, __shfl_xor_sync(0xffffffffu, ss, o));
+    return ss;  // ||T_bar_c||^2 in every lane
+}
+__device__ __forceinline__ float slot_weight(float ss) { return ss > 0.f ? rsqrtf(ss) : 0.f; }
+
+// One warp per block row: the K raw rows are copied bit-exactly (state / checkpoint), the bf16
+// T_bar and w_c written, and mu updated by (new - old) contributions -- the old one recomputed
+// from the slot's raw rows before they are overwritten (same arithmetic as when it was added).
 __global__ void __launch_bounds__(256) k_enqueue_k(const __nv_bfloat16 *__restrict__ g, const int64_t *__restrict__ y,
                                                    int64_t m_glob, int K, int d, int64_t E, int64_t C,
                                                    int64_t lo, int64_t hi, __nv_bfloat16 *__restrict__ Traw,
                                                    __nv_bfloat16 *__restrict__ Tbar, float *__restrict__ wslot,
-                                                   __nv_bfloat16 *__restrict__ wmu, int64_t *__restrict__ lab,
-                                                   Scalars *sc, const int64_t *__restrict__ dst_seq,
-                                                   unsigned long long *__restrict__ mu_fx) {
+                                                   int64_t *__restrict__ lab, Scalars *sc,
+                                                   const int64_t *__restrict__ dst_seq,
+                                                   unsigned long long *__restrict__ mu_fx, int64_t occ_before) {
     __shared__ float wmax[8];
     __shared__ long long smu[MU_WARPS][512];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -209,53 +233,37 @@ __global__ void __launch_bounds__(256) k_enqueue_k(const __nv_bfloat16 *__restri
             if (lane == 0) latch(sc, ERR_DEVICE, DET_BAD_LABEL);
             continue;
         }
-        float acc[16];
-#pragma unroll
-        for (int e = 0; e < 16; ++e) acc[e] = 0.f;
-        for (int kk = 0; kk < K; ++kk) {
-            const __nv_bfloat16 *src = g + (j * K + kk) * d;
-            __nv_bfloat16 *dst = Traw + ((c - lo) * K + kk) * d;
+        __nv_bfloat16 *dst = Traw + (c - lo) * K * d;
+        float mf[16];
+        if (c < occ_before) {  // an occupied slot: its contribution leaves (wold = 0: zero center)
+            const float wold = wslot[c - lo];
+            slot_mean16(dst, K, d, lane, mf);
 #pragma unroll
             for (int e = 0; e < 16; ++e) {
                 const int col = e * 32 + lane;
-                if (col < d) {
-                    const __nv_bfloat16 v = src[col];
-                    dst[col] = v;
-                    acc[e] += __bfloat162float(v);
-                }
+                if (col < d) smu[wib][col] -= mu_fx_of(__fmul_rn(wold, mf[e]));
             }
         }
-        float ss = 0.f;
-        const float invK = 1.0f / static_cast<float>(K);
-        const float wold = wslot[c - lo];  // the overwritten slot's mu contribution leaves
-        float mfv[16];
+        __syncwarp();  // (every lane has read the old rows)
+        {   // 16-byte vector copy (rows of K d bf16 are multiples of 256 B, 16-B aligned)
+            const int4 *src = reinterpret_cast<const int4 *>(g + j * K * d);
+            int4 *d4 = reinterpret_cast<int4 *>(dst);
+            for (int i = lane; i < K * d / 8; i += 32) d4[i] = __ldcs(src + i);
+        }
+        __syncwarp();
+        const float ss = slot_mean16(dst, K, d, lane, mf);
+        const float wv = slot_weight(ss);
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
             const int col = e * 32 + lane;
-            mfv[e] = 0.f;
             if (col < d) {
-                const __nv_bfloat16 m = __float2bfloat16_rn(acc[e] * invK);
-                const float ob = __bfloat162float(Tbar[(c - lo) * d + col]);
-                smu[wib][col] -= mu_fx_of(__fmul_rn(wold, ob));
-                Tbar[(c - lo) * d + col] = m;
-                const float mf = __bfloat162float(m);
-                mfv[e] = mf;
-                ss += mf * mf;
+                Tbar[(c - lo) * d + col] = __float2bfloat16_rn(mf[e]);
+                smu[wib][col] += mu_fx_of(__fmul_rn(wv, mf[e]));
             }
         }
-#pragma unroll
-        for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-        const float wv = ss > 0.f ? rsqrtf(ss) : 0.f;  // (every lane holds the full ss)
-#pragma unroll
-        for (int e = 0; e < 16; ++e) {
-            const int col = e * 32 + lane;
-            if (col < d) smu[wib][col] += mu_fx_of(__fmul_rn(wv, mfv[e]));
-        }
-        __syncwarp();  // (every lane has read wold)
         if (lane == 0) {
             lab[c - lo] = yl;
             wslot[c - lo] = wv;
-            wmu[c - lo] = __float2bfloat16_rn(wv);
         }
         nmax = fmaxf(nmax, ss);
     }
@@ -271,30 +279,47 @@ __global__ void __launch_bounds__(256) k_enqueue_k(const __nv_bfloat16 *__restri
     }
 }
 
-// set_state with K >= 2: rebuild T_bar, w and the norm bound from the raw features
+// set_state with K >= 2: rebuild T_bar, w and the norm bound from the raw features (one warp
+// per slot, the same arithmetic as k_enqueue_k)
 __global__ void __launch_bounds__(256) k_rebuild_k(const __nv_bfloat16 *__restrict__ Traw, int64_t rows, int K, int d,
                                                    __nv_bfloat16 *__restrict__ Tbar, float *__restrict__ wslot,
-                                                   __nv_bfloat16 *__restrict__ wmu, Scalars *sc) {
+                                                   Scalars *sc) {
     const int lane = threadIdx.x & 31;
     const int64_t r = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     if (r >= rows) return;
-    float ss = 0.f;
-    for (int col = lane; col < d; col += 32) {
-        float acc = 0.f;
-        for (int kk = 0; kk < K; ++kk) acc += __bfloat162float(Traw[(r * K + kk) * d + col]);
-        const __nv_bfloat16 m = __float2bfloat16_rn(acc * (1.0f / static_cast<float>(K)));
-        Tbar[r * d + col] = m;
-        ss += __bfloat162float(m) * __bfloat162float(m);
-    }
+    float mf[16];
+    const float ss = slot_mean16(Traw + r * K * d, K, d, lane, mf);
 #pragma unroll
-    for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    for (int e = 0; e < 16; ++e) {
+        const int col = e * 32 + lane;
+        if (col < d) Tbar[r * d + col] = __float2bfloat16_rn(mf[e]);
+    }
     if (lane == 0) {
-        const float wv = ss > 0.f ? rsqrtf(ss) : 0.f;
-        wslot[r] = wv;
-        wmu[r] = __float2bfloat16_rn(wv);
-        float nrm = sqrtf(ss);
+        wslot[r] = slot_weight(ss);
+        const float nrm = sqrtf(ss);
         if (nrm > 0.f) atomicMax(&sc->tmax_bits, __float_as_int(nrm));
     }
+}
+
+// set_state with K >= 2: mu over the restored slots [0, rows) of the shard from scratch (one
+// warp per slot, the same per-slot contributions as k_enqueue_k)
+__global__ void __launch_bounds__(256) k_mu_sum_k(const __nv_bfloat16 *__restrict__ Traw, const float *__restrict__ wslot,
+                                                  int64_t rows, int K, int d, unsigned long long *__restrict__ mu_fx) {
+    __shared__ long long smu[MU_WARPS][512];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    mu_block_init(smu, d);
+    for (int64_t r = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + wib; r < rows;
+         r += static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5)) {
+        float mf[16];
+        slot_mean16(Traw + r * K * d, K, d, lane, mf);
+        const float w = wslot[r];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+            const int col = e * 32 + lane;
+            if (col < d) smu[wib][col] += mu_fx_of(__fmul_rn(w, mf[e]));
+        }
+    }
+    mu_block_flush(smu, d, mu_fx);
 }
 
 // ------------------------------------------------------------------ the pool sum mu (L_cos)
@@ -704,6 +729,7 @@ struct CompactArgs {
     const int32_t *pairing;   // [N] or null
     int64_t N, C, lo, hi, E, M_last;
     float s, log2e_s;         // s, s*log2(e)
+    float a_scale;            // 1/K: GEMM 1 sums the K raw rows of a slot (NEXT-1), a_r takes the 1/K
     int R_max;
     int neg_mode;             // 0: mu path; 1 (hinge) / 2 (max): out-of-pool rows are compacted
                               // after the in-pool rows (index neg0 + j, neg0 = n_pos rounded up to 32) and run through the kernel
@@ -795,7 +821,7 @@ __global__ void __launch_bounds__(1024) k_compact(CompactArgs a) {
                 const int kn = neg0 + static_cast<int>(i - k);  // i - k = out-of-pool rows before i
                 a.comp_idx[i] = -2 - kn;
                 a.pos_row[kn] = static_cast<int>(i);
-                a.row_ab[kn] = make_float2(a.inv_n[i], 0.f);  // e = <x, T> / ||x|| = cosine
+                a.row_ab[kn] = make_float2(a.inv_n[i] * a.a_scale, 0.f);  // e = <x, T_bar> / ||x|| = cosine
                 a.row_tgt[kn] = -2;
                 a.ttgt[kn] = -INFINITY;
             } else if (ts >= 0) {
@@ -806,7 +832,7 @@ __global__ void __launch_bounds__(1024) k_compact(CompactArgs a) {
                     a.row_hent[k] = he;
                     if (he >= 0) a.hgseq[he] = ts;  // rows sharing a label share the target
                 }
-                a.row_ab[k] = make_float2(a.log2e_s * a.inv_n[i], B);
+                a.row_ab[k] = make_float2(a.log2e_s * a.inv_n[i] * a.a_scale, B);
                 const int64_t slot = ts % a.C;
                 a.row_tgt[k] = (slot >= a.lo && slot < a.hi) ? static_cast<int>(slot - a.lo) : -1;
                 a.ttgt[k] = -INFINITY;
@@ -846,7 +872,8 @@ __global__ void __launch_bounds__(1024) k_compact(CompactArgs a) {
 __global__ void __launch_bounds__(256) k_gather(const uint8_t *__restrict__ x, const int *__restrict__ pos_row,
                                                 const Scalars *__restrict__ sc, int row_bytes,
                                                 uint8_t *__restrict__ Xp, const uint8_t *__restrict__ T,
-                                                const int *__restrict__ row_tgt, float2 *__restrict__ row_ab) {
+                                                const int *__restrict__ row_tgt, float2 *__restrict__ row_ab,
+                                                float kf) {
     // one warp per compacted row, 8 rows per CTA
     const int k = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
     if (k >= sc->n_rows || (k >= sc->n_pos && k < sc->neg0)) {
@@ -883,7 +910,7 @@ __global__ void __launch_bounds__(256) k_gather(const uint8_t *__restrict__ x, c
     if (lane == 0 && ts != -2) {  // (-2: out-of-pool row of NEXT-3, (a, b) final)
         float2 ab = row_ab[k];
         const float floor_b = ab.y - 100.f;  // ab.y holds the global bound on entry
-        const float zt = ab.x * dot;
+        const float zt = ab.x * dot * kf;  // (a_r carries 1/K, T holds the mean: K = 1 for one feature)
         ab.y = ts >= 0 ? fmaxf(zt, floor_b) : floor_b;
         row_ab[k] = ab;
     }
@@ -908,6 +935,9 @@ struct CombineArgs {
     int64_t N, C_occ;
     int d, dtype, G, n_tiles;
     int rows_per_group;         // 64 (TP64 kernel) or 128 (producer/consumer kernel)
+    int tail_ok;                // the partials come from dcp_pc_kernel, whose 64-row tail group runs
+                                // two ranges per unit (pc_choose_S / pc_unit): its segments are every
+                                // second range
     float s, margin_l2;
     uint8_t *dx;                // [N, d] dtype
     double *rowloss;            // [N]
@@ -980,8 +1010,16 @@ __device__ __forceinline__ void load_bf16_row(const __nv_bfloat16 *row, int d, i
     }
 }
 
+// The fused kernel's schedule as the partials were written: S ranges, and the range step of row
+// group rg's segments (2 for dcp_pc_kernel's 64-row tail group, else 1).
+__device__ __forceinline__ int comb_sched(const CombineArgs &a, int n_rg, int rg, int &step) {
+    const int tail = a.tail_ok ? pc_tail_group(a.sc->n_rows, a.rows_per_group, a.neg_mode, 1) : 0;
+    step = (tail && rg == n_rg - 1) ? 2 : 1;
+    return a.tail_ok ? pc_choose_S(n_rg, a.G, a.n_tiles, tail) : tp_choose_S(n_rg, a.G, a.n_tiles);
+}
+
 // sum the partials of compacted row k over its segments (fixed range order);
-// the schedule (tp_choose_S) is the main kernel's.  Segments are read in batches of B so
+// the schedule (comb_sched) is the main kernel's.  Segments are read in batches of B so
 // that the L2 latency is paid once per batch; the accumulation order is the segment order.
 __device__ __forceinline__ void gather_row_partials(const CombineArgs &a, int n_rg, int k, float (&o)[16],
                                                     float &lsum, float &mx) {
@@ -992,21 +1030,23 @@ __device__ __forceinline__ void gather_row_partials(const CombineArgs &a, int n_
     mx = -INFINITY;
     zero16(o);
     if (a.n_tiles <= 0) return;
-    const int S = tp_choose_S(n_rg, a.G, a.n_tiles);
+    int step;
+    const int S = comb_sched(a, n_rg, rg, step);
+    const int nseg = (S + step - 1) / step;
     constexpr int B = 4;
-    for (int s0 = 0; s0 < S; s0 += B) {
+    for (int s0 = 0; s0 < nseg; s0 += B) {
         float lv[B], mv[B];
         float4 ov[B][4];
 #pragma unroll
         for (int u = 0; u < B; ++u) {
-            const int s = s0 + u;
+            const int s = (s0 + u) * step;
             lv[u] = 0.f;
             mv[u] = -INFINITY;
 #pragma unroll
             for (int j = 0; j < 4; ++j) ov[u][j] = make_float4(0.f, 0.f, 0.f, 0.f);
             if (s >= S) continue;
             const int t0 = tp_range_begin(s, a.n_tiles, S);
-            const int t1 = tp_range_begin(s + 1, a.n_tiles, S);
+            const int t1 = tp_range_begin(s + step < S ? s + step : S, a.n_tiles, S);
             if (t1 <= t0) continue;
             const long long seg = static_cast<long long>(s) * n_rg + rg;
             lv[u] = a.seg_l[seg * RG + r];
@@ -1020,7 +1060,7 @@ __device__ __forceinline__ void gather_row_partials(const CombineArgs &a, int n_
         }
 #pragma unroll
         for (int u = 0; u < B; ++u) {
-            if (s0 + u >= S) break;
+            if (s0 + u >= nseg) break;
             lsum += lv[u];
             mx = fmaxf(mx, mv[u]);
 #pragma unroll
@@ -1042,10 +1082,11 @@ __device__ __forceinline__ void gather_row_max(const CombineArgs &a, int n_rg, i
     cmax = -INFINITY;
     carg = -1;
     if (a.n_tiles <= 0) return;
-    const int S = tp_choose_S(n_rg, a.G, a.n_tiles);
-    for (int s = 0; s < S; ++s) {
+    int step;
+    const int S = comb_sched(a, n_rg, rg, step);
+    for (int s = 0; s < S; s += step) {
         const int t0 = tp_range_begin(s, a.n_tiles, S);
-        const int t1 = tp_range_begin(s + 1, a.n_tiles, S);
+        const int t1 = tp_range_begin(s + step < S ? s + step : S, a.n_tiles, S);
         if (t1 <= t0) continue;
         const long long seg = static_cast<long long>(s) * n_rg + rg;
         const float v = a.seg_mx[seg * RG + r];
@@ -1272,10 +1313,11 @@ __global__ void __launch_bounds__(256, 2) k_local_rows(CombineArgs a, float4 *__
         const int rg = k / RG, r = k % RG;
         float lsum = 0.f, mx = -INFINITY;
         if (a.n_tiles > 0) {
-            const int S = tp_choose_S(n_rg, a.G, a.n_tiles);
-            for (int s = lane; s < S; s += 32) {  // lanes split the segments, fixed-order tree below
+            int step;
+            const int S = comb_sched(a, n_rg, rg, step);
+            for (int s = lane * step; s < S; s += 32 * step) {  // lanes split the segments, fixed-order tree below
                 const int t0 = tp_range_begin(s, a.n_tiles, S);
-                const int t1 = tp_range_begin(s + 1, a.n_tiles, S);
+                const int t1 = tp_range_begin(s + step < S ? s + step : S, a.n_tiles, S);
                 if (t1 <= t0) continue;
                 const long long seg = static_cast<long long>(s) * n_rg + rg;
                 lsum += a.seg_l[seg * RG + r];

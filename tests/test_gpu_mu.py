@@ -46,10 +46,8 @@ def test_mu_running_sum_exact(dcp, W, K, dtype, C, d, m_loc, nblk, refresh):
     n_lab = 3 * C if refresh else 50 * C
     for b in range(nblk):
         G = synth.unit_rows(900 + C, synth.S_PRE, b, 0, Mg * K, d, dtype=tdt)
-        if K > 1:  # the 2^-9 grid on which the K-mean is exact in bf16 (R5; mean-cosine losses
-            # are near 0, so T_bar's rounding would otherwise dominate the comparison)
-            G = np.clip(np.rint(oracle.bf16_to_f64(G) * 512), -127, 127) / 512
-            G = oracle.f64_to_bf16(G).reshape(Mg, K, d)
+        if K > 1:  # arbitrary bf16 features, K per slot (NEXT-1: exact-mean logits)
+            G = G.reshape(Mg, K, d)
         y = rng.choice(n_lab, size=Mg, replace=False).astype(np.int64)
         head.enqueue(to_dev(G, tdt), lt(y))
         pool.enqueue(G, y, refresh=refresh)

@@ -299,11 +299,13 @@ def test_determinism(dcp):
         G, yy = synth.prefill_block(cfg, b)
         head.enqueue(to_dev(G, synth.BF16), lt(yy))
     stp = synth.step_inputs(cfg, 0)
+    head.enqueue(to_dev(stp.g, synth.BF16), lt(stp.gy))   # D4: the step's block first (pairing names it)
     x, y, pr = to_dev(stp.x, synth.BF16), lt(stp.y), it(stp.pairing)
     outs = []
     for _ in range(3):
         l, d = head.loss_fwd_bwd(x, y, pr, 64, 0.35)
         outs.append((l.clone(), d.clone()))
+    head.check()
     for l, d in outs[1:]:
         assert torch.equal(l, outs[0][0]) and torch.equal(d, outs[0][1])
 

@@ -4,8 +4,8 @@ fp64 oracle (orc_loss_v), for K = 1 and K = 2, world 1 and the emulated world 2.
 
 Out-of-pool rows are noisy copies of pool features (labels not in the pool), so the hardest
 negative is unique by a wide margin and the bf16 GEMM picks the oracle's slot.  For K = 2
-the features lie on a grid on which the mean over K is exact in bf16 (the hinge is
-discontinuous at cos = 0: both sides must decide on the same T_bar)."""
+the features are arbitrary bf16 rows: the logits GEMM contracts x with the K raw rows of a
+slot, so the cosines (and the hinge decision at cos = 0) use the exact mean (reading R5)."""
 import numpy as np
 import pytest
 import torch
@@ -36,12 +36,8 @@ def _setup(dcp, W, K, C, d, n_loc, m_loc, seed):
     n_id = 3 * C
     for b in range(C // (m_loc * W) + 2):
         G = synth.unit_rows(seed, synth.S_PRE, b, 0, m_loc * W * K, d)
-        if K > 1:
-            # features on a 2^-9 grid (|i| < 128): the K = 2 mean is exact in bf16, so the
-            # GPU's stored T_bar (bf16, R5) equals the oracle's exact mean and the
-            # hinge decisions cos > 0 are taken on the same values
-            G = np.clip(np.rint(oracle.bf16_to_f64(G) * 512), -127, 127) / 512
-            G = oracle.f64_to_bf16(G).reshape(m_loc * W, K, d)
+        if K > 1:  # arbitrary bf16 features, K per slot (NEXT-1: exact-mean logits)
+            G = G.reshape(m_loc * W, K, d)
         y = synth.uniform_labels(seed, synth.S_PRE_LAB, b, 0, m_loc * W, n_id)
         head.enqueue(to_dev(G, synth.BF16), lt(y))
         pool.enqueue(G, y)
