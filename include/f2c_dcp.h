@@ -239,6 +239,16 @@ int f2c_dcp_profile_read(f2c_dcp *h, double *main_ms, int64_t *launches, int64_t
  * (cta_group::2 SM pairs, 256-row groups); *ctas = its persistent grid (CTAs).  Host only. */
 int f2c_dcp_fused_kernel(f2c_dcp *h, int64_t n_global, int32_t *kind, int32_t *ctas);
 
+/* C5 routing plan of a pure Eq. 7 enqueue across `world` ranks (SURVEY 8(e) stage 0, P:143-151;
+ * host only: no handle, no device).  The global block is every rank's m_local rows in rank order,
+ * block row j goes to slot (E + j) mod C (Eq. 7 on the ring, D6), and slot p belongs to rank q
+ * with floor(qC/W) <= p < floor((q+1)C/W).  Writes pieces[4 i .. 4 i + 3] = (source rank,
+ * destination rank, first global block row, rows): every run of block rows of one sender whose
+ * slots are contiguous inside one destination shard, ordered by source rank then block row -- the
+ * order in which both ends issue their sends and receives.  At most 2 world + 1 pieces.
+ * Returns the piece count, or -1 for invalid arguments or max_pieces too small. */
+int64_t f2c_c5_plan(int64_t C, int32_t world, int64_t E, int64_t m_local, int64_t *pieces, int64_t max_pieces);
+
 /* Release host resources and the NCCL communicator.  The caller frees state_buf. */
 void f2c_dcp_destroy(f2c_dcp *h);
 

@@ -69,6 +69,8 @@ struct NcclApi {
     int (*GetUniqueId)(nccl_uid_t *) = nullptr;
     int (*GroupStart)() = nullptr;
     int (*GroupEnd)() = nullptr;
+    int (*Send)(const void *, size_t, int, int, nccl_comm_t, cudaStream_t) = nullptr;
+    int (*Recv)(void *, size_t, int, int, nccl_comm_t, cudaStream_t) = nullptr;
     const char *(*GetErrorString)(int) = nullptr;
     int (*CommGetAsyncError)(nccl_comm_t, int *) = nullptr;
     bool ok = false;
@@ -89,10 +91,12 @@ static NcclApi &nccl() {
             api.GroupStart = (decltype(api.GroupStart))dlsym(h, "ncclGroupStart");
             api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(h, "ncclGetUniqueId");
             api.GroupEnd = (decltype(api.GroupEnd))dlsym(h, "ncclGroupEnd");
+            api.Send = (decltype(api.Send))dlsym(h, "ncclSend");
+            api.Recv = (decltype(api.Recv))dlsym(h, "ncclRecv");
             api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
             api.CommGetAsyncError = (decltype(api.CommGetAsyncError))dlsym(h, "ncclCommGetAsyncError");
             api.ok = api.CommInitRank && api.AllGather && api.AllReduce && api.ReduceScatter &&
-                     api.GroupStart && api.GroupEnd;
+                     api.GroupStart && api.GroupEnd && api.Send && api.Recv;
         }
     }
     return api;
@@ -115,9 +119,9 @@ struct Layout {
     size_t T, lab, sc, x_all, y_all, pair_all, blk_x, blk_y, inv_n, hslot, hkeys, hvals, tseq,
         comp_idx, pos_row, X_pos, row_ab, row_tgt, ttgt, seg_l, seg_mx, seg_O, rowloss, st_lse,
         st_cos, st_phi, st_ell, seg_arg, rs_buf, rs_all, dx_part, tseq_ext, dx32, tmax_glob, mu_fx, Traw, wslot,
-        hgseq, row_hent, dup_cnt, dup_off, dup_list, ekeys, evals, ehslot, rseq, dst_seq, prog, total;
+        hgseq, row_hent, dup_cnt, dup_off, dup_list, ekeys, evals, ehslot, rseq, dst_seq, prog, ikeys, ivals, total;
     int64_t C_loc, N, Mg, R_max, S_max;
-    int H, He;
+    int H, He, HI;
 };
 
 static Layout make_layout(int64_t C, int d, int dtype, int W, int rank, int64_t n_loc, int64_t m_loc,
@@ -206,6 +210,13 @@ static Layout make_layout(int64_t C, int d, int dtype, int W, int rank, int64_t 
     L.rseq = take(static_cast<size_t>(L.Mg) * 8);
     L.dst_seq = take(static_cast<size_t>(L.Mg) * 8);
     L.prog = take(static_cast<size_t>(L.S_max) * 8);  // fused kernel: per unit progress (range pacing)
+    // the shard's label index (label -> newest seq, LabelIndex): >= 4 entries per slot, rebuilt by
+    // the host before its keys (labels ever inserted since the last rebuild) pass half of it
+    int HI = 1024;
+    while (HI < 4 * L.C_loc) HI <<= 1;
+    L.HI = HI;
+    L.ikeys = take(static_cast<size_t>(HI) * 8);
+    L.ivals = take(static_cast<size_t>(HI) * 8);
     L.total = align_up(o, 1024);
     return L;
 }
@@ -220,6 +231,8 @@ struct Rank {
     template <typename P>
     P *at(size_t off) const { return reinterpret_cast<P *>(base + off); }
     Scalars *sc() const { return at<Scalars>(L.sc); }
+    LabelIndex ix() const { return LabelIndex{at<int64_t>(L.ikeys), at<long long>(L.ivals), L.HI}; }
+    int64_t idx_keys_bound = 0;  // upper bound of the keys in the label index since its last rebuild
 };
 
 struct f2c_dcp {
@@ -454,6 +467,7 @@ int f2c_dcp_create_k(int64_t C, int32_t K, int32_t d, int32_t dtype, int32_t wor
             }
         }
         k_hash_clear<<<64, 256>>>(R.at<int64_t>(R.L.hkeys), R.at<unsigned long long>(R.L.hvals), R.L.H);
+        k_idx_clear<<<256, 256>>>(R.ix());
         k_hash_clear<<<64, 256>>>(R.at<int64_t>(R.L.ekeys), R.at<unsigned long long>(R.L.evals), R.L.He);
         if (dtype == F2C_BF16) {
             if ((rc = make_tmap_bf16(&R.tmT, R.base + R.L.T, R.hi - R.lo, d, TP_TILE)) ||
@@ -582,6 +596,55 @@ static int nccl_check(int r, const char *what) {
     return F2C_OK;
 }
 
+// ============================================================================ label index
+// Rebuild the shard's label index from its occupied slots (clear + one pass over the labels).
+static int idx_rebuild(f2c_dcp *h, Rank &R, cudaStream_t st) {
+    k_idx_clear<<<static_cast<unsigned>(R.L.HI / 256 < 4096 ? (R.L.HI + 255) / 256 : 4096), 256, 0, st>>>(R.ix());
+    LAUNCH_CHECK();
+    const int64_t occ = occ_local(h, R);
+    if (occ > 0) {
+        int64_t blocks = (occ + 255) / 256;
+        if (blocks > h->G * 16) blocks = h->G * 16;
+        k_idx_build<<<static_cast<unsigned>(blocks), 256, 0, st>>>(R.ix(), R.at<int64_t>(R.L.lab), occ, R.lo, h->C, h->E);
+        LAUNCH_CHECK();
+    }
+    R.idx_keys_bound = occ;
+    return F2C_OK;
+}
+
+// ============================================================================ C5 routing
+static int shard_of(int64_t p, int64_t C, int W) {
+    int q = static_cast<int>((p * W) / C);
+    while (q + 1 < W && p >= shard_lo(C, W, q + 1)) ++q;
+    while (q > 0 && p < shard_lo(C, W, q)) --q;
+    return q;
+}
+
+extern "C" int64_t f2c_c5_plan(int64_t C, int32_t world, int64_t E, int64_t m_local, int64_t *pieces,
+                               int64_t max_pieces) {
+    if (C < 1 || world < 1 || C < world || E < 0 || m_local < 1 || m_local * world > C || !pieces) return -1;
+    int64_t n = 0;
+    for (int r = 0; r < world; ++r) {
+        int64_t j = r * m_local;
+        const int64_t end = j + m_local;
+        while (j < end) {
+            const int64_t p = (E + j) % C;
+            const int q = shard_of(p, C, world);
+            int64_t len = end - j;
+            const int64_t to_shard_end = shard_lo(C, world, q + 1) - p;  // (the ring wraps at C = lo(W))
+            if (len > to_shard_end) len = to_shard_end;
+            if (n >= max_pieces) return -1;
+            pieces[4 * n] = r;
+            pieces[4 * n + 1] = q;
+            pieces[4 * n + 2] = j;
+            pieces[4 * n + 3] = len;
+            ++n;
+            j += len;
+        }
+    }
+    return n;
+}
+
 // ============================================================================ enqueue
 // NEXT-3 refresh-in-place (reading R7), part 1 on every shard: block-label hash, scan of the
 // shard's labels -> rseq[j] = newest local write index of label y_j or -1
@@ -590,17 +653,8 @@ static int refresh_resolve(f2c_dcp *h, Rank &R, const int64_t *y, int64_t m_glob
     k_blk_insert<<<static_cast<unsigned>((m_glob + 255) / 256), 256, 0, st>>>(y, m_glob, R.at<int64_t>(L.ekeys), L.He,
                                                                              R.at<int>(L.ehslot), R.sc());
     LAUNCH_CHECK();
-    const int64_t occ = occ_local(h, R);
-    if (occ > 0) {
-        int64_t blocks = (occ + 255) / 256;
-        if (blocks > h->G * 16) blocks = h->G * 16;
-        k_scan_pool<<<static_cast<unsigned>(blocks), 256, 0, st>>>(R.at<int64_t>(L.lab), occ, R.lo, h->C, h->E,
-                                                                   R.at<int64_t>(L.ekeys),
-                                                                   R.at<unsigned long long>(L.evals), L.He);
-        LAUNCH_CHECK();
-    }
-    k_resolve<<<static_cast<unsigned>((m_glob + 255) / 256), 256, 0, st>>>(
-        R.at<int>(L.ehslot), R.at<unsigned long long>(L.evals), m_glob, R.at<int64_t>(L.rseq));
+    // sigma_j = newest local write index of y_j, from the label index (one lookup per block row)
+    k_idx_lookup<<<static_cast<unsigned>((m_glob + 255) / 256), 256, 0, st>>>(R.ix(), y, m_glob, R.at<int64_t>(L.rseq));
     LAUNCH_CHECK();
     return F2C_OK;
 }
@@ -616,6 +670,9 @@ static int refresh_plan(f2c_dcp *h, Rank &R, int64_t m_glob, cudaStream_t st) {
 
 static int enqueue_rank(f2c_dcp *h, Rank &R, const uint8_t *g, const int64_t *y, int64_t m_glob,
                         cudaStream_t st) {
+    int rc;
+    if (R.idx_keys_bound + m_glob > R.L.HI / 2 && (rc = idx_rebuild(h, R, st))) return rc;
+    R.idx_keys_bound += m_glob;  // (at most one new key per row that lands in this shard)
     if (h->K > 1) {
         int64_t blocks = (m_glob + 7) / 8;
         if (blocks > static_cast<int64_t>(h->G) * 8) blocks = static_cast<int64_t>(h->G) * 8;
@@ -623,7 +680,7 @@ static int enqueue_rank(f2c_dcp *h, Rank &R, const uint8_t *g, const int64_t *y,
             reinterpret_cast<const __nv_bfloat16 *>(g), y, m_glob, h->K, h->d, h->E, h->C, R.lo, R.hi,
             R.at<__nv_bfloat16>(R.L.Traw), R.at<__nv_bfloat16>(R.L.T), R.at<float>(R.L.wslot),
             R.at<int64_t>(R.L.lab), R.sc(), h->refresh ? R.at<int64_t>(R.L.dst_seq) : nullptr,
-            R.at<unsigned long long>(R.L.mu_fx), h->E < h->C ? h->E : h->C);
+            R.at<unsigned long long>(R.L.mu_fx), h->E < h->C ? h->E : h->C, R.ix());
         LAUNCH_CHECK();
         return F2C_OK;
     }
@@ -633,7 +690,7 @@ static int enqueue_rank(f2c_dcp *h, Rank &R, const uint8_t *g, const int64_t *y,
     k_enqueue<<<static_cast<unsigned>(blocks), 256, 0, st>>>(
         g, y, m_glob, h->E, h->C, R.lo, R.hi, row_bytes, h->dtype, R.base + R.L.T,
         R.at<int64_t>(R.L.lab), R.sc(), h->refresh ? R.at<int64_t>(R.L.dst_seq) : nullptr,
-        R.at<unsigned long long>(R.L.mu_fx));
+        R.at<unsigned long long>(R.L.mu_fx), R.ix());
     LAUNCH_CHECK();
     return F2C_OK;
 }
@@ -656,9 +713,47 @@ extern "C" int f2c_dcp_enqueue(f2c_dcp *h, const void *g_feats, const int64_t *l
     const size_t es = h->dtype == F2C_BF16 ? 2 : 4;
     const uint8_t *gx = static_cast<const uint8_t *>(g_feats);
     const int64_t *gy = labels;
-    if (h->multi && !h->emulated) {
-        // C5: route the block to the owners; every rank receives the whole block
-        // (all-gather) and keeps the rows of its slot range.
+    if (h->multi && !h->emulated && !h->refresh) {
+        // C5: route every block row to the rank that owns its slot (E + j) mod C: grouped
+        // ncclSend / ncclRecv of the pieces of f2c_c5_plan into the owner's staging rows (the
+        // enqueue kernel still needs each overwritten slot's old row and label, so the receive
+        // cannot land in the pool itself); a rank's own rows are a device copy.  Each rank receives
+        // exactly the rows it owns (the block's slots span one or two shards).
+        NvtxRange nvc("f2c: C5 enqueue routed to the owners");
+        Rank &R = h->ranks[0];
+        NcclApi &api = nccl();
+        const int me = R.rank;
+        const size_t rb = static_cast<size_t>(h->K) * h->d * es;
+        std::vector<int64_t> pc(4 * (2 * static_cast<size_t>(h->W) + 2));
+        const int64_t np = f2c_c5_plan(h->C, h->W, h->E, m_local, pc.data(), static_cast<int64_t>(pc.size() / 4));
+        if (np < 0) return fail(F2C_EINVAL, "C5 plan failed");
+        uint8_t *bx = R.base + R.L.blk_x;
+        int64_t *by = R.at<int64_t>(R.L.blk_y);
+        const uint8_t *gsrc = static_cast<const uint8_t *>(g_feats);
+        for (int64_t i = 0; i < np; ++i) {  // own rows: device copies
+            const int64_t src = pc[4 * i], dst = pc[4 * i + 1], j = pc[4 * i + 2], len = pc[4 * i + 3];
+            if (src != me || dst != me) continue;
+            CUDA_TRY(cudaMemcpyAsync(bx + j * rb, gsrc + (j - me * m_local) * rb, len * rb, cudaMemcpyDeviceToDevice, st));
+            CUDA_TRY(cudaMemcpyAsync(by + j, labels + (j - me * m_local), len * 8, cudaMemcpyDeviceToDevice, st));
+        }
+        api.GroupStart();
+        for (int64_t i = 0; i < np; ++i) {
+            const int64_t src = pc[4 * i], dst = pc[4 * i + 1], j = pc[4 * i + 2], len = pc[4 * i + 3];
+            if (src == dst) continue;
+            if (src == me) {
+                api.Send(gsrc + (j - me * m_local) * rb, len * rb, NCCL_INT8, static_cast<int>(dst), h->comm, st);
+                api.Send(labels + (j - me * m_local), len, NCCL_INT64, static_cast<int>(dst), h->comm, st);
+            } else if (dst == me) {
+                api.Recv(bx + j * rb, len * rb, NCCL_INT8, static_cast<int>(src), h->comm, st);
+                api.Recv(by + j, len, NCCL_INT64, static_cast<int>(src), h->comm, st);
+            }
+        }
+        if ((rc = nccl_check(api.GroupEnd(), "C5 send/recv"))) return rc;
+        gx = bx;
+        gy = by;
+    } else if (h->multi && !h->emulated) {
+        // refresh-in-place (NEXT-3, R7): destinations depend on residency over all shards, so
+        // every rank receives the whole block (all-gather) and keeps the rows its plan assigns it
         Rank &R = h->ranks[0];
         NcclApi &api = nccl();
         api.GroupStart();
@@ -747,48 +842,32 @@ struct StepCtx {
 };
 
 
-// a2 + a3: norms, label hash, local target resolve (tseq = newest local seq or -1)
-static int phase_resolve(f2c_dcp *h, Rank &R, const StepCtx &c, bool materialize_tseq = true) {
-    NvtxRange nv("f2c: a2+a3 norms, label hash, target resolve");
+// a2 + a3: norms, batch-label hash (the stale-duplicate lists of NEXT-3 use it) and the local
+// target resolve from the shard's label index: tseq = newest local seq of the row's label or -1
+static int phase_resolve(f2c_dcp *h, Rank &R, const StepCtx &c) {
+    NvtxRange nv("f2c: a2+a3 norms, label index lookup");
     const Layout &L = R.L;
     const unsigned rows_blocks = static_cast<unsigned>((c.N * 32 + 255) / 256);
     if (h->dtype == F2C_BF16)
         k_rownorm_insert<__nv_bfloat16><<<rows_blocks, 256, 0, c.st>>>(
             reinterpret_cast<const __nv_bfloat16 *>(c.x), c.y, c.N, h->d, R.at<float>(L.inv_n),
-            R.at<int64_t>(L.hkeys), L.H, R.at<int>(L.hslot), R.sc());
+            R.at<int64_t>(L.hkeys), L.H, R.at<int>(L.hslot), R.sc(), R.ix(), R.at<int64_t>(L.tseq));
     else
         k_rownorm_insert<float><<<rows_blocks, 256, 0, c.st>>>(
             reinterpret_cast<const float *>(c.x), c.y, c.N, h->d, R.at<float>(L.inv_n),
-            R.at<int64_t>(L.hkeys), L.H, R.at<int>(L.hslot), R.sc());
+            R.at<int64_t>(L.hkeys), L.H, R.at<int>(L.hslot), R.sc(), R.ix(), R.at<int64_t>(L.tseq));
     LAUNCH_CHECK();
-    const int64_t C_occ = h->E < h->C ? h->E : h->C;
-    int64_t occ_loc = C_occ - R.lo;
-    if (occ_loc > R.hi - R.lo) occ_loc = R.hi - R.lo;
-    if (occ_loc < 0) occ_loc = 0;
-    if (occ_loc > 0) {
-        int64_t blocks = (occ_loc + 255) / 256;
-        if (blocks > h->G * 16) blocks = h->G * 16;
-        k_scan_pool<<<static_cast<unsigned>(blocks), 256, 0, c.st>>>(
-            R.at<int64_t>(L.lab), occ_loc, R.lo, h->C, h->E, R.at<int64_t>(L.hkeys),
-            R.at<unsigned long long>(L.hvals), L.H);
-        LAUNCH_CHECK();
-    }
-    if (materialize_tseq) {  // (W = 1: k_compact resolves from the hash itself)
-        k_resolve<<<static_cast<unsigned>((c.N + 255) / 256), 256, 0, c.st>>>(
-            R.at<int>(L.hslot), R.at<unsigned long long>(L.hvals), c.N, R.at<int64_t>(L.tseq));
-        LAUNCH_CHECK();
-    }
     return F2C_OK;
 }
 
 // a3 split + compaction + gather
-static int phase_compact(f2c_dcp *h, Rank &R, const StepCtx &c, const int *tmax_bits, bool resolve_here = false) {
+static int phase_compact(f2c_dcp *h, Rank &R, const StepCtx &c, const int *tmax_bits) {
     NvtxRange nv("f2c: a3 split + compaction + gather");
     const Layout &L = R.L;
     CompactArgs a;
     a.tseq = R.at<int64_t>(L.tseq);
-    a.rs_hslot = resolve_here ? R.at<int>(L.hslot) : nullptr;
-    a.rs_hvals = resolve_here ? R.at<unsigned long long>(L.hvals) : nullptr;
+    a.rs_hslot = nullptr;  // (tseq comes from the label index)
+    a.rs_hvals = nullptr;
     a.inv_n = R.at<float>(L.inv_n);
     a.pairing = c.pair;
     a.N = c.N; a.C = h->C; a.lo = R.lo; a.hi = R.hi; a.E = h->E; a.M_last = h->M_last;
@@ -1116,8 +1195,8 @@ extern "C" int f2c_dcp_loss_fwd_bwd(f2c_dcp *h, const void *x, const int64_t *la
     const Layout &L = R.L;
     StepCtx c{n_local, s, m, static_cast<const uint8_t *>(x), labels, pairing, st};
     h->last_N = c.N;
-    if ((rc = phase_resolve(h, R, c, false))) return rc;
-    if ((rc = phase_compact(h, R, c, &R.sc()->tmax_bits, true))) return rc;
+    if ((rc = phase_resolve(h, R, c))) return rc;
+    if ((rc = phase_compact(h, R, c, &R.sc()->tmax_bits))) return rc;
     const int64_t occ = occ_local(h, R);
     if ((rc = phase_main(h, R, c, occ))) return rc;
     if ((rc = phase_refine(h, R, c, occ))) return rc;
@@ -1301,6 +1380,11 @@ extern "C" int f2c_dcp_set_state(f2c_dcp *h, const void *feats_host, const int64
     }
     CUDA_TRY(cudaDeviceSynchronize());
     h->E = enq_count;
+    for (Rank &R : h->ranks) {
+        int rc = idx_rebuild(h, R, nullptr);
+        if (rc) return rc;
+    }
+    CUDA_TRY(cudaDeviceSynchronize());
     h->M_last = 0;            // (no block since the restore: pairing checks fail until the next enqueue)
     h->last_refresh = false;
     return F2C_OK;

@@ -59,6 +59,88 @@ __device__ __forceinline__ uint64_t hash64(uint64_t z) {
     return z;
 }
 
+// ------------------------------------------------------------------ a3: the shard's label index
+// label -> newest write index (seq) of the label among this shard's slots, or -1 once that slot
+// has been overwritten.  Older copies of a label are overwritten before its newest one (ring
+// order; a refresh-in-place keeps a slot's seq), so value -1 means the label has left the shard,
+// and target resolution (D8) is one lookup per batch row instead of a pass over the pool labels.
+// The enqueue kernels update it for every appended row: evict (old label, old seq) with a CAS
+// that only succeeds if that seq is still the label's newest, then insert (label, new seq) with
+// atomicMax -- the two commute, so rows of one block may update the same label in any order.
+// Open addressing with linear probing over HI (a power of two) entries; keys are never removed,
+// and the host rebuilds the table from the shard's labels (k_idx_build) before the key count can
+// exceed HI / 2.
+struct LabelIndex {
+    int64_t *keys;   // [HI], -1 = empty
+    long long *vals; // [HI], newest seq or -1
+    int HI;
+};
+__device__ __forceinline__ int idx_find(const LabelIndex &ix, int64_t key) {
+    unsigned h = static_cast<unsigned>(hash64(static_cast<uint64_t>(key))) & (ix.HI - 1);
+    for (;;) {
+        const int64_t k = ix.keys[h];
+        if (k == key) return static_cast<int>(h);
+        if (k == -1) return -1;
+        h = (h + 1) & (ix.HI - 1);
+    }
+}
+__device__ __forceinline__ int idx_claim(const LabelIndex &ix, int64_t key) {
+    unsigned h = static_cast<unsigned>(hash64(static_cast<uint64_t>(key))) & (ix.HI - 1);
+    for (;;) {
+        const unsigned long long old = atomicCAS(reinterpret_cast<unsigned long long *>(ix.keys + h),
+                                                 static_cast<unsigned long long>(-1ll), static_cast<unsigned long long>(key));
+        if (old == static_cast<unsigned long long>(-1ll) || old == static_cast<unsigned long long>(key))
+            return static_cast<int>(h);
+        h = (h + 1) & (ix.HI - 1);
+    }
+}
+__device__ __forceinline__ void idx_evict(const LabelIndex &ix, int64_t key, long long seq) {
+    const int h = idx_find(ix, key);
+    if (h >= 0) atomicCAS(reinterpret_cast<unsigned long long *>(ix.vals + h), static_cast<unsigned long long>(seq),
+                          static_cast<unsigned long long>(-1ll));
+}
+__device__ __forceinline__ void idx_insert(const LabelIndex &ix, int64_t key, long long seq) {
+    atomicMax(ix.vals + idx_claim(ix, key), seq);
+}
+__device__ __forceinline__ long long idx_lookup(const LabelIndex &ix, int64_t key) {
+    const int h = idx_find(ix, key);
+    return h < 0 ? -1ll : ix.vals[h];
+}
+// an enqueued row's index update (lane 0 of its warp): the row is written at seq qn; pure Eq. 7
+// appends every row, a refresh-in-place enqueue (dst_seq) only the rows with qn >= E (a refreshed
+// row keeps its label and seq).  The slot's previous content (qn - C, when qn >= C) had label yo.
+__device__ __forceinline__ void idx_enqueue_row(const LabelIndex &ix, int64_t qn, int64_t E, int64_t C, int64_t yo,
+                                                int64_t yn) {
+    if (ix.keys == nullptr || qn < E) return;
+    if (qn >= C && yo >= 0) idx_evict(ix, yo, qn - C);
+    idx_insert(ix, yn, qn);
+}
+
+__global__ void k_idx_clear(LabelIndex ix) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ix.HI; i += gridDim.x * blockDim.x) {
+        ix.keys[i] = -1;
+        ix.vals[i] = -1;
+    }
+}
+// (re)build from the shard's occupied slots [0, n_occ_loc): seq(c) = c + C floor((E-1-c) / C)
+__global__ void k_idx_build(LabelIndex ix, const int64_t *__restrict__ lab, int64_t n_occ_loc, int64_t lo, int64_t C,
+                            int64_t E) {
+    for (int64_t cl = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; cl < n_occ_loc;
+         cl += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t L = lab[cl];
+        if (L < 0) continue;
+        const int64_t c = lo + cl;
+        idx_insert(ix, L, c + C * ((E - 1 - c) / C));
+    }
+}
+// newest local seq of each of n labels (-1: not in this shard)
+__global__ void k_idx_lookup(LabelIndex ix, const int64_t *__restrict__ y, int64_t n, int64_t *__restrict__ seq) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int64_t key = y[i];
+    seq[i] = key < 0 ? -1 : idx_lookup(ix, key);
+}
+
 template <typename T>
 __device__ __forceinline__ float to_f(T v);
 template <>
@@ -108,7 +190,7 @@ __global__ void __launch_bounds__(256) k_enqueue(const uint8_t *__restrict__ g, 
                                                  int row_bytes, int dtype, uint8_t *__restrict__ T,
                                                  int64_t *__restrict__ lab, Scalars *sc,
                                                  const int64_t *__restrict__ dst_seq,
-                                                 unsigned long long *__restrict__ mu_fx) {
+                                                 unsigned long long *__restrict__ mu_fx, LabelIndex ix) {
     __shared__ float wmax[8];
     __shared__ long long smu[MU_WARPS][512];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -118,13 +200,15 @@ __global__ void __launch_bounds__(256) k_enqueue(const uint8_t *__restrict__ g, 
     float nmax = 0.f;
     for (int64_t j = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + wib; j < m_glob; j += nwarps) {
         // pure Eq. 7: row j -> slot (E + j) mod C; refresh-in-place (NEXT-3): the planned slot
-        const int64_t c = (dst_seq ? dst_seq[j] : E + j) % C;
+        const int64_t qn = dst_seq ? dst_seq[j] : E + j;
+        const int64_t c = qn % C;
         if (c < lo || c >= hi) continue;
         const int64_t yl = y[j];
         if (yl < 0) {
             if (lane == 0) latch(sc, ERR_DEVICE, DET_BAD_LABEL);
             continue;
         }
+        if (lane == 0) idx_enqueue_row(ix, qn, E, C, lab[c - lo], yl);
         const int4 *src = reinterpret_cast<const int4 *>(g + j * row_bytes);
         int4 *dst = reinterpret_cast<int4 *>(T + (c - lo) * row_bytes);
         const int nvec = row_bytes / 16;
@@ -218,7 +302,8 @@ __global__ void __launch_bounds__(256) k_enqueue_k(const __nv_bfloat16 *__restri
                                                    __nv_bfloat16 *__restrict__ Tbar, float *__restrict__ wslot,
                                                    int64_t *__restrict__ lab, Scalars *sc,
                                                    const int64_t *__restrict__ dst_seq,
-                                                   unsigned long long *__restrict__ mu_fx, int64_t occ_before) {
+                                                   unsigned long long *__restrict__ mu_fx, int64_t occ_before,
+                                                   LabelIndex ix) {
     __shared__ float wmax[8];
     __shared__ long long smu[MU_WARPS][512];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -226,13 +311,15 @@ __global__ void __launch_bounds__(256) k_enqueue_k(const __nv_bfloat16 *__restri
     mu_block_init(smu, d);
     float nmax = 0.f;
     for (int64_t j = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + wib; j < m_glob; j += nwarps) {
-        const int64_t c = (dst_seq ? dst_seq[j] : E + j) % C;
+        const int64_t qn = dst_seq ? dst_seq[j] : E + j;
+        const int64_t c = qn % C;
         if (c < lo || c >= hi) continue;
         const int64_t yl = y[j];
         if (yl < 0) {
             if (lane == 0) latch(sc, ERR_DEVICE, DET_BAD_LABEL);
             continue;
         }
+        if (lane == 0) idx_enqueue_row(ix, qn, E, C, lab[c - lo], yl);
         __nv_bfloat16 *dst = Traw + (c - lo) * K * d;
         float mf[16];
         if (c < occ_before) {  // an occupied slot: its contribution leaves (wold = 0: zero center)
@@ -451,7 +538,8 @@ __global__ void k_hash_clear(int64_t *keys, unsigned long long *vals, int H) {
 template <typename T>
 __global__ void k_rownorm_insert(const T *__restrict__ x, const int64_t *__restrict__ y, int64_t N,
                                  int d, float *__restrict__ inv_n, int64_t *keys, int H,
-                                 int *__restrict__ hslot, Scalars *sc) {
+                                 int *__restrict__ hslot, Scalars *sc, LabelIndex ix,
+                                 int64_t *__restrict__ tseq) {
     const int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (i >= N) return;
@@ -488,8 +576,10 @@ __global__ void k_rownorm_insert(const T *__restrict__ x, const int64_t *__restr
         if (key < 0) {
             latch(sc, ERR_DEVICE, DET_BAD_LABEL);
             hslot[i] = -1;
+            tseq[i] = -1;
             return;
         }
+        tseq[i] = idx_lookup(ix, key);  // a3: the target = the label's newest slot of this shard (D8)
         unsigned h = static_cast<unsigned>(hash64(static_cast<uint64_t>(key))) & (H - 1);
         for (;;) {
             unsigned long long old = atomicCAS(reinterpret_cast<unsigned long long *>(keys + h),
@@ -504,45 +594,13 @@ __global__ void k_rownorm_insert(const T *__restrict__ x, const int64_t *__restr
     }
 }
 
-// a3 (part 2): one coalesced pass over the shard's occupied slot labels; a slot whose
-// label is in the batch raises that label's newest write index seq(c) (D8).
-__global__ void k_scan_pool(const int64_t *__restrict__ lab, int64_t n_occ_loc, int64_t lo,
-                            int64_t C, int64_t E, const int64_t *__restrict__ keys,
-                            unsigned long long *vals, int H) {
-    for (int64_t cl = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; cl < n_occ_loc;
-         cl += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int64_t L = lab[cl];
-        if (L < 0) continue;
-        unsigned h = static_cast<unsigned>(hash64(static_cast<uint64_t>(L))) & (H - 1);
-        for (;;) {
-            const int64_t k = keys[h];
-            if (k == -1) break;
-            if (k == L) {
-                const int64_t c = lo + cl;
-                const int64_t seq = c + C * ((E - 1 - c) / C);
-                atomicMax(vals + h, static_cast<unsigned long long>(seq + 1));
-                break;
-            }
-            h = (h + 1) & (H - 1);
-        }
-    }
-}
-
-__global__ void k_resolve(const int *__restrict__ hslot, const unsigned long long *__restrict__ vals,
-                          int64_t N, int64_t *__restrict__ tseq) {
-    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= N) return;
-    const int h = hslot[i];
-    tseq[i] = h < 0 ? -1 : static_cast<int64_t>(vals[h]) - 1;
-}
-
 // ------------------------------------------------------------------ NEXT-3: refresh-in-place enqueue
 // SPEC's insert_batch (reading R7): a block row whose label is resident
 // overwrites that slot's features in place (age kept); the other rows are appended at
 // E, E+1, ... in block order -- together with the resident rows whose slot those appends
 // would overwrite (the smallest fixed point n = n0 + #{sigma_j < E + n - C}).  The block's
-// labels go into their own hash (k_blk_insert), the shard's labels are scanned with
-// k_scan_pool / k_resolve (sigma_j = newest write index, -1 = not resident; W > 1: MAX
+// labels go into their own hash (k_blk_insert: the S:277 duplicate check), sigma_j = newest write
+// index (-1 = not resident) comes from the shard's label index (k_idx_lookup; W > 1: MAX
 // all-reduce), and one CTA plans the destinations (k_refresh_plan).
 __global__ void k_blk_insert(const int64_t *__restrict__ y, int64_t M, int64_t *keys, int H,
                              int *__restrict__ hslot, Scalars *sc) {
