@@ -111,73 +111,6 @@ __host__ __device__ inline int tp_range_begin(int s, int n_tiles, int S) {
     return s * q + (s < rem ? s : rem);
 }
 
-// dcp_pc_kernel's schedule.  As TPSched (range-major units, segment id s * R + rg), except that a
-// 64-row tail row group (M = 64 MMAs: half the work per tile of a full group) takes TWO
-// consecutive ranges per unit with their tiles interleaved (s, s+1, s, s+1, ...): it then keeps
-// pace with the full row groups of both ranges, which read the same tiles at the same time
-// (shared through L2), and needs half as many clusters, so S can grow until all clusters work.
-// Its partial goes to the segment of its first range s (s even); the combine skips s + 1.
-__host__ __device__ inline int pc_tail_group(int n_rows, int rows_per_group, int neg_mode, int tail_ok) {
-    const int n_rg = (n_rows + rows_per_group - 1) / rows_per_group;
-    return (tail_ok && neg_mode == 0 && n_rg > 0 && n_rows - (n_rg - 1) * rows_per_group <= 64) ? 1 : 0;
-}
-__host__ __device__ inline int pc_units(int R, int S, int tail) { return tail ? (R - 1) * S + (S + 1) / 2 : R * S; }
-__host__ __device__ inline int pc_choose_S(int R, int G, int n_tiles, int tail) {
-    if (!tail) return tp_choose_S(R, G, n_tiles);
-    if (n_tiles <= 0 || R <= 0) return 1;
-    // (the same bounds as tp_choose_S: S * R <= 2G + R segments, which the state layout sizes)
-    int s_lo = G / R;
-    if (s_lo < 1) s_lo = 1;
-    int s_hi = (2 * G) / R + 1;
-    if (s_hi > n_tiles) s_hi = n_tiles;
-    if (s_lo > s_hi) s_lo = s_hi;
-    int best = s_lo;
-    float best_eff = -1.f;
-    const float work = static_cast<float>(n_tiles) * (static_cast<float>(R) - 0.5f) / static_cast<float>(G);
-    for (int S = s_lo; S <= s_hi; ++S) {
-        const int U = pc_units(R, S, 1);
-        const int waves = (U + G - 1) / G;
-        const float t = static_cast<float>(waves) * static_cast<float>((n_tiles + S - 1) / S);
-        const float eff = work / t * (waves == 1 ? 1.06f : 1.f);
-        if (eff > best_eff + 0.01f) {
-            best_eff = eff;
-            best = S;
-        }
-    }
-    return best;
-}
-// unit u -> row group rg, first range s, ranges covered m (1, or 2 for the tail group): blocks of
-// two ranges, each block = the full groups of range s, those of range s + 1, then the tail unit
-__host__ __device__ inline void pc_unit(int u, int R, int S, int tail, int &rg, int &s, int &m) {
-    if (!tail) {
-        s = u / R;
-        rg = u - s * R;
-        m = 1;
-        return;
-    }
-    const int per2 = 2 * (R - 1) + 1;
-    const int p = u / per2, r = u - p * per2;
-    s = 2 * p;
-    m = 1;
-    if (s + 1 < S) {            // a full block of two ranges
-        if (r < 2 * (R - 1)) {
-            s += r / (R - 1);
-            rg = r - (r / (R - 1)) * (R - 1);
-        } else {
-            rg = R - 1;
-            m = 2;
-        }
-    } else {                    // S odd: the last range alone
-        rg = r;                 // (r < R - 1: full groups, r = R - 1: the tail)
-    }
-}
-// tile i of a unit over [t0, t1) whose ranges split at mid (m = 2: interleaved; m = 1: mid = t1)
-__host__ __device__ inline int pc_unit_tile(int i, int t0, int mid, int t1) {
-    const int lb = t1 - mid;                 // second range (<= the first: tp_range_begin)
-    if (i < 2 * lb) return (i & 1) ? mid + (i >> 1) : t0 + (i >> 1);
-    return t0 + (i - lb);
-}
-
 struct TPSched {
     int R, S, n_tiles, G;
     int u, U;

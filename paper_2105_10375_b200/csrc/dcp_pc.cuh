@@ -75,23 +75,15 @@ constexpr int PC_P_CHUNKS = 4;     // P transfer pieces (see the mover)
 // the cluster's unit list, computed once per CTA (TPSched) and read by every role
 struct PCUnitIt {
     const int4 *u;
-    const int *um;
     int n, i;
-    // a unit: row group rg, tiles [t0, t1) split at mid into its ranges (pc_unit_tile), segment seg
-    __device__ bool next(int &rg, int &t0, int &t1, int &seg, int &mid) {
+    __device__ bool next(int &rg, int &t0, int &t1, int &seg) {
         if (i >= n) return false;
-        const int4 v = u[i];
-        mid = um ? um[i] : v.z;
-        ++i;
+        const int4 v = u[i++];
         rg = v.x;
         t0 = v.y;
         t1 = v.z;
         seg = v.w;
         return true;
-    }
-    __device__ bool next(int &rg, int &t0, int &t1, int &seg) {  // (one range per unit: dcp_pc4_kernel)
-        int mid;
-        return next(rg, t0, t1, seg, mid);
     }
 };
 
@@ -113,7 +105,6 @@ struct PCAux {
     float red_mx[2][PC_R];
     int red_arg[2][PC_R];
     int4 units[PC_MAX_UNITS];          // this cluster's (row group, t0, t1, segment) list
-    int umid[PC_MAX_UNITS];            // and where each unit's second range starts (t1: one range)
     int n_units;
     int single_wave;                   // every cluster runs at most one unit (range pacing)
     int range_len;                     // tiles per range (n_tiles / S, the same in every cluster)
@@ -324,7 +315,9 @@ __device__ __forceinline__ void tmem_wait_st() {
 // EXCL: the NEXT-3 "exclude stale self-duplicates" variant, a separate instantiation so the
 // default softmax loop is compiled exactly as without it (measured: a runtime flag there cost
 // 10 % at c3)
-template <bool EXCL>
+// NEG: the NEXT-3 hinge / max variants, whose out-of-pool rows run through the kernel as cosine rows
+// (K >= 2: with their weights through an smem ring); the default instantiation carries none of it
+template <bool EXCL, bool NEG>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
     dcp_pc_kernel(const __grid_constant__ CUtensorMap tm3p, const __grid_constant__ CUtensorMap tm3q,
                   const __grid_constant__ CUtensorMap tmO, const PCParams p) {
@@ -400,25 +393,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
             mbar_arrive_expect_tx(&aux->pfull[1], PC_PBYTES);
         }
         fence_mbar_init();
-        // the cluster's units (pc_unit: a 64-row tail group takes two interleaved ranges)
-        const int Gc = static_cast<int>(gridDim.x >> 1);
-        const int tail = tail64(n_rg - 1) ? 1 : 0;
-        const int S = pc_choose_S(n_rg, Gc, n_tiles, tail);
-        const int U = n_tiles > 0 ? pc_units(n_rg, S, tail) : 0;
-        int n = 0;
-        for (int u = static_cast<int>(blockIdx.x >> 1); u < U && n < PC_MAX_UNITS; u += Gc) {
-            int ug, us, um;
-            pc_unit(u, n_rg, S, tail, ug, us, um);
-            const int a0 = tp_range_begin(us, n_tiles, S), a1 = tp_range_begin(us + 1, n_tiles, S);
-            const int b1 = tp_range_begin(us + um < S ? us + um : S, n_tiles, S);
-            if (b1 <= a0) continue;
-            aux->units[n] = make_int4(ug, a0, b1, us * n_rg + ug);
-            aux->umid[n] = a1;
-            ++n;
-        }
+        TPSched ts;
+        ts.init(blockIdx.x >> 1, gridDim.x >> 1, n_rg, n_tiles);
+        int n = 0, a, b, c, s;
+        while (n < PC_MAX_UNITS && ts.next(a, b, c, s)) aux->units[n++] = make_int4(a, b, c, s);
         aux->n_units = n;
-        aux->single_wave = U <= Gc;
-        aux->range_len = n_tiles / S;
+        aux->single_wave = ts.U <= ts.G;
+        aux->range_len = n_tiles / ts.S;
         PC_STAMP(1);
     }
     if (warp == 9) {
@@ -435,8 +416,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
     if (threadIdx.x == 0) PC_STAMP(2);
     const uint32_t tmem = aux->tmem_base;
 
-    PCUnitIt sch{aux->units, aux->umid, aux->n_units, 0};
-    int rg, t0, t1, seg, mid;
+    PCUnitIt sch{aux->units, aux->n_units, 0};
+    int rg, t0, t1, seg;
 
     if (crank == 0) {
         // ================================================================= PRODUCER
@@ -452,26 +433,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                 // groups and long ranges; measured 1.5-8.5 % slower at c2 / c1 / c3r_8 otherwise)
                 const bool pace = p.prog != nullptr && aux->single_wave && n_rg >= 2 && n_rg <= 8 &&
                                   tail64(n_rg - 1) && aux->range_len >= 512;
-                while (sch.next(rg, t0, t1, seg, mid)) {
+                while (sch.next(rg, t0, t1, seg)) {
                     int spins = 0;  // (per unit: a stalled peer costs at most PC_PACE_SPINS polls per unit)
-                    const bool wmu = p.wslot != nullptr && p.neg_mode != 0 && rg * PC_R + PC_R - 1 >= neg0;
+                    const bool wmu = NEG && p.wslot != nullptr && p.neg_mode != 0 && rg * PC_R + PC_R - 1 >= neg0;
                     unsigned long long *pg0 = pace ? p.prog + (seg - rg) : nullptr;  // this range's row groups
-                    const bool upace = pace && !tail64(rg);  // (the tail group keeps pace by construction)
-                    for (int i = 0; i < t1 - t0; ++i) {
-                        const int t = pc_unit_tile(i, t0, mid, t1);
-                        if (upace && (i % PC_PACE_EVERY) == 0) {
+                    for (int t = t0; t < t1; ++t) {
+                        if (pace && ((t - t0) % PC_PACE_EVERY) == 0) {
                             const unsigned long long mine = (static_cast<unsigned long long>(p.epoch) << 32) |
-                                                            static_cast<unsigned long long>(i);
+                                                            static_cast<unsigned long long>(t - t0);
                             asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(pg0 + rg), "l"(mine) : "memory");
                             while (spins < PC_PACE_SPINS) {  // wait while > LAG tiles ahead of the slowest
                                 long long slow = 1ll << 40;
-                                for (int g = 0; g < n_rg - 1; ++g) {  // (full groups; the tail group never waits)
+                                for (int g = 0; g < n_rg; ++g) {
                                     unsigned long long v;
                                     asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(pg0 + g) : "memory");
                                     const long long dn = (v >> 32) == p.epoch ? static_cast<long long>(v & 0xffffffffull) : 0;
                                     slow = dn < slow ? dn : slow;
                                 }
-                                if (slow + PC_PACE_LAG >= i) break;
+                                if (slow + PC_PACE_LAG >= t - t0) break;
                                 ++spins;
                                 __nanosleep(256);
                             }
@@ -500,7 +479,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                             tma_load_3d(sT + st * PC_P_STAGE_BYTES, &tm3p, &aux->tfull[st], 0, tl * PC_TILE, g * cps_p);
                         }
                     }
-                    if (upace) {  // range done: never hold the others back
+                    if (pace) {  // range done: never hold the others back
                         const unsigned long long fin = (static_cast<unsigned long long>(p.epoch) << 32) | 0xfffffffull;
                         asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(pg0 + rg), "l"(fin) : "memory");
                     }
@@ -512,12 +491,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                 // descriptors advance by immediates: the start-address field holds addr >> 4
                 const uint64_t bdesc0 = umma_desc_sw128(smem_u32(sT), 16, 1024);
                 uint32_t pc = 0, jt = 0, sg = 0;
-                while (sch.next(rg, t0, t1, seg, mid)) {
+                while (sch.next(rg, t0, t1, seg)) {
                     const uint32_t idesc = umma_idesc_bf16(tail64(rg) ? 64 : 128, PC_TILE, 0, 0);
                     mbar_wait(&aux->xready, sg & 1);
                     if (lane == 0 && sg == 0) PC_STAMP(4);
                     tc_fence_after();
-                    for (int i = 0; i < t1 - t0; ++i, ++jt) {
+                    for (int t = t0; t < t1; ++t, ++jt) {
                         unsigned long long *dbg = (p.dbg && blockIdx.x == 2u * p.dbg_cluster && jt < 64 && lane == 0) ? p.dbg + jt * 16 : nullptr;
                         const uint32_t sb = jt & 1, sph = (jt >> 1) & 1;
                         const uint32_t dcol = tmem + S_COL + sb * PC_TILE;
@@ -541,7 +520,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                         umma_commit_e(&aux->sfull[sb]);
                         }
                         if (dbg) dbg[1] = clock64();
-                        if (i == t1 - t0 - 1) umma_commit_e(&aux->xfree);
+                        if (t == t1 - 1) umma_commit_e(&aux->xfree);
                     }
                     ++sg;
                 }
@@ -550,8 +529,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
             // -------- P mover: staging buffer -> consumer's P slot (DSMEM bulk copy)
             if (lane == 0 && !(p.dbg_flags & 4096)) {
                 uint32_t jt = 0;
-                while (sch.next(rg, t0, t1, seg, mid)) {
-                    for (int i = 0; i < t1 - t0; ++i, ++jt) {
+                while (sch.next(rg, t0, t1, seg)) {
+                    for (int t = t0; t < t1; ++t, ++jt) {
                         const uint32_t b = jt & 1, ph = (jt >> 1) & 1;
                         mbar_wait(&aux->pready[b], ph);
                         mbar_wait(&aux->pslot_free[b], ph ^ 1);
@@ -599,7 +578,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                 tmem_wait_st();
             }
             uint32_t jt = 0, sg = 0, wc_n = 0;
-            while (sch.next(rg, t0, t1, seg, mid)) {
+            while (sch.next(rg, t0, t1, seg)) {
                 const bool m64 = tail64(rg);
                 const int r = m64 ? (lane < 16 ? q * 16 + lane : -1) : q * 32 + lane;
                 const bool rv = r >= 0;
@@ -633,13 +612,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                 int barg = -1;
                 // K >= 2: this unit's tiles bring their weights through the smem ring (it holds
                 // out-of-pool rows of NEXT-3 hinge / max)
-                const bool wmu = p.wslot != nullptr && p.neg_mode != 0 && rg * PC_R + PC_R - 1 >= neg0;
+                const bool wmu = NEG && p.wslot != nullptr && p.neg_mode != 0 && rg * PC_R + PC_R - 1 >= neg0;
                 // NEXT-3: out-of-pool rows compacted after the in-pool rows (a = 1/||x||, b = 0)
                 // (the padding rows after n_rows take this path too: zero operands, discarded
                 // results, and no divergence with the last out-of-pool rows of their warp)
-                const bool negrow = p.neg_mode != 0 && row >= neg0;
-                for (int i = 0; i < t1 - t0; ++i, ++jt) {
-                    const int t = pc_unit_tile(i, t0, mid, t1);
+                const bool negrow = NEG && p.neg_mode != 0 && row >= neg0;
+                for (int t = t0; t < t1; ++t, ++jt) {
                     const uint32_t sb = jt & 1, sph = (jt >> 1) & 1;
                     mbar_wait(&aux->sfull[sb], sph);
                     tc_fence_after();
@@ -868,9 +846,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
             // -------- TMA: pool stages [cps chunks x 128 slots x 64 d] (3D box) = one d block
             if (lane == 0) {
                 uint32_t qc = 0;
-                while (sch.next(rg, t0, t1, seg, mid)) {
-                    for (int i = 0; i < t1 - t0; ++i) {
-                        const int t = pc_unit_tile(i, t0, mid, t1);
+                while (sch.next(rg, t0, t1, seg)) {
+                    for (int t = t0; t < t1; ++t)
                         for (int g = 0; g < nstg; ++g, ++qc) {
                             const uint32_t st = qc % PC_Q_NSTAGE, ph = (qc / PC_Q_NSTAGE) & 1;
                             mbar_wait(&aux->qempty[st], ph ^ 1);
@@ -882,7 +859,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                             const int tl = (p.dbg_flags & 16384) ? (t & 15) : t;
                             tma_load_3d(sT + st * PC_STAGE_BYTES, &tm3q, &aux->qfull[st], 0, tl * PC_TILE, g * cps);
                         }
-                    }
                 }
             }
         } else if (warp == 9) {
@@ -890,11 +866,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
             {  // whole warp; one elected lane issues
                 const uint32_t sPa = smem_u32(sP), sTa = smem_u32(sT);
                 uint32_t qc = 0, jt = 0, sg = 0;
-                while (sch.next(rg, t0, t1, seg, mid)) {
+                while (sch.next(rg, t0, t1, seg)) {
                     const int mm = tail64(rg) ? 64 : 128;  // (M = 64 reads P rows 0-63 of each chunk)
                     const uint32_t idesc = cps == 4 ? umma_idesc_bf16(mm, 256, 0, 1) : umma_idesc_bf16(mm, 128, 0, 1);
-                    for (int i = 0; i < t1 - t0; ++i, ++jt) {
-                        const bool first = (i == 0);
+                    for (int t = t0; t < t1; ++t, ++jt) {
+                        const bool first = (t == t0);
                         const uint32_t b = jt & 1, ph = (jt >> 1) & 1;
                         mbar_wait(&aux->pfull[b], ph);
                         unsigned long long *dbg = (p.dbg && blockIdx.x == 2u * p.dbg_cluster + 1 && jt < 64 && lane == 0) ? p.dbg + jt * 16 : nullptr;
@@ -920,7 +896,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                         }
                         umma_commit_mc_e(&aux->pslot_free[b], 0x1);  // tell the producer slot b is free
                         if (dbg) dbg[7] = clock64();
-                        if (i == t1 - t0 - 1) umma_commit_e(&aux->ofull);
+                        if (t == t1 - 1) umma_commit_e(&aux->ofull);
                     }
                     ++sg;
                 }
@@ -936,7 +912,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
             // [32 rows x 16 fp32] box of seg_O (row-per-lane global stores scatter one row per
             // lane and took ~45K cycles per unit)
             const uint32_t stg = smem_u32(smem + PC_OFF_OSTG + warp * 2048);
-            while (sch.next(rg, t0, t1, seg, mid)) {
+            while (sch.next(rg, t0, t1, seg)) {
                 mbar_wait(&aux->ofull, sg & 1);
                 tc_fence_after();
                 const bool m64 = tail64(rg);

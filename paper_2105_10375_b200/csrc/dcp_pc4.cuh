@@ -226,7 +226,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(P4_THREADS, 1)
     tc_fence_after();
     const uint32_t tmem = aux->tmem_base;
 
-    PCUnitIt sch{aux->units, nullptr, aux->n_units, 0};
+    PCUnitIt sch{aux->units, aux->n_units, 0};
     int rg, t0, t1, seg;
 
     if (crank < 2) {

@@ -496,9 +496,13 @@ int f2c_dcp_create_k(int64_t C, int32_t K, int32_t d, int32_t dtype, int32_t wor
     }
     if (cudaFuncSetAttribute(dcp_tp64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              TP_SMEM_BYTES) != cudaSuccess ||
-        cudaFuncSetAttribute(dcp_pc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(dcp_pc_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              PC_SMEM_BYTES) != cudaSuccess ||
-        cudaFuncSetAttribute(dcp_pc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(dcp_pc_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             PC_SMEM_BYTES) != cudaSuccess ||
+        cudaFuncSetAttribute(dcp_pc_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             PC_SMEM_BYTES) != cudaSuccess ||
+        cudaFuncSetAttribute(dcp_pc_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              PC_SMEM_BYTES) != cudaSuccess ||
         cudaFuncSetAttribute(dcp_pc4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              P4_SMEM_BYTES) != cudaSuccess) {
@@ -520,7 +524,7 @@ int f2c_dcp_create_k(int64_t C, int32_t K, int32_t d, int32_t dtype, int32_t wor
         cfg.attrs = at;
         cfg.numAttrs = 1;
         int ncl = 0;
-        if (cudaOccupancyMaxActiveClusters(&ncl, dcp_pc_kernel<false>, &cfg) != cudaSuccess) {
+        if (cudaOccupancyMaxActiveClusters(&ncl, dcp_pc_kernel<false, false>, &cfg) != cudaSuccess) {
             cudaGetLastError();
             ncl = 0;
         }
@@ -983,10 +987,11 @@ static int phase_main(f2c_dcp *h, Rank &R, const StepCtx &c, int64_t occ_loc, co
         q.prog = (h->dbg_flags & 262144) ? nullptr : R.at<unsigned long long>(L.prog);  // (262144: no pacing, A/B)
         if (kind == 2)
             dcp_pc4_kernel<<<h->G4 * 4, P4_THREADS, P4_SMEM_BYTES, c.st>>>(R.tm4p, R.tm3p, q);
-        else if (q.excl)
-            dcp_pc_kernel<true><<<(h->G / 2) * 2, PC_THREADS, smem, c.st>>>(R.tm3p, R.tm3q, R.tmO, q);
-        else
-            dcp_pc_kernel<false><<<(h->G / 2) * 2, PC_THREADS, smem, c.st>>>(R.tm3p, R.tm3q, R.tmO, q);
+        else {
+            auto kern = q.excl ? (q.neg_mode ? dcp_pc_kernel<true, true> : dcp_pc_kernel<true, false>)
+                               : (q.neg_mode ? dcp_pc_kernel<false, true> : dcp_pc_kernel<false, false>);
+            kern<<<(h->G / 2) * 2, PC_THREADS, smem, c.st>>>(R.tm3p, R.tm3q, R.tmO, q);
+        }
     }
     LAUNCH_CHECK();
     if (e1) CUDA_TRY(cudaEventRecord(e1, c.st));
@@ -1017,7 +1022,6 @@ static CombineArgs combine_args(f2c_dcp *h, Rank &R, const StepCtx &c, int64_t o
     const int kind = kernel_kind(h, c.N);
     a.G = kind == 1 ? h->G : kind == 2 ? h->G4 : h->G / 2;
     a.rows_per_group = kind == 1 ? TP_R : kind == 2 ? P4_RG : PC_R;
-    a.tail_ok = kind == 0 && !(h->dbg_flags & 32768);
     a.n_tiles = static_cast<int>((occ + TP_TILE - 1) / TP_TILE);
     a.s = c.s;
     a.margin_l2 = c.s * c.m * 1.4426950408889634f;

@@ -993,9 +993,6 @@ struct CombineArgs {
     int64_t N, C_occ;
     int d, dtype, G, n_tiles;
     int rows_per_group;         // 64 (TP64 kernel) or 128 (producer/consumer kernel)
-    int tail_ok;                // the partials come from dcp_pc_kernel, whose 64-row tail group runs
-                                // two ranges per unit (pc_choose_S / pc_unit): its segments are every
-                                // second range
     float s, margin_l2;
     uint8_t *dx;                // [N, d] dtype
     double *rowloss;            // [N]
@@ -1068,16 +1065,8 @@ __device__ __forceinline__ void load_bf16_row(const __nv_bfloat16 *row, int d, i
     }
 }
 
-// The fused kernel's schedule as the partials were written: S ranges, and the range step of row
-// group rg's segments (2 for dcp_pc_kernel's 64-row tail group, else 1).
-__device__ __forceinline__ int comb_sched(const CombineArgs &a, int n_rg, int rg, int &step) {
-    const int tail = a.tail_ok ? pc_tail_group(a.sc->n_rows, a.rows_per_group, a.neg_mode, 1) : 0;
-    step = (tail && rg == n_rg - 1) ? 2 : 1;
-    return a.tail_ok ? pc_choose_S(n_rg, a.G, a.n_tiles, tail) : tp_choose_S(n_rg, a.G, a.n_tiles);
-}
-
 // sum the partials of compacted row k over its segments (fixed range order);
-// the schedule (comb_sched) is the main kernel's.  Segments are read in batches of B so
+// the schedule (tp_choose_S) is the main kernel's.  Segments are read in batches of B so
 // that the L2 latency is paid once per batch; the accumulation order is the segment order.
 __device__ __forceinline__ void gather_row_partials(const CombineArgs &a, int n_rg, int k, float (&o)[16],
                                                     float &lsum, float &mx) {
@@ -1088,23 +1077,21 @@ __device__ __forceinline__ void gather_row_partials(const CombineArgs &a, int n_
     mx = -INFINITY;
     zero16(o);
     if (a.n_tiles <= 0) return;
-    int step;
-    const int S = comb_sched(a, n_rg, rg, step);
-    const int nseg = (S + step - 1) / step;
+    const int S = tp_choose_S(n_rg, a.G, a.n_tiles);
     constexpr int B = 4;
-    for (int s0 = 0; s0 < nseg; s0 += B) {
+    for (int s0 = 0; s0 < S; s0 += B) {
         float lv[B], mv[B];
         float4 ov[B][4];
 #pragma unroll
         for (int u = 0; u < B; ++u) {
-            const int s = (s0 + u) * step;
+            const int s = s0 + u;
             lv[u] = 0.f;
             mv[u] = -INFINITY;
 #pragma unroll
             for (int j = 0; j < 4; ++j) ov[u][j] = make_float4(0.f, 0.f, 0.f, 0.f);
             if (s >= S) continue;
             const int t0 = tp_range_begin(s, a.n_tiles, S);
-            const int t1 = tp_range_begin(s + step < S ? s + step : S, a.n_tiles, S);
+            const int t1 = tp_range_begin(s + 1, a.n_tiles, S);
             if (t1 <= t0) continue;
             const long long seg = static_cast<long long>(s) * n_rg + rg;
             lv[u] = a.seg_l[seg * RG + r];
@@ -1118,7 +1105,7 @@ __device__ __forceinline__ void gather_row_partials(const CombineArgs &a, int n_
         }
 #pragma unroll
         for (int u = 0; u < B; ++u) {
-            if (s0 + u >= nseg) break;
+            if (s0 + u >= S) break;
             lsum += lv[u];
             mx = fmaxf(mx, mv[u]);
 #pragma unroll
@@ -1140,11 +1127,10 @@ __device__ __forceinline__ void gather_row_max(const CombineArgs &a, int n_rg, i
     cmax = -INFINITY;
     carg = -1;
     if (a.n_tiles <= 0) return;
-    int step;
-    const int S = comb_sched(a, n_rg, rg, step);
-    for (int s = 0; s < S; s += step) {
+    const int S = tp_choose_S(n_rg, a.G, a.n_tiles);
+    for (int s = 0; s < S; ++s) {
         const int t0 = tp_range_begin(s, a.n_tiles, S);
-        const int t1 = tp_range_begin(s + step < S ? s + step : S, a.n_tiles, S);
+        const int t1 = tp_range_begin(s + 1, a.n_tiles, S);
         if (t1 <= t0) continue;
         const long long seg = static_cast<long long>(s) * n_rg + rg;
         const float v = a.seg_mx[seg * RG + r];
@@ -1371,11 +1357,10 @@ __global__ void __launch_bounds__(256, 2) k_local_rows(CombineArgs a, float4 *__
         const int rg = k / RG, r = k % RG;
         float lsum = 0.f, mx = -INFINITY;
         if (a.n_tiles > 0) {
-            int step;
-            const int S = comb_sched(a, n_rg, rg, step);
-            for (int s = lane * step; s < S; s += 32 * step) {  // lanes split the segments, fixed-order tree below
+            const int S = tp_choose_S(n_rg, a.G, a.n_tiles);
+            for (int s = lane; s < S; s += 32) {  // lanes split the segments, fixed-order tree below
                 const int t0 = tp_range_begin(s, a.n_tiles, S);
-                const int t1 = tp_range_begin(s + step < S ? s + step : S, a.n_tiles, S);
+                const int t1 = tp_range_begin(s + 1, a.n_tiles, S);
                 if (t1 <= t0) continue;
                 const long long seg = static_cast<long long>(s) * n_rg + rg;
                 lsum += a.seg_l[seg * RG + r];
