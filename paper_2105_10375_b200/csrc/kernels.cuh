@@ -106,14 +106,19 @@ __device__ __forceinline__ long long idx_lookup(const LabelIndex &ix, int64_t ke
     const int h = idx_find(ix, key);
     return h < 0 ? -1ll : ix.vals[h];
 }
-// an enqueued row's index update (lane 0 of its warp): the row is written at seq qn; pure Eq. 7
-// appends every row, a refresh-in-place enqueue (dst_seq) only the rows with qn >= E (a refreshed
-// row keeps its label and seq).  The slot's previous content (qn - C, when qn >= C) had label yo.
-__device__ __forceinline__ void idx_enqueue_row(const LabelIndex &ix, int64_t qn, int64_t E, int64_t C, int64_t yo,
-                                                int64_t yn) {
-    if (ix.keys == nullptr || qn < E) return;
-    if (qn >= C && yo >= 0) idx_evict(ix, yo, qn - C);
-    idx_insert(ix, yn, qn);
+// an enqueued row's index update (lanes 0 and 1 of its warp, concurrently: the two operations
+// commute): the row is written at seq qn; pure Eq. 7 appends every row, a refresh-in-place enqueue
+// (dst_seq) only the rows with qn >= E (a refreshed row keeps its label and seq).  The slot's
+// previous content (qn - C, when qn >= C) had label yo (lane 0 evicts it), lane 1 inserts yn.
+__device__ __forceinline__ void idx_enqueue_row(const LabelIndex &ix, int lane, int64_t qn, int64_t E, int64_t C,
+                                                const int64_t *slot_label, int64_t yn) {
+    if (ix.keys == nullptr || qn < E || lane > 1) return;
+    if (lane == 0) {
+        const int64_t yo = *slot_label;
+        if (qn >= C && yo >= 0) idx_evict(ix, yo, qn - C);
+    } else {
+        idx_insert(ix, yn, qn);
+    }
 }
 
 __global__ void k_idx_clear(LabelIndex ix) {
@@ -208,7 +213,7 @@ __global__ void __launch_bounds__(256) k_enqueue(const uint8_t *__restrict__ g, 
             if (lane == 0) latch(sc, ERR_DEVICE, DET_BAD_LABEL);
             continue;
         }
-        if (lane == 0) idx_enqueue_row(ix, qn, E, C, lab[c - lo], yl);
+        idx_enqueue_row(ix, lane, qn, E, C, lab + (c - lo), yl);
         const int4 *src = reinterpret_cast<const int4 *>(g + j * row_bytes);
         int4 *dst = reinterpret_cast<int4 *>(T + (c - lo) * row_bytes);
         const int nvec = row_bytes / 16;
@@ -319,7 +324,7 @@ __global__ void __launch_bounds__(256) k_enqueue_k(const __nv_bfloat16 *__restri
             if (lane == 0) latch(sc, ERR_DEVICE, DET_BAD_LABEL);
             continue;
         }
-        if (lane == 0) idx_enqueue_row(ix, qn, E, C, lab[c - lo], yl);
+        idx_enqueue_row(ix, lane, qn, E, C, lab + (c - lo), yl);
         __nv_bfloat16 *dst = Traw + (c - lo) * K * d;
         float mf[16];
         if (c < occ_before) {  // an occupied slot: its contribution leaves (wold = 0: zero center)

@@ -3,7 +3,7 @@
 # ncu --set full of one fused-kernel launch.  Post-process here with scripts/summarize_ncu.py.
 set -e
 W=${1:-c3}
-CMD="python bench.py --workload $W --steps 3 --warmup 3 --no-cpu-baseline --also none"
+CMD="python bench.py --workload $W --steps 3 --warmup 3 --no-cpu-baseline --also none --trials 1 --no-w-parity"
 $CMD > gpurun_out/plain_$W.log 2>&1
 ncu --nvtx --nvtx-include "timed_steps/" --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
     --clock-control none --csv --log-file gpurun_out/launches_$W.csv $CMD > gpurun_out/ncu_l_$W.log 2>&1
