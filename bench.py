@@ -626,7 +626,9 @@ def kernel_bench(args):
         torch.cuda.synchronize()
         if i >= 3:
             ts.append(e0.elapsed_time(e1))
-    byt = M * d * 2 * 2 + M * 8 * 2
+    # the block read, the overwritten rows read (their mu contributions leave, R3), the slot rows
+    # and labels written; the label index's few random 8-B accesses per row are not counted
+    byt = M * d * 2 * 3 + M * 8 * 2
     out["enqueue"] = {"rows": M, "bytes": byt, "best_ms": min(ts), "GBps": byt / (min(ts) * 1e-3) / 1e9,
                       "frac_of_measured_copy": byt / (min(ts) * 1e-3) / 1e9 / pk["hbm_gbs"]}
     head.close()

@@ -677,6 +677,8 @@ static int enqueue_rank(f2c_dcp *h, Rank &R, const uint8_t *g, const int64_t *y,
     int rc;
     if (R.idx_keys_bound + m_glob > R.L.HI / 2 && (rc = idx_rebuild(h, R, st))) return rc;
     R.idx_keys_bound += m_glob;  // (at most one new key per row that lands in this shard)
+    // (timing experiment only, results void: F2C_DBG_FLAGS bit 1 << 20 skips the label index update)
+    const LabelIndex ixe = (h->dbg_flags & (1 << 20)) ? LabelIndex{nullptr, nullptr, 0} : R.ix();
     if (h->K > 1) {
         int64_t blocks = (m_glob + 7) / 8;
         if (blocks > static_cast<int64_t>(h->G) * 8) blocks = static_cast<int64_t>(h->G) * 8;
@@ -684,7 +686,7 @@ static int enqueue_rank(f2c_dcp *h, Rank &R, const uint8_t *g, const int64_t *y,
             reinterpret_cast<const __nv_bfloat16 *>(g), y, m_glob, h->K, h->d, h->E, h->C, R.lo, R.hi,
             R.at<__nv_bfloat16>(R.L.Traw), R.at<__nv_bfloat16>(R.L.T), R.at<float>(R.L.wslot),
             R.at<int64_t>(R.L.lab), R.sc(), h->refresh ? R.at<int64_t>(R.L.dst_seq) : nullptr,
-            R.at<unsigned long long>(R.L.mu_fx), h->E < h->C ? h->E : h->C, R.ix());
+            R.at<unsigned long long>(R.L.mu_fx), h->E < h->C ? h->E : h->C, ixe);
         LAUNCH_CHECK();
         return F2C_OK;
     }
@@ -694,7 +696,7 @@ static int enqueue_rank(f2c_dcp *h, Rank &R, const uint8_t *g, const int64_t *y,
     k_enqueue<<<static_cast<unsigned>(blocks), 256, 0, st>>>(
         g, y, m_glob, h->E, h->C, R.lo, R.hi, row_bytes, h->dtype, R.base + R.L.T,
         R.at<int64_t>(R.L.lab), R.sc(), h->refresh ? R.at<int64_t>(R.L.dst_seq) : nullptr,
-        R.at<unsigned long long>(R.L.mu_fx), R.ix());
+        R.at<unsigned long long>(R.L.mu_fx), ixe);
     LAUNCH_CHECK();
     return F2C_OK;
 }

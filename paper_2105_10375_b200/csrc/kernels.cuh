@@ -106,18 +106,38 @@ __device__ __forceinline__ long long idx_lookup(const LabelIndex &ix, int64_t ke
     const int h = idx_find(ix, key);
     return h < 0 ? -1ll : ix.vals[h];
 }
-// an enqueued row's index update (lanes 0 and 1 of its warp, concurrently: the two operations
-// commute): the row is written at seq qn; pure Eq. 7 appends every row, a refresh-in-place enqueue
-// (dst_seq) only the rows with qn >= E (a refreshed row keeps its label and seq).  The slot's
-// previous content (qn - C, when qn >= C) had label yo (lane 0 evicts it), lane 1 inserts yn.
-__device__ __forceinline__ void idx_enqueue_row(const LabelIndex &ix, int lane, int64_t qn, int64_t E, int64_t C,
-                                                const int64_t *slot_label, int64_t yn) {
-    if (ix.keys == nullptr || qn < E || lane > 1) return;
-    if (lane == 0) {
-        const int64_t yo = *slot_label;
-        if (qn >= C && yo >= 0) idx_evict(ix, yo, qn - C);
-    } else {
-        idx_insert(ix, yn, qn);
+// slot of block row j: (E + j) mod C with e0 = E mod C (j < m_glob <= C, so one conditional
+// subtract: a 64-bit modulo per row and lane cost more than the row copy itself), or the planned
+// write index of a refresh-in-place enqueue
+__device__ __forceinline__ int64_t enq_slot(int64_t j, int64_t e0, int64_t C, const int64_t *__restrict__ dst_seq) {
+    if (dst_seq) return dst_seq[j] % C;
+    const int64_t c = e0 + j;
+    return c >= C ? c - C : c;
+}
+
+// The label pass of an enqueue (one THREAD per block row, so the index's dependent DRAM round
+// trips of all rows overlap; the feature copy runs in separate warp-per-row loops that never touch
+// the labels): the row is written at seq qn -- pure Eq. 7 appends every row, a refresh-in-place
+// enqueue (dst_seq) only the rows with qn >= E (a refreshed row keeps its label and seq).  Evict
+// the slot's previous label (content qn - C, when qn >= C) if that seq is still its newest, insert
+// the new label, write the slot's label.
+__device__ __forceinline__ void enqueue_labels(const int64_t *__restrict__ y, int64_t m_glob, int64_t E, int64_t C,
+                                               int64_t lo, int64_t hi, int64_t *__restrict__ lab,
+                                               const int64_t *__restrict__ dst_seq, const LabelIndex &ix) {
+    const int64_t e0 = E % C;
+    for (int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < m_glob;
+         j += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t qn = dst_seq ? dst_seq[j] : E + j;
+        const int64_t c = enq_slot(j, e0, C, dst_seq);
+        if (c < lo || c >= hi) continue;
+        const int64_t yl = y[j];
+        if (yl < 0) continue;  // (latched by the copy loop)
+        if (ix.keys != nullptr && qn >= E) {
+            const int64_t yo = lab[c - lo];
+            if (qn >= C && yo >= 0) idx_evict(ix, yo, qn - C);
+            idx_insert(ix, yl, qn);
+        }
+        lab[c - lo] = yl;
     }
 }
 
@@ -188,7 +208,7 @@ __device__ __forceinline__ void mu_block_flush(const long long (*smu)[512], int 
 }
 // Eq. 7 / Algorithm 1: global block row j -> slot (E+j) mod C.
 // One warp per block row; the rows owned by this shard [lo, hi) are copied with
-// 16-byte vector loads/stores (bit-exact), labels written by lane 0, and the running
+// 16-byte vector loads/stores (bit-exact; labels and the label index: enqueue_labels), and the running
 // max row norm (the softmax reference bound) updated.
 __global__ void __launch_bounds__(256) k_enqueue(const uint8_t *__restrict__ g, const int64_t *__restrict__ y,
                                                  int64_t m_glob, int64_t E, int64_t C, int64_t lo, int64_t hi,
@@ -201,24 +221,32 @@ __global__ void __launch_bounds__(256) k_enqueue(const uint8_t *__restrict__ g, 
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
     const int epv = dtype == 0 ? 8 : 4;  // elements per 16-byte vector
+    enqueue_labels(y, m_glob, E, C, lo, hi, lab, dst_seq, ix);
     mu_block_init(smu, (row_bytes / 16) * epv);  // d columns
+    // the lane's mu partial in registers: a lane owns the same <= 16 columns of every row it copies
+    // (per-element smem updates were 16-way bank-conflicted and bounded the kernel)
+    long long acc[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) acc[i] = 0;
+    const int nvec = row_bytes / 16;
     float nmax = 0.f;
+    const int64_t e0 = E % C;
     for (int64_t j = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + wib; j < m_glob; j += nwarps) {
         // pure Eq. 7: row j -> slot (E + j) mod C; refresh-in-place (NEXT-3): the planned slot
-        const int64_t qn = dst_seq ? dst_seq[j] : E + j;
-        const int64_t c = qn % C;
+        const int64_t c = enq_slot(j, e0, C, dst_seq);
         if (c < lo || c >= hi) continue;
         const int64_t yl = y[j];
         if (yl < 0) {
             if (lane == 0) latch(sc, ERR_DEVICE, DET_BAD_LABEL);
             continue;
         }
-        idx_enqueue_row(ix, lane, qn, E, C, lab + (c - lo), yl);
         const int4 *src = reinterpret_cast<const int4 *>(g + j * row_bytes);
         int4 *dst = reinterpret_cast<int4 *>(T + (c - lo) * row_bytes);
-        const int nvec = row_bytes / 16;
         float ss = 0.f;
-        for (int u0 = 0; u0 < nvec; u0 += 64) {  // 2 independent 16-B loads in flight per lane
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {  // 2 independent 16-B loads in flight per lane
+            const int u0 = h2 * 64;
+            if (u0 >= nvec) break;
             int4 v[2], ov[2];
 #pragma unroll
             for (int q = 0; q < 2; ++q) {
@@ -243,22 +271,39 @@ __global__ void __launch_bounds__(256) k_enqueue(const uint8_t *__restrict__ g, 
                         const float a = __uint_as_float(w[i] << 16), b = __uint_as_float(w[i] & 0xffff0000u);
                         ss += a * a + b * b;
                         const float oa = __uint_as_float(o[i] << 16), ob = __uint_as_float(o[i] & 0xffff0000u);
-                        const int col = u * 8 + 2 * i;
-                        smu[wib][col] += mu_fx_of(a) - mu_fx_of(oa);
-                        smu[wib][col + 1] += mu_fx_of(b) - mu_fx_of(ob);
+                        acc[(q * 8 + 2 * i) & 15] += mu_fx_of(a) - mu_fx_of(oa);
+                        acc[(q * 8 + 2 * i + 1) & 15] += mu_fx_of(b) - mu_fx_of(ob);
                     } else {
                         const float a = __uint_as_float(w[i]);
                         ss += a * a;
-                        smu[wib][u * 4 + i] += mu_fx_of(a) - mu_fx_of(__uint_as_float(o[i]));
+                        acc[h2 * 8 + q * 4 + i] += mu_fx_of(a) - mu_fx_of(__uint_as_float(o[i]));
                     }
                 }
             }
         }
 #pragma unroll
         for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-        if (lane == 0) lab[c - lo] = yl;
         nmax = fmaxf(nmax, ss);
     }
+    // the lane's mu partial -> its columns of the warp's smem row (each column owned by one lane)
+#pragma unroll
+    for (int h2 = 0; h2 < 2; ++h2)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            const int u = h2 * 64 + q * 32 + lane;
+            if (u >= nvec) continue;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                if (dtype == 0) {
+                    if (h2 == 0) {
+                        smu[wib][u * 8 + 2 * i] = acc[q * 8 + 2 * i];
+                        smu[wib][u * 8 + 2 * i + 1] = acc[q * 8 + 2 * i + 1];
+                    }
+                } else {
+                    smu[wib][u * 4 + i] = acc[h2 * 8 + q * 4 + i];
+                }
+            }
+        }
     mu_block_flush(smu, (row_bytes / 16) * epv, mu_fx);
     // one atomic per block for the running norm bound (the softmax reference, R1)
     if (lane == 0) wmax[wib] = nmax;
@@ -313,18 +358,18 @@ __global__ void __launch_bounds__(256) k_enqueue_k(const __nv_bfloat16 *__restri
     __shared__ long long smu[MU_WARPS][512];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+    enqueue_labels(y, m_glob, E, C, lo, hi, lab, dst_seq, ix);
     mu_block_init(smu, d);
     float nmax = 0.f;
+    const int64_t e0 = E % C;
     for (int64_t j = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + wib; j < m_glob; j += nwarps) {
-        const int64_t qn = dst_seq ? dst_seq[j] : E + j;
-        const int64_t c = qn % C;
+        const int64_t c = enq_slot(j, e0, C, dst_seq);
         if (c < lo || c >= hi) continue;
         const int64_t yl = y[j];
         if (yl < 0) {
             if (lane == 0) latch(sc, ERR_DEVICE, DET_BAD_LABEL);
             continue;
         }
-        idx_enqueue_row(ix, lane, qn, E, C, lab + (c - lo), yl);
         __nv_bfloat16 *dst = Traw + (c - lo) * K * d;
         float mf[16];
         if (c < occ_before) {  // an occupied slot: its contribution leaves (wold = 0: zero center)
@@ -353,10 +398,7 @@ __global__ void __launch_bounds__(256) k_enqueue_k(const __nv_bfloat16 *__restri
                 smu[wib][col] += mu_fx_of(__fmul_rn(wv, mf[e]));
             }
         }
-        if (lane == 0) {
-            lab[c - lo] = yl;
-            wslot[c - lo] = wv;
-        }
+        if (lane == 0) wslot[c - lo] = wv;
         nmax = fmaxf(nmax, ss);
     }
     mu_block_flush(smu, d, mu_fx);

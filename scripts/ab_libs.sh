@@ -1,5 +1,5 @@
 for L in ${LIBS:-lib_1b0c2e2 lib_wt2}; do
-  for W in c3r_8 c3 c2; do
+  for W in ${WLS:-c3r_8 c3 c2}; do
     F2C_LIB=ab/$L.so python bench.py --workload $W --also none --no-cpu-baseline --no-w-parity --steps 10 --warmup 3 --trials 1 > gpurun_out/ab_${L}_$W.json 2>&1
     python -c "
 import json,sys
