@@ -227,6 +227,28 @@ __device__ __forceinline__ void umma_ts_stage8(uint32_t d_tmem, uint32_t a_tmem,
         "l"(bdesc + 6), "l"(bdesc + 1024), "l"(bdesc + 1026), "l"(bdesc + 1028), "l"(bdesc + 1030)
         : "memory");
 }
+// The same stage for an fp32 pool (kind::tf32, K = 8 per MMA: a 128-B chunk row is 32 fp32, so the
+// A / B descriptor steps are those of bf16)
+__device__ __forceinline__ void umma_ts_stage8_tf32(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
+                                               uint32_t acc0, uint64_t *bar) {
+    asm volatile(
+        "{\n.reg .pred e, p, t;\n.reg .b32 r;\n"
+        "elect.sync r|e, 0xffffffff;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "setp.eq.b32 t, 0, 0;\n"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1+8], %6, %3, t;\n"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1+16], %7, %3, t;\n"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1+24], %8, %3, t;\n"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1+32], %9, %3, t;\n"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1+40], %10, %3, t;\n"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1+48], %11, %3, t;\n"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1+56], %12, %3, t;\n"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%5];\n}\n" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(acc0), "r"(smem_u32(bar)), "l"(bdesc + 2), "l"(bdesc + 4),
+        "l"(bdesc + 6), "l"(bdesc + 1024), "l"(bdesc + 1026), "l"(bdesc + 1028), "l"(bdesc + 1030)
+        : "memory");
+}
 // One consumer stage of GEMM 2: 8 SS MMAs over the tile's 128 slots (K steps of 16) and the
 // commit that releases the pool stage.  a/b descriptors advance by +2 (32 B) / +128 (2 KB)
 // per K step, plus +1024 (16 KB) for the A chunk after 4 steps.
@@ -317,7 +339,9 @@ __device__ __forceinline__ void tmem_wait_st() {
 // 10 % at c3)
 // NEG: the NEXT-3 hinge / max variants, whose out-of-pool rows run through the kernel as cosine rows
 // (K >= 2: with their weights through an smem ring); the default instantiation carries none of it
-template <bool EXCL, bool NEG>
+// TF32: an fp32 pool (F2C_F32, d <= 256): GEMM 1 in kind::tf32 over the fp32 rows with x_hat as fp32 in
+// TMEM (d columns); GEMM 2 and everything after it read the pool's bf16 shadow, unchanged
+template <bool EXCL, bool NEG, bool TF32>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
     dcp_pc_kernel(const __grid_constant__ CUtensorMap tm3p, const __grid_constant__ CUtensorMap tm3q,
                   const __grid_constant__ CUtensorMap tmO, const PCParams p) {
@@ -336,7 +360,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
     // producer stages: 2 chunks (32 KB) of the K d-wide raw rows of a tile (NEXT-1: GEMM 1 contracts
     // over K d, stage g pairs with x_hat stage g mod (d / 128)); consumer stages: one GEMM-2 d block
     // (2 or 4 chunks) of T_bar
-    const int cps_p = 2, xstg = nchunk / 2, nstg_p = xstg * p.kf;
+    const int cps_p = 2, xstg = TF32 ? d / 64 : nchunk / 2, nstg_p = xstg * p.kf;
     const int cps = (d % 256 == 0) ? 4 : 2;
     const int nstg = nchunk / cps;
     const uint32_t stage_bytes = static_cast<uint32_t>(cps) * 16384;
@@ -492,7 +516,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                 const uint64_t bdesc0 = umma_desc_sw128(smem_u32(sT), 16, 1024);
                 uint32_t pc = 0, jt = 0, sg = 0;
                 while (sch.next(rg, t0, t1, seg)) {
-                    const uint32_t idesc = umma_idesc_bf16(tail64(rg) ? 64 : 128, PC_TILE, 0, 0);
+                    const uint32_t idesc = TF32 ? umma_idesc_tf32(tail64(rg) ? 64 : 128, PC_TILE, 0, 0)
+                                                : umma_idesc_bf16(tail64(rg) ? 64 : 128, PC_TILE, 0, 0);
                     mbar_wait(&aux->xready, sg & 1);
                     if (lane == 0 && sg == 0) PC_STAMP(4);
                     tc_fence_after();
@@ -500,7 +525,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                         unsigned long long *dbg = (p.dbg && blockIdx.x == 2u * p.dbg_cluster && jt < 64 && lane == 0) ? p.dbg + jt * 16 : nullptr;
                         const uint32_t sb = jt & 1, sph = (jt >> 1) & 1;
                         const uint32_t dcol = tmem + S_COL + sb * PC_TILE;
-                        if (nstg_p == 4 && p.kf == 1) {  // d = 512, K = 1: the whole tile in one elected issue
+                        if (!TF32 && nstg_p == 4 && p.kf == 1) {  // d = 512, K = 1: the whole tile in one elected issue
                             if (dbg) dbg[0] = clock64();
                             gemm1_tile_issue(dcol, tmem + X_COL, bdesc0, idesc, smem_u32(&aux->sempty[sb]), sph ^ 1,
                                              smem_u32(&aux->tfull[0]), smem_u32(&aux->tempty[0]), jt & 1,
@@ -515,7 +540,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                             mbar_wait(&aux->tfull[st], ph);
                             tc_fence_after();
                             const uint64_t bst = bdesc0 + static_cast<uint64_t>(st * (PC_P_STAGE_BYTES >> 4));
-                            umma_ts_stage8(dcol, tmem + X_COL + (g % xstg) * 64, bst, idesc, g != 0, &aux->tempty[st]);
+                            if (TF32)
+                                umma_ts_stage8_tf32(dcol, tmem + X_COL + (g % xstg) * 64, bst, idesc, g != 0, &aux->tempty[st]);
+                            else
+                                umma_ts_stage8(dcol, tmem + X_COL + (g % xstg) * 64, bst, idesc, g != 0, &aux->tempty[st]);
                         }
                         umma_commit_e(&aux->sfull[sb]);
                         }
@@ -590,9 +618,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                 mbar_wait(&aux->xfree, (sg & 1) ^ 1);
                 tc_fence_after();
                 {
-                    const uint4 *src = reinterpret_cast<const uint4 *>(p.X_pos + static_cast<size_t>(row) * d * 2) +
-                                       h * (d / 16);
-                    const int ncol = d / 4;  // 32-bit columns per half row (d/2 bf16)
+                    constexpr int ES = TF32 ? 4 : 2;
+                    const uint4 *src = reinterpret_cast<const uint4 *>(p.X_pos + static_cast<size_t>(row) * d * ES) +
+                                       h * (d * ES / 32);
+                    const int ncol = d * ES / 8;  // 32-bit columns per half row (d/2 bf16 or fp32 elements)
                     for (int c0 = 0; c0 < ncol; c0 += 32) {
                         uint32_t w[32];
 #pragma unroll

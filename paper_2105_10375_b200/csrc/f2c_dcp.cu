@@ -119,7 +119,7 @@ struct Layout {
     size_t T, lab, sc, x_all, y_all, pair_all, blk_x, blk_y, inv_n, hslot, hkeys, hvals, tseq,
         comp_idx, pos_row, X_pos, row_ab, row_tgt, ttgt, seg_l, seg_mx, seg_O, rowloss, st_lse,
         st_cos, st_phi, st_ell, seg_arg, rs_buf, rs_all, dx_part, tseq_ext, dx32, tmax_glob, mu_fx, Traw, wslot,
-        hgseq, row_hent, dup_cnt, dup_off, dup_list, ekeys, evals, ehslot, rseq, dst_seq, prog, ikeys, ivals, total;
+        hgseq, row_hent, dup_cnt, dup_off, dup_list, ekeys, evals, ehslot, rseq, dst_seq, prog, ikeys, ivals, Tsh, total;
     int64_t C_loc, N, Mg, R_max, S_max;
     int H, He, HI;
 };
@@ -164,7 +164,7 @@ static Layout make_layout(int64_t C, int d, int dtype, int W, int rank, int64_t 
     L.tseq = take(static_cast<size_t>(L.N) * 8);
     L.comp_idx = take(static_cast<size_t>(L.N) * 4);
     L.pos_row = take(static_cast<size_t>(L.R_max) * 4);
-    L.X_pos = take(static_cast<size_t>(L.R_max) * d * 2, 1024);
+    L.X_pos = take(static_cast<size_t>(L.R_max) * d * es, 1024);
     L.row_ab = take(static_cast<size_t>(L.R_max) * 8);
     L.row_tgt = take(static_cast<size_t>(L.R_max) * 4);
     L.ttgt = take(static_cast<size_t>(L.R_max) * 4);
@@ -217,6 +217,8 @@ static Layout make_layout(int64_t C, int d, int dtype, int W, int rank, int64_t 
     L.HI = HI;
     L.ikeys = take(static_cast<size_t>(HI) * 8);
     L.ivals = take(static_cast<size_t>(HI) * 8);
+    // an fp32 pool's bf16 shadow (RNE of T, kept by the enqueue): the operand of the P x pool GEMM
+    L.Tsh = take(dtype == F2C_F32 ? static_cast<size_t>(L.C_loc) * d * 2 : 0, 1024);
     L.total = align_up(o, 1024);
     return L;
 }
@@ -282,6 +284,7 @@ struct f2c_dcp {
 // measured faster on every bench shape but one).
 static int kernel_kind(const f2c_dcp *h, int64_t N) {
     (void)N;
+    if (h->dtype == F2C_F32) return 0;  // (tf32 logits: dcp_pc_kernel only)
     const bool dflt = h->neg_mode() == 0 && !h->excl_dup;
     if (h->use_tp64 && dflt) return 1;
     if (dflt && h->K == 1 && h->d % 256 == 0 && h->G4 > 0 && h->pc4_mode > 0) return 2;
@@ -336,6 +339,21 @@ static int make_tmap_pool3d(CUtensorMap *m, void *ptr, int64_t rows, int d, cuui
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(F2C_ECUDA, "cuTensorMapEncodeTiled(3d) failed (%d)", (int)r);
+    return F2C_OK;
+}
+
+// An fp32 pool viewed as [d/32 chunks][rows][32]: one box [32, 128, 2] lands two chunk-major SW128
+// blocks of [128 slots x 32 fp32] (16 KB each) -- the tf32 producer stage (64 d columns)
+static int make_tmap_pool3d_f32(CUtensorMap *m, void *ptr, int64_t rows, int d) {
+    auto fn = encode_fn();
+    if (!fn) return fail(F2C_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    cuuint64_t dims[3] = {32, static_cast<cuuint64_t>(rows < 1 ? 1 : rows), static_cast<cuuint64_t>(d / 32)};
+    cuuint64_t strides[2] = {static_cast<cuuint64_t>(d) * 4, 128};
+    cuuint32_t box[3] = {32, 128, 2};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, ptr, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(F2C_ECUDA, "cuTensorMapEncodeTiled(3d f32) failed (%d)", (int)r);
     return F2C_OK;
 }
 
@@ -480,6 +498,14 @@ int f2c_dcp_create_k(int64_t C, int32_t K, int32_t d, int32_t dtype, int32_t wor
                 delete h;
                 return rc;
             }
+        } else if (d <= 256) {
+            // fp32 pool: the producer reads the fp32 rows (tf32 logits), the consumer the bf16 shadow
+            if ((rc = make_tmap_pool3d_f32(&R.tm3p, R.base + R.L.T, R.hi - R.lo, d)) ||
+                (rc = make_tmap_pool3d(&R.tm3q, R.base + R.L.Tsh, R.hi - R.lo, d, (d % 256 == 0) ? 4 : 2)) ||
+                (rc = make_tmap_segO(&R.tmO, R.base + R.L.seg_O, R.L.S_max * 128, d))) {
+                delete h;
+                return rc;
+            }
         }
         h->ranks.push_back(R);
     }
@@ -496,13 +522,21 @@ int f2c_dcp_create_k(int64_t C, int32_t K, int32_t d, int32_t dtype, int32_t wor
     }
     if (cudaFuncSetAttribute(dcp_tp64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              TP_SMEM_BYTES) != cudaSuccess ||
-        cudaFuncSetAttribute(dcp_pc_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(dcp_pc_kernel<false, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              PC_SMEM_BYTES) != cudaSuccess ||
-        cudaFuncSetAttribute(dcp_pc_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(dcp_pc_kernel<true, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              PC_SMEM_BYTES) != cudaSuccess ||
-        cudaFuncSetAttribute(dcp_pc_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(dcp_pc_kernel<false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              PC_SMEM_BYTES) != cudaSuccess ||
-        cudaFuncSetAttribute(dcp_pc_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(dcp_pc_kernel<true, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             PC_SMEM_BYTES) != cudaSuccess ||
+        cudaFuncSetAttribute(dcp_pc_kernel<false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             PC_SMEM_BYTES) != cudaSuccess ||
+        cudaFuncSetAttribute(dcp_pc_kernel<true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             PC_SMEM_BYTES) != cudaSuccess ||
+        cudaFuncSetAttribute(dcp_pc_kernel<false, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             PC_SMEM_BYTES) != cudaSuccess ||
+        cudaFuncSetAttribute(dcp_pc_kernel<true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              PC_SMEM_BYTES) != cudaSuccess ||
         cudaFuncSetAttribute(dcp_pc4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              P4_SMEM_BYTES) != cudaSuccess) {
@@ -524,7 +558,7 @@ int f2c_dcp_create_k(int64_t C, int32_t K, int32_t d, int32_t dtype, int32_t wor
         cfg.attrs = at;
         cfg.numAttrs = 1;
         int ncl = 0;
-        if (cudaOccupancyMaxActiveClusters(&ncl, dcp_pc_kernel<false, false>, &cfg) != cudaSuccess) {
+        if (cudaOccupancyMaxActiveClusters(&ncl, dcp_pc_kernel<false, false, false>, &cfg) != cudaSuccess) {
             cudaGetLastError();
             ncl = 0;
         }
@@ -696,7 +730,7 @@ static int enqueue_rank(f2c_dcp *h, Rank &R, const uint8_t *g, const int64_t *y,
     k_enqueue<<<static_cast<unsigned>(blocks), 256, 0, st>>>(
         g, y, m_glob, h->E, h->C, R.lo, R.hi, row_bytes, h->dtype, R.base + R.L.T,
         R.at<int64_t>(R.L.lab), R.sc(), h->refresh ? R.at<int64_t>(R.L.dst_seq) : nullptr,
-        R.at<unsigned long long>(R.L.mu_fx), ixe);
+        R.at<unsigned long long>(R.L.mu_fx), ixe, h->dtype == F2C_F32 ? R.at<__nv_bfloat16>(R.L.Tsh) : nullptr);
     LAUNCH_CHECK();
     return F2C_OK;
 }
@@ -914,10 +948,11 @@ static int phase_compact(f2c_dcp *h, Rank &R, const StepCtx &c, const int *tmax_
             R.at<int>(L.dup_cnt), R.at<int>(L.dup_off), R.at<int2>(L.dup_list));
         LAUNCH_CHECK();
     }
-    const int row_bytes = h->d * 2;
+    const int row_bytes = h->d * (h->dtype == F2C_BF16 ? 2 : 4);
     k_gather<<<static_cast<unsigned>(L.R_max / 8), 256, 0, c.st>>>(c.x, R.at<int>(L.pos_row), R.sc(), row_bytes,
                                                           R.base + L.X_pos, R.base + L.T, R.at<int>(L.row_tgt),
-                                                          R.at<float2>(L.row_ab), static_cast<float>(h->K));
+                                                          R.at<float2>(L.row_ab), static_cast<float>(h->K),
+                                                          h->dtype == F2C_F32 ? 1 : 0);
     LAUNCH_CHECK();
     return F2C_OK;
 }
@@ -990,8 +1025,13 @@ static int phase_main(f2c_dcp *h, Rank &R, const StepCtx &c, int64_t occ_loc, co
         if (kind == 2)
             dcp_pc4_kernel<<<h->G4 * 4, P4_THREADS, P4_SMEM_BYTES, c.st>>>(R.tm4p, R.tm3p, q);
         else {
-            auto kern = q.excl ? (q.neg_mode ? dcp_pc_kernel<true, true> : dcp_pc_kernel<true, false>)
-                               : (q.neg_mode ? dcp_pc_kernel<false, true> : dcp_pc_kernel<false, false>);
+            decltype(&dcp_pc_kernel<false, false, false>) kern;
+            if (h->dtype == F2C_F32)
+                kern = q.excl ? (q.neg_mode ? dcp_pc_kernel<true, true, true> : dcp_pc_kernel<true, false, true>)
+                              : (q.neg_mode ? dcp_pc_kernel<false, true, true> : dcp_pc_kernel<false, false, true>);
+            else
+                kern = q.excl ? (q.neg_mode ? dcp_pc_kernel<true, true, false> : dcp_pc_kernel<true, false, false>)
+                              : (q.neg_mode ? dcp_pc_kernel<false, true, false> : dcp_pc_kernel<false, false, false>);
             kern<<<(h->G / 2) * 2, PC_THREADS, smem, c.st>>>(R.tm3p, R.tm3q, R.tmO, q);
         }
     }
@@ -1013,7 +1053,7 @@ static CombineArgs combine_args(f2c_dcp *h, Rank &R, const StepCtx &c, int64_t o
     a.seg_l = R.at<float>(L.seg_l);
     a.seg_mx = R.at<float>(L.seg_mx);
     a.seg_O = R.at<float>(L.seg_O);
-    a.T = R.base + L.T;
+    a.T = R.base + (h->dtype == F2C_F32 ? L.Tsh : L.T);  // (bf16: the GEMM-2 operand rows)
     a.mu_fx = R.at<long long>(L.mu_fx);
     a.sc = R.sc();
     a.sc_w = R.sc();
@@ -1074,7 +1114,7 @@ static int loss_multi(f2c_dcp *h, const uint8_t *x, const int64_t *labels, const
                       int64_t n_local, float s, float m, float *loss, uint8_t *dx, cudaStream_t st) {
     const int W = h->W;
     const int64_t N = n_local * W;
-    const size_t rb = static_cast<size_t>(h->d) * 2;
+    const size_t rb = static_cast<size_t>(h->d) * (h->dtype == F2C_BF16 ? 2 : 4);
     int rc;
     h->last_N = N;
     std::vector<StepCtx> ctx(h->ranks.size());
@@ -1160,18 +1200,25 @@ static int loss_multi(f2c_dcp *h, const uint8_t *x, const int64_t *labels, const
                                                                h->ranks[q].at<float>(h->ranks[q].L.dx_part), N * h->d);
             LAUNCH_CHECK();
         }
-        k_cast_bf16<<<grid_for(N * h->d), 256, 0, st>>>(R0.at<float>(R0.L.dx_part), reinterpret_cast<__nv_bfloat16 *>(dx),
-                                                        N * h->d);
-        LAUNCH_CHECK();
+        if (h->dtype == F2C_F32) {
+            CUDA_TRY(cudaMemcpyAsync(dx, R0.at<float>(R0.L.dx_part), N * h->d * 4, cudaMemcpyDeviceToDevice, st));
+        } else {
+            k_cast_bf16<<<grid_for(N * h->d), 256, 0, st>>>(R0.at<float>(R0.L.dx_part),
+                                                            reinterpret_cast<__nv_bfloat16 *>(dx), N * h->d);
+            LAUNCH_CHECK();
+        }
     } else {
         Rank &R = h->ranks[0];
         NvtxRange nvc("f2c: C4 reduce-scatter dx");
-        if ((rc = nccl_check(nccl().ReduceScatter(R.at<float>(R.L.dx_part), R.at<float>(R.L.dx32), n_local * h->d,
-                                                  NCCL_FLOAT32, NCCL_SUM, h->comm, st), "C4 reduce-scatter")))
+        float *rs_out = h->dtype == F2C_F32 ? static_cast<float *>(static_cast<void *>(dx)) : R.at<float>(R.L.dx32);
+        if ((rc = nccl_check(nccl().ReduceScatter(R.at<float>(R.L.dx_part), rs_out, n_local * h->d, NCCL_FLOAT32,
+                                                  NCCL_SUM, h->comm, st), "C4 reduce-scatter")))
             return rc;
-        k_cast_bf16<<<grid_for(n_local * h->d), 256, 0, st>>>(R.at<float>(R.L.dx32), reinterpret_cast<__nv_bfloat16 *>(dx),
-                                                              n_local * h->d);
-        LAUNCH_CHECK();
+        if (h->dtype != F2C_F32) {
+            k_cast_bf16<<<grid_for(n_local * h->d), 256, 0, st>>>(R.at<float>(R.L.dx32),
+                                                                  reinterpret_cast<__nv_bfloat16 *>(dx), n_local * h->d);
+            LAUNCH_CHECK();
+        }
     }
     return F2C_OK;
 }
@@ -1189,8 +1236,8 @@ extern "C" int f2c_dcp_loss_fwd_bwd(f2c_dcp *h, const void *x, const int64_t *la
     if (x == dx) return fail(F2C_EINVAL, "dx must not alias x");
     if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(dx)) & 15)
         return fail(F2C_EINVAL, "x and dx must be 16-byte aligned");
-    if (h->dtype != F2C_BF16)
-        return fail(F2C_EINVAL, "the fp32 loss path is not part of this build (DESIGN.md D21); use bf16");
+    if (h->dtype == F2C_F32 && h->d > 256)
+        return fail(F2C_EINVAL, "fp32 pools: the loss path (tf32 logits, x_hat as fp32 in TMEM) needs d <= 256");
     int rc = latched(h, false);
     if (rc) return rc;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -1367,6 +1414,13 @@ extern "C" int f2c_dcp_set_state(f2c_dcp *h, const void *feats_host, const int64
             k_pool_norm_max<<<static_cast<unsigned>((occ * 32 + 255) / 256), 256>>>(
                 R.base + R.L.T, occ, static_cast<int>(rb), h->dtype, R.sc());
             CUDA_TRY(cudaGetLastError());
+        }
+        if (h->dtype == F2C_F32) {  // the bf16 shadow of the restored fp32 rows (zeros beyond occ)
+            CUDA_TRY(cudaMemset(R.base + R.L.Tsh, 0, n * static_cast<size_t>(h->d) * 2));
+            if (occ > 0) {
+                k_cast_bf16<<<grid_for(occ * h->d), 256>>>(R.at<float>(R.L.T), R.at<__nv_bfloat16>(R.L.Tsh), occ * h->d);
+                CUDA_TRY(cudaGetLastError());
+            }
         }
         // mu over the restored slots lo .. lo + occ - 1
         CUDA_TRY(cudaMemset(R.base + R.L.mu_fx, 0, static_cast<size_t>(h->d) * 8));

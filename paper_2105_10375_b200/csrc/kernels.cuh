@@ -215,7 +215,8 @@ __global__ void __launch_bounds__(256) k_enqueue(const uint8_t *__restrict__ g, 
                                                  int row_bytes, int dtype, uint8_t *__restrict__ T,
                                                  int64_t *__restrict__ lab, Scalars *sc,
                                                  const int64_t *__restrict__ dst_seq,
-                                                 unsigned long long *__restrict__ mu_fx, LabelIndex ix) {
+                                                 unsigned long long *__restrict__ mu_fx, LabelIndex ix,
+                                                 __nv_bfloat16 *__restrict__ Tsh) {
     __shared__ float wmax[8];
     __shared__ long long smu[MU_WARPS][512];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -278,6 +279,14 @@ __global__ void __launch_bounds__(256) k_enqueue(const uint8_t *__restrict__ g, 
                         ss += a * a;
                         acc[h2 * 8 + q * 4 + i] += mu_fx_of(a) - mu_fx_of(__uint_as_float(o[i]));
                     }
+                }
+                if (dtype != 0 && Tsh) {  // fp32 pool: its bf16 shadow (the P x pool GEMM's operand)
+                    const __nv_bfloat162 s0 = __floats2bfloat162_rn(__uint_as_float(w[0]), __uint_as_float(w[1]));
+                    const __nv_bfloat162 s1 = __floats2bfloat162_rn(__uint_as_float(w[2]), __uint_as_float(w[3]));
+                    uint2 sv;
+                    sv.x = *reinterpret_cast<const uint32_t *>(&s0);
+                    sv.y = *reinterpret_cast<const uint32_t *>(&s1);
+                    reinterpret_cast<uint2 *>(Tsh + (c - lo) * (row_bytes / 4))[u] = sv;
                 }
             }
         }
@@ -978,7 +987,7 @@ __global__ void __launch_bounds__(256) k_gather(const uint8_t *__restrict__ x, c
                                                 const Scalars *__restrict__ sc, int row_bytes,
                                                 uint8_t *__restrict__ Xp, const uint8_t *__restrict__ T,
                                                 const int *__restrict__ row_tgt, float2 *__restrict__ row_ab,
-                                                float kf) {
+                                                float kf, int f32) {
     // one warp per compacted row, 8 rows per CTA
     const int k = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
     if (k >= sc->n_rows || (k >= sc->n_pos && k < sc->neg0)) {
@@ -1004,10 +1013,15 @@ __global__ void __launch_bounds__(256) k_gather(const uint8_t *__restrict__ x, c
                                    static_cast<uint32_t>(v.z), static_cast<uint32_t>(v.w)};
             const uint32_t b[4] = {static_cast<uint32_t>(w.x), static_cast<uint32_t>(w.y),
                                    static_cast<uint32_t>(w.z), static_cast<uint32_t>(w.w)};
+            if (f32) {
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
-                dot += __uint_as_float(a[i] << 16) * __uint_as_float(b[i] << 16) +
-                       __uint_as_float(a[i] & 0xffff0000u) * __uint_as_float(b[i] & 0xffff0000u);
+                for (int i = 0; i < 4; ++i) dot += __uint_as_float(a[i]) * __uint_as_float(b[i]);
+            } else {
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    dot += __uint_as_float(a[i] << 16) * __uint_as_float(b[i] << 16) +
+                           __uint_as_float(a[i] & 0xffff0000u) * __uint_as_float(b[i] & 0xffff0000u);
+            }
         }
     }
 #pragma unroll
@@ -1034,7 +1048,7 @@ struct CombineArgs {
     const int *row_tgt;         // [R_max] (local slot)
     const float *ttgt;          // [R_max]
     const float *seg_l, *seg_mx, *seg_O;
-    const uint8_t *T;           // local pool
+    const uint8_t *T;           // local pool, bf16 (an fp32 pool's bf16 shadow: the operand of GEMM 2)
     const Scalars *sc;
     Scalars *sc_w;
     int64_t N, C_occ;
@@ -1108,6 +1122,48 @@ __device__ __forceinline__ void load_bf16_row(const __nv_bfloat16 *row, int d, i
             v[4 * j + 3] = __uint_as_float(u.y & 0xffff0000u) * scale;
         } else {
             v[4 * j] = v[4 * j + 1] = v[4 * j + 2] = v[4 * j + 3] = 0.f;
+        }
+    }
+}
+
+// row i of x (dtype: 0 bf16, 1 fp32) -> fp32 lane elements (times scale)
+__device__ __forceinline__ void load_x_row(const uint8_t *x, int dtype, int64_t i, int d, int lane, float scale,
+                                           float (&v)[16]) {
+    if (dtype == 0) {
+        load_bf16_row(reinterpret_cast<const __nv_bfloat16 *>(x) + i * d, d, lane, scale, v);
+        return;
+    }
+    const float *row = reinterpret_cast<const float *>(x) + i * d;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int dd = 128 * j + 4 * lane;
+        if (dd < d) {
+            const float4 u = *reinterpret_cast<const float4 *>(row + dd);
+            v[4 * j + 0] = u.x * scale;
+            v[4 * j + 1] = u.y * scale;
+            v[4 * j + 2] = u.z * scale;
+            v[4 * j + 3] = u.w * scale;
+        } else {
+            v[4 * j] = v[4 * j + 1] = v[4 * j + 2] = v[4 * j + 3] = 0.f;
+        }
+    }
+}
+// lane elements -> row i of dx in the input dtype
+__device__ __forceinline__ void store_dx_row(uint8_t *dx, int dtype, int64_t i, int d, int lane, const float (&out)[16]) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int dd = 128 * j + 4 * lane;
+        if (dd >= d) continue;
+        if (dtype == 0) {
+            const __nv_bfloat162 p0 = __floats2bfloat162_rn(out[4 * j], out[4 * j + 1]);
+            const __nv_bfloat162 p1 = __floats2bfloat162_rn(out[4 * j + 2], out[4 * j + 3]);
+            uint2 u;
+            u.x = *reinterpret_cast<const uint32_t *>(&p0);
+            u.y = *reinterpret_cast<const uint32_t *>(&p1);
+            *reinterpret_cast<uint2 *>(reinterpret_cast<__nv_bfloat16 *>(dx) + i * d + dd) = u;
+        } else {
+            *reinterpret_cast<float4 *>(reinterpret_cast<float *>(dx) + i * d + dd) =
+                make_float4(out[4 * j], out[4 * j + 1], out[4 * j + 2], out[4 * j + 3]);
         }
     }
 }
@@ -1294,7 +1350,7 @@ __device__ __forceinline__ void combine_row(const CombineArgs &a, int64_t i) {
     const int k = a.comp_idx[i];
     const float inv = a.inv_n[i];
     float xh[16], g[16];
-    load_bf16_row(reinterpret_cast<const __nv_bfloat16 *>(a.x) + i * a.d, a.d, lane, inv, xh);
+    load_x_row(a.x, a.dtype, i, a.d, lane, inv, xh);
     double row_loss = 0.0;
     if (k >= 0) {
         float o[16], lsum, mx;
@@ -1363,19 +1419,7 @@ __device__ __forceinline__ void combine_row(const CombineArgs &a, int64_t i) {
     }
     float out[16];
     jacobian(g, xh, inv, out);
-    __nv_bfloat16 *dxr = reinterpret_cast<__nv_bfloat16 *>(a.dx) + i * a.d;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        const int dd = 128 * j + 4 * lane;
-        if (dd < a.d) {
-            const __nv_bfloat162 p0 = __floats2bfloat162_rn(out[4 * j], out[4 * j + 1]);
-            const __nv_bfloat162 p1 = __floats2bfloat162_rn(out[4 * j + 2], out[4 * j + 3]);
-            uint2 u;
-            u.x = *reinterpret_cast<const uint32_t *>(&p0);
-            u.y = *reinterpret_cast<const uint32_t *>(&p1);
-            *reinterpret_cast<uint2 *>(dxr + dd) = u;
-        }
-    }
+    store_dx_row(a.dx, a.dtype, i, a.d, lane, out);
     if (lane == 0) a.rowloss[i] = row_loss;
 }
 
@@ -1426,7 +1470,7 @@ __global__ void __launch_bounds__(256, 2) k_local_rows(CombineArgs a, float4 *__
     } else {
         float mu[16], xh[16];
         load_mu(a, lane, mu);
-        load_bf16_row(reinterpret_cast<const __nv_bfloat16 *>(a.x) + i * a.d, a.d, lane, a.inv_n[i], xh);
+        load_x_row(a.x, a.dtype, i, a.d, lane, a.inv_n[i], xh);
         float dot = 0.f;
 #pragma unroll
         for (int q = 0; q < 16; ++q) dot += xh[q] * mu[q];
@@ -1448,7 +1492,7 @@ __device__ __forceinline__ void finalize_row(const CombineArgs &a, const float4 
     const int k = a.comp_idx[i];
     const float inv = a.inv_n[i];
     float xh[16], g[16];
-    load_bf16_row(reinterpret_cast<const __nv_bfloat16 *>(a.x) + i * a.d, a.d, lane, inv, xh);
+    load_x_row(a.x, a.dtype, i, a.d, lane, inv, xh);
     double row_loss = 0.0;
     if (k >= 0) {
         // every shard used its own reference b_r: rescale to the common B* = max_r b_r
@@ -1543,6 +1587,7 @@ __global__ void __launch_bounds__(256, 2) k_finalize_multi(CombineArgs a, const 
     loss_tail(a, loss);
 }
 
+// fp32 -> bf16 (the multi-rank dx output; the bf16 shadow of an fp32 pool after set_state)
 __global__ void k_cast_bf16(const float *__restrict__ src, __nv_bfloat16 *__restrict__ dst, int64_t n) {
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x)
