@@ -27,8 +27,11 @@
  *     latch.  Calls issued while the latching kernel is still queued or running
  *     cannot see it yet; f2c_dcp_check() synchronises and always reports it.
  *   - dtype: F2C_BF16 (pool and features bf16, fp32 accumulation) or F2C_F32
- *     (fp32 storage; the loss path of this build requires F2C_BF16, see
- *     DESIGN.md section 9, D21).  Feature dimension d: multiple of 128, <= 512.
+ *     (fp32 pool, features, x and dx; BJ:7's c0, reading D21): the logits are
+ *     tf32 tensor-core products of the fp32 values (fp32 accumulation) and the
+ *     P x pool product reads a bf16 shadow of the pool kept by the enqueue; the
+ *     F2C_F32 loss call needs d <= 256 (x_hat lives in TMEM as fp32), F2C_EINVAL
+ *     otherwise.  Feature dimension d: multiple of 128, <= 512.
  *   - No CPU fallback: on a host without a usable sm_100 device every entry point
  *     that launches work returns F2C_ECUDA.
  */

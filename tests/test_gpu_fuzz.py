@@ -41,42 +41,47 @@ def _case(i):
     excl = bool(rng.random() < 0.25)
     refresh = bool(rng.random() < 0.2)
     n_lab = int(rng.integers(max(2, m_loc * W + 1), 4 * C + 10))
+    # fp32 pools (tf32 logits, BJ:7 / D21) where they apply: K = 1, d <= 256
+    dt = synth.F32 if (K == 1 and d <= 256 and rng.random() < 0.35) else synth.BF16
     return dict(W=W, K=K, d=d, C=C, m_loc=m_loc, n_loc=n_loc, fill=fill, s=s, m=m, phi_mode=phi_mode,
-                hinge=hinge, lam=lam, excl=excl, refresh=refresh, n_lab=n_lab, seed=2000 + i)
+                hinge=hinge, lam=lam, excl=excl, refresh=refresh, n_lab=n_lab, seed=2000 + i, dt=dt)
 
 
 @pytest.mark.parametrize("i", range(N_CASES))
 def test_fuzz_parity(dcp, i):
     c = _case(i)
     W, K, d, C, m_loc = c["W"], c["K"], c["d"], c["C"], c["m_loc"]
-    head = dcp.DCPHead(C, d, dcp.BF16, world=W, rank=0 if W == 1 else -1, n_local_max=c["n_loc"],
+    dt = c["dt"]
+    head = dcp.DCPHead(C, d, dt, world=W, rank=0 if W == 1 else -1, n_local_max=c["n_loc"],
                        m_local_max=m_loc, K=K)
     head.set_lcos(c["phi_mode"], c["hinge"], c["lam"])
     head.set_dup_mode(c["excl"])
     head.set_enqueue_mode(c["refresh"])
-    pool = oracle.Pool(C, d, oracle.BF16, K=K)
+    pool = oracle.Pool(C, d, dt, K=K)
     rng = np.random.default_rng(c["seed"])
     Mg = m_loc * W
     nblk = max(1, int(c["fill"] * C / Mg))
     for b in range(nblk):
-        G = synth.unit_rows(c["seed"], synth.S_PRE, b, 0, Mg * K, d)
+        G = synth.unit_rows(c["seed"], synth.S_PRE, b, 0, Mg * K, d, dt)
         if K > 1:  # arbitrary bf16 features, K per slot (NEXT-1: exact-mean logits)
             G = G.reshape(Mg, K, d)
         y = rng.choice(c["n_lab"], size=Mg, replace=False).astype(np.int64)
-        head.enqueue(to_dev(G, synth.BF16), lt(y))
+        head.enqueue(to_dev(G, dt), lt(y))
         pool.enqueue(G, y, refresh=c["refresh"])
     N = c["n_loc"] * W
-    X = synth.unit_rows(c["seed"] + 1, synth.S_INST, 0, 0, N, d)
+    X = synth.unit_rows(c["seed"] + 1, synth.S_INST, 0, 0, N, d, dt)
     occ = pool.C_occ
     y = rng.integers(0, c["n_lab"], N).astype(np.int64)
     y[::2] = pool.lab[:occ][rng.integers(0, occ, len(y[::2]))]
     if c["phi_mode"] == oracle.PHI_MAX:
         # hardest negatives far from ties: out-of-pool rows are noisy copies of pool centers
         neg = np.where(~np.isin(y, pool.lab[:occ]))[0]
-        Tb = oracle.bf16_to_f64(pool.T).reshape(C, K, d).mean(axis=1)
+        Tf = oracle.bf16_to_f64(pool.T) if dt == synth.BF16 else pool.T.astype(np.float64)
+        Tb = Tf.reshape(C, K, d).mean(axis=1)
         v = Tb[rng.integers(0, occ, len(neg))] + 0.25 * rng.standard_normal((len(neg), d)) / np.sqrt(d)
-        X[neg] = oracle.f64_to_bf16(v / np.maximum(np.linalg.norm(v, axis=1, keepdims=True), 1e-12))
-    loss, dx = head.loss_fwd_bwd(to_dev(X, synth.BF16), lt(y), None, c["s"], c["m"])
+        v = v / np.maximum(np.linalg.norm(v, axis=1, keepdims=True), 1e-12)
+        X[neg] = oracle.f64_to_bf16(v) if dt == synth.BF16 else v.astype(np.float32)
+    loss, dx = head.loss_fwd_bwd(to_dev(X, dt), lt(y), None, c["s"], c["m"])
     torch.cuda.synchronize()
     head.check()
     ref = pool.loss(X, y, None, c["s"], c["m"], phi_mode=c["phi_mode"], hinge=c["hinge"], lam=c["lam"],
