@@ -11,6 +11,10 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <condition_variable>
+#include <map>
+#include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -223,6 +227,52 @@ static Layout make_layout(int64_t C, int d, int dtype, int W, int rank, int64_t 
     return L;
 }
 
+// ============================================================================ loopback transport
+// Test transport (F2C_LOOPBACK=1 at create, world > 1): the W ranks are W handles of ONE process on
+// one device, each driven by its own host thread and stream, and every collective of the protocol is
+// executed by device copies between the ranks' buffers, in the order NCCL requires (every rank issues
+// the same sequence of collectives; point-to-point pieces match by (source, destination) order).  It
+// runs the real multi-rank code path -- separate handles and state buffers, rank != 0 shards, the C5
+// routing plan, the split of the reduce-scatter -- where a real communicator needs one GPU per rank.
+// A batch (an NCCL group, or a single call): (1) every rank records `ready` on its stream and
+// publishes its operations; barrier; (2) every rank enqueues, on its own stream, the copies and
+// reductions that produce ITS outputs, after waiting on the producers' `ready`; records `done`;
+// barrier; (3) every rank's stream waits on all `done` events (no rank overwrites a buffer another
+// rank still reads); barrier.  Kernels never wait on each other: only streams do, through events.
+struct LbOp {
+    int kind;  // 0 all-gather (bytes per rank), 1 all-reduce MAX int64 (count), 2 reduce-scatter SUM fp32
+               // (count per rank), 3 send (bytes, peer), 4 recv (bytes, peer)
+    const void *send;
+    void *recv;
+    size_t n;
+    int peer;
+};
+struct LbSlot {
+    std::vector<LbOp> ops;
+    cudaEvent_t ready = nullptr, done = nullptr;
+};
+struct LbGroup {
+    int W = 0;
+    std::mutex mu;
+    std::condition_variable cv;
+    int arrived = 0;
+    long gen = 0;
+    std::vector<LbSlot> slot;
+    void barrier() {
+        std::unique_lock<std::mutex> lk(mu);
+        const long g = gen;
+        if (++arrived == W) {
+            arrived = 0;
+            ++gen;
+            cv.notify_all();
+        } else {
+            cv.wait(lk, [&] { return gen != g; });
+        }
+    }
+};
+static std::mutex g_lb_mu;
+static std::map<std::string, std::shared_ptr<LbGroup>> g_lb_groups;
+
 // ============================================================================ handle
 struct Rank {
     int rank;
@@ -257,6 +307,10 @@ struct f2c_dcp {
     std::vector<Rank> ranks;  // 1 (real rank) or W (emulated world)
     cudaStream_t last_stream = nullptr;
     nccl_comm_t comm = nullptr;
+    std::shared_ptr<LbGroup> lb;   // loopback transport (tests), else null
+    std::string lb_key;
+    std::vector<LbOp> lb_ops;      // operations of the open batch
+    int lb_grouping = 0;
     int64_t last_N = 0;
     bool multi = false;  // multi-rank protocol (world > 1, or the F2C_FORCE_MULTI test hook)
     // bench instrumentation
@@ -273,6 +327,13 @@ struct f2c_dcp {
     int dbg_cluster = 0;            // debug timestamps of this cluster (F2C_DBG_CLUSTER)
     ~f2c_dcp() {
         for (cudaEvent_t e : ev) cudaEventDestroy(e);
+        if (lb) {
+            LbSlot &sl = lb->slot[ranks[0].rank];
+            if (sl.ready) cudaEventDestroy(sl.ready);
+            if (sl.done) cudaEventDestroy(sl.done);
+            std::lock_guard<std::mutex> g(g_lb_mu);
+            if (lb.use_count() <= 2) g_lb_groups.erase(lb_key);  // (this handle and the registry)
+        }
         if (n_app_host) cudaFreeHost(n_app_host);
         if (err_host) cudaFreeHost(err_host);
     }
@@ -594,7 +655,29 @@ int f2c_dcp_create_k(int64_t C, int32_t K, int32_t d, int32_t dtype, int32_t wor
         if (getenv("F2C_VERBOSE")) fprintf(stderr, "f2c: dcp_pc4_kernel clusters %d (of %d SMs)\n", h->G4, h->G);
     }
     h->multi = world > 1 || (rank == 0 && force_multi());
-    if (h->multi && !h->emulated) {
+    const char *lbv = getenv("F2C_LOOPBACK");
+    if (h->multi && !h->emulated && world > 1 && lbv && lbv[0] == '1') {
+        // loopback test transport: join the in-process group named by the unique id's bytes
+        h->lb_key.assign(static_cast<const char *>(nccl_uid), 128);
+        std::lock_guard<std::mutex> g(g_lb_mu);
+        auto &grp = g_lb_groups[h->lb_key];
+        if (!grp) {
+            grp = std::make_shared<LbGroup>();
+            grp->W = world;
+            grp->slot.resize(world);
+        }
+        if (grp->W != world) {
+            delete h;
+            return fail(F2C_EINVAL, "loopback group: world %d != %d", world, grp->W);
+        }
+        h->lb = grp;
+        LbSlot &sl = grp->slot[rank];
+        if (cudaEventCreateWithFlags(&sl.ready, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&sl.done, cudaEventDisableTiming) != cudaSuccess) {
+            delete h;
+            return fail(F2C_ECUDA, "loopback events");
+        }
+    } else if (h->multi && !h->emulated) {
         NcclApi &api = nccl();
         if (!api.ok) {
             delete h;
@@ -632,6 +715,112 @@ static int nccl_check(int r, const char *what) {
     if (r != 0)
         return fail(F2C_ENCCL, "%s: %s", what, nccl().GetErrorString ? nccl().GetErrorString(r) : "?");
     return F2C_OK;
+}
+
+// The protocol's collectives through NCCL or the loopback transport.  comm_group_start / _end
+// bracket a batch (an NCCL group); outside a bracket every call is a batch of its own.
+static unsigned grid_for(int64_t n);
+static int lb_flush(f2c_dcp *h, cudaStream_t st, const char *what) {
+    LbGroup &G = *h->lb;
+    const int me = h->ranks[0].rank;
+    LbSlot &mine = G.slot[me];
+    mine.ops = h->lb_ops;
+    h->lb_ops.clear();
+    CUDA_TRY(cudaEventRecord(mine.ready, st));
+    G.barrier();
+    // phase 2: this rank's outputs
+    std::vector<int> sent_seen(G.W, 0);  // per source: matched sends to me so far
+    for (size_t k = 0; k < mine.ops.size(); ++k) {
+        const LbOp &o = mine.ops[k];
+        if (o.kind == 0) {
+            for (int q = 0; q < G.W; ++q) {
+                const LbOp &oq = G.slot[q].ops[k];
+                if (oq.kind != 0 || oq.n != o.n) return fail(F2C_ENCCL, "%s: loopback all-gather mismatch", what);
+                CUDA_TRY(cudaStreamWaitEvent(st, G.slot[q].ready, 0));
+                CUDA_TRY(cudaMemcpyAsync(static_cast<uint8_t *>(o.recv) + q * o.n, oq.send, o.n, cudaMemcpyDeviceToDevice, st));
+            }
+        } else if (o.kind == 1) {
+            // MAX into my buffer from every peer's (a peer's buffer read while it is being maxed itself
+            // still holds values between its own and the global maximum: the result is the same)
+            for (int q = 0; q < G.W; ++q) {
+                if (q == me) continue;
+                const LbOp &oq = G.slot[q].ops[k];
+                if (oq.kind != 1 || oq.n != o.n) return fail(F2C_ENCCL, "%s: loopback all-reduce mismatch", what);
+                CUDA_TRY(cudaStreamWaitEvent(st, G.slot[q].ready, 0));
+                k_max_i64_into<<<grid_for(static_cast<int64_t>(o.n)), 256, 0, st>>>(
+                    static_cast<int64_t *>(o.recv), static_cast<const int64_t *>(oq.send), static_cast<int64_t>(o.n));
+                LAUNCH_CHECK();
+            }
+        } else if (o.kind == 2) {
+            // my chunk: sum over ranks in rank order
+            for (int q = 0; q < G.W; ++q) {
+                const LbOp &oq = G.slot[q].ops[k];
+                if (oq.kind != 2 || oq.n != o.n) return fail(F2C_ENCCL, "%s: loopback reduce-scatter mismatch", what);
+                CUDA_TRY(cudaStreamWaitEvent(st, G.slot[q].ready, 0));
+                const float *src = static_cast<const float *>(oq.send) + static_cast<size_t>(me) * o.n;
+                if (q == 0) {
+                    CUDA_TRY(cudaMemcpyAsync(o.recv, src, o.n * 4, cudaMemcpyDeviceToDevice, st));
+                } else {
+                    k_add_f32_into<<<grid_for(static_cast<int64_t>(o.n)), 256, 0, st>>>(static_cast<float *>(o.recv), src,
+                                                                                      static_cast<int64_t>(o.n));
+                    LAUNCH_CHECK();
+                }
+            }
+        } else if (o.kind == 4) {
+            // the n-th receive from q matches q's n-th send to me
+            const int q = o.peer;
+            int seen = 0;
+            const LbOp *match = nullptr;
+            for (const LbOp &oq : G.slot[q].ops)
+                if (oq.kind == 3 && oq.peer == me && seen++ == sent_seen[q]) {
+                    match = &oq;
+                    break;
+                }
+            if (!match || match->n != o.n) return fail(F2C_ENCCL, "%s: loopback send/recv mismatch", what);
+            ++sent_seen[q];
+            CUDA_TRY(cudaStreamWaitEvent(st, G.slot[q].ready, 0));
+            CUDA_TRY(cudaMemcpyAsync(o.recv, match->send, o.n, cudaMemcpyDeviceToDevice, st));
+        }
+    }
+    CUDA_TRY(cudaEventRecord(mine.done, st));
+    G.barrier();
+    for (int q = 0; q < G.W; ++q)
+        if (q != me) CUDA_TRY(cudaStreamWaitEvent(st, G.slot[q].done, 0));
+    G.barrier();  // (nobody re-records its events before every peer has waited on them)
+    return F2C_OK;
+}
+static void comm_group_start(f2c_dcp *h) {
+    if (h->lb) ++h->lb_grouping;
+    else nccl().GroupStart();
+}
+static int comm_group_end(f2c_dcp *h, cudaStream_t st, const char *what) {
+    if (h->lb) return --h->lb_grouping == 0 ? lb_flush(h, st, what) : F2C_OK;
+    return nccl_check(nccl().GroupEnd(), what);
+}
+static int lb_add(f2c_dcp *h, LbOp o, cudaStream_t st, const char *what) {
+    h->lb_ops.push_back(o);
+    return h->lb_grouping ? F2C_OK : lb_flush(h, st, what);
+}
+static int comm_allgather(f2c_dcp *h, const void *send, void *recv, size_t bytes, cudaStream_t st, const char *what) {
+    if (h->lb) return lb_add(h, LbOp{0, send, recv, bytes, -1}, st, what);
+    return nccl_check(nccl().AllGather(send, recv, bytes, NCCL_INT8, h->comm, st), what);
+}
+static int comm_allreduce_max_i64(f2c_dcp *h, int64_t *buf, size_t count, cudaStream_t st, const char *what) {
+    if (h->lb) return lb_add(h, LbOp{1, buf, buf, count, -1}, st, what);
+    return nccl_check(nccl().AllReduce(buf, buf, count, NCCL_INT64, NCCL_MAX, h->comm, st), what);
+}
+static int comm_reduce_scatter_f32(f2c_dcp *h, const float *send, float *recv, size_t count, cudaStream_t st,
+                                   const char *what) {
+    if (h->lb) return lb_add(h, LbOp{2, send, recv, count, -1}, st, what);
+    return nccl_check(nccl().ReduceScatter(send, recv, count, NCCL_FLOAT32, NCCL_SUM, h->comm, st), what);
+}
+static int comm_send(f2c_dcp *h, const void *p, size_t bytes, int peer, cudaStream_t st, const char *what) {
+    if (h->lb) return lb_add(h, LbOp{3, p, nullptr, bytes, peer}, st, what);
+    return nccl_check(nccl().Send(p, bytes, NCCL_INT8, peer, h->comm, st), what);
+}
+static int comm_recv(f2c_dcp *h, void *p, size_t bytes, int peer, cudaStream_t st, const char *what) {
+    if (h->lb) return lb_add(h, LbOp{4, nullptr, p, bytes, peer}, st, what);
+    return nccl_check(nccl().Recv(p, bytes, NCCL_INT8, peer, h->comm, st), what);
 }
 
 // ============================================================================ label index
@@ -761,7 +950,6 @@ extern "C" int f2c_dcp_enqueue(f2c_dcp *h, const void *g_feats, const int64_t *l
         // exactly the rows it owns (the block's slots span one or two shards).
         NvtxRange nvc("f2c: C5 enqueue routed to the owners");
         Rank &R = h->ranks[0];
-        NcclApi &api = nccl();
         const int me = R.rank;
         const size_t rb = static_cast<size_t>(h->K) * h->d * es;
         std::vector<int64_t> pc(4 * (2 * static_cast<size_t>(h->W) + 2));
@@ -776,30 +964,29 @@ extern "C" int f2c_dcp_enqueue(f2c_dcp *h, const void *g_feats, const int64_t *l
             CUDA_TRY(cudaMemcpyAsync(bx + j * rb, gsrc + (j - me * m_local) * rb, len * rb, cudaMemcpyDeviceToDevice, st));
             CUDA_TRY(cudaMemcpyAsync(by + j, labels + (j - me * m_local), len * 8, cudaMemcpyDeviceToDevice, st));
         }
-        api.GroupStart();
+        comm_group_start(h);
         for (int64_t i = 0; i < np; ++i) {
             const int64_t src = pc[4 * i], dst = pc[4 * i + 1], j = pc[4 * i + 2], len = pc[4 * i + 3];
             if (src == dst) continue;
             if (src == me) {
-                api.Send(gsrc + (j - me * m_local) * rb, len * rb, NCCL_INT8, static_cast<int>(dst), h->comm, st);
-                api.Send(labels + (j - me * m_local), len, NCCL_INT64, static_cast<int>(dst), h->comm, st);
+                comm_send(h, gsrc + (j - me * m_local) * rb, len * rb, static_cast<int>(dst), st, "C5");
+                comm_send(h, labels + (j - me * m_local), len * 8, static_cast<int>(dst), st, "C5");
             } else if (dst == me) {
-                api.Recv(bx + j * rb, len * rb, NCCL_INT8, static_cast<int>(src), h->comm, st);
-                api.Recv(by + j, len, NCCL_INT64, static_cast<int>(src), h->comm, st);
+                comm_recv(h, bx + j * rb, len * rb, static_cast<int>(src), st, "C5");
+                comm_recv(h, by + j, len * 8, static_cast<int>(src), st, "C5");
             }
         }
-        if ((rc = nccl_check(api.GroupEnd(), "C5 send/recv"))) return rc;
+        if ((rc = comm_group_end(h, st, "C5 send/recv"))) return rc;
         gx = bx;
         gy = by;
     } else if (h->multi && !h->emulated) {
         // refresh-in-place (NEXT-3, R7): destinations depend on residency over all shards, so
         // every rank receives the whole block (all-gather) and keeps the rows its plan assigns it
         Rank &R = h->ranks[0];
-        NcclApi &api = nccl();
-        api.GroupStart();
-        api.AllGather(g_feats, R.base + R.L.blk_x, m_local * h->K * h->d * es, NCCL_INT8, h->comm, st);
-        api.AllGather(labels, R.base + R.L.blk_y, m_local, NCCL_INT64, h->comm, st);
-        if ((rc = nccl_check(api.GroupEnd(), "enqueue all-gather"))) return rc;
+        comm_group_start(h);
+        comm_allgather(h, g_feats, R.base + R.L.blk_x, m_local * h->K * h->d * es, st, "enqueue all-gather");
+        comm_allgather(h, labels, R.base + R.L.blk_y, m_local * 8, st, "enqueue all-gather");
+        if ((rc = comm_group_end(h, st, "enqueue all-gather"))) return rc;
         gx = R.base + R.L.blk_x;
         gy = R.at<int64_t>(R.L.blk_y);
     }
@@ -821,9 +1008,7 @@ extern "C" int f2c_dcp_enqueue(f2c_dcp *h, const void *g_feats, const int64_t *l
                                          m_glob * 8, cudaMemcpyDeviceToDevice, st));
         } else if (h->multi) {
             Rank &R = h->ranks[0];
-            if ((rc = nccl_check(nccl().AllReduce(R.at<int64_t>(R.L.rseq), R.at<int64_t>(R.L.rseq), m_glob, NCCL_INT64,
-                                                  NCCL_MAX, h->comm, st), "refresh all-reduce")))
-                return rc;
+            if ((rc = comm_allreduce_max_i64(h, R.at<int64_t>(R.L.rseq), m_glob, st, "refresh all-reduce"))) return rc;
         }
         for (Rank &R : h->ranks)
             if ((rc = refresh_plan(h, R, m_glob, st))) return rc;
@@ -1123,13 +1308,12 @@ static int loss_multi(f2c_dcp *h, const uint8_t *x, const int64_t *labels, const
         for (size_t q = 0; q < h->ranks.size(); ++q) ctx[q] = StepCtx{N, s, m, x, labels, pairing, st};
     } else {
         Rank &R = h->ranks[0];
-        NcclApi &api = nccl();
         NvtxRange nvc("f2c: C1 all-gather x, labels, pairing");
-        api.GroupStart();
-        api.AllGather(x, R.base + R.L.x_all, n_local * rb, NCCL_INT8, h->comm, st);
-        api.AllGather(labels, R.base + R.L.y_all, n_local, NCCL_INT64, h->comm, st);
-        if (pairing) api.AllGather(pairing, R.base + R.L.pair_all, n_local * 4, NCCL_INT8, h->comm, st);
-        if ((rc = nccl_check(api.GroupEnd(), "C1 all-gather"))) return rc;
+        comm_group_start(h);
+        comm_allgather(h, x, R.base + R.L.x_all, n_local * rb, st, "C1");
+        comm_allgather(h, labels, R.base + R.L.y_all, n_local * 8, st, "C1");
+        if (pairing) comm_allgather(h, pairing, R.base + R.L.pair_all, n_local * 4, st, "C1");
+        if ((rc = comm_group_end(h, st, "C1 all-gather"))) return rc;
         ctx[0] = StepCtx{N, s, m, R.base + R.L.x_all, R.at<int64_t>(R.L.y_all),
                          pairing ? R.at<int32_t>(R.L.pair_all) : nullptr, st};
     }
@@ -1153,9 +1337,7 @@ static int loss_multi(f2c_dcp *h, const uint8_t *x, const int64_t *labels, const
     } else {
         Rank &R = h->ranks[0];
         NvtxRange nvc("f2c: C2 MAX all-reduce");
-        if ((rc = nccl_check(nccl().AllReduce(R.at<int64_t>(R.L.tseq_ext), R.at<int64_t>(R.L.tseq_ext), N + 1,
-                                              NCCL_INT64, NCCL_MAX, h->comm, st), "C2 all-reduce")))
-            return rc;
+        if ((rc = comm_allreduce_max_i64(h, R.at<int64_t>(R.L.tseq_ext), N + 1, st, "C2 all-reduce"))) return rc;
     }
     // ---- compaction, fused kernel on the local shard, local row partials
     for (size_t q = 0; q < h->ranks.size(); ++q) {
@@ -1181,8 +1363,7 @@ static int loss_multi(f2c_dcp *h, const uint8_t *x, const int64_t *labels, const
     } else {
         Rank &R = h->ranks[0];
         NvtxRange nvc("f2c: C3 all-gather row partials");
-        if ((rc = nccl_check(nccl().AllGather(R.at<float4>(R.L.rs_buf), R.at<float4>(R.L.rs_all), N * 4, NCCL_FLOAT32,
-                                              h->comm, st), "C3 all-gather")))
+        if ((rc = comm_allgather(h, R.at<float4>(R.L.rs_buf), R.at<float4>(R.L.rs_all), N * 16, st, "C3 all-gather")))
             return rc;
     }
     // ---- finalisation (identical on every rank) + linear dx share, then C4
@@ -1211,8 +1392,7 @@ static int loss_multi(f2c_dcp *h, const uint8_t *x, const int64_t *labels, const
         Rank &R = h->ranks[0];
         NvtxRange nvc("f2c: C4 reduce-scatter dx");
         float *rs_out = h->dtype == F2C_F32 ? static_cast<float *>(static_cast<void *>(dx)) : R.at<float>(R.L.dx32);
-        if ((rc = nccl_check(nccl().ReduceScatter(R.at<float>(R.L.dx_part), rs_out, n_local * h->d, NCCL_FLOAT32,
-                                                  NCCL_SUM, h->comm, st), "C4 reduce-scatter")))
+        if ((rc = comm_reduce_scatter_f32(h, R.at<float>(R.L.dx_part), rs_out, n_local * h->d, st, "C4 reduce-scatter")))
             return rc;
         if (h->dtype != F2C_F32) {
             k_cast_bf16<<<grid_for(n_local * h->d), 256, 0, st>>>(R.at<float>(R.L.dx32),
