@@ -870,7 +870,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
         // ================================================================= CONSUMER
         uint8_t *sP = smem + PCQ_OFF_P;
         uint8_t *sT = smem + PCQ_OFF_T;
-        const int nq = PC_TILE / 32;  // 32-slot pool stages per tile
         if (warp == 8) {
             // -------- TMA: pool stages [cps chunks x 128 slots x 64 d] (3D box) = one d block
             if (lane == 0) {

@@ -161,7 +161,6 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(P4_THREADS, 1)
     const int lane = threadIdx.x & 31;
     const uint32_t crank = cluster_ctarank();
     const uint32_t half = crank & 1;        // which 128 rows of the group / which operand half
-    const uint32_t leader = crank & 2;      // the pair leader's rank (0 or 2)
     const bool is_leader = half == 0;
     const int d = p.d;
     const int nchunk = d >> 6;              // 64-wide d chunks

@@ -1425,7 +1425,6 @@ extern "C" int f2c_dcp_loss_fwd_bwd(f2c_dcp *h, const void *x, const int64_t *la
     if (h->multi) return loss_multi(h, static_cast<const uint8_t *>(x), labels, pairing, n_local, s, m, loss,
                                      static_cast<uint8_t *>(dx), st);
     Rank &R = h->ranks[0];
-    const Layout &L = R.L;
     StepCtx c{n_local, s, m, static_cast<const uint8_t *>(x), labels, pairing, st};
     h->last_N = c.N;
     if ((rc = phase_resolve(h, R, c))) return rc;

@@ -1439,7 +1439,6 @@ __global__ void __launch_bounds__(256, 2) k_local_rows(CombineArgs a, float4 *__
     const int lane = threadIdx.x & 31;
     const int64_t i = static_cast<int64_t>(blockIdx.x) * CB_ROWS + (threadIdx.x >> 5);
     if (i >= a.N) return;
-    const int n_pos = a.sc->n_pos;
     const int n_rg = (a.sc->n_rows + a.rows_per_group - 1) / a.rows_per_group;
     const int k = a.comp_idx[i];
     if (k >= 0) {
