@@ -43,6 +43,10 @@ def _case(i):
     n_lab = int(rng.integers(max(2, m_loc * W + 1), 4 * C + 10))
     # fp32 pools (tf32 logits, BJ:7 / D21) where they apply: K = 1, d <= 256
     dt = synth.F32 if (K == 1 and d <= 256 and rng.random() < 0.35) else synth.BF16
+    if dt == synth.F32:
+        # tf32 logits round the cosines by ~1e-4: a sum / mean hinge then has near-zero cosines on
+        # both sides of 0 in most rows (D21); fp32 pools are fuzzed without the hinge
+        hinge = False
     return dict(W=W, K=K, d=d, C=C, m_loc=m_loc, n_loc=n_loc, fill=fill, s=s, m=m, phi_mode=phi_mode,
                 hinge=hinge, lam=lam, excl=excl, refresh=refresh, n_lab=n_lab, seed=2000 + i, dt=dt)
 
@@ -90,4 +94,21 @@ def test_fuzz_parity(dcp, i):
     assert E == int(pool.E[0]), c
     np.testing.assert_array_equal(labs, pool.lab)
     assert_loss_close(float(loss.item()), ref.L, what=f"loss {c}")
-    assert_dx_close(from_dev(dx), ref.dx, what=f"dx {c}")
+    rows = np.arange(N)
+    if c["hinge"]:
+        # The hinge max(0, cos) is discontinuous at cos = 0: a pair whose cosine lies within the GPU's
+        # rounding of 0 may be decided either way, and each decision moves that row's gradient by a
+        # whole (weighted) center.  Both decisions are correct; such rows are compared through their
+        # loss only (their phi terms differ by < the rounding), the rest element by element.  The logits
+        # are fp32 accumulations of exact bf16 products (K d terms), accurate to ~1e-7.
+        occ = pool.C_occ
+        Tf = oracle.bf16_to_f64(pool.T) if dt == synth.BF16 else pool.T.astype(np.float64)
+        Tb = Tf.reshape(C, K, d).mean(axis=1)[:occ]
+        Xf = oracle.bf16_to_f64(X) if dt == synth.BF16 else X.astype(np.float64)
+        xh = Xf / np.linalg.norm(Xf, axis=1, keepdims=True)
+        neg = np.where(ref.tslot < 0)[0]
+        tol = 2e-6 * np.linalg.norm(Tb, axis=1)   # (~20x the fp32-accumulation error of the logits)
+        amb = (np.abs(xh[neg] @ Tb.T) < tol[None, :]).any(axis=1)
+        assert amb.sum() <= max(3, 0.25 * len(neg)), (int(amb.sum()), len(neg), c)
+        rows = np.setdiff1d(rows, neg[amb])
+    assert_dx_close(from_dev(dx)[rows], ref.dx[rows], what=f"dx {c}")
