@@ -375,18 +375,19 @@ def roofline_block(cfg, world, d, npos_avg, t_launch, ms_step, clocks, pk, share
             traffic = json.load(open(prof_file)).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
-    # the decomposition's own ceiling: L2 -> SM delivery.  Every 128-row group streams the shard
-    # through BOTH CTAs of its pair (producer: GEMM 1, consumer: GEMM 2) and ships P (32 KB per tile)
-    # over DSMEM; ncu shows these bytes near the chip's measured LTS cap
+    # the decomposition's data movement into the SMs: every 128-row group streams the shard through
+    # BOTH CTAs of its pair (producer: GEMM 1, consumer: GEMM 2) and ships P (32 KB per tile) over DSMEM.
+    # Against the L2 -> SM TMA rate this chip sustains (profiles/r02_tma_l2_bench.txt): not the bound
+    #
     groups = math.ceil(npos_avg / 128) if npos_avg > 0 else 0
     n_tiles = math.ceil(C_loc / 128)
     l2_bytes = groups * (2 * C_loc * d * 2 + n_tiles * 128 * 128 * 2)
-    l2_peak = 6300 * 1.958e9 / 1e12       # TB/s
+    l2_peak = 20.9                         # TB/s, measured: 148 SMs TMA-streaming L2-resident 128-row boxes
     l2_ach = l2_bytes / t_launch / 1e12
     secondary = {"bound": "l2_to_sm", "achieved": l2_ach, "peak": l2_peak, "unit": "TB/s", "frac": l2_ach / l2_peak,
                  "bytes_per_launch": l2_bytes,
-                 "peak_source": "B300_MICROARCH.md: measured LTS throughput cap ~6300 B/cyc full-chip (TMA = LDG), x "
-                                "1.958 GHz L2 clock (ncu lts__cycles_elapsed.avg.per_second, profiles/r02_ncu_main_c3.txt)",
+                 "peak_source": "scripts/tma_bench.cu on this B200: 148 CTAs streaming L2-resident [128 x 64] bf16 "
+                                "SW128 TMA boxes, 20.1-20.9 TB/s (profiles/r02_tma_l2_bench.txt)",
                  "bytes_definition": "row groups x (2 CTAs x C_loc x d x 2 B pool tiles + tiles x 32 KB P over DSMEM)"}
     return {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
             "frac": achieved / peak, "traffic": traffic,
