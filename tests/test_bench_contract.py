@@ -71,3 +71,24 @@ def test_world_size_must_match_gpus():
     r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "4", "--dry-run"],
                        capture_output=True, text=True, env=env, cwd=ROOT, timeout=120)
     assert r.returncode != 0 and "refusing" in r.stderr
+
+
+def test_roofline_peak_follows_the_clock():
+    """the tensor roofline divides by the measured burst peak when the SM clock sat near
+    its maximum during the timed region, by the sustained (power-capped) peak otherwise; both
+    fractions and the step-level T_roof / T_step are always reported."""
+    import bench
+    import synth
+    pk = {"hbm_gbs": 6546.6, "bf16_tflops": 1630.3, "bf16_tflops_sustained": 1378.5}
+    cfg = synth.CONFIGS["c3"]
+    args = (cfg, 1, 512, 535.0, 4.4e-3, 4.6)
+    near = bench.roofline_block(*args, {"sm_mhz": 1940.0, "sm_max_mhz": 1965.0}, pk, 0.96)
+    low = bench.roofline_block(*args, {"sm_mhz": 1450.0, "sm_max_mhz": 1965.0}, pk, 0.96)
+    assert near["peak"] == 1630.3 and low["peak"] == 1378.5
+    assert near["frac"] == near["frac_vs_burst"] and low["frac"] == low["frac_vs_sustained"]
+    flops = 4.0 * 535.0 * cfg.C * 512
+    assert abs(near["achieved"] - flops / 4.4e-3 / 1e12) < 1e-9
+    st = near["step"]
+    assert abs(st["t_roof_ms"] - flops / 1630.3e12 * 1e3) < 1e-9 and abs(st["frac"] - st["t_roof_ms"] / 4.6) < 1e-12
+    assert near["executed_mma_flops_per_launch"] == 4.0 * (512 + 64) * cfg.C * 512   # 4 groups + a 64-row tail unit
+    assert 0 < near["secondary"]["frac"] < 1
