@@ -201,9 +201,10 @@ int f2c_dcp_get_state(f2c_dcp *h, void *feats_host, int64_t *labels_host, int64_
 /* Restore a pool (same layout as get_state).  Slots >= min(E, C) must be empty
  * (label -1); their features are ignored and stored as zeros.  The next enqueue
  * writes at E mod C.  The derived state is rebuilt from the restored slots: the
- * running norm bound (R1), T_bar and w_c for K >= 2 (R5), and the pool sum mu of the
- * L_cos gradient (R3; the enqueue keeps it as an exact fixed-point running sum, so a
- * restored handle continues bit-identically). */
+ * running norm bound (R1), T_bar and w_c for K >= 2 (R5), an fp32 pool's bf16 shadow
+ * (D21), the label index of target resolution (label -> newest write index, DESIGN.md
+ * section 6), and the pool sum mu of the L_cos gradient (R3; the enqueue keeps it as an
+ * exact fixed-point running sum, so a restored handle continues bit-identically). */
 int f2c_dcp_set_state(f2c_dcp *h, const void *feats_host, const int64_t *labels_host,
                       int64_t enq_count);
 

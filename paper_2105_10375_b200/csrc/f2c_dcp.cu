@@ -1091,8 +1091,6 @@ static int phase_compact(f2c_dcp *h, Rank &R, const StepCtx &c, const int *tmax_
     const Layout &L = R.L;
     CompactArgs a;
     a.tseq = R.at<int64_t>(L.tseq);
-    a.rs_hslot = nullptr;  // (tseq comes from the label index)
-    a.rs_hvals = nullptr;
     a.inv_n = R.at<float>(L.inv_n);
     a.pairing = c.pair;
     a.N = c.N; a.C = h->C; a.lo = R.lo; a.hi = R.hi; a.E = h->E; a.M_last = h->M_last;

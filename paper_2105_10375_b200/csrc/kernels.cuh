@@ -835,10 +835,8 @@ __global__ void k_dup_fill(const int64_t *__restrict__ lab, int64_t n_occ_loc, i
 // rows, compaction of the in-pool rows in batch order, per-row softmax coefficients,
 // the pairing check (D13), and coefficients (0, +inf) -- p = 0 -- for the padding rows.
 struct CompactArgs {
-    int64_t *tseq;            // [N] global write index of the target or -1 (written here when
-                              // hslot/hvals are given: W = 1 resolves inside this kernel)
-    const int *rs_hslot;      // [N] or null
-    const unsigned long long *rs_hvals;  // [H] or null
+    const int64_t *tseq;      // [N] global write index of the target or -1 (the label index lookup;
+                              // W > 1: after the MAX all-reduce)
     const float *inv_n;       // [N]
     const int32_t *pairing;   // [N] or null
     int64_t N, C, lo, hi, E, M_last;
@@ -873,13 +871,7 @@ __global__ void __launch_bounds__(1024) k_compact(CompactArgs a) {
     const int tid = threadIdx.x, nt = blockDim.x;
     const int lane = tid & 31, w = tid >> 5;
     const int64_t c0 = static_cast<int64_t>(blockIdx.x) * nt;
-    // target write index of row i: resolved here from the label hash (W = 1), or given (W > 1,
-    // after the MAX all-reduce)
-    auto tseq_of = [&](int64_t i) -> int64_t {
-        if (!a.rs_hslot) return a.tseq[i];
-        const int h = a.rs_hslot[i];
-        return h < 0 ? -1 : static_cast<int64_t>(a.rs_hvals[h]) - 1;
-    };
+    auto tseq_of = [&](int64_t i) -> int64_t { return a.tseq[i]; };
     int cnt = 0, before = 0;
     for (int64_t i = tid; i < a.N; i += nt) {
         const int f = tseq_of(i) >= 0;
@@ -914,7 +906,6 @@ __global__ void __launch_bounds__(1024) k_compact(CompactArgs a) {
     {
         const int64_t i = c0 + tid;
         const int64_t ts = i < a.N ? tseq_of(i) : -1;
-        if (a.rs_hslot && i < a.N) a.tseq[i] = ts;  // (row_stats reads it)
         const bool f = i < a.N && ts >= 0;
         const unsigned bal = __ballot_sync(0xffffffffu, f);
         __syncthreads();  // (wsum reuse)
