@@ -599,6 +599,31 @@ __global__ void k_rownorm_insert(const T *__restrict__ x, const int64_t *__restr
     const int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (i >= N) return;
+    // the two label lookups first, on their own lanes (their dependent round trips overlap each
+    // other and the row's loads): lane 1 -- the shard's label index (a3: the target = the label's
+    // newest slot of this shard, D8); lane 2 -- the batch-label hash (stale-duplicate lists, R8)
+    const int64_t key = y[i];
+    if (key < 0) {
+        if (lane == 0) {
+            latch(sc, ERR_DEVICE, DET_BAD_LABEL);
+            hslot[i] = -1;
+            tseq[i] = -1;
+        }
+    } else if (lane == 1) {
+        tseq[i] = idx_lookup(ix, key);
+    } else if (lane == 2) {
+        unsigned h = static_cast<unsigned>(hash64(static_cast<uint64_t>(key))) & (H - 1);
+        for (;;) {
+            unsigned long long old = atomicCAS(reinterpret_cast<unsigned long long *>(keys + h),
+                                               static_cast<unsigned long long>(-1ll),
+                                               static_cast<unsigned long long>(key));
+            if (old == static_cast<unsigned long long>(-1ll) ||
+                old == static_cast<unsigned long long>(key))
+                break;
+            h = (h + 1) & (H - 1);
+        }
+        hslot[i] = static_cast<int>(h);
+    }
     float ss = 0.f;
     {  // 16-byte vector loads (d is a multiple of 128, rows 16-byte aligned)
         const uint4 *row = reinterpret_cast<const uint4 *>(x + i * d);
@@ -628,25 +653,6 @@ __global__ void k_rownorm_insert(const T *__restrict__ x, const int64_t *__restr
         } else {
             inv_n[i] = 1.0f / nrm;
         }
-        const int64_t key = y[i];
-        if (key < 0) {
-            latch(sc, ERR_DEVICE, DET_BAD_LABEL);
-            hslot[i] = -1;
-            tseq[i] = -1;
-            return;
-        }
-        tseq[i] = idx_lookup(ix, key);  // a3: the target = the label's newest slot of this shard (D8)
-        unsigned h = static_cast<unsigned>(hash64(static_cast<uint64_t>(key))) & (H - 1);
-        for (;;) {
-            unsigned long long old = atomicCAS(reinterpret_cast<unsigned long long *>(keys + h),
-                                               static_cast<unsigned long long>(-1ll),
-                                               static_cast<unsigned long long>(key));
-            if (old == static_cast<unsigned long long>(-1ll) ||
-                old == static_cast<unsigned long long>(key))
-                break;
-            h = (h + 1) & (H - 1);
-        }
-        hslot[i] = static_cast<int>(h);
     }
 }
 
