@@ -174,3 +174,50 @@ def test_loopback_world_variants(dcp, monkeypatch, variant):
     assert_dx_close(np.concatenate([o[1] for o in out]), ref.dx)
     np.testing.assert_array_equal(np.concatenate([o[2] for o in out]), pool.lab)
     assert all(o[3] == int(pool.E[0]) for o in out)
+
+
+@pytest.mark.slow
+def test_c3_w8_loopback_full_size_sampled_rows(dcp, monkeypatch):
+    """BJ:10 at W = 8 through the real per-rank code path: eight handles of 524,288 slots each (global
+    batch 8192, global enqueue block 4096, the pool prefilled through C5), one step with pairing;
+    sampled rows of ranks 0, 3 and 7 against the single-pool oracle (D16), properties on all rows."""
+    from test_gpu_fullsize import _check
+    uid = _loopback(monkeypatch)
+    cfg, W = synth.CONFIGS["c3"], 8
+    M = cfg.M_loc
+    nblk = cfg.prefill_blocks(W)
+    sts = [synth.step_inputs(cfg, 0, r, W) for r in range(W)]
+
+    def rank_fn(r):
+        head = dcp.DCPHead(cfg.C, cfg.d, dcp.BF16, W, r, n_local_max=cfg.N_loc(), m_local_max=M, nccl_uid=uid)
+        for b in range(nblk):
+            g, y = synth.prefill_block(cfg, b, r, W)
+            head.enqueue(to_dev(g, synth.BF16), lt(y))
+        st = sts[r]
+        head.enqueue(to_dev(st.g, synth.BF16), lt(st.gy))
+        loss, dx = head.loss_fwd_bwd(to_dev(st.x, synth.BF16), lt(st.y), it(st.pairing), cfg.s, cfg.m)
+        torch.cuda.current_stream().synchronize()
+        head.check()
+        rs = head.row_stats(cfg.N_loc() * W)
+        out = (loss, from_dev(dx), rs)
+        head.close()
+        return out
+
+    out = _run_ranks(W, rank_fn)
+    pool = oracle.Pool(cfg.C, cfg.d, oracle.BF16)
+    for b in range(nblk):
+        parts = [synth.prefill_block(cfg, b, r, W) for r in range(W)]
+        pool.enqueue(np.concatenate([p[0] for p in parts]), np.concatenate([p[1] for p in parts]))
+    pool.enqueue(np.concatenate([s.g for s in sts]), np.concatenate([s.gy for s in sts]))
+    x = np.concatenate([s.x for s in sts])
+    y = np.concatenate([s.y for s in sts])
+    pr = np.concatenate([s.pairing for s in sts])
+    rng = np.random.default_rng(3)
+    rows = np.sort(np.concatenate([r * 2 * M + rng.choice(M, 1, replace=False) for r in (0, 3, 7)] +
+                                  [r * 2 * M + M + rng.choice(M, 1, replace=False) for r in (0, 3, 7)]))
+    ref = pool.loss_rows(x, y, pr, cfg.s, cfg.m, rows)
+    losses = [float(o[0].item()) for o in out]
+    assert all(v == losses[0] for v in losses)
+    gdx = np.concatenate([o[1] for o in out])
+    _check(cfg, out[0][0], gdx, out[0][2], ref, rows)
+    assert out[0][2]["N_pos"] >= cfg.M_glob(W)
