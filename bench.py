@@ -235,17 +235,8 @@ class Clocks:
 def _nccl_uid(world, rank, dev):
     """The library's NCCL communicator is bootstrapped from a unique id made by rank 0 and
     broadcast over the torch process group (torch only for plumbing)."""
-    import torch
-    import torch.distributed as dist
-    if world == 1:
-        return None
-    if rank == 0:
-        raw = bytes(torch.cuda.nccl.unique_id())
-        t = torch.tensor(list(raw), dtype=torch.uint8, device=dev)
-    else:
-        t = torch.zeros(128, dtype=torch.uint8, device=dev)
-    dist.broadcast(t, 0)
-    return bytes(t.cpu().tolist())
+    import paper_2105_10375_b200 as dcp
+    return None if world == 1 else dcp.nccl_unique_id(dev)
 
 
 def w_parity(world, rank, local_rank, dev, emulate=0):

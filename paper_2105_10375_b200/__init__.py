@@ -7,6 +7,7 @@ There is no CPU fallback: constructing a head without the built library or
 without an sm_100 device raises.
 """
 from .dcp import (BF16, F32, PHI_MAX, PHI_MEAN, PHI_SUM, DCPError, DCPHead, gnet_ema, lib_path,
-                  load_library)
+                  load_library, nccl_unique_id)
 
-__all__ = ["BF16", "F32", "PHI_MAX", "PHI_MEAN", "PHI_SUM", "DCPError", "DCPHead", "gnet_ema", "lib_path", "load_library"]
+__all__ = ["BF16", "F32", "PHI_MAX", "PHI_MEAN", "PHI_SUM", "DCPError", "DCPHead", "gnet_ema", "lib_path", "load_library",
+           "nccl_unique_id"]

@@ -281,6 +281,21 @@ class DCPHead:
             pass
 
 
+def nccl_unique_id(device=None) -> bytes | None:
+    """The 128-byte NCCL unique id a world > 1 DCPHead needs (f2c_dcp_create): made by rank 0 and
+    broadcast over the default torch.distributed process group (plumbing only); None for world 1."""
+    import torch.distributed as dist
+    if not dist.is_initialized() or dist.get_world_size() == 1:
+        return None
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    if dist.get_rank() == 0:
+        t = torch.tensor(list(bytes(torch.cuda.nccl.unique_id())), dtype=torch.uint8, device=dev)
+    else:
+        t = torch.zeros(128, dtype=torch.uint8, device=dev)
+    dist.broadcast(t, 0)
+    return bytes(t.cpu().tolist())
+
+
 def gnet_ema(p: torch.Tensor, g: torch.Tensor, momentum: float, stream=None):
     """In-place g <- m g + (1-m) p (fp32, fp64 arithmetic, bit-exact)."""
     for name, t in (("p", p), ("g", g)):
