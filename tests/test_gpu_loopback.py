@@ -41,11 +41,13 @@ def _run_ranks(W, fn):
         except Exception as e:  # pragma: no cover - reported below
             err.append((r, e))
 
-    ts = [threading.Thread(target=work, args=(r,)) for r in range(W)]
+    # daemon threads: a rank stuck in a transport barrier (a protocol bug) cannot keep the process alive
+    ts = [threading.Thread(target=work, args=(r,), daemon=True) for r in range(W)]
     for t in ts:
         t.start()
     for t in ts:
         t.join(timeout=600)
+    assert not any(t.is_alive() for t in ts), "a rank did not finish (loopback transport deadlock?)"
     assert not err, err
     return out
 
