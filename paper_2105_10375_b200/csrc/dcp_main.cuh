@@ -75,8 +75,13 @@ struct TPAux {
 // row groups, so every pool tile is read from HBM about once and served to the R
 // row groups from L2.  S balances R*S units over G CTAs (waves) while keeping
 // ranges long; the combine kernel recomputes the same S.  Unit id = segment id.
+// timing experiments only (F2C_FORCE_S, set at create): force the number of ranges S
+__constant__ int g_force_S;
 __host__ __device__ inline int tp_choose_S(int R, int G, int n_tiles) {
     if (n_tiles <= 0 || R <= 0) return 1;
+#ifdef __CUDA_ARCH__
+    if (g_force_S > 0) return g_force_S < n_tiles ? g_force_S : n_tiles;
+#endif
     int s_lo = G / R;
     if (s_lo < 1) s_lo = 1;
     int s_hi = (2 * G) / R + 1;
@@ -103,6 +108,26 @@ __host__ __device__ inline int tp_choose_S(int R, int G, int n_tiles) {
     return best;
 }
 
+// dcp_pc_kernel's schedule (round 2): S is chosen once per loss call, by k_compact as soon as the row
+// count is known (one thread per candidate S, a block-wide argmin; sc->S_sched), and read by the fused
+// kernel and the combine.  Candidates: R S <= 512 (the partial-buffer bound the layout always holds)
+// and at most 30 units per cluster; cost t(S) = waves (ceil(n_tiles / S) + 8), the 8 tile-equivalents
+// being the fixed per-unit cost (prologue, O drain); ties go to the smaller S.  Multi-wave schedules
+// with fine ranges measured faster where one wave leaves clusters idle (c3, 5 row groups on 74
+// clusters: S = 59 instead of 14, -3 to -5 %; c3r_8, 34 groups: S = 13 instead of 2, -2 to -6 %);
+// c2 keeps its single wave (profiles/r02_ab_schedule_waves.txt).
+__host__ __device__ inline int pc_s_hi(int R, int G, int n_tiles) {
+    if (R <= 0 || n_tiles <= 0) return 1;
+    int s_hi = 512 / R;
+    if (30 * G / R < s_hi) s_hi = 30 * G / R;
+    if (s_hi > n_tiles) s_hi = n_tiles;
+    return s_hi < 1 ? 1 : s_hi;
+}
+__host__ __device__ inline float pc_sched_cost(int S, int R, int G, int n_tiles) {
+    const int waves = (R * S + G - 1) / G;
+    return static_cast<float>(waves) * (static_cast<float>((n_tiles + S - 1) / S) + 8.f);
+}
+
 // First tile of range s when n_tiles tiles are cut into S ranges: q or q + 1 tiles each (the
 // first n_tiles % S ranges get one more).  32-bit arithmetic only: 64-bit divisions cost ~100
 // instructions each, and this runs in every CTA's prologue and in every combine row.
@@ -114,11 +139,11 @@ __host__ __device__ inline int tp_range_begin(int s, int n_tiles, int S) {
 struct TPSched {
     int R, S, n_tiles, G;
     int u, U;
-    __device__ void init(int b, int G_, int R_, int nt) {
+    __device__ void init(int b, int G_, int R_, int nt, int S_fixed = 0) {
         R = R_;
         G = G_;
         n_tiles = nt;
-        S = tp_choose_S(R, G, nt);
+        S = S_fixed > 0 ? S_fixed : tp_choose_S(R, G, nt);
         U = nt > 0 ? R * S : 0;
         u = b;
     }

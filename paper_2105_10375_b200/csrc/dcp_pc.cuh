@@ -124,6 +124,7 @@ struct PCParams {
     const uint8_t *X_pos;  // [R_max, d] bf16 compacted rows
     const float *wslot;    // K >= 2: per-slot 1/||T_bar_c|| (fp32, padded by one tile; the NEXT-3
                            // out-of-pool rows' weight ring reads it); null for K = 1
+    const int *S_sched;    // device: the range count S of this call's schedule (k_compact, pc_sched_cost)
     int kf;                // features per slot K: GEMM 1 contracts x_hat with the K raw rows of a slot
                            // (K d columns; 1/K is folded into a_r, so the logits use the exact mean)
     float margin_l2;       // s * m * log2(e)
@@ -418,7 +419,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
         }
         fence_mbar_init();
         TPSched ts;
-        ts.init(blockIdx.x >> 1, gridDim.x >> 1, n_rg, n_tiles);
+        ts.init(blockIdx.x >> 1, gridDim.x >> 1, n_rg, n_tiles, *p.S_sched);
         int n = 0, a, b, c, s;
         while (n < PC_MAX_UNITS && ts.next(a, b, c, s)) aux->units[n++] = make_int4(a, b, c, s);
         aux->n_units = n;

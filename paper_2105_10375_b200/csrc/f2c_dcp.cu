@@ -580,6 +580,9 @@ int f2c_dcp_create_k(int64_t C, int32_t K, int32_t d, int32_t dtype, int32_t wor
         h->pc4_mode = !kv ? 0 : strcmp(kv, "pc4") == 0 ? 1 : strcmp(kv, "pc") == 0 ? -1 : 0;
         const char *fl = getenv("F2C_DBG_FLAGS");  // timing experiments only (results void)
         h->dbg_flags = fl ? atoi(fl) : 0;
+        const char *fs = getenv("F2C_FORCE_S");    // timing experiments: force the range count S
+        const int force_s = fs ? atoi(fs) : 0;
+        cudaMemcpyToSymbol(g_force_S, &force_s, sizeof force_s);
     }
     if (cudaFuncSetAttribute(dcp_tp64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              TP_SMEM_BYTES) != cudaSuccess ||
@@ -1112,6 +1115,11 @@ static int phase_compact(f2c_dcp *h, Rank &R, const StepCtx &c, const int *tmax_
     a.hslot = R.at<int>(L.hslot);
     a.row_hent = R.at<int>(L.row_hent);
     a.hgseq = R.at<int64_t>(L.hgseq);
+    {
+        const int64_t occ_t = occ_local(h, R);
+        a.G_pc = kernel_kind(h, c.N) == 0 ? h->G / 2 : 0;
+        a.n_tiles_pc = static_cast<int>((occ_t + PC_TILE - 1) / PC_TILE);
+    }
     k_compact<<<static_cast<unsigned>((c.N + 1023) / 1024), 1024, 0, c.st>>>(a);
     LAUNCH_CHECK();
     const int64_t occ = occ_local(h, R);
@@ -1184,6 +1192,7 @@ static int phase_main(f2c_dcp *h, Rank &R, const StepCtx &c, int64_t occ_loc, co
         q.X_pos = R.base + L.X_pos;
         q.wslot = h->K > 1 ? R.at<float>(L.wslot) : nullptr;
         q.kf = h->K;
+        q.S_sched = &R.sc()->S_sched;
         q.margin_l2 = p.margin_l2;
         q.ttgt = p.ttgt;
         q.seg_l = p.seg_l;
@@ -1247,6 +1256,7 @@ static CombineArgs combine_args(f2c_dcp *h, Rank &R, const StepCtx &c, int64_t o
     const int kind = kernel_kind(h, c.N);
     a.G = kind == 1 ? h->G : kind == 2 ? h->G4 : h->G / 2;
     a.rows_per_group = kind == 1 ? TP_R : kind == 2 ? P4_RG : PC_R;
+    a.wide = kind == 0 ? 1 : 0;
     a.n_tiles = static_cast<int>((occ + TP_TILE - 1) / TP_TILE);
     a.s = c.s;
     a.margin_l2 = c.s * c.m * 1.4426950408889634f;

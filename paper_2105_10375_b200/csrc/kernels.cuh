@@ -33,6 +33,7 @@ struct Scalars {          // lives at the start of the per-rank scratch
     long long n_app;      // rows appended by the last refresh-in-place enqueue (NEXT-3)
     unsigned loss_done;   // CTAs of the final per-row kernel done (the last one sums the loss)
     int refine;           // R1 fallback: some row's reference was lowered, re-run the fused kernel
+    int S_sched;          // dcp_pc_kernel's range count for this loss call (k_compact)
     int *err_mirror;      // mapped pinned host words {err, detail} of this shard: the host reads
                           // them at the next call on the handle without synchronising
 };
@@ -867,6 +868,7 @@ struct CompactArgs {
     const int *hslot;         // [N]
     int *row_hent;            // [R_max]
     int64_t *hgseq;           // [H]
+    int G_pc, n_tiles_pc;     // dcp_pc_kernel's clusters and tiles: choose its S here (G_pc = 0: other kernels)
 };
 __global__ void __launch_bounds__(1024) k_compact(CompactArgs a) {
     // CTA b compacts rows [b*1024, (b+1)*1024).  Every CTA counts the in-pool rows of the
@@ -965,6 +967,24 @@ __global__ void __launch_bounds__(1024) k_compact(CompactArgs a) {
         a.row_tgt[r] = -1;
         a.ttgt[r] = -INFINITY;
     }
+    if (a.G_pc > 0) {  // dcp_pc_kernel's S: one candidate per thread, argmin (cost, then S)
+        __shared__ unsigned long long best;
+        if (tid == 0) best = ~0ull;
+        __syncthreads();
+        const int R = (n_rows + PC_R - 1) / PC_R;
+        const int s_hi = pc_s_hi(R, a.G_pc, a.n_tiles_pc);
+        for (int S = tid + 1; S <= s_hi; S += nt) {
+            const float c = pc_sched_cost(S, R, a.G_pc, a.n_tiles_pc);
+            atomicMin(&best, (static_cast<unsigned long long>(__float_as_uint(c)) << 32) | static_cast<unsigned>(S));
+        }
+        __syncthreads();
+        if (tid == 0) {
+            int S = static_cast<int>(best & 0xffffffffull);
+            if (g_force_S > 0) S = g_force_S;  // (timing experiments)
+            if (S > a.n_tiles_pc) S = a.n_tiles_pc;
+            a.sc->S_sched = S < 1 ? 1 : S;
+        }
+    }
     if (tid == 0) {
         a.sc->refine = 0;
         a.sc->neg0 = neg0;
@@ -1051,6 +1071,7 @@ struct CombineArgs {
     int64_t N, C_occ;
     int d, dtype, G, n_tiles;
     int rows_per_group;         // 64 (TP64 kernel) or 128 (producer/consumer kernel)
+    int wide;                   // the partials come from dcp_pc_kernel: its S is sc->S_sched
     float s, margin_l2;
     uint8_t *dx;                // [N, d] dtype
     double *rowloss;            // [N]
@@ -1177,7 +1198,7 @@ __device__ __forceinline__ void gather_row_partials(const CombineArgs &a, int n_
     mx = -INFINITY;
     zero16(o);
     if (a.n_tiles <= 0) return;
-    const int S = tp_choose_S(n_rg, a.G, a.n_tiles);
+    const int S = (a.wide ? a.sc->S_sched : tp_choose_S(n_rg, a.G, a.n_tiles));
     constexpr int B = 4;
     for (int s0 = 0; s0 < S; s0 += B) {
         float lv[B], mv[B];
@@ -1227,7 +1248,7 @@ __device__ __forceinline__ void gather_row_max(const CombineArgs &a, int n_rg, i
     cmax = -INFINITY;
     carg = -1;
     if (a.n_tiles <= 0) return;
-    const int S = tp_choose_S(n_rg, a.G, a.n_tiles);
+    const int S = (a.wide ? a.sc->S_sched : tp_choose_S(n_rg, a.G, a.n_tiles));
     for (int s = 0; s < S; ++s) {
         const int t0 = tp_range_begin(s, a.n_tiles, S);
         const int t1 = tp_range_begin(s + 1, a.n_tiles, S);
@@ -1444,7 +1465,7 @@ __global__ void __launch_bounds__(256, 2) k_local_rows(CombineArgs a, float4 *__
         const int rg = k / RG, r = k % RG;
         float lsum = 0.f, mx = -INFINITY;
         if (a.n_tiles > 0) {
-            const int S = tp_choose_S(n_rg, a.G, a.n_tiles);
+            const int S = (a.wide ? a.sc->S_sched : tp_choose_S(n_rg, a.G, a.n_tiles));
             for (int s = lane; s < S; s += 32) {  // lanes split the segments, fixed-order tree below
                 const int t0 = tp_range_begin(s, a.n_tiles, S);
                 const int t1 = tp_range_begin(s + 1, a.n_tiles, S);
