@@ -176,7 +176,7 @@ def _variant(args):
 
 
 def _config(cfg, world, ema_overlap=True, K=1, variant="default (D8, D10, pure Eq. 7)"):
-    return {"workload": cfg.name, "model": "DCP head (F2C)", "C": cfg.C, "C_per_gpu": cfg.C // world,
+    return {"workload": cfg.name, "C": cfg.C, "C_per_gpu": cfg.C // world,
             "d": cfg.d, "global_batch": cfg.N_loc() * world, "M_glob": cfg.M_glob(world),
             "n_id": cfg.n_id, "s": cfg.s, "m": cfg.m, "pair_noise_sigma": cfg.sigma,
             "ema_params": EMA_PARAMS, "K": K, "variant": variant, "parallelism": f"slot-range sharded pool x{world}",
