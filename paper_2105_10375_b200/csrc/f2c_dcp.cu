@@ -323,6 +323,7 @@ struct f2c_dcp {
     int pc4_mode = 0;               // 1: the 2-SM pair kernel where it applies (F2C_KERNEL=pc4)
     int G4 = 0;                     // co-resident 4-CTA clusters of dcp_pc4_kernel (its persistent grid / 4)
     unsigned int epoch = 0;         // fused-kernel launch tag (range pacing)
+    int enq_occ = 8, enq_occ_k = 8; // resident k_enqueue / k_enqueue_k CTAs per SM (occupancy at create)
     int dbg_flags = 0;              // timing experiments (F2C_DBG_FLAGS)
     int dbg_cluster = 0;            // debug timestamps of this cluster (F2C_DBG_CLUSTER)
     ~f2c_dcp() {
@@ -606,6 +607,17 @@ int f2c_dcp_create_k(int64_t C, int32_t K, int32_t d, int32_t dtype, int32_t wor
                              P4_SMEM_BYTES) != cudaSuccess) {
         delete h;
         return fail(F2C_ECUDA, "cudaFuncSetAttribute(smem) failed");
+    }
+    {
+        int occ = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_enqueue, 256, 0) == cudaSuccess && occ >= 1)
+            h->enq_occ = occ;
+        else
+            cudaGetLastError();
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_enqueue_k, 256, 0) == cudaSuccess && occ >= 1)
+            h->enq_occ_k = occ;
+        else
+            cudaGetLastError();
     }
     {   // dcp_pc_kernel's range pacing assumes every 2-CTA cluster of its persistent grid is
         // resident at once: size the grid by what the device can co-schedule (GPC floorsweeping,
@@ -907,7 +919,7 @@ static int enqueue_rank(f2c_dcp *h, Rank &R, const uint8_t *g, const int64_t *y,
     const LabelIndex ixe = (h->dbg_flags & (1 << 20)) ? LabelIndex{nullptr, nullptr, 0} : R.ix();
     if (h->K > 1) {
         int64_t blocks = (m_glob + 7) / 8;
-        if (blocks > static_cast<int64_t>(h->G) * 8) blocks = static_cast<int64_t>(h->G) * 8;
+        if (blocks > static_cast<int64_t>(h->G) * h->enq_occ_k) blocks = static_cast<int64_t>(h->G) * h->enq_occ_k;
         k_enqueue_k<<<static_cast<unsigned>(blocks), 256, 0, st>>>(
             reinterpret_cast<const __nv_bfloat16 *>(g), y, m_glob, h->K, h->d, h->E, h->C, R.lo, R.hi,
             R.at<__nv_bfloat16>(R.L.Traw), R.at<__nv_bfloat16>(R.L.T), R.at<float>(R.L.wslot),
@@ -918,7 +930,9 @@ static int enqueue_rank(f2c_dcp *h, Rank &R, const uint8_t *g, const int64_t *y,
     }
     const int row_bytes = h->d * (h->dtype == F2C_BF16 ? 2 : 4);
     int64_t blocks = (m_glob + 7) / 8;                 // 8 rows (warps) per block per pass
-    if (blocks > static_cast<int64_t>(h->G) * 8) blocks = static_cast<int64_t>(h->G) * 8;
+    // one wave of resident CTAs (grid-stride over the rows): more CTAs only queue behind the first
+    // wave and leave a tail
+    if (blocks > static_cast<int64_t>(h->G) * h->enq_occ) blocks = static_cast<int64_t>(h->G) * h->enq_occ;
     k_enqueue<<<static_cast<unsigned>(blocks), 256, 0, st>>>(
         g, y, m_glob, h->E, h->C, R.lo, R.hi, row_bytes, h->dtype, R.base + R.L.T,
         R.at<int64_t>(R.L.lab), R.sc(), h->refresh ? R.at<int64_t>(R.L.dst_seq) : nullptr,
