@@ -1260,6 +1260,9 @@ static CombineArgs combine_args(f2c_dcp *h, Rank &R, const StepCtx &c, int64_t o
     a.seg_mx = R.at<float>(L.seg_mx);
     a.seg_O = R.at<float>(L.seg_O);
     a.T = R.base + (h->dtype == F2C_F32 ? L.Tsh : L.T);  // (bf16: the GEMM-2 operand rows)
+    a.Tc = R.base + (h->K > 1 ? L.Traw : L.T);            // (exact centers: fp32 rows, K raw rows, bf16 rows)
+    a.Tc_kind = h->dtype == F2C_F32 ? 1 : (h->K > 1 ? 2 : 0);
+    a.Kc = h->K;
     a.mu_fx = R.at<long long>(L.mu_fx);
     a.sc = R.sc();
     a.sc_w = R.sc();

@@ -1066,6 +1066,11 @@ struct CombineArgs {
     const float *ttgt;          // [R_max]
     const float *seg_l, *seg_mx, *seg_O;
     const uint8_t *T;           // local pool, bf16 (an fp32 pool's bf16 shadow: the operand of GEMM 2)
+    // the exact center of a slot for the gradient's target / hardest-negative rows: the bf16 row (K = 1),
+    // the fp32 row of an fp32 pool (D21), or the fp32 mean of the K raw rows (R5)
+    const uint8_t *Tc;
+    int Tc_kind;                // 0 bf16 rows (= T), 1 fp32 rows, 2 K raw bf16 rows per slot
+    int Kc;
     const Scalars *sc;
     Scalars *sc_w;
     int64_t N, C_occ;
@@ -1298,10 +1303,32 @@ __device__ __forceinline__ void neg_row_local(const CombineArgs &a, int n_rg, in
         zero16(g);
     }
 }
+// slot c's exact center (lane layout of load_bf16_row), times scale
+__device__ __forceinline__ void load_center(const CombineArgs &a, int c, int lane, float scale, float (&v)[16]) {
+    if (a.Tc_kind == 1) {
+        load_x_row(a.Tc, 1, c, a.d, lane, scale, v);
+        return;
+    }
+    if (a.Tc_kind == 0) {
+        load_bf16_row(reinterpret_cast<const __nv_bfloat16 *>(a.Tc) + static_cast<int64_t>(c) * a.d, a.d, lane, scale, v);
+        return;
+    }
+    // K raw rows: fp32 sum over k, then x 1/K (the enqueue's arithmetic, slot_mean16)
+    const __nv_bfloat16 *raw = reinterpret_cast<const __nv_bfloat16 *>(a.Tc) + static_cast<int64_t>(c) * a.Kc * a.d;
+    float acc[16], r[16];
+    zero16(acc);
+    for (int k = 0; k < a.Kc; ++k) {
+        load_bf16_row(raw + static_cast<int64_t>(k) * a.d, a.d, lane, 1.f, r);
+#pragma unroll
+        for (int q = 0; q < 16; ++q) acc[q] = __fadd_rn(acc[q], r[q]);
+    }
+    const float invK = 1.0f / static_cast<float>(a.Kc);
+#pragma unroll
+    for (int q = 0; q < 16; ++q) v[q] = __fmul_rn(acc[q], invK) * scale;
+}
 __device__ __forceinline__ void add_center(const CombineArgs &a, int carg, float coef, float (&g)[16]) {
     const float wc = a.wslot ? a.wslot[carg] : 1.f;
-    const __nv_bfloat16 *Tc = reinterpret_cast<const __nv_bfloat16 *>(a.T) + static_cast<int64_t>(carg) * a.d;
-    load_bf16_row(Tc, a.d, threadIdx.x & 31, coef * wc, g);
+    load_center(a, carg, threadIdx.x & 31, coef * wc, g);
 }
 
 // normalisation Jacobian and output: dst = (g - (g . x_hat) x_hat) / ||x||
@@ -1382,8 +1409,7 @@ __device__ __forceinline__ void combine_row(const CombineArgs &a, int64_t i) {
         const double w = static_cast<double>(a.s) / static_cast<double>(n_pos);
         const float alpha = static_cast<float>(w / l), beta = static_cast<float>(w * (lr / l));
         float Tt[16];
-        load_bf16_row(reinterpret_cast<const __nv_bfloat16 *>(a.T) + static_cast<int64_t>(ts < 0 ? 0 : ts) * a.d,
-                      a.d, lane, 1.f, Tt);
+        load_center(a, ts < 0 ? 0 : ts, lane, 1.f, Tt);
 #pragma unroll
         for (int q = 0; q < 16; ++q) g[q] = alpha * o[q] - beta * Tt[q];
         const double ell = log1p(lr * exp2(-tt));  // = lse - z_t
@@ -1532,8 +1558,7 @@ __device__ __forceinline__ void finalize_row(const CombineArgs &a, const float4 
         const float alpha = static_cast<float>(w / l) * my_scale;
         const float beta = ts >= 0 ? static_cast<float>(w * (lr / l)) : 0.f;
         float Tt[16];
-        load_bf16_row(reinterpret_cast<const __nv_bfloat16 *>(a.T) + static_cast<int64_t>(ts < 0 ? 0 : ts) * a.d,
-                      a.d, lane, 1.f, Tt);
+        load_center(a, ts < 0 ? 0 : ts, lane, 1.f, Tt);
 #pragma unroll
         for (int q = 0; q < 16; ++q) g[q] = alpha * o[q] - beta * Tt[q];
         const double ell = log1p(lr * exp2(-static_cast<double>(tt)));
