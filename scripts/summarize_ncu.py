@@ -101,7 +101,23 @@ open(os.path.join(out, f"{tag}_ncu_main_{w}.txt"), "w").write("\n".join(lines) +
 print("\n".join(lines))
 dr = float(m["dram__bytes_read.sum"][0]) * {"Gbyte": 1e9, "Mbyte": 1e6, "byte": 1}[m["dram__bytes_read.sum"][1]]
 dw = float(m["dram__bytes_write.sum"][0]) * {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1}[m["dram__bytes_write.sum"][1]]
-json.dump({"kernel": "dcp_pc_kernel", "workload": w, "tag": tag, "dram_bytes_per_launch": dr + dw,
-           "dram_read_bytes": dr, "dram_write_bytes": dw, "metrics": js,
-           "source": f"ncu --set full --clock-control none ({tag}, gpurun_out/prof_{w}.ncu-rep)"},
-          open(os.path.join(out, f"ncu_main_{w}.json"), "w"), indent=1)
+rec = {"kernel": "dcp_pc_kernel", "workload": w, "tag": tag, "dram_bytes_per_launch": dr + dw,
+       "dram_read_bytes": dr, "dram_write_bytes": dw, "metrics": js,
+       "source": f"ncu --set full --clock-control none ({tag}, gpurun_out/prof_{w}.ncu-rep)"}
+# the counters-only pass over 10 timed launches (profile_round.sh): its median is the per-launch figure
+dv = os.path.join(ROOT, "gpurun_out", f"dramvar_{w}.csv")
+if os.path.exists(dv):
+    rows = [l for l in open(dv) if l.startswith('"')]
+    per_id = collections.defaultdict(dict)
+    for r in csv.DictReader(io.StringIO("".join(rows))):
+        per_id[r["ID"]][r["Metric Name"]] = float(r["Metric Value"].replace(",", ""))
+    tot_b = sorted(v["dram__bytes_read.sum"] + v["dram__bytes_write.sum"] for v in per_id.values())
+    med = tot_b[len(tot_b) // 2]
+    rec.update({"dram_bytes_set_full": dr + dw, "dram_bytes_per_launch": med, "dram_bytes_launches": tot_b,
+                "source": f"median of {len(tot_b)} timed launches, ncu --metrics dram__bytes_read.sum,"
+                          f"dram__bytes_write.sum --clock-control none ({tag}); dram_bytes_set_full: the "
+                          f"--set full capture (gpurun_out/prof_{w}.ncu-rep)"})
+    with open(os.path.join(out, f"{tag}_ncu_main_{w}.txt"), "a") as f:
+        f.write(f"DRAM bytes per launch, counters-only pass over {len(tot_b)} timed launches: median "
+                f"{med / 1e9:.3f} GB (min {tot_b[0] / 1e9:.3f}, max {tot_b[-1] / 1e9:.3f})\n")
+json.dump(rec, open(os.path.join(out, f"ncu_main_{w}.json"), "w"), indent=1)
