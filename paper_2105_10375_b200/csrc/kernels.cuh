@@ -543,9 +543,10 @@ __device__ __forceinline__ float ema1(float gv, float pv, double m, double om) {
     return __double2float_rn(__dadd_rn(__dmul_rn(m, static_cast<double>(gv)),
                                        __dmul_rn(om, static_cast<double>(pv))));
 }
-// One CTA per 1024 float4 (16 KB of g): short-lived CTAs, so a concurrently launched
+// One CTA per 256 float4 (4 KB of g): short-lived CTAs, so a concurrently launched
 // persistent kernel (the fused loss kernel) gets its SMs back within microseconds when the
-// EMA runs on a side stream; four independent 16-B loads per thread in flight.
+// EMA runs on a side stream; four independent 16-B loads per thread in flight (two of p, two
+// of g).  (Measured: 4 float4 per array per thread, or 160 / 192-thread CTAs, were slower.)
 // Small CTAs (128 threads, <= 40 registers, no smem) fit next to the fused loss kernel on an
 // SM (its CTA leaves ~6K registers and ~24 KB of smem free), so an EMA on a side stream can run
 // concurrently with it instead of waiting for its SMs.
