@@ -15,6 +15,7 @@ from helpers import assert_dx_close, assert_loss_close, from_dev, lt, to_dev
 pytestmark = pytest.mark.gpu
 
 N_CASES = int(os.environ.get("F2C_FUZZ_CASES", "64"))  # (a longer sweep: F2C_FUZZ_CASES=512)
+FIRST = int(os.environ.get("F2C_FUZZ_FIRST", "0"))  # first case index (sweeps beyond the default cases)
 
 
 @pytest.fixture(scope="module")
@@ -51,7 +52,7 @@ def _case(i):
                 hinge=hinge, lam=lam, excl=excl, refresh=refresh, n_lab=n_lab, seed=2000 + i, dt=dt)
 
 
-@pytest.mark.parametrize("i", range(N_CASES))
+@pytest.mark.parametrize("i", range(FIRST, FIRST + N_CASES))
 def test_fuzz_parity(dcp, i):
     c = _case(i)
     W, K, d, C, m_loc = c["W"], c["K"], c["d"], c["C"], c["m_loc"]

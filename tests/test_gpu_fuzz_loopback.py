@@ -15,6 +15,7 @@ from test_gpu_loopback import _loopback, _run_ranks
 
 pytestmark = pytest.mark.gpu
 N_CASES = int(os.environ.get("F2C_FUZZ_LB_CASES", "24"))
+FIRST = int(os.environ.get("F2C_FUZZ_FIRST", "0"))  # first case index (sweeps beyond the default cases)
 
 
 @pytest.fixture(scope="module")
@@ -44,7 +45,7 @@ def _case(i):
                 m=float(rng.choice([0.0, 0.35])))
 
 
-@pytest.mark.parametrize("i", range(N_CASES))
+@pytest.mark.parametrize("i", range(FIRST, FIRST + N_CASES))
 def test_fuzz_loopback(dcp, monkeypatch, i):
     c = _case(i)
     W, K, d, dt, C, m_loc, n_loc = c["W"], c["K"], c["d"], c["dt"], c["C"], c["m_loc"], c["n_loc"]

@@ -16,6 +16,7 @@ from helpers import assert_dx_close, assert_loss_close, from_dev, lt, to_dev
 pytestmark = pytest.mark.gpu
 
 N_CASES = int(os.environ.get("F2C_FUZZ_MED_CASES", "1"))
+FIRST = int(os.environ.get("F2C_FUZZ_FIRST", "0"))  # first case index (sweeps beyond the default cases)
 
 
 @pytest.fixture(scope="module")
@@ -47,7 +48,7 @@ def _case(i):
                 hinge=hinge, lam=lam, excl=excl, refresh=refresh, n_lab=n_lab, seed=92000 + i, clusters=clusters)
 
 
-@pytest.mark.parametrize("i", range(N_CASES))
+@pytest.mark.parametrize("i", range(FIRST, FIRST + N_CASES))
 def test_fuzz_medium_parity(dcp, i, monkeypatch):
     c = _case(i)
     if c["clusters"]:
