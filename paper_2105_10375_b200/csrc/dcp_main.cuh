@@ -80,12 +80,15 @@ __constant__ int g_force_S;
 __host__ __device__ inline int tp_choose_S(int R, int G, int n_tiles) {
     if (n_tiles <= 0 || R <= 0) return 1;
 #ifdef __CUDA_ARCH__
-    if (g_force_S > 0) return g_force_S < n_tiles ? g_force_S : n_tiles;
 #endif
     int s_lo = G / R;
     if (s_lo < 1) s_lo = 1;
     int s_hi = (2 * G) / R + 1;
     if (s_hi > n_tiles) s_hi = n_tiles;
+#ifdef __CUDA_ARCH__
+    // (the forced count stays within the candidates' bound: R S <= 2G + R, the partial buffer's size)
+    if (g_force_S > 0) return g_force_S < s_hi ? g_force_S : s_hi;
+#endif
     if (s_lo > s_hi) s_lo = s_hi;
     int best = s_lo;
     // (single precision: this runs in every CTA's prologue and in every combine row, and fp64

@@ -981,7 +981,7 @@ __global__ void __launch_bounds__(1024) k_compact(CompactArgs a) {
         __syncthreads();
         if (tid == 0) {
             int S = static_cast<int>(best & 0xffffffffull);
-            if (g_force_S > 0) S = g_force_S;  // (timing experiments)
+            if (g_force_S > 0) S = g_force_S < s_hi ? g_force_S : s_hi;  // (timing experiments; within the layout's bounds)
             if (S > a.n_tiles_pc) S = a.n_tiles_pc;
             a.sc->S_sched = S < 1 ? 1 : S;
         }
