@@ -359,13 +359,15 @@ def roofline_block(cfg, world, d, npos_avg, t_launch, ms_step, clocks, pk, share
     hbm_bytes = C_loc * d * 2 + N * d * 2 * 2 + cfg.M_glob(world) * d * 2 * 2 + EMA_PARAMS * 12
     nvl_bytes = 0.0 if world == 1 else (N * d * 2 + N * 16 * world + N * d * 4 + cfg.M_glob(world) * d * 2) * (world - 1) / world
     t_roof = max(flops_alg / (burst * 1e12), hbm_bytes / (pk["hbm_gbs"] * 1e9), nvl_bytes / 900e9)
-    traffic = None
+    traffic, traffic_src = None, None
     prof_file = os.path.join(ROOT, "profiles", f"ncu_main_{cfg.name}.json")
     if os.path.exists(prof_file):
         try:
-            traffic = json.load(open(prof_file)).get("dram_bytes_per_launch")
+            prof = json.load(open(prof_file))
+            traffic = prof.get("dram_bytes_per_launch")
+            traffic_src = f"profiles/ncu_main_{cfg.name}.json: {prof.get('source')}"
         except Exception:
-            traffic = None
+            traffic, traffic_src = None, None
     # the decomposition's data movement into the SMs: every 128-row group streams the shard through
     # BOTH CTAs of its pair (producer: GEMM 1, consumer: GEMM 2) and ships P (32 KB per tile) over DSMEM.
     # Against the L2 -> SM TMA rate this chip sustains (profiles/r02_tma_l2_bench.txt): not the bound
@@ -381,7 +383,7 @@ def roofline_block(cfg, world, d, npos_avg, t_launch, ms_step, clocks, pk, share
                                 "SW128 TMA boxes, 20.1-20.9 TB/s (profiles/r02_tma_l2_bench.txt)",
                  "bytes_definition": "row groups x (2 CTAs x C_loc x d x 2 B pool tiles + tiles x 32 KB P over DSMEM)"}
     return {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-            "frac": achieved / peak, "traffic": traffic,
+            "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
             "kernel": "dcp_pc_kernel (producer: TMEM-A logits GEMM + softmax -> DSMEM P; consumer: P x pool GEMM, O in TMEM)",
             "peak_kind": ("burst bf16 (median SM clock within 5 % of max)" if near_max else
                           "sustained bf16 (SM clock > 5 % below max: power-capped run)"),
