@@ -206,7 +206,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(P4_THREADS, 1)
             for (int i = 0; i < P4_NSLOT; ++i) mbar_arrive_expect_tx(&aux->pfull[i], P4_PBYTES);
         fence_mbar_init();
         TPSched ts;
-        ts.init(blockIdx.x >> 2, gridDim.x >> 2, n_rg, n_tiles);
+        ts.init(blockIdx.x >> 2, gridDim.x >> 2, n_rg, n_tiles, *p.S_sched);  // (k_compact's multi-wave choice)
         int n = 0, a, b, c, s;
         while (n < PC_MAX_UNITS && ts.next(a, b, c, s)) aux->units[n++] = make_int4(a, b, c, s);
         aux->n_units = n;

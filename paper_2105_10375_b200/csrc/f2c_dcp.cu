@@ -1131,7 +1131,11 @@ static int phase_compact(f2c_dcp *h, Rank &R, const StepCtx &c, const int *tmax_
     a.hgseq = R.at<int64_t>(L.hgseq);
     {
         const int64_t occ_t = occ_local(h, R);
-        a.G_pc = kernel_kind(h, c.N) == 0 ? h->G / 2 : 0;
+        // the fused kernel's range count S (dcp_pc_kernel; dcp_pc4_kernel with its 256-row groups)
+        const int kind = kernel_kind(h, c.N);
+        a.G_pc = kind == 0 ? h->G / 2 : kind == 2 ? h->G4 : 0;
+        a.rg_pc = kind == 2 ? P4_RG : PC_R;
+        a.seg_cap = static_cast<int>(L.S_max * 128 / a.rg_pc);
         a.n_tiles_pc = static_cast<int>((occ_t + PC_TILE - 1) / PC_TILE);
     }
     k_compact<<<static_cast<unsigned>((c.N + 1023) / 1024), 1024, 0, c.st>>>(a);
@@ -1273,7 +1277,7 @@ static CombineArgs combine_args(f2c_dcp *h, Rank &R, const StepCtx &c, int64_t o
     const int kind = kernel_kind(h, c.N);
     a.G = kind == 1 ? h->G : kind == 2 ? h->G4 : h->G / 2;
     a.rows_per_group = kind == 1 ? TP_R : kind == 2 ? P4_RG : PC_R;
-    a.wide = kind == 0 ? 1 : 0;
+    a.wide = kind == 0 || kind == 2 ? 1 : 0;  // (both take S from k_compact)
     a.n_tiles = static_cast<int>((occ + TP_TILE - 1) / TP_TILE);
     a.s = c.s;
     a.margin_l2 = c.s * c.m * 1.4426950408889634f;

@@ -870,6 +870,8 @@ struct CompactArgs {
     int *row_hent;            // [R_max]
     int64_t *hgseq;           // [H]
     int G_pc, n_tiles_pc;     // dcp_pc_kernel's clusters and tiles: choose its S here (G_pc = 0: other kernels)
+    int rg_pc;                // rows per group of that kernel: 128 (dcp_pc_kernel) or 256 (dcp_pc4_kernel)
+    int seg_cap;              // segments of rg_pc rows the partial buffers hold (dcp_pc4_kernel)
 };
 __global__ void __launch_bounds__(1024) k_compact(CompactArgs a) {
     // CTA b compacts rows [b*1024, (b+1)*1024).  Every CTA counts the in-pool rows of the
@@ -972,8 +974,9 @@ __global__ void __launch_bounds__(1024) k_compact(CompactArgs a) {
         __shared__ unsigned long long best;
         if (tid == 0) best = ~0ull;
         __syncthreads();
-        const int R = (n_rows + PC_R - 1) / PC_R;
-        const int s_hi = pc_s_hi(R, a.G_pc, a.n_tiles_pc);
+        const int R = (n_rows + a.rg_pc - 1) / a.rg_pc;
+        int s_hi = pc_s_hi(R, a.G_pc, a.n_tiles_pc);
+        if (a.rg_pc != PC_R && R > 0 && s_hi > a.seg_cap / R) s_hi = a.seg_cap / R < 1 ? 1 : a.seg_cap / R;
         for (int S = tid + 1; S <= s_hi; S += nt) {
             const float c = pc_sched_cost(S, R, a.G_pc, a.n_tiles_pc);
             atomicMin(&best, (static_cast<unsigned long long>(__float_as_uint(c)) << 32) | static_cast<unsigned>(S));
@@ -1077,7 +1080,7 @@ struct CombineArgs {
     int64_t N, C_occ;
     int d, dtype, G, n_tiles;
     int rows_per_group;         // 64 (TP64 kernel) or 128 (producer/consumer kernel)
-    int wide;                   // the partials come from dcp_pc_kernel: its S is sc->S_sched
+    int wide;                   // the partials come from dcp_pc_kernel / dcp_pc4_kernel: their S is sc->S_sched
     float s, margin_l2;
     uint8_t *dx;                // [N, d] dtype
     double *rowloss;            // [N]
