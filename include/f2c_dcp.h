@@ -243,12 +243,6 @@ int f2c_dcp_profile_read(f2c_dcp *h, double *main_ms, int64_t *launches, int64_t
  * (cta_group::2 SM pairs, 256-row groups); *ctas = its persistent grid (CTAs).  Host only. */
 int f2c_dcp_fused_kernel(f2c_dcp *h, int64_t n_global, int32_t *kind, int32_t *ctas);
 
-/* The fused kernel's schedule in the last loss call, as k_compact chose it on the device for this
- * handle's first shard: *S = tile ranges per row group, *tail_G = clusters
- * that ran dcp_pc_kernel's tail role for a last row group of <= 32 rows (0 = none; F2C_TAIL=0 /
- * F2C_TAIL=1 at create forbid / force it where it applies).  Synchronises the device. */
-int f2c_dcp_schedule(f2c_dcp *h, int32_t *S, int32_t *tail_G);
-
 /* C5 routing plan of a pure Eq. 7 enqueue across `world` ranks (SURVEY 8(e) stage 0, P:143-151;
  * host only: no handle, no device).  The global block is every rank's m_local rows in rank order,
  * block row j goes to slot (E + j) mod C (Eq. 7 on the ring, D6), and slot p belongs to rank q

@@ -77,10 +77,6 @@ struct TPAux {
 // ranges long; the combine kernel recomputes the same S.  Unit id = segment id.
 // timing experiments only (F2C_FORCE_S, set at create): force the number of ranges S
 __constant__ int g_force_S;
-// dcp_pc_kernel's tail role (dcp_tail.cuh), set at create: F2C_TAIL = 0 never / 1 always (where it
-// applies) / unset: by the schedule's cost; F2C_TAIL_TAU = a tail tile's cost in pair tiles (tuning)
-__constant__ int g_tail_mode;
-__constant__ float g_tail_tau = 0.6f;
 __host__ __device__ inline int tp_choose_S(int R, int G, int n_tiles) {
     if (n_tiles <= 0 || R <= 0) return 1;
 #ifdef __CUDA_ARCH__

@@ -125,7 +125,6 @@ struct PCParams {
     const float *wslot;    // K >= 2: per-slot 1/||T_bar_c|| (fp32, padded by one tile; the NEXT-3
                            // out-of-pool rows' weight ring reads it); null for K = 1
     const int *S_sched;    // device: the range count S of this call's schedule (k_compact, pc_sched_cost)
-    const int *tail_G;     // device: clusters running the tail role (dcp_tail.cuh; 0 = none; k_compact)
     int kf;                // features per slot K: GEMM 1 contracts x_hat with the K raw rows of a slot
                            // (K d columns; 1/K is folded into a_r, so the logits use the exact mean)
     float margin_l2;       // s * m * log2(e)
@@ -343,10 +342,6 @@ __device__ __forceinline__ void tmem_wait_st() {
 // (K >= 2: with their weights through an smem ring); the default instantiation carries none of it
 // TF32: an fp32 pool (F2C_F32, d <= 256): GEMM 1 in kind::tf32 over the fp32 rows with x_hat as fp32 in
 // TMEM (d columns); GEMM 2 and everything after it read the pool's bf16 shadow, unchanged
-}  // namespace f2c
-#include "dcp_tail.cuh"
-namespace f2c {
-
 template <bool EXCL, bool NEG, bool TF32>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
     dcp_pc_kernel(const __grid_constant__ CUtensorMap tm3p, const __grid_constant__ CUtensorMap tm3q,
@@ -393,17 +388,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
     const bool dbgc = p.dbg && (blockIdx.x >> 1) == static_cast<unsigned>(p.dbg_cluster);
 #define PC_STAMP(k) do { if (dbgc) p.dbg[1040 + (blockIdx.x & 1) * 8 + (k)] = clock64(); } while (0)
     if (threadIdx.x == 0) PC_STAMP(0);
-    // the last <= 32-row group on its own clusters, one range per CTA (default variant only)
-    int tG = 0;
-    if constexpr (!EXCL && !NEG && !TF32) {
-        tG = p.tail_G != nullptr ? *p.tail_G : 0;
-        const int gm = static_cast<int>(gridDim.x >> 1) - tG;
-        if (tG > 0 && static_cast<int>(blockIdx.x >> 1) >= gm) {
-            dcp_tail_role(tm3p, p, smem, 2 * (static_cast<int>(blockIdx.x >> 1) - gm) + static_cast<int>(crank), 2 * tG,
-                          *p.S_sched * (n_rg - 1), n_rows);
-            return;
-        }
-    }
     if (threadIdx.x == 0) {
         for (int i = 0; i < PC_P_NSTAGE; ++i) {
             mbar_init(&aux->tfull[i], 1);
@@ -435,7 +419,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
         }
         fence_mbar_init();
         TPSched ts;
-        ts.init(blockIdx.x >> 1, (gridDim.x >> 1) - tG, tG > 0 ? n_rg - 1 : n_rg, n_tiles, *p.S_sched);
+        ts.init(blockIdx.x >> 1, gridDim.x >> 1, n_rg, n_tiles, *p.S_sched);
         int n = 0, a, b, c, s;
         while (n < PC_MAX_UNITS && ts.next(a, b, c, s)) aux->units[n++] = make_int4(a, b, c, s);
         aux->n_units = n;
@@ -473,7 +457,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PC_THREADS, 1)
                 // (only where it pays: a 64-row tail unit -- the row group that drifts ahead --, few row
                 // groups and long ranges; measured 1.5-8.5 % slower at c2 / c1 / c3r_8 otherwise)
                 const bool pace = p.prog != nullptr && aux->single_wave && n_rg >= 2 && n_rg <= 8 &&
-                                  tail64(n_rg - 1) && aux->range_len >= 512 && tG == 0;
+                                  tail64(n_rg - 1) && aux->range_len >= 512;
                 while (sch.next(rg, t0, t1, seg)) {
                     int spins = 0;  // (per unit: a stalled peer costs at most PC_PACE_SPINS polls per unit)
                     const bool wmu = NEG && p.wslot != nullptr && p.neg_mode != 0 && rg * PC_R + PC_R - 1 >= neg0;

@@ -353,12 +353,6 @@ static int kernel_kind(const f2c_dcp *h, int64_t N) {
     return 0;
 }
 
-// dcp_pc_kernel's default instantiation runs (bf16 pool, K = 1, no NEXT-3 variant): its tail role
-// (dcp_tail.cuh) may take a last group of <= 32 rows (k_compact decides per call)
-static bool tail_role_ok(const f2c_dcp *h, int64_t N) {
-    return kernel_kind(h, N) == 0 && h->dtype == F2C_BF16 && h->K == 1 && !h->excl_dup && h->neg_mode() == 0;
-}
-
 static int64_t occ_local(const f2c_dcp *h, const Rank &R) {
     const int64_t C_occ = h->E < h->C ? h->E : h->C;
     int64_t o = C_occ - R.lo;
@@ -590,12 +584,6 @@ int f2c_dcp_create_k(int64_t C, int32_t K, int32_t d, int32_t dtype, int32_t wor
         const char *fs = getenv("F2C_FORCE_S");    // timing experiments: force the range count S
         const int force_s = fs ? atoi(fs) : 0;
         cudaMemcpyToSymbol(g_force_S, &force_s, sizeof force_s);
-        const char *ft = getenv("F2C_TAIL");       // the tail role (experiment): off unless F2C_TAIL=1 (forced) / auto
-        const int tail_mode = !ft ? -1 : strcmp(ft, "auto") == 0 ? 0 : atoi(ft) == 0 ? -1 : 1;
-        cudaMemcpyToSymbol(g_tail_mode, &tail_mode, sizeof tail_mode);
-        const char *fa = getenv("F2C_TAIL_TAU");   // (tuning: a tail tile's cost in pair tiles)
-        const float tau = fa ? static_cast<float>(atof(fa)) : 0.6f;
-        cudaMemcpyToSymbol(g_tail_tau, &tau, sizeof tau);
     }
     if (cudaFuncSetAttribute(dcp_tp64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              TP_SMEM_BYTES) != cudaSuccess ||
@@ -1148,7 +1136,6 @@ static int phase_compact(f2c_dcp *h, Rank &R, const StepCtx &c, const int *tmax_
         a.G_pc = kind == 0 ? h->G / 2 : kind == 2 ? h->G4 : 0;
         a.rg_pc = kind == 2 ? P4_RG : PC_R;
         a.seg_cap = static_cast<int>(L.S_max * 128 / a.rg_pc);
-        a.tail_ok = tail_role_ok(h, c.N) ? 1 : 0;
         a.n_tiles_pc = static_cast<int>((occ_t + PC_TILE - 1) / PC_TILE);
     }
     k_compact<<<static_cast<unsigned>((c.N + 1023) / 1024), 1024, 0, c.st>>>(a);
@@ -1224,7 +1211,6 @@ static int phase_main(f2c_dcp *h, Rank &R, const StepCtx &c, int64_t occ_loc, co
         q.wslot = h->K > 1 ? R.at<float>(L.wslot) : nullptr;
         q.kf = h->K;
         q.S_sched = &R.sc()->S_sched;
-        q.tail_G = &R.sc()->tail_G;
         q.margin_l2 = p.margin_l2;
         q.ttgt = p.ttgt;
         q.seg_l = p.seg_l;
@@ -1234,8 +1220,7 @@ static int phase_main(f2c_dcp *h, Rank &R, const StepCtx &c, int64_t occ_loc, co
         // unit's GEMM 2 waits less; long units keep the direct drain and the smaller smem
         // footprint (measured: c1 +4-7 %, c2/c3 -1 % with staging)
         q.drain_tma = (p.n_slots + PC_TILE - 1) / PC_TILE <= 2048;
-        // (the tail role's ring, rows and P^T need the larger footprint)
-        const int smem = q.drain_tma || tail_role_ok(h, c.N) ? PC_SMEM_BYTES : PC_SMEM_BYTES_NOSTG;
+        const int smem = q.drain_tma ? PC_SMEM_BYTES : PC_SMEM_BYTES_NOSTG;
         q.excl = h->excl_dup;
         q.dup_off = R.at<int>(L.dup_off);
         q.dup_list = R.at<int2>(L.dup_list);
@@ -1721,16 +1706,6 @@ extern "C" int f2c_dcp_debug_timestamps(f2c_dcp *h, unsigned long long *dev_buf)
     h->dbg_flags = fl ? atoi(fl) : 0;
     const char *cl = getenv("F2C_DBG_CLUSTER");
     h->dbg_cluster = cl ? atoi(cl) : 0;
-    return F2C_OK;
-}
-
-extern "C" int f2c_dcp_schedule(f2c_dcp *h, int32_t *S, int32_t *tail_G) {
-    if (!h || !S || !tail_G) return fail(F2C_EINVAL, "NULL argument");
-    CUDA_TRY(cudaDeviceSynchronize());
-    Scalars s;
-    CUDA_TRY(cudaMemcpy(&s, h->ranks[0].sc(), sizeof s, cudaMemcpyDeviceToHost));
-    *S = s.S_sched;
-    *tail_G = s.tail_G;
     return F2C_OK;
 }
 

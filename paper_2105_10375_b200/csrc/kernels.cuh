@@ -34,7 +34,6 @@ struct Scalars {          // lives at the start of the per-rank scratch
     unsigned loss_done;   // CTAs of the final per-row kernel done (the last one sums the loss)
     int refine;           // R1 fallback: some row's reference was lowered, re-run the fused kernel
     int S_sched;          // dcp_pc_kernel's range count for this loss call (k_compact)
-    int tail_G;           // clusters running dcp_pc_kernel's tail role this call (0 = none; k_compact)
     int *err_mirror;      // mapped pinned host words {err, detail} of this shard: the host reads
                           // them at the next call on the handle without synchronising
 };
@@ -872,8 +871,7 @@ struct CompactArgs {
     int64_t *hgseq;           // [H]
     int G_pc, n_tiles_pc;     // dcp_pc_kernel's clusters and tiles: choose its S here (G_pc = 0: other kernels)
     int rg_pc;                // rows per group of that kernel: 128 (dcp_pc_kernel) or 256 (dcp_pc4_kernel)
-    int seg_cap;              // segments of rg_pc rows the partial buffers hold
-    int tail_ok;              // dcp_pc_kernel's default instantiation runs: the tail role may be chosen
+    int seg_cap;              // segments of rg_pc rows the partial buffers hold (dcp_pc4_kernel)
 };
 __global__ void __launch_bounds__(1024) k_compact(CompactArgs a) {
     // CTA b compacts rows [b*1024, (b+1)*1024).  Every CTA counts the in-pool rows of the
@@ -973,11 +971,8 @@ __global__ void __launch_bounds__(1024) k_compact(CompactArgs a) {
         a.ttgt[r] = -INFINITY;
     }
     if (a.G_pc > 0) {  // dcp_pc_kernel's S: one candidate per thread, argmin (cost, then S)
-        __shared__ unsigned long long best, best_t;
-        if (tid == 0) {
-            best = ~0ull;
-            best_t = ~0ull;
-        }
+        __shared__ unsigned long long best;
+        if (tid == 0) best = ~0ull;
         __syncthreads();
         const int R = (n_rows + a.rg_pc - 1) / a.rg_pc;
         int s_hi = pc_s_hi(R, a.G_pc, a.n_tiles_pc);
@@ -986,37 +981,13 @@ __global__ void __launch_bounds__(1024) k_compact(CompactArgs a) {
             const float c = pc_sched_cost(S, R, a.G_pc, a.n_tiles_pc);
             atomicMin(&best, (static_cast<unsigned long long>(__float_as_uint(c)) << 32) | static_cast<unsigned>(S));
         }
-        // the tail role (dcp_tail.cuh): a last group of <= 32 rows runs on tG clusters as 2 tG single-CTA
-        // ranges, the other R - 1 groups on the remaining clusters; cost = the slower of the two, a
-        // tail tile counted as g_tail_tau of a pair's tile.  Candidates (tG <= G / 4, S) one per thread.
-        const bool tail_cand = a.tail_ok && g_tail_mode >= 0 && a.rg_pc == PC_R && R >= 2 &&
-                               n_rows - (R - 1) * PC_R <= TL_N && a.n_tiles_pc > 0;
-        if (tail_cand) {
-            const int tg_hi = a.G_pc / 4 > 0 ? a.G_pc / 4 : 1;
-            const int sh = pc_s_hi(R - 1, a.G_pc - 1 > 0 ? a.G_pc - 1 : 1, a.n_tiles_pc);
-            for (int i = tid; i < tg_hi * sh; i += nt) {
-                const int tg = 1 + i / sh, S = 1 + i % sh, gm = a.G_pc - tg;
-                if (gm < 1 || S > pc_s_hi(R - 1, gm, a.n_tiles_pc) || (R - 1) * S + 2 * tg > a.seg_cap) continue;
-                const float ct = static_cast<float>((a.n_tiles_pc + 2 * tg - 1) / (2 * tg)) * g_tail_tau + 8.f;
-                const float c = fmaxf(pc_sched_cost(S, R - 1, gm, a.n_tiles_pc), ct);
-                atomicMin(&best_t, (static_cast<unsigned long long>(__float_as_uint(c)) << 32) |
-                                       (static_cast<unsigned long long>(tg) << 20) | static_cast<unsigned>(S));
-            }
-        }
         __syncthreads();
         if (tid == 0) {
-            int S = static_cast<int>(best & 0xfffffull), tg = 0;
-            if (tail_cand && best_t != ~0ull && (g_tail_mode > 0 || (best_t >> 32) < (best >> 32))) {
-                S = static_cast<int>(best_t & 0xfffffull);
-                tg = static_cast<int>((best_t >> 20) & 0xfffull);
-            }
-            if (g_force_S > 0 && tg == 0) S = g_force_S < s_hi ? g_force_S : s_hi;  // (timing experiments; within the layout's bounds)
+            int S = static_cast<int>(best & 0xffffffffull);
+            if (g_force_S > 0) S = g_force_S < s_hi ? g_force_S : s_hi;  // (timing experiments; within the layout's bounds)
             if (S > a.n_tiles_pc) S = a.n_tiles_pc;
             a.sc->S_sched = S < 1 ? 1 : S;
-            a.sc->tail_G = tg;
         }
-    } else if (tid == 0) {
-        a.sc->tail_G = 0;
     }
     if (tid == 0) {
         a.sc->refine = 0;
@@ -1224,21 +1195,6 @@ __device__ __forceinline__ void store_dx_row(uint8_t *dx, int dtype, int64_t i, 
     }
 }
 
-// The segments of row group rg of a loss call: Sx ranges of the shard's tiles, range s in segment
-// base + s stride.  dcp_pc_kernel's tail role (sc->tail_G > 0) puts the last group's 2 tail_G ranges
-// after the other groups' S (n_rg - 1) segments.
-struct SegRange {
-    int S, base, stride;
-};
-__device__ __forceinline__ SegRange seg_range(const CombineArgs &a, int n_rg, int rg, int S) {
-    const int tg = a.wide ? a.sc->tail_G : 0;
-    if (tg > 0) {
-        if (rg == n_rg - 1) return SegRange{2 * tg, S * (n_rg - 1), 1};
-        return SegRange{S, rg, n_rg - 1};
-    }
-    return SegRange{S, rg, n_rg};
-}
-
 // sum the partials of compacted row k over its segments (fixed range order);
 // the schedule (tp_choose_S) is the main kernel's.  Segments are read in batches of B so
 // that the L2 latency is paid once per batch; the accumulation order is the segment order.
@@ -1251,8 +1207,7 @@ __device__ __forceinline__ void gather_row_partials(const CombineArgs &a, int n_
     mx = -INFINITY;
     zero16(o);
     if (a.n_tiles <= 0) return;
-    const SegRange sr = seg_range(a, n_rg, rg, a.wide ? a.sc->S_sched : tp_choose_S(n_rg, a.G, a.n_tiles));
-    const int S = sr.S;
+    const int S = (a.wide ? a.sc->S_sched : tp_choose_S(n_rg, a.G, a.n_tiles));
     constexpr int B = 4;
     for (int s0 = 0; s0 < S; s0 += B) {
         float lv[B], mv[B];
@@ -1268,7 +1223,7 @@ __device__ __forceinline__ void gather_row_partials(const CombineArgs &a, int n_
             const int t0 = tp_range_begin(s, a.n_tiles, S);
             const int t1 = tp_range_begin(s + 1, a.n_tiles, S);
             if (t1 <= t0) continue;
-            const long long seg = static_cast<long long>(s) * sr.stride + sr.base;
+            const long long seg = static_cast<long long>(s) * n_rg + rg;
             lv[u] = a.seg_l[seg * RG + r];
             mv[u] = a.seg_mx[seg * RG + r];
             const float *src = a.seg_O + (seg * RG + r) * a.d;
@@ -1302,13 +1257,12 @@ __device__ __forceinline__ void gather_row_max(const CombineArgs &a, int n_rg, i
     cmax = -INFINITY;
     carg = -1;
     if (a.n_tiles <= 0) return;
-    const SegRange sr = seg_range(a, n_rg, rg, a.wide ? a.sc->S_sched : tp_choose_S(n_rg, a.G, a.n_tiles));
-    const int S = sr.S;
+    const int S = (a.wide ? a.sc->S_sched : tp_choose_S(n_rg, a.G, a.n_tiles));
     for (int s = 0; s < S; ++s) {
         const int t0 = tp_range_begin(s, a.n_tiles, S);
         const int t1 = tp_range_begin(s + 1, a.n_tiles, S);
         if (t1 <= t0) continue;
-        const long long seg = static_cast<long long>(s) * sr.stride + sr.base;
+        const long long seg = static_cast<long long>(s) * n_rg + rg;
         const float v = a.seg_mx[seg * RG + r];
         if (v > cmax) {
             cmax = v;
@@ -1541,13 +1495,12 @@ __global__ void __launch_bounds__(256, 2) k_local_rows(CombineArgs a, float4 *__
         const int rg = k / RG, r = k % RG;
         float lsum = 0.f, mx = -INFINITY;
         if (a.n_tiles > 0) {
-            const SegRange sr = seg_range(a, n_rg, rg, a.wide ? a.sc->S_sched : tp_choose_S(n_rg, a.G, a.n_tiles));
-            const int S = sr.S;
+            const int S = (a.wide ? a.sc->S_sched : tp_choose_S(n_rg, a.G, a.n_tiles));
             for (int s = lane; s < S; s += 32) {  // lanes split the segments, fixed-order tree below
                 const int t0 = tp_range_begin(s, a.n_tiles, S);
                 const int t1 = tp_range_begin(s + 1, a.n_tiles, S);
                 if (t1 <= t0) continue;
-                const long long seg = static_cast<long long>(s) * sr.stride + sr.base;
+                const long long seg = static_cast<long long>(s) * n_rg + rg;
                 lsum += a.seg_l[seg * RG + r];
                 mx = fmaxf(mx, a.seg_mx[seg * RG + r]);
             }

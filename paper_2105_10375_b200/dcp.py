@@ -55,7 +55,6 @@ def load_library():
     L.f2c_dcp_profile.argtypes = [P, i32]
     L.f2c_dcp_profile_read.argtypes = [P, P, P, P]
     L.f2c_dcp_fused_kernel.argtypes = [P, i64, P, P]
-    L.f2c_dcp_schedule.argtypes = [P, P, P]
     L.f2c_dcp_destroy.argtypes = [P]
     L.f2c_dcp_destroy.restype = None
     L.f2c_dcp_set_lcos.argtypes = [P, i32, i32, ctypes.c_double]
@@ -64,8 +63,7 @@ def load_library():
     for f in (L.f2c_dcp_create, L.f2c_dcp_create_k, L.f2c_dcp_set_lcos, L.f2c_dcp_set_dup_mode,
               L.f2c_dcp_set_enqueue_mode, L.f2c_dcp_enqueue, L.f2c_dcp_loss_fwd_bwd, L.f2c_gnet_ema,
               L.f2c_dcp_get_state, L.f2c_dcp_set_state, L.f2c_dcp_row_stats, L.f2c_dcp_check,
-              L.f2c_last_launch_count, L.f2c_dcp_profile, L.f2c_dcp_profile_read, L.f2c_dcp_fused_kernel,
-              L.f2c_dcp_schedule):
+              L.f2c_last_launch_count, L.f2c_dcp_profile, L.f2c_dcp_profile_read, L.f2c_dcp_fused_kernel):
         f.restype = ctypes.c_int
     _lib = L
     return L
@@ -266,13 +264,6 @@ class DCPHead:
         k, c = ctypes.c_int32(), ctypes.c_int32()
         _check(load_library().f2c_dcp_fused_kernel(self._h, n_global, ctypes.byref(k), ctypes.byref(c)))
         return k.value, c.value
-
-    def schedule(self):
-        """(S, tail_G) of the last loss call: tile ranges per row group and the clusters that ran
-        the fused kernel's tail role (include/f2c_dcp.h)."""
-        S, tg = ctypes.c_int32(), ctypes.c_int32()
-        _check(load_library().f2c_dcp_schedule(self._h, ctypes.byref(S), ctypes.byref(tg)))
-        return S.value, tg.value
 
     @staticmethod
     def last_launch_count() -> int:
